@@ -1,0 +1,162 @@
+/*
+ * dsa_b200.h -- C-ABI of the B200-native Dynamic Sparse Attention hot path.
+ *
+ * Plain pointers and sizes only (no torch / C++ types).  All device pointers
+ * are caller-owned CUDA global memory; every entry point is stream-ordered
+ * and asynchronous on the `stream` it is given (a cudaStream_t passed as
+ * void*, NULL = legacy default stream), thread-safe, and allocation-free on
+ * the hot path (scratch lives in the caller's workspace).  Errors never
+ * cross the boundary as exceptions: each call returns a dsa_status and a
+ * thread-local message is kept for dsa_last_error().  The C++ shim
+ * (include/dsattn_gpu.hpp) maps the codes back onto the reference exception
+ * types (ShapeError / ParamError / ConfigError / IoError; P/include/dsattn/
+ * errors.hpp:9-31) so reference callers and CLI exit codes are unchanged.
+ *
+ * Reference interfaces replaced (P/ = /root/reference/proj/):
+ *   dsa_predict          <- Matrix quantize(const Matrix&, QuantSpec) applied to
+ *                           matmul(Q,P) / matmul(K,P)   P/include/dsattn/predictor.hpp:31-49,
+ *                           P/src/predictor.cpp:34-45,67-80; kernels::matmul/quantize
+ *                           P/include/dsattn/kernels.hpp:22-35
+ *   dsa_select           <- predicted_topk_mask / threshold_mask / colvec_mask
+ *                           P/include/dsattn/maskgen.hpp:14-31 (+ block mode)
+ *   dsa_sparse_attention <- sddmm -> sparse_softmax -> spmm per head
+ *                           P/include/dsattn/sparse.hpp:47-55, P/src/sparse.cpp:38-91
+ *   dsa_pipeline         <- the per-head composition above (predict -> select -> attend)
+ *   dsa_counters         <- OpCounters P/include/dsattn/sparse.hpp:14-21
+ *   dsa_last_error       <- exception what() strings
+ */
+#ifndef DSA_B200_H
+#define DSA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DSA_ABI_VERSION 1
+
+typedef enum dsa_status {
+    DSA_OK = 0,
+    DSA_ERR_SHAPE = 1,   /* ShapeError  (dimension mismatch)          */
+    DSA_ERR_PARAM = 2,   /* ParamError  (out-of-range value)          */
+    DSA_ERR_CONFIG = 3,  /* ConfigError (bad preset / unknown key)    */
+    DSA_ERR_CUDA = 4,    /* CUDA runtime / launch failure             */
+    DSA_ERR_IO = 5,      /* IoError                                   */
+    DSA_ERR_UNSUPPORTED = 6 /* valid config outside the built kernels */
+} dsa_status;
+
+typedef enum dsa_dtype { DSA_F32 = 0, DSA_BF16 = 1 } dsa_dtype;
+
+typedef enum dsa_quant_scope {
+    DSA_QUANT_PER_TENSOR = 0, /* reference: one scale per (b,h) tensor, predictor.cpp:37-41 */
+    DSA_QUANT_PER_ROW = 1     /* extension: one scale per row of Q~ / K~         */
+} dsa_quant_scope;
+
+typedef enum dsa_mask_mode {
+    DSA_MASK_ROW_TOPK = 0,  /* keep `keep` keys per query row (maskgen.cpp:11-20)           */
+    DSA_MASK_COLVEC = 1,    /* vec_v query rows x 1 key column, max-pooled (maskgen.cpp:33) */
+    DSA_MASK_BLOCK = 2,     /* block x block tiles, mean-pooled, optional forced diagonal  */
+    DSA_MASK_THRESHOLD = 3  /* p~ >= frac_den / (frac_num * L), optional causal, cap       */
+} dsa_mask_mode;
+
+/* One (batch x heads) problem; pairs = batch * heads.  Q/K/V/Z are
+ * [pairs][L][d] row-major in `dtype`; P is [d][k] float32. */
+typedef struct dsa_config {
+    int64_t batch, heads, L, d, k;
+    int32_t dtype;        /* dsa_dtype                                           */
+    int32_t bits;         /* prediction precision: 2, 4 or 8 (QuantSpec bits)    */
+    int32_t quant_scope;  /* dsa_quant_scope                                     */
+    int32_t round_proj_f32; /* 1: round Q.P through float (f32 Matrix semantics) */
+    int32_t mask_mode;    /* dsa_mask_mode                                       */
+    int32_t scale;        /* 1: scores scaled by 1/sqrt(d) (sparse.cpp:48)       */
+    int64_t keep;         /* ROW_TOPK: keys/row; COLVEC: columns/band; BLOCK: blocks/block-row */
+    int32_t vec_v;        /* COLVEC band height                                  */
+    int32_t block;        /* BLOCK tile edge                                     */
+    int32_t force_diag;   /* BLOCK: diagonal tile always kept (counts in keep)   */
+    int32_t causal;       /* THRESHOLD: candidates j <= i                        */
+    int64_t frac_num, frac_den; /* THRESHOLD: theta = frac_den / (frac_num * L)  */
+    int64_t cap;          /* THRESHOLD: max kept per row                         */
+} dsa_config;
+
+/* Device mask.  Layout by mode (all column lists ascending):
+ *   ROW_TOPK : cols[pairs][L][keep]
+ *   COLVEC   : cols[pairs][ceil(L/vec_v)][keep]        (shared by the band's rows)
+ *   BLOCK    : cols[pairs][ceil(L/block)][keep]        (block-column indices)
+ *   THRESHOLD: rowptr[pairs*L + 1] (uint64, global CSR), cols[capacity]
+ * empty_rows (optional, uint8[pairs*L]) flags rows with no kept key
+ * (sparse.cpp:63-66). */
+typedef struct dsa_mask {
+    uint32_t* cols;
+    uint64_t* rowptr;
+    int64_t capacity; /* entries available in cols */
+    uint8_t* empty_rows;
+} dsa_mask;
+
+typedef struct dsa_counts {
+    uint64_t nnz;          /* kept positions over all pairs                */
+    uint64_t sddmm_mults;  /* nnz * d   (sparse.cpp:51)                    */
+    uint64_t spmm_mults;   /* nnz * d   (sparse.cpp:89)                    */
+    uint64_t softmax_exps; /* nnz       (sparse.cpp:75)                    */
+    uint64_t empty_rows;
+    double flops_predict;  /* 4 L d k per pair                             */
+    double flops_score;    /* 2 L^2 k per pair (causal: L(L+1) k)          */
+    double flops_attention;/* 4 nnz d                                      */
+    double bytes_predict;  /* compulsory HBM bytes per phase */
+    double bytes_attention;
+} dsa_counts;
+
+/* ----------------------------------------------------------------- meta */
+int dsa_abi_version(void);
+const char* dsa_last_error(void);
+const char* dsa_build_info(void);
+dsa_status dsa_config_validate(const dsa_config* cfg);
+/* Scratch bytes needed by dsa_predict / dsa_select / dsa_pipeline. */
+size_t dsa_workspace_bytes(const dsa_config* cfg);
+/* Entries needed in dsa_mask.cols (THRESHOLD: worst case from cap, theta, causal). */
+int64_t dsa_mask_capacity(const dsa_config* cfg);
+
+/* ------------------------------------------------------------ hot path */
+/* (1) projection + quantisation.  levels_q/levels_k: [pairs][L][k] integer
+ * levels held exactly in bf16 (uint16 bits); scale_q/scale_k: [pairs]
+ * (PER_TENSOR) or [pairs][L] (PER_ROW) doubles. */
+dsa_status dsa_predict(const dsa_config* cfg, const void* q, const void* k, const float* p,
+                       uint16_t* levels_q, uint16_t* levels_k, double* scale_q, double* scale_k,
+                       void* workspace, size_t workspace_bytes, void* stream);
+
+/* (2) exact-integer approximate scores -> mask selection. */
+dsa_status dsa_select(const dsa_config* cfg, const uint16_t* levels_q, const uint16_t* levels_k,
+                      const double* scale_q, const double* scale_k, const dsa_mask* mask,
+                      void* workspace, size_t workspace_bytes, void* stream);
+
+/* (3) SDDMM -> sparse row softmax -> SpMM over the mask; z: [pairs][L][d]
+ * in cfg->dtype.  Empty rows give zero output rows, flagged in
+ * mask->empty_rows when non-NULL. */
+dsa_status dsa_sparse_attention(const dsa_config* cfg, const void* q, const void* k,
+                                const void* v, const dsa_mask* mask, void* z, void* stream);
+
+/* (1)->(2)->(3).  mask_out may be NULL (mask kept in the workspace only). */
+dsa_status dsa_pipeline(const dsa_config* cfg, const void* q, const void* k, const void* v,
+                        const float* p, void* z, const dsa_mask* mask_out, void* workspace,
+                        size_t workspace_bytes, void* stream);
+
+/* Exact operation counts for a computed mask (synchronises `stream`). */
+dsa_status dsa_counters(const dsa_config* cfg, const dsa_mask* mask, dsa_counts* out,
+                        void* stream);
+
+/* ------------------------------------------------------ synthetic inputs */
+/* Seeded BASELINE generator (host): Q/K/V ~ N(0,1), a shared unit vector u
+ * added at +3 to `planted_per_mille`/1000 of the key positions and at +0.5 to
+ * every query, optional local band (+1.0 score bias inside 32-row windows),
+ * P ~ N(0, 1/k) rounded to f32.  Pair p is generated from its own substream,
+ * so any pair range can be regenerated independently.  q/k/v receive
+ * [npairs][L][d] in cfg->dtype; p (may be NULL) receives [d][k]. */
+dsa_status dsa_generate(const dsa_config* cfg, uint64_t seed, int32_t planted_per_mille,
+                        int32_t band_width, int64_t pair0, int64_t npairs, void* q, void* k,
+                        void* v, float* p, int32_t threads);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DSA_B200_H */

@@ -1,0 +1,427 @@
+// C-ABI entry points (include/dsa_b200.h): validation, workspace planning
+// and stream-ordered launches of the sm_100a kernels.  No exceptions cross
+// this boundary; errors become dsa_status codes + dsa_last_error().
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "dsa_b200.h"
+#include "dsa_internal.h"
+#include "kernels.h"
+
+#define DSA_STR2(x) #x
+#define DSA_STR(x) DSA_STR2(x)
+
+namespace dsa {
+
+namespace {
+thread_local std::string g_last_error;
+
+constexpr size_t kAlign = 256;
+size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+int64_t pairs_of(const dsa_config& c) { return c.batch * c.heads; }
+int qmax_of(int bits) { return (1 << (bits - 1)) - 1; }
+int64_t span_of(const dsa_config& c) {
+    const int64_t q = qmax_of(c.bits);
+    return 2 * c.k * q * q + 1;
+}
+int64_t nbands(const dsa_config& c) {
+    return c.mask_mode == DSA_MASK_COLVEC ? ceil_div(c.L, c.vec_v)
+           : c.mask_mode == DSA_MASK_BLOCK ? ceil_div(c.L, c.block)
+                                           : c.L;
+}
+
+void check_cuda(cudaError_t e, const char* where) {
+    if (e != cudaSuccess) throw_cuda(e, where);
+}
+
+void validate(const dsa_config* cp) {
+    if (!cp) throw Error(DSA_ERR_PARAM, "dsa: null config");
+    const dsa_config& c = *cp;
+    if (c.batch < 1 || c.heads < 1) throw Error(DSA_ERR_SHAPE, "dsa: batch and heads must be >= 1");
+    if (c.L < 1) throw Error(DSA_ERR_SHAPE, "Matrix: dimensions must be positive");
+    if (c.L >= (int64_t{1} << 31)) throw Error(DSA_ERR_SHAPE, "dsa: L must be < 2^31");
+    if (c.d != 16 && c.d != 32 && c.d != 64 && c.d != 128)
+        throw Error(DSA_ERR_UNSUPPORTED, "dsa: head dim d must be one of 16, 32, 64, 128");
+    if (c.k != 16 && c.k != 32) throw Error(DSA_ERR_UNSUPPORTED, "dsa: projection width k must be 16 or 32");
+    if (c.k > c.d) throw Error(DSA_ERR_PARAM, "init_projection: need 1 <= k <= d");
+    if (c.dtype != DSA_F32 && c.dtype != DSA_BF16) throw Error(DSA_ERR_PARAM, "dsa: dtype must be F32 or BF16");
+    if (c.bits != 2 && c.bits != 4 && c.bits != 8) {
+        if (c.bits == 0 || c.bits == 16)
+            throw Error(DSA_ERR_UNSUPPORTED, "dsa: full/16-bit prediction levels are not integer-exact on the tensor-core path");
+        throw Error(DSA_ERR_PARAM, "QuantSpec: bits must be one of {2,4,8,16,full}");
+    }
+    if (c.quant_scope != DSA_QUANT_PER_TENSOR && c.quant_scope != DSA_QUANT_PER_ROW)
+        throw Error(DSA_ERR_PARAM, "dsa: unknown quant_scope");
+    switch (c.mask_mode) {
+        case DSA_MASK_ROW_TOPK:
+            if (c.keep < 1 || c.keep > c.L) throw Error(DSA_ERR_PARAM, "row_topk_indices: k_keep out of range");
+            if (c.L * (c.quant_scope == DSA_QUANT_PER_ROW ? 8 : 4) > 200 * 1024)
+                throw Error(DSA_ERR_UNSUPPORTED, "dsa: row top-k supports L <= 51200 (25600 per-row)");
+            break;
+        case DSA_MASK_COLVEC:
+            if (c.vec_v < 1) throw Error(DSA_ERR_PARAM, "colvec_mask: vector height must be >= 1");
+            if (c.keep < 1 || c.keep > c.L) throw Error(DSA_ERR_PARAM, "row_topk_indices: k_keep out of range");
+            if (c.quant_scope != DSA_QUANT_PER_TENSOR)
+                throw Error(DSA_ERR_UNSUPPORTED, "dsa: colvec mode needs per-tensor levels");
+            if (c.L * 4 > 200 * 1024) throw Error(DSA_ERR_UNSUPPORTED, "dsa: colvec supports L <= 51200");
+            break;
+        case DSA_MASK_BLOCK:
+            if (c.block < 1) throw Error(DSA_ERR_PARAM, "dsa: block must be >= 1");
+            if (c.keep < 1 || c.keep > ceil_div(c.L, c.block))
+                throw Error(DSA_ERR_PARAM, "row_topk_indices: k_keep out of range");
+            if (c.quant_scope != DSA_QUANT_PER_TENSOR)
+                throw Error(DSA_ERR_UNSUPPORTED, "dsa: block mode needs per-tensor levels");
+            break;
+        case DSA_MASK_THRESHOLD:
+            if (c.frac_num < 1 || c.frac_den < 1) throw Error(DSA_ERR_PARAM, "threshold_mask: theta must be finite");
+            if (c.cap < 1) throw Error(DSA_ERR_PARAM, "dsa: cap must be >= 1");
+            if (c.quant_scope != DSA_QUANT_PER_TENSOR)
+                throw Error(DSA_ERR_UNSUPPORTED, "dsa: threshold mode needs per-tensor levels");
+            if (c.L * 4 > 200 * 1024) throw Error(DSA_ERR_UNSUPPORTED, "dsa: threshold supports L <= 51200");
+            if (c.frac_num * c.L > (int64_t{1} << 22)) throw Error(DSA_ERR_PARAM, "dsa: frac_num * L too large");
+            break;
+        default: throw Error(DSA_ERR_PARAM, "dsa: unknown mask_mode");
+    }
+}
+
+int64_t capacity_of(const dsa_config& c) {
+    const int64_t P = pairs_of(c);
+    switch (c.mask_mode) {
+        case DSA_MASK_ROW_TOPK: return P * c.L * c.keep;
+        case DSA_MASK_COLVEC: return P * ceil_div(c.L, c.vec_v) * c.keep;
+        case DSA_MASK_BLOCK: return P * ceil_div(c.L, c.block) * c.keep;
+        default: {
+            // sum_i <= 1 => at most floor(L * num / den) keys reach theta.
+            const int64_t bound = std::min<int64_t>(c.cap, (c.L * c.frac_num) / c.frac_den);
+            int64_t per_pair = 0;
+            if (c.causal) {
+                // rows i < bound keep at most i + 1 candidates, the rest `bound`
+                const int64_t b = std::min<int64_t>(std::max<int64_t>(bound, 0), c.L);
+                per_pair = (b * (b + 1)) / 2 + (c.L - b) * b;
+            } else {
+                per_pair = c.L * bound;
+            }
+            return P * std::max<int64_t>(per_pair, 1);
+        }
+    }
+}
+
+// Workspace: [x64 | amax | pooled | etab | counts | scan | levels | scales | mask]
+struct Plan {
+    size_t x64 = 0, amax = 0, pooled = 0, etab = 0, counts = 0, scan = 0, lq = 0, lk = 0, sq = 0,
+           sk = 0, cols = 0, rowptr = 0, total = 0;
+    size_t scan_bytes = 0;
+};
+
+Plan plan(const dsa_config& c, bool pipeline, bool own_mask) {
+    Plan p;
+    const int64_t P = pairs_of(c);
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t o = off;
+        off += align_up(bytes);
+        return o;
+    };
+    const bool per_tensor = c.quant_scope == DSA_QUANT_PER_TENSOR;
+    p.x64 = take(per_tensor ? sizeof(double) * P * 2 * c.L * c.k : 0);
+    p.amax = take(per_tensor ? sizeof(unsigned long long) * P * 2 : 0);
+    p.pooled = take(c.mask_mode == DSA_MASK_BLOCK ? sizeof(int32_t) * P * 2 * ceil_div(c.L, c.block) * c.k : 0);
+    p.etab = take(c.mask_mode == DSA_MASK_THRESHOLD ? sizeof(int64_t) * P * span_of(c) : 0);
+    p.counts = take(c.mask_mode == DSA_MASK_THRESHOLD ? sizeof(uint64_t) * P * c.L : 0);
+    if (c.mask_mode == DSA_MASK_THRESHOLD) p.scan_bytes = select_scan_tmp_bytes(P * c.L);
+    p.scan = take(p.scan_bytes);
+    if (pipeline) {
+        p.lq = take(sizeof(uint16_t) * P * c.L * c.k);
+        p.lk = take(sizeof(uint16_t) * P * c.L * c.k);
+        const int64_t ns = per_tensor ? P : P * c.L;
+        p.sq = take(sizeof(double) * ns);
+        p.sk = take(sizeof(double) * ns);
+        if (own_mask) {
+            p.cols = take(sizeof(uint32_t) * capacity_of(c));
+            p.rowptr = take(c.mask_mode == DSA_MASK_THRESHOLD ? sizeof(uint64_t) * (P * c.L + 1) : 0);
+        }
+    }
+    p.total = off;
+    return p;
+}
+
+template <class T>
+T* at(void* ws, size_t off) {
+    return reinterpret_cast<T*>(static_cast<char*>(ws) + off);
+}
+
+void check_ws(const Plan& p, void* ws, size_t bytes) {
+    if (p.total > 0 && (!ws || bytes < p.total))
+        throw Error(DSA_ERR_PARAM, "dsa: workspace too small (need " + std::to_string(p.total) + " bytes)");
+}
+
+void do_predict(const dsa_config& c, const void* q, const void* k, const float* p, uint16_t* lq,
+                uint16_t* lk, double* sq, double* sk, const Plan& pl, void* ws, cudaStream_t st) {
+    if (!q || !k || !p || !lq || !lk || !sq || !sk) throw Error(DSA_ERR_PARAM, "dsa_predict: null pointer");
+    PredictArgs a{};
+    a.q = q;
+    a.k = k;
+    a.p = p;
+    a.pairs = pairs_of(c);
+    a.L = c.L;
+    a.D = c.d;
+    a.KD = c.k;
+    a.bf16 = c.dtype == DSA_BF16;
+    a.per_row = c.quant_scope == DSA_QUANT_PER_ROW;
+    a.round_f32 = c.round_proj_f32;
+    a.qmax = static_cast<double>(qmax_of(c.bits));
+    a.lq = lq;
+    a.lk = lk;
+    a.sq = sq;
+    a.sk = sk;
+    a.xws = at<double>(ws, pl.x64);
+    a.amax = at<unsigned long long>(ws, pl.amax);
+    run_predict(a, st);
+    check_cuda(cudaGetLastError(), "dsa_predict launch");
+}
+
+void do_select(const dsa_config& c, const uint16_t* lq, const uint16_t* lk, const double* sq,
+               const double* sk, const dsa_mask& m, const Plan& pl, void* ws, cudaStream_t st) {
+    if (!lq || !lk || !sq || !sk || !m.cols) throw Error(DSA_ERR_PARAM, "dsa_select: null pointer");
+    if (m.capacity < capacity_of(c) && c.mask_mode != DSA_MASK_THRESHOLD)
+        throw Error(DSA_ERR_PARAM, "dsa_select: mask capacity too small");
+    if (c.mask_mode == DSA_MASK_THRESHOLD && (!m.rowptr || m.capacity < capacity_of(c)))
+        throw Error(DSA_ERR_PARAM, "dsa_select: threshold mode needs rowptr and capacity >= dsa_mask_capacity()");
+    SelectArgs a{};
+    a.mode = c.mask_mode;
+    a.pairs = pairs_of(c);
+    a.L = c.L;
+    a.KD = c.k;
+    a.D = c.d;
+    a.per_row = c.quant_scope == DSA_QUANT_PER_ROW;
+    a.lq = lq;
+    a.lk = lk;
+    a.sq = sq;
+    a.sk = sk;
+    a.keep = c.keep;
+    a.vec_v = c.vec_v;
+    a.block = c.block;
+    a.force_diag = c.force_diag;
+    a.causal = c.causal;
+    a.frac_num = c.frac_num;
+    a.frac_den = c.frac_den;
+    a.cap = c.cap;
+    a.qmax = qmax_of(c.bits);
+    a.cols = m.cols;
+    a.rowptr = m.rowptr;
+    a.capacity = m.capacity;
+    a.empty_rows = m.empty_rows;
+    a.pooled = at<int32_t>(ws, pl.pooled);
+    a.etab = at<int64_t>(ws, pl.etab);
+    a.counts = at<uint64_t>(ws, pl.counts);
+    a.span = span_of(c);
+    a.scan_tmp = at<void>(ws, pl.scan);
+    a.scan_tmp_bytes = pl.scan_bytes;
+    if (m.empty_rows && c.mask_mode != DSA_MASK_THRESHOLD)
+        check_cuda(cudaMemsetAsync(m.empty_rows, 0, pairs_of(c) * c.L, st), "dsa_select memset");
+    run_select(a, st);
+    check_cuda(cudaGetLastError(), "dsa_select launch");
+}
+
+void do_attention(const dsa_config& c, const void* q, const void* k, const void* v,
+                  const dsa_mask& m, void* z, cudaStream_t st) {
+    if (!q || !k || !v || !z || !m.cols) throw Error(DSA_ERR_PARAM, "dsa_sparse_attention: null pointer");
+    if (c.mask_mode == DSA_MASK_THRESHOLD && !m.rowptr)
+        throw Error(DSA_ERR_PARAM, "dsa_sparse_attention: threshold mask needs rowptr");
+    AttnArgs a{};
+    a.mode = c.mask_mode;
+    a.pairs = pairs_of(c);
+    a.L = c.L;
+    a.D = c.d;
+    a.bf16 = c.dtype == DSA_BF16;
+    a.scale = c.scale;
+    a.q = q;
+    a.k = k;
+    a.v = v;
+    a.cols = m.cols;
+    a.rowptr = m.rowptr;
+    a.keep = c.keep;
+    a.vec_v = c.vec_v;
+    a.block = c.block;
+    a.z = z;
+    a.empty_rows = m.empty_rows;
+    run_attention(a, st);
+    check_cuda(cudaGetLastError(), "dsa_sparse_attention launch");
+}
+
+void require_device() {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0)
+        throw Error(DSA_ERR_CUDA, "dsa: no CUDA device available (the B200 path has no CPU fallback)");
+}
+
+}  // namespace
+
+void set_last_error(const std::string& m) { g_last_error = m; }
+
+[[noreturn]] void throw_unsupported(const std::string& what) { throw Error(DSA_ERR_UNSUPPORTED, "dsa: " + what); }
+[[noreturn]] void throw_cuda(cudaError_t e, const char* where) {
+    throw Error(DSA_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+}  // namespace dsa
+
+using namespace dsa;
+
+extern "C" {
+
+int dsa_abi_version(void) { return DSA_ABI_VERSION; }
+const char* dsa_last_error(void) { return g_last_error.c_str(); }
+const char* dsa_build_info(void) {
+    return "dsa_b200 sm_100a, CUDA runtime " DSA_STR(CUDART_VERSION);
+}
+
+dsa_status dsa_config_validate(const dsa_config* cfg) {
+    return guard([&] { validate(cfg); });
+}
+
+size_t dsa_workspace_bytes(const dsa_config* cfg) {
+    size_t out = 0;
+    dsa_status s = guard([&] {
+        validate(cfg);
+        out = plan(*cfg, true, true).total;
+    });
+    return s == DSA_OK ? out : 0;
+}
+
+int64_t dsa_mask_capacity(const dsa_config* cfg) {
+    int64_t out = -1;
+    guard([&] {
+        validate(cfg);
+        out = capacity_of(*cfg);
+    });
+    return out;
+}
+
+dsa_status dsa_predict(const dsa_config* cfg, const void* q, const void* k, const float* p,
+                       uint16_t* levels_q, uint16_t* levels_k, double* scale_q, double* scale_k,
+                       void* workspace, size_t workspace_bytes, void* stream) {
+    return guard([&] {
+        validate(cfg);
+        require_device();
+        Plan pl = plan(*cfg, false, false);
+        check_ws(pl, workspace, workspace_bytes);
+        do_predict(*cfg, q, k, p, levels_q, levels_k, scale_q, scale_k, pl, workspace,
+                   static_cast<cudaStream_t>(stream));
+    });
+}
+
+dsa_status dsa_select(const dsa_config* cfg, const uint16_t* levels_q, const uint16_t* levels_k,
+                      const double* scale_q, const double* scale_k, const dsa_mask* mask,
+                      void* workspace, size_t workspace_bytes, void* stream) {
+    return guard([&] {
+        validate(cfg);
+        require_device();
+        if (!mask) throw Error(DSA_ERR_PARAM, "dsa_select: null mask");
+        Plan pl = plan(*cfg, false, false);
+        check_ws(pl, workspace, workspace_bytes);
+        do_select(*cfg, levels_q, levels_k, scale_q, scale_k, *mask, pl, workspace,
+                  static_cast<cudaStream_t>(stream));
+    });
+}
+
+dsa_status dsa_sparse_attention(const dsa_config* cfg, const void* q, const void* k,
+                                const void* v, const dsa_mask* mask, void* z, void* stream) {
+    return guard([&] {
+        validate(cfg);
+        require_device();
+        if (!mask) throw Error(DSA_ERR_PARAM, "dsa_sparse_attention: null mask");
+        do_attention(*cfg, q, k, v, *mask, z, static_cast<cudaStream_t>(stream));
+    });
+}
+
+dsa_status dsa_pipeline(const dsa_config* cfg, const void* q, const void* k, const void* v,
+                        const float* p, void* z, const dsa_mask* mask_out, void* workspace,
+                        size_t workspace_bytes, void* stream) {
+    return guard([&] {
+        validate(cfg);
+        require_device();
+        const dsa_config& c = *cfg;
+        Plan pl = plan(c, true, mask_out == nullptr);
+        check_ws(pl, workspace, workspace_bytes);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        uint16_t* lq = at<uint16_t>(workspace, pl.lq);
+        uint16_t* lk = at<uint16_t>(workspace, pl.lk);
+        double* sq = at<double>(workspace, pl.sq);
+        double* sk = at<double>(workspace, pl.sk);
+        dsa_mask m{};
+        if (mask_out) {
+            m = *mask_out;
+        } else {
+            m.cols = at<uint32_t>(workspace, pl.cols);
+            m.rowptr = c.mask_mode == DSA_MASK_THRESHOLD ? at<uint64_t>(workspace, pl.rowptr) : nullptr;
+            m.capacity = capacity_of(c);
+            m.empty_rows = nullptr;
+        }
+        do_predict(c, q, k, p, lq, lk, sq, sk, pl, workspace, st);
+        do_select(c, lq, lk, sq, sk, m, pl, workspace, st);
+        do_attention(c, q, k, v, m, z, st);
+    });
+}
+
+dsa_status dsa_counters(const dsa_config* cfg, const dsa_mask* mask, dsa_counts* out, void* stream) {
+    return guard([&] {
+        validate(cfg);
+        if (!out) throw Error(DSA_ERR_PARAM, "dsa_counters: null output");
+        const dsa_config& c = *cfg;
+        const int64_t P = pairs_of(c);
+        std::memset(out, 0, sizeof(*out));
+        uint64_t nnz = 0, empty = 0;
+        const double e = c.dtype == DSA_BF16 ? 2.0 : 4.0;
+        switch (c.mask_mode) {
+            case DSA_MASK_ROW_TOPK:
+            case DSA_MASK_COLVEC: nnz = static_cast<uint64_t>(P * c.L * c.keep); break;
+            case DSA_MASK_BLOCK: {
+                // every kept block of block-row ib covers rows(ib) x cols(jb) positions
+                if (!mask || !mask->cols) throw Error(DSA_ERR_PARAM, "dsa_counters: block mode needs the mask");
+                const int64_t nb = ceil_div(c.L, c.block);
+                std::vector<uint32_t> h(static_cast<size_t>(P * nb * c.keep));
+                check_cuda(cudaMemcpyAsync(h.data(), mask->cols, h.size() * 4, cudaMemcpyDeviceToHost,
+                                           static_cast<cudaStream_t>(stream)), "dsa_counters copy");
+                check_cuda(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "dsa_counters sync");
+                for (int64_t pr = 0; pr < P; ++pr)
+                    for (int64_t ib = 0; ib < nb; ++ib) {
+                        const int64_t rows = std::min<int64_t>(c.block, c.L - ib * c.block);
+                        for (int64_t t = 0; t < c.keep; ++t) {
+                            const int64_t jb = h[(pr * nb + ib) * c.keep + t];
+                            nnz += static_cast<uint64_t>(rows * std::min<int64_t>(c.block, c.L - jb * c.block));
+                        }
+                    }
+                break;
+            }
+            default: {
+                if (!mask || !mask->rowptr) throw Error(DSA_ERR_PARAM, "dsa_counters: threshold mode needs rowptr");
+                std::vector<uint64_t> rp(static_cast<size_t>(P * c.L + 1));
+                check_cuda(cudaMemcpyAsync(rp.data(), mask->rowptr, rp.size() * 8, cudaMemcpyDeviceToHost,
+                                           static_cast<cudaStream_t>(stream)), "dsa_counters copy");
+                check_cuda(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "dsa_counters sync");
+                nnz = rp.back();
+                for (size_t r = 0; r + 1 < rp.size(); ++r) empty += rp[r + 1] == rp[r];
+            }
+        }
+        out->nnz = nnz;
+        out->sddmm_mults = nnz * static_cast<uint64_t>(c.d);
+        out->spmm_mults = nnz * static_cast<uint64_t>(c.d);
+        out->softmax_exps = nnz;
+        out->empty_rows = empty;
+        const double L = static_cast<double>(c.L);
+        out->flops_predict = 4.0 * L * c.d * c.k * P;
+        out->flops_score = (c.mask_mode == DSA_MASK_THRESHOLD && c.causal ? L * (L + 1) : 2.0 * L * L) * c.k * P;
+        out->flops_attention = 4.0 * static_cast<double>(nnz) * c.d;
+        out->bytes_predict = (2.0 * L * c.d * e + 2.0 * L * c.k * 2.0) * P + c.d * c.k * 4.0;
+        out->bytes_attention = 4.0 * L * c.d * e * P;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,148 @@
+// Phase 3: SDDMM -> sparse row softmax -> SpMM over a predicted mask
+// (P/src/sparse.cpp:38-91), as one pass per query row with an online
+// softmax (running max / sum rescaling) so kept scores never touch HBM.
+//
+// Generic CUDA-core kernel, one warp per query row: for each chunk of 32
+// kept keys a lane computes one full <q, k_j> (K row gathered with 16-byte
+// vector loads), the warp agrees on the running max, then every lane
+// accumulates its slice of d for the chunk's V rows (coalesced row reads).
+// Covers every mask layout (row lists, band lists, block lists, CSR).
+// The tensor-core kernels (attention_tc.cu) take over structured masks.
+#include <cuda_bf16.h>
+
+#include "device_common.cuh"
+#include "kernels.h"
+
+namespace dsa {
+namespace {
+
+constexpr int kWarpsPerCta = 4;
+
+struct RowList {
+    const uint32_t* cols;
+    int count;       // entries in cols
+    int expand;      // BLOCK: each entry expands to `expand` keys
+};
+
+__device__ __forceinline__ RowList row_list(const AttnArgs& a, int64_t pair, int64_t i) {
+    RowList r{nullptr, 0, 1};
+    switch (a.mode) {
+        case kRowTopk:
+            r.cols = a.cols + (pair * a.L + i) * a.keep;
+            r.count = static_cast<int>(a.keep);
+            break;
+        case kColvec: {
+            const int64_t nb = (a.L + a.vec_v - 1) / a.vec_v;
+            r.cols = a.cols + (pair * nb + i / a.vec_v) * a.keep;
+            r.count = static_cast<int>(a.keep);
+            break;
+        }
+        case kBlock: {
+            const int64_t nb = (a.L + a.block - 1) / a.block;
+            r.cols = a.cols + (pair * nb + i / a.block) * a.keep;
+            r.count = static_cast<int>(a.keep);
+            r.expand = static_cast<int>(a.block);
+            break;
+        }
+        default: {
+            const uint64_t b = a.rowptr[pair * a.L + i], e = a.rowptr[pair * a.L + i + 1];
+            r.cols = a.cols + b;
+            r.count = static_cast<int>(e - b);
+        }
+    }
+    return r;
+}
+
+template <class T, int D>
+__device__ __forceinline__ float dot_row(const float* qs, const T* __restrict__ krow) {
+    constexpr int kVec = 16 / sizeof(T);
+    const uint4* src = reinterpret_cast<const uint4*>(krow);
+    float acc = 0.f;
+#pragma unroll
+    for (int t0 = 0; t0 < D; t0 += kVec) {
+        uint4 raw = __ldg(src + t0 / kVec);
+        const T* e = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+        for (int u = 0; u < kVec; ++u) acc = fmaf(qs[t0 + u], to_float(e[u]), acc);
+    }
+    return acc;
+}
+
+template <class T, int D>
+__global__ void __launch_bounds__(kWarpsPerCta * 32) attn_rows_generic(AttnArgs a) {
+    constexpr int kPer = (D + 31) / 32;  // output dims per lane
+    __shared__ float qs[kWarpsPerCta][D];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t row_global = static_cast<int64_t>(blockIdx.x) * kWarpsPerCta + warp;
+    if (row_global >= a.pairs * a.L) return;
+    const int64_t pair = row_global / a.L, i = row_global % a.L;
+    const T* q = static_cast<const T*>(a.q) + (pair * a.L + i) * D;
+    const T* kb = static_cast<const T*>(a.k) + pair * a.L * D;
+    const T* vb = static_cast<const T*>(a.v) + pair * a.L * D;
+    const float sc = a.scale ? rsqrtf(static_cast<float>(D)) : 1.f;
+    for (int c = lane; c < D; c += 32) qs[warp][c] = to_float(q[c]) * sc;
+    __syncwarp();
+    const RowList rl = row_list(a, pair, i);
+    const int total = rl.count * rl.expand;
+    float m = -INFINITY, l = 0.f, acc[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) acc[u] = 0.f;
+    for (int p0 = 0; p0 < total; p0 += 32) {
+        const int p = p0 + lane;
+        int j = -1;
+        if (p < total) {
+            j = rl.expand == 1 ? static_cast<int>(rl.cols[p])
+                               : static_cast<int>(rl.cols[p / rl.expand]) * rl.expand + p % rl.expand;
+            if (j >= a.L) j = -1;  // ragged last block
+        }
+        const float s = j >= 0 ? dot_row<T, D>(qs[warp], kb + static_cast<int64_t>(j) * D) : -INFINITY;
+        const float mnew = fmaxf(m, warp_max(s));
+        const float w = j >= 0 ? expf(s - mnew) : 0.f;
+        const float corr = m == -INFINITY ? 0.f : expf(m - mnew);
+        l = l * corr + warp_sum(w);
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) acc[u] *= corr;
+        m = mnew;
+        const int nvalid = min(32, total - p0);
+        for (int t = 0; t < nvalid; ++t) {
+            const float wt = __shfl_sync(0xffffffffu, w, t);
+            const int jt = __shfl_sync(0xffffffffu, j, t);
+            if (jt < 0) continue;
+            const T* vrow = vb + static_cast<int64_t>(jt) * D;
+#pragma unroll
+            for (int u = 0; u < kPer; ++u) {
+                const int c = lane + 32 * u;
+                if (c < D) acc[u] = fmaf(wt, to_float(vrow[c]), acc[u]);
+            }
+        }
+    }
+    T* z = static_cast<T*>(a.z) + (pair * a.L + i) * D;
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+        const int c = lane + 32 * u;
+        if (c < D) z[c] = from_float<T>(acc[u] * inv);
+    }
+    if (lane == 0 && a.empty_rows) a.empty_rows[pair * a.L + i] = (l > 0.f) ? 0 : 1;
+}
+
+template <class T>
+void dispatch(const AttnArgs& a, cudaStream_t st) {
+    const unsigned grid = static_cast<unsigned>(ceil_div_i(a.pairs * a.L, kWarpsPerCta));
+    switch (a.D) {
+        case 16: attn_rows_generic<T, 16><<<grid, kWarpsPerCta * 32, 0, st>>>(a); break;
+        case 32: attn_rows_generic<T, 32><<<grid, kWarpsPerCta * 32, 0, st>>>(a); break;
+        case 64: attn_rows_generic<T, 64><<<grid, kWarpsPerCta * 32, 0, st>>>(a); break;
+        case 128: attn_rows_generic<T, 128><<<grid, kWarpsPerCta * 32, 0, st>>>(a); break;
+        default: throw_unsupported("head dim d must be one of 16, 32, 64, 128");
+    }
+}
+
+}  // namespace
+
+void run_attention(const AttnArgs& a, cudaStream_t st) {
+    if (a.bf16) dispatch<__nv_bfloat16>(a, st);
+    else dispatch<float>(a, st);
+}
+
+}  // namespace dsa

@@ -1,0 +1,80 @@
+// Host-visible launch interfaces of the device kernels (internal).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <string>
+
+namespace dsa {
+
+[[noreturn]] void throw_unsupported(const std::string& what);
+[[noreturn]] void throw_cuda(cudaError_t e, const char* where);
+
+inline int64_t ceil_div_i(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+struct PredictArgs {
+    const void* q;
+    const void* k;
+    const float* p;
+    int64_t pairs, L, D, KD;
+    int bf16, per_row, round_f32;
+    double qmax;
+    uint16_t* lq;
+    uint16_t* lk;
+    double* sq;
+    double* sk;
+    double* xws;                // per-tensor: [pairs][2][L][KD] f64 scratch
+    unsigned long long* amax;  // per-tensor: [pairs][2]
+};
+void run_predict(const PredictArgs& a, cudaStream_t st);
+
+enum SelectMode { kRowTopk = 0, kColvec = 1, kBlock = 2, kThreshold = 3 };
+
+struct SelectArgs {
+    int mode;
+    int64_t pairs, L, KD, D;
+    int per_row;
+    const uint16_t* lq;
+    const uint16_t* lk;
+    const double* sq;
+    const double* sk;
+    int64_t keep;
+    int64_t vec_v;
+    int64_t block;
+    int force_diag;
+    int causal;
+    int64_t frac_num, frac_den, cap;
+    int qmax;
+    uint32_t* cols;
+    uint64_t* rowptr;   // threshold: [pairs*L + 1]
+    int64_t capacity;
+    uint8_t* empty_rows;
+    // scratch
+    int32_t* pooled;    // block: [pairs][2][nb][KD]
+    int64_t* etab;      // threshold: [pairs][span]
+    uint64_t* counts;   // threshold: [pairs*L]
+    int64_t span;
+    void* scan_tmp;
+    size_t scan_tmp_bytes;
+};
+void run_select(const SelectArgs& a, cudaStream_t st);
+size_t select_scan_tmp_bytes(int64_t n);
+
+struct AttnArgs {
+    int mode;
+    int64_t pairs, L, D;
+    int bf16, scale;
+    const void* q;
+    const void* k;
+    const void* v;
+    const uint32_t* cols;
+    const uint64_t* rowptr;
+    int64_t keep, vec_v, block;
+    void* z;
+    uint8_t* empty_rows;
+};
+void run_attention(const AttnArgs& a, cudaStream_t st);
+
+}  // namespace dsa

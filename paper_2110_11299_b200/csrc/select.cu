@@ -1,0 +1,475 @@
+// Phase 2: exact-integer approximate scores -> mask selection.
+//
+// Selection semantics are the reference's row_topk_indices comparator
+// (value descending, then LOWEST column index; output ascending,
+// P/src/linalg.cpp:69-85) applied to the exact integer score
+// S[i][j] = <levels_q[i], levels_k[j]>.  Ties are never
+// broken by arrival order: a radix select finds the exact k-th key T, every
+// key better than T is kept, and keys equal to T are admitted in ascending
+// column order (prefix counts) until `keep` is reached.
+//
+// This file holds the CTA-per-row CUDA-core kernels, used for every mode
+// and shape; the tensor-core fast paths (select_tc.cu) take over the
+// configurations they are specialised for.
+#include <cub/cub.cuh>
+#include <cuda_bf16.h>
+
+#include "device_common.cuh"
+#include "kernels.h"
+
+namespace dsa {
+namespace {
+
+constexpr int kNT = 256;
+constexpr int kWarps = kNT / 32;
+
+struct SelSmem {
+    uint32_t hist[256];
+    uint32_t wtot[2][kWarps];
+    unsigned long long red[kWarps];
+    unsigned long long bcast[4];
+};
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+template <class KeyT>
+__device__ __forceinline__ int key_bits() { return static_cast<int>(sizeof(KeyT) * 8); }
+
+// Block-wide radix select: the keep-th smallest key T (1-based) among
+// keys[0..n) and rem = how many keys equal to T belong to the first `keep`.
+// Only the digits where keys differ are visited (AND/OR pre-scan).
+template <class KeyT>
+__device__ void block_radix_select(const KeyT* keys, int n, int keep, SelSmem& s, KeyT& T,
+                                   uint32_t& rem) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    KeyT a = ~KeyT(0), o = 0;
+    for (int j = tid; j < n; j += kNT) {
+        a &= keys[j];
+        o |= keys[j];
+    }
+    // block AND / OR
+    unsigned long long aa = a, oo = o;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        aa &= __shfl_xor_sync(0xffffffffu, aa, off);
+        oo |= __shfl_xor_sync(0xffffffffu, oo, off);
+    }
+    if (lane == 0) s.red[warp] = aa;
+    __syncthreads();
+    if (tid == 0) {
+        unsigned long long ta = ~0ull;
+        for (int w = 0; w < kWarps; ++w) ta &= s.red[w];
+        s.bcast[0] = ta;
+    }
+    __syncthreads();
+    if (lane == 0) s.red[warp] = oo;
+    __syncthreads();
+    if (tid == 0) {
+        unsigned long long to = 0;
+        for (int w = 0; w < kWarps; ++w) to |= s.red[w];
+        s.bcast[1] = to;
+        const unsigned long long diff = (s.bcast[0] ^ to);
+        int top = diff ? 63 - __clzll(static_cast<long long>(diff)) : 0;
+        s.bcast[2] = static_cast<unsigned long long>(top);
+        s.bcast[3] = static_cast<unsigned long long>(keep);
+    }
+    __syncthreads();
+    const unsigned long long common = s.bcast[0];
+    const int top = static_cast<int>(s.bcast[2]);
+    KeyT prefix = static_cast<KeyT>(common);  // bits above `top` are common to all keys
+    uint32_t r = static_cast<uint32_t>(keep);
+    int shift = (top / 8) * 8;
+    for (; shift >= 0; shift -= 8) {
+        for (int i = tid; i < 256; i += kNT) s.hist[i] = 0;
+        __syncthreads();
+        const KeyT hi_mask = (shift + 8 >= key_bits<KeyT>()) ? KeyT(0) : (~KeyT(0) << (shift + 8));
+        for (int j = tid; j < n; j += kNT) {
+            const KeyT key = keys[j];
+            if ((key & hi_mask) == (prefix & hi_mask))
+                atomicAdd(&s.hist[static_cast<uint32_t>(key >> shift) & 255u], 1u);
+        }
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t c[8], tot = 0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                c[u] = s.hist[lane * 8 + u];
+                tot += c[u];
+            }
+            uint32_t incl = tot;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
+                if (lane >= off) incl += y;
+            }
+            const uint32_t excl = incl - tot;
+            const bool mine = excl < r && r <= incl;
+            const unsigned who = __ballot_sync(0xffffffffu, mine);
+            if (mine) {
+                uint32_t cum = excl;
+                int dsel = 0;
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    if (cum + c[u] >= r) {
+                        dsel = u;
+                        break;
+                    }
+                    cum += c[u];
+                }
+                s.bcast[0] = static_cast<unsigned long long>(lane * 8 + dsel);
+                s.bcast[1] = static_cast<unsigned long long>(r - cum);
+            }
+            (void)who;
+        }
+        __syncthreads();
+        const KeyT digit = static_cast<KeyT>(s.bcast[0]);
+        r = static_cast<uint32_t>(s.bcast[1]);
+        prefix = (prefix & ~(KeyT(255) << shift)) | (digit << shift);
+        __syncthreads();
+    }
+    T = prefix;
+    rem = r;
+}
+
+// Ordered emission: writes, in ascending index order, every j with
+// lt(j), plus the first `rem` (by index) with eq(j).  Returns the count.
+template <class Flags>
+__device__ uint32_t block_emit(int n, uint32_t rem, Flags flags, uint32_t* out, SelSmem& s) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint32_t base_out = 0, base_eq = 0;
+    for (int j0 = 0; j0 < n; j0 += kNT) {
+        const int j = j0 + tid;
+        bool lt = false, eq = false;
+        if (j < n) flags(j, lt, eq);
+        const unsigned beq = __ballot_sync(0xffffffffu, eq);
+        if (lane == 0) s.wtot[0][warp] = __popc(beq);
+        __syncthreads();
+        uint32_t eq_off = 0, eq_tot = 0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+            const uint32_t t = s.wtot[0][w];
+            eq_off += w < warp ? t : 0;
+            eq_tot += t;
+        }
+        const uint32_t eq_rank = base_eq + eq_off + __popc(beq & lanemask_lt());
+        const bool take = lt || (eq && eq_rank < rem);
+        const unsigned bt = __ballot_sync(0xffffffffu, take);
+        if (lane == 0) s.wtot[1][warp] = __popc(bt);
+        __syncthreads();
+        uint32_t t_off = 0, t_tot = 0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+            const uint32_t t = s.wtot[1][w];
+            t_off += w < warp ? t : 0;
+            t_tot += t;
+        }
+        if (take && out) out[base_out + t_off + __popc(bt & lanemask_lt())] = static_cast<uint32_t>(j);
+        base_out += t_tot;
+        base_eq += eq_tot;
+        __syncthreads();
+    }
+    return base_out;
+}
+
+template <int KD>
+__device__ __forceinline__ void load_levels(const uint16_t* __restrict__ row, float (&x)[KD]) {
+    const uint4* src = reinterpret_cast<const uint4*>(row);
+#pragma unroll
+    for (int v = 0; v < KD / 8; ++v) {
+        uint4 r = __ldg(src + v);
+        const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            x[v * 8 + 2 * u] = __uint_as_float(w[u] << 16);
+            x[v * 8 + 2 * u + 1] = __uint_as_float(w[u] & 0xffff0000u);
+        }
+    }
+}
+
+// Exact: |products| <= 127^2 and |sums| < 2^24, so fp32 FMA is exact.
+template <int KD>
+__device__ __forceinline__ int score_with(const float (&q)[KD], const uint16_t* __restrict__ krow) {
+    float kk[KD];
+    load_levels<KD>(krow, kk);
+    float acc = 0.f;
+#pragma unroll
+    for (int t = 0; t < KD; ++t) acc = fmaf(q[t], kk[t], acc);
+    return static_cast<int>(acc);
+}
+
+// ---------------------------------------------------------------- top-k
+template <class KeyT, int KD>
+__global__ void __launch_bounds__(kNT) topk_rows_generic(SelectArgs a) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    KeyT* keys = reinterpret_cast<KeyT*>(dsm);
+    __shared__ SelSmem s;
+    const int64_t i = blockIdx.x, pair = blockIdx.y;
+    const int L = static_cast<int>(a.L);
+    float q[KD];
+    load_levels<KD>(a.lq + (pair * a.L + i) * KD, q);
+    const uint16_t* lk = a.lk + pair * a.L * KD;
+    for (int j = threadIdx.x; j < L; j += kNT) {
+        const int sc = score_with<KD>(q, lk + static_cast<int64_t>(j) * KD);
+        if constexpr (sizeof(KeyT) == 8)
+            keys[j] = rank_key_f64(static_cast<double>(sc) * a.sk[pair * a.L + j]);
+        else
+            keys[j] = rank_key_i32(sc);
+    }
+    __syncthreads();
+    KeyT T;
+    uint32_t rem;
+    block_radix_select<KeyT>(keys, L, static_cast<int>(a.keep), s, T, rem);
+    uint32_t* out = a.cols + (pair * a.L + i) * a.keep;
+    block_emit(L, rem, [&](int j, bool& lt, bool& eq) {
+        lt = keys[j] < T;
+        eq = keys[j] == T;
+    }, out, s);
+}
+
+// -------------------------------------------------------------- colvec
+template <int KD>
+__global__ void __launch_bounds__(kNT) colvec_generic(SelectArgs a) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    uint32_t* keys = reinterpret_cast<uint32_t*>(dsm);
+    __shared__ SelSmem s;
+    const int64_t b = blockIdx.x, pair = blockIdx.y;
+    const int L = static_cast<int>(a.L);
+    const int64_t r0 = b * a.vec_v, r1 = min(r0 + a.vec_v, a.L);
+    const uint16_t* lk = a.lk + pair * a.L * KD;
+    const uint16_t* lq = a.lq + pair * a.L * KD;
+    for (int j = threadIdx.x; j < L; j += kNT) {
+        float kk[KD];
+        load_levels<KD>(lk + static_cast<int64_t>(j) * KD, kk);
+        int best = INT32_MIN;
+        for (int64_t r = r0; r < r1; ++r) {
+            float q[KD];
+            load_levels<KD>(lq + r * KD, q);
+            float acc = 0.f;
+#pragma unroll
+            for (int t = 0; t < KD; ++t) acc = fmaf(q[t], kk[t], acc);
+            best = max(best, static_cast<int>(acc));
+        }
+        keys[j] = rank_key_i32(best);
+    }
+    __syncthreads();
+    uint32_t T, rem;
+    block_radix_select<uint32_t>(keys, L, static_cast<int>(a.keep), s, T, rem);
+    uint32_t* out = a.cols + (pair * ((a.L + a.vec_v - 1) / a.vec_v) + b) * a.keep;
+    block_emit(L, rem, [&](int j, bool& lt, bool& eq) {
+        lt = keys[j] < T;
+        eq = keys[j] == T;
+    }, out, s);
+}
+
+// --------------------------------------------------------------- block
+// pooled[pair][0|1][nb][KD] = sum of the block's rows of levels (exact int).
+__global__ void pool_levels_kernel(SelectArgs a, int64_t nb) {
+    const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t total = a.pairs * 2 * nb * a.KD;
+    if (idx >= total) return;
+    const int64_t t = idx % a.KD, blk = (idx / a.KD) % nb, which = (idx / (a.KD * nb)) % 2,
+                  pair = idx / (a.KD * nb * 2);
+    const uint16_t* lv = (which ? a.lk : a.lq) + pair * a.L * a.KD;
+    int acc = 0;
+    for (int64_t r = blk * a.block; r < min((blk + 1) * a.block, a.L); ++r)
+        acc += level_to_int(lv[r * a.KD + t]);
+    a.pooled[idx] = acc;
+}
+
+__global__ void __launch_bounds__(kNT) block_generic(SelectArgs a, int64_t nb) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    uint64_t* keys = reinterpret_cast<uint64_t*>(dsm);
+    __shared__ SelSmem s;
+    const int64_t ib = blockIdx.x, pair = blockIdx.y;
+    const int32_t* pq = a.pooled + ((pair * 2 + 0) * nb + ib) * a.KD;
+    const int32_t* pk = a.pooled + (pair * 2 + 1) * nb * a.KD;
+    const int64_t r = a.L - (nb - 1) * a.block;  // width of the last (possibly ragged) block
+    for (int64_t jb = threadIdx.x; jb < nb; jb += kNT) {
+        int64_t sum = 0;
+        for (int t = 0; t < a.KD; ++t) sum += static_cast<int64_t>(pq[t]) * pk[jb * a.KD + t];
+        const int64_t width = jb == nb - 1 ? r : a.block;
+        // mean ranking, exactly: common denominator block * r
+        const int64_t val = width == a.block ? sum * r : sum * a.block;
+        keys[jb] = (a.force_diag && jb == ib) ? 0ull : rank_key_i64(val) | 1ull;
+    }
+    __syncthreads();
+    uint64_t T;
+    uint32_t rem;
+    block_radix_select<uint64_t>(keys, static_cast<int>(nb), static_cast<int>(a.keep), s, T, rem);
+    uint32_t* out = a.cols + (pair * nb + ib) * a.keep;
+    block_emit(static_cast<int>(nb), rem, [&](int j, bool& lt, bool& eq) {
+        lt = keys[j] < T;
+        eq = keys[j] == T;
+    }, out, s);
+}
+
+// ----------------------------------------------------------- threshold
+// E[pair][t] = rint(det_exp(c * -t) * 2^40), c = s_q s_k / sqrt(d).
+__global__ void exp_table_kernel(SelectArgs a) {
+    const int64_t pair = blockIdx.y;
+    const double c = a.sq[pair] * a.sk[pair] / sqrt(static_cast<double>(a.D));
+    for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < a.span;
+         t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const double e = det_exp(c * static_cast<double>(-t));
+        a.etab[pair * a.span + t] = static_cast<int64_t>(rint(e * 1099511627776.0));
+    }
+}
+
+__device__ __forceinline__ bool keep_rule(uint64_t e, uint64_t z, uint64_t ln, uint64_t den) {
+    // e * ln >= z * den, exact in 128 bits
+    const uint64_t lh = __umul64hi(e, ln), ll = e * ln;
+    const uint64_t rh = __umul64hi(z, den), rl = z * den;
+    return lh != rh ? lh > rh : ll >= rl;
+}
+
+// emit == 0: write the kept count to counts[pair*L + i]; emit == 1: write
+// the kept columns at rowptr[pair*L + i].
+template <int KD>
+__global__ void __launch_bounds__(kNT) threshold_generic(SelectArgs a, uint64_t* counts, int emit) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    uint32_t* keys = reinterpret_cast<uint32_t*>(dsm);
+    __shared__ SelSmem s;
+    const int64_t i = blockIdx.x, pair = blockIdx.y;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n = a.causal ? static_cast<int>(i) + 1 : static_cast<int>(a.L);
+    float q[KD];
+    load_levels<KD>(a.lq + (pair * a.L + i) * KD, q);
+    const uint16_t* lk = a.lk + pair * a.L * KD;
+    int mx = INT32_MIN;
+    for (int j = tid; j < n; j += kNT) {
+        const int sc = score_with<KD>(q, lk + static_cast<int64_t>(j) * KD);
+        keys[j] = static_cast<uint32_t>(sc);
+        mx = max(mx, sc);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    if (lane == 0) s.red[warp] = static_cast<unsigned long long>(static_cast<uint32_t>(mx));
+    __syncthreads();
+    int M = INT32_MIN;
+    for (int w = 0; w < kWarps; ++w) M = max(M, static_cast<int>(static_cast<uint32_t>(s.red[w])));
+    __syncthreads();
+    const int64_t* E = a.etab + pair * a.span;
+    unsigned long long z = 0;
+    for (int j = tid; j < n; j += kNT) z += static_cast<unsigned long long>(__ldg(E + (M - static_cast<int>(keys[j]))));
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) z += __shfl_xor_sync(0xffffffffu, z, off);
+    if (lane == 0) s.red[warp] = z;
+    __syncthreads();
+    unsigned long long Z = 0;
+    for (int w = 0; w < kWarps; ++w) Z += s.red[w];
+    __syncthreads();
+    const uint64_t ln = static_cast<uint64_t>(a.L) * static_cast<uint64_t>(a.frac_num);
+    const uint64_t den = static_cast<uint64_t>(a.frac_den);
+    // rank keys: kept -> rank_key_i32(score) (< UINT32_MAX), dropped -> UINT32_MAX
+    unsigned cnt_local = 0;
+    for (int j = tid; j < n; j += kNT) {
+        const int sc = static_cast<int>(keys[j]);
+        const bool kept = keep_rule(static_cast<uint64_t>(__ldg(E + (M - sc))), Z, ln, den);
+        keys[j] = kept ? rank_key_i32(sc) : 0xffffffffu;
+        cnt_local += kept;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) cnt_local += __shfl_xor_sync(0xffffffffu, cnt_local, off);
+    if (lane == 0) s.red[warp] = cnt_local;
+    __syncthreads();
+    uint32_t cnt = 0;
+    for (int w = 0; w < kWarps; ++w) cnt += static_cast<uint32_t>(s.red[w]);
+    __syncthreads();
+    const uint32_t take = cnt > static_cast<uint32_t>(a.cap) ? static_cast<uint32_t>(a.cap) : cnt;
+    if (!emit) {
+        if (tid == 0) {
+            counts[pair * a.L + i] = take;
+            if (a.empty_rows) a.empty_rows[pair * a.L + i] = take == 0;
+        }
+        return;
+    }
+    uint32_t* out = a.cols + a.rowptr[pair * a.L + i];
+    if (cnt <= static_cast<uint32_t>(a.cap)) {
+        block_emit(n, 0u, [&](int j, bool& lt, bool& eq) {
+            lt = keys[j] != 0xffffffffu;
+            eq = false;
+        }, out, s);
+    } else {
+        uint32_t T, rem;
+        block_radix_select<uint32_t>(keys, n, static_cast<int>(a.cap), s, T, rem);
+        block_emit(n, rem, [&](int j, bool& lt, bool& eq) {
+            lt = keys[j] < T;
+            eq = keys[j] == T;
+        }, out, s);
+    }
+}
+
+template <int KD>
+void launch_select(const SelectArgs& a, cudaStream_t st) {
+    const unsigned P = static_cast<unsigned>(a.pairs);
+    switch (a.mode) {
+        case kRowTopk: {
+            if (a.per_row) {
+                const size_t sm = static_cast<size_t>(a.L) * 8;
+                auto kern = topk_rows_generic<uint64_t, KD>;
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+                kern<<<dim3(static_cast<unsigned>(a.L), P), kNT, sm, st>>>(a);
+            } else {
+                const size_t sm = static_cast<size_t>(a.L) * 4;
+                auto kern = topk_rows_generic<uint32_t, KD>;
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+                kern<<<dim3(static_cast<unsigned>(a.L), P), kNT, sm, st>>>(a);
+            }
+            break;
+        }
+        case kColvec: {
+            const size_t sm = static_cast<size_t>(a.L) * 4;
+            auto kern = colvec_generic<KD>;
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+            kern<<<dim3(static_cast<unsigned>(ceil_div_i(a.L, a.vec_v)), P), kNT, sm, st>>>(a);
+            break;
+        }
+        case kBlock: {
+            const int64_t nb = ceil_div_i(a.L, a.block);
+            const int64_t total = a.pairs * 2 * nb * a.KD;
+            pool_levels_kernel<<<static_cast<unsigned>(ceil_div_i(total, 256)), 256, 0, st>>>(a, nb);
+            const size_t sm = static_cast<size_t>(nb) * 8;
+            cudaFuncSetAttribute(block_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+            block_generic<<<dim3(static_cast<unsigned>(nb), P), kNT, sm, st>>>(a, nb);
+            break;
+        }
+        case kThreshold: {
+            exp_table_kernel<<<dim3(static_cast<unsigned>(std::min<int64_t>(ceil_div_i(a.span, 256), 64)), P), 256, 0, st>>>(a);
+            const size_t sm = static_cast<size_t>(a.L) * 4;
+            auto kern = threshold_generic<KD>;
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+            const int64_t n = a.pairs * a.L;
+            uint64_t* counts = a.counts;
+            kern<<<dim3(static_cast<unsigned>(a.L), P), kNT, sm, st>>>(a, counts, 0);
+            cudaMemsetAsync(a.rowptr, 0, sizeof(uint64_t), st);
+            size_t tb = a.scan_tmp_bytes;
+            cub::DeviceScan::InclusiveSum(a.scan_tmp, tb, counts, a.rowptr + 1, static_cast<int64_t>(n), st);
+            kern<<<dim3(static_cast<unsigned>(a.L), P), kNT, sm, st>>>(a, counts, 1);
+            break;
+        }
+        default: throw_unsupported("unknown mask mode");
+    }
+}
+
+}  // namespace
+
+size_t select_scan_tmp_bytes(int64_t n) {
+    size_t b = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, b, static_cast<const uint64_t*>(nullptr),
+                                  static_cast<uint64_t*>(nullptr), n);
+    return b;
+}
+
+void run_select(const SelectArgs& a, cudaStream_t st) {
+    switch (a.KD) {
+        case 16: launch_select<16>(a, st); break;
+        case 32: launch_select<32>(a, st); break;
+        default: throw_unsupported("projection width k must be 16 or 32");
+    }
+}
+
+}  // namespace dsa

@@ -1,0 +1,252 @@
+"""Host-side mirror of the reference attention-operator interface over the
+C-ABI (PyTorch is used only for device memory and streams).
+
+Names follow the reference entry points (P/include/dsattn/predictor.hpp:31-49,
+maskgen.hpp:14-31, sparse.hpp:47-59): ``quantize``-style prediction
+(``predict``), mask selection (``predicted_topk_mask``, ``colvec_mask``,
+``block_mask``, ``threshold_mask`` -> ``select``), ``sparse_attention`` and
+the fused ``pipeline``.  Errors surface as the reference exception types
+(errors.py).  Everything runs batched over (b, h) pairs with tensors shaped
+[pairs, L, d] on one CUDA device.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _abi
+from .errors import ParamError, ShapeError
+from .presets import DTYPES, MASK_MODES, QUANT_SCOPES, Preset
+
+
+def config_of(p: Preset, pairs: int | None = None) -> _abi.DsaConfig:
+    """dsa_config for a preset; `pairs` overrides batch*heads (heads := 1)."""
+    c = _abi.DsaConfig()
+    if pairs is None:
+        c.batch, c.heads = p.batch, p.heads
+    else:
+        c.batch, c.heads = pairs, 1
+    c.L, c.d, c.k = p.L, p.d, p.k
+    c.dtype = DTYPES[p.dtype]
+    c.bits = p.bits
+    c.quant_scope = QUANT_SCOPES[p.quant_scope]
+    c.round_proj_f32 = int(p.round_proj_f32)
+    c.mask_mode = MASK_MODES[p.mask_mode]
+    c.scale = int(p.scale)
+    c.keep = p.keep
+    c.vec_v, c.block, c.force_diag = p.vec_v, p.block, int(p.force_diag)
+    c.causal = int(p.causal)
+    c.frac_num, c.frac_den, c.cap = p.frac_num, p.frac_den, p.cap
+    return c
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(stream) -> int | None:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    return stream.cuda_stream
+
+
+def torch_dtype(p: Preset) -> torch.dtype:
+    return torch.bfloat16 if p.dtype == "bf16" else torch.float32
+
+
+def validate(p: Preset, pairs: int | None = None) -> None:
+    c = config_of(p, pairs)
+    _abi.check(_abi.lib().dsa_config_validate(C.byref(c)))
+
+
+def workspace_bytes(p: Preset, pairs: int | None = None) -> int:
+    c = config_of(p, pairs)
+    n = _abi.lib().dsa_workspace_bytes(C.byref(c))
+    if n == 0:
+        _abi.check(_abi.lib().dsa_config_validate(C.byref(c)))
+    return int(n)
+
+
+def mask_capacity(p: Preset, pairs: int | None = None) -> int:
+    c = config_of(p, pairs)
+    n = _abi.lib().dsa_mask_capacity(C.byref(c))
+    if n < 0:
+        _abi.check(_abi.lib().dsa_config_validate(C.byref(c)))
+    return int(n)
+
+
+# ------------------------------------------------------------------ inputs
+def generate(p: Preset, pair0: int = 0, npairs: int | None = None, threads: int = 0,
+             pinned: bool = False):
+    """Seeded BASELINE inputs on the host: q, k, v as torch CPU tensors
+    [npairs, L, d] in the preset dtype, plus P [d, k] float32."""
+    import os
+    npairs = p.pairs if npairs is None else npairs
+    dt = torch_dtype(p)
+    shape = (npairs, p.L, p.d)
+    q = torch.empty(shape, dtype=dt, pin_memory=pinned)
+    k = torch.empty(shape, dtype=dt, pin_memory=pinned)
+    v = torch.empty(shape, dtype=dt, pin_memory=pinned)
+    P = torch.empty((p.d, p.k), dtype=torch.float32, pin_memory=pinned)
+    c = config_of(p)
+    _abi.check(_abi.lib().dsa_generate(C.byref(c), p.seed, p.planted_per_mille, p.band_width,
+                                       pair0, npairs, q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                       P.data_ptr(), threads or (os.cpu_count() or 1)))
+    return q, k, v, P
+
+
+# ------------------------------------------------------------------ phases
+@dataclass
+class Levels:
+    lq: torch.Tensor   # [pairs, L, k] bf16 (exact integer levels)
+    lk: torch.Tensor
+    sq: torch.Tensor   # f64 [pairs] or [pairs, L]
+    sk: torch.Tensor
+
+
+@dataclass
+class Mask:
+    mode: str
+    cols: torch.Tensor
+    rowptr: torch.Tensor | None
+    empty_rows: torch.Tensor | None
+
+    def as_c(self) -> _abi.DsaMask:
+        m = _abi.DsaMask()
+        m.cols = _ptr(self.cols)
+        m.rowptr = _ptr(self.rowptr)
+        m.capacity = self.cols.numel()
+        m.empty_rows = _ptr(self.empty_rows)
+        return m
+
+
+def _check_inputs(p: Preset, pairs: int, *ts: torch.Tensor) -> None:
+    for t in ts:
+        if t.shape != (pairs, p.L, p.d):
+            raise ShapeError(f"dsa: expected [{pairs}, {p.L}, {p.d}], got {list(t.shape)}")
+        if t.dtype != torch_dtype(p):
+            raise ParamError(f"dsa: expected {torch_dtype(p)}, got {t.dtype}")
+        if not t.is_cuda or not t.is_contiguous():
+            raise ParamError("dsa: inputs must be contiguous CUDA tensors")
+
+
+def _ws(nbytes: int, device) -> torch.Tensor:
+    return torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
+
+
+def predict(p: Preset, q: torch.Tensor, k: torch.Tensor, P: torch.Tensor, stream=None) -> Levels:
+    pairs = q.shape[0]
+    _check_inputs(p, pairs, q, k)
+    c = config_of(p, pairs)
+    dev = q.device
+    lq = torch.empty((pairs, p.L, p.k), dtype=torch.bfloat16, device=dev)
+    lk = torch.empty_like(lq)
+    ns = (pairs,) if p.quant_scope == "tensor" else (pairs, p.L)
+    sq = torch.empty(ns, dtype=torch.float64, device=dev)
+    sk = torch.empty_like(sq)
+    ws = _ws(workspace_bytes(p, pairs), dev)
+    _abi.check(_abi.lib().dsa_predict(C.byref(c), _ptr(q), _ptr(k), _ptr(P.contiguous()), _ptr(lq),
+                                      _ptr(lk), _ptr(sq), _ptr(sk), _ptr(ws), ws.numel(),
+                                      _stream(stream)))
+    return Levels(lq, lk, sq, sk)
+
+
+def alloc_mask(p: Preset, pairs: int, device, empty_rows: bool = True) -> Mask:
+    cap = mask_capacity(p, pairs)
+    cols = torch.empty(cap, dtype=torch.int32, device=device)
+    rowptr = (torch.empty(pairs * p.L + 1, dtype=torch.int64, device=device)
+              if p.mask_mode == "threshold" else None)
+    er = torch.zeros(pairs * p.L, dtype=torch.uint8, device=device) if empty_rows else None
+    return Mask(p.mask_mode, cols, rowptr, er)
+
+
+def select(p: Preset, lv: Levels, stream=None, mask: Mask | None = None) -> Mask:
+    pairs = lv.lq.shape[0]
+    c = config_of(p, pairs)
+    dev = lv.lq.device
+    m = mask or alloc_mask(p, pairs, dev)
+    ws = _ws(workspace_bytes(p, pairs), dev)
+    cm = m.as_c()
+    _abi.check(_abi.lib().dsa_select(C.byref(c), _ptr(lv.lq), _ptr(lv.lk), _ptr(lv.sq),
+                                     _ptr(lv.sk), C.byref(cm), _ptr(ws), ws.numel(),
+                                     _stream(stream)))
+    return m
+
+
+def sparse_attention(p: Preset, q, k, v, mask: Mask, stream=None, out=None) -> torch.Tensor:
+    pairs = q.shape[0]
+    _check_inputs(p, pairs, q, k, v)
+    c = config_of(p, pairs)
+    z = out if out is not None else torch.empty_like(q)
+    cm = mask.as_c()
+    _abi.check(_abi.lib().dsa_sparse_attention(C.byref(c), _ptr(q), _ptr(k), _ptr(v), C.byref(cm),
+                                               _ptr(z), _stream(stream)))
+    return z
+
+
+class Pipeline:
+    """predict -> select -> sparse attention with a pre-sized workspace
+    (allocation-free per call; capturable in a CUDA graph)."""
+
+    def __init__(self, p: Preset, pairs: int | None = None, device="cuda", keep_mask=False):
+        self.p = p
+        self.pairs = p.pairs if pairs is None else pairs
+        self.cfg = config_of(p, self.pairs)
+        self.ws = _ws(workspace_bytes(p, self.pairs), device)
+        self.mask = alloc_mask(p, self.pairs, device) if keep_mask else None
+        self._cmask = self.mask.as_c() if self.mask else None
+
+    def __call__(self, q, k, v, P, out=None, stream=None) -> torch.Tensor:
+        z = out if out is not None else torch.empty_like(q)
+        mp = C.byref(self._cmask) if self._cmask is not None else None
+        _abi.check(_abi.lib().dsa_pipeline(C.byref(self.cfg), _ptr(q), _ptr(k), _ptr(v), _ptr(P),
+                                           _ptr(z), mp, _ptr(self.ws), self.ws.numel(),
+                                           _stream(stream)))
+        return z
+
+
+def counters(p: Preset, mask: Mask, pairs: int, stream=None) -> dict:
+    c = config_of(p, pairs)
+    out = _abi.DsaCounts()
+    cm = mask.as_c()
+    _abi.check(_abi.lib().dsa_counters(C.byref(c), C.byref(cm), C.byref(out), _stream(stream)))
+    return {f: getattr(out, f) for f, _ in out._fields_}
+
+
+# --------------------------------------------------------- mask utilities
+def mask_rows(p: Preset, mask: Mask, pairs: int) -> list[list[np.ndarray]]:
+    """Per pair, per query row, the kept key columns (host, ascending)."""
+    cols = mask.cols.cpu().numpy().astype(np.int64)
+    out = []
+    if p.mask_mode == "threshold":
+        rp = mask.rowptr.cpu().numpy()
+        for pr in range(pairs):
+            out.append([cols[rp[pr * p.L + i]:rp[pr * p.L + i + 1]] for i in range(p.L)])
+        return out
+    if p.mask_mode == "row_topk":
+        c3 = cols[: pairs * p.L * p.keep].reshape(pairs, p.L, p.keep)
+        return [[c3[pr, i] for i in range(p.L)] for pr in range(pairs)]
+    if p.mask_mode == "colvec":
+        nb = -(-p.L // p.vec_v)
+        c3 = cols[: pairs * nb * p.keep].reshape(pairs, nb, p.keep)
+        return [[c3[pr, i // p.vec_v] for i in range(p.L)] for pr in range(pairs)]
+    nb = -(-p.L // p.block)
+    c3 = cols[: pairs * nb * p.keep].reshape(pairs, nb, p.keep)
+    res = []
+    for pr in range(pairs):
+        rows = []
+        for ib in range(nb):
+            ks = np.concatenate([np.arange(b * p.block, min((b + 1) * p.block, p.L)) for b in c3[pr, ib]])
+            rows.extend([ks] * (min((ib + 1) * p.block, p.L) - ib * p.block))
+        res.append(rows)
+    return res
+
+
+def to_csr(rows: list[np.ndarray]) -> tuple[np.ndarray, np.ndarray]:
+    rp = np.zeros(len(rows) + 1, dtype=np.uint64)
+    rp[1:] = np.cumsum([len(r) for r in rows])
+    cols = np.concatenate(rows).astype(np.uint32) if rows and rp[-1] > 0 else np.zeros(0, np.uint32)
+    return rp, cols
