@@ -141,6 +141,10 @@ dsa_status dsa_pipeline(const dsa_config* cfg, const void* q, const void* k, con
                         const float* p, void* z, const dsa_mask* mask_out, void* workspace,
                         size_t workspace_bytes, void* stream);
 
+/* Kernels launched by this library since load (process-wide, monotonic);
+ * bench.py reads it around timed regions. */
+uint64_t dsa_launch_counter(void);
+
 /* Exact operation counts for a computed mask (synchronises `stream`). */
 dsa_status dsa_counters(const dsa_config* cfg, const dsa_mask* mask, dsa_counts* out,
                         void* stream);

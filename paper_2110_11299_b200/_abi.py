@@ -50,6 +50,7 @@ _SIGS = {
     "dsa_sparse_attention": (C.c_int, [C.POINTER(DsaConfig), _P, _P, _P, C.POINTER(DsaMask), _P, _P]),
     "dsa_pipeline": (C.c_int, [C.POINTER(DsaConfig), _P, _P, _P, _P, _P, C.POINTER(DsaMask), _P,
                                C.c_size_t, _P]),
+    "dsa_launch_counter": (C.c_uint64, []),
     "dsa_counters": (C.c_int, [C.POINTER(DsaConfig), C.POINTER(DsaMask), C.POINTER(DsaCounts), _P]),
     "dsa_generate": (C.c_int, [C.POINTER(DsaConfig), C.c_uint64, C.c_int32, C.c_int32, C.c_int64,
                                C.c_int64, _P, _P, _P, _P, C.c_int32]),

@@ -3,6 +3,7 @@
 // this boundary; errors become dsa_status codes + dsa_last_error().
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -265,6 +266,9 @@ void require_device() {
 
 void set_last_error(const std::string& m) { g_last_error = m; }
 
+static std::atomic<uint64_t> g_launches{0};
+void note_launch(int n) { g_launches.fetch_add(static_cast<uint64_t>(n), std::memory_order_relaxed); }
+
 [[noreturn]] void throw_unsupported(const std::string& what) { throw Error(DSA_ERR_UNSUPPORTED, "dsa: " + what); }
 [[noreturn]] void throw_cuda(cudaError_t e, const char* where) {
     throw Error(DSA_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
@@ -277,6 +281,7 @@ using namespace dsa;
 extern "C" {
 
 int dsa_abi_version(void) { return DSA_ABI_VERSION; }
+uint64_t dsa_launch_counter(void) { return g_launches.load(std::memory_order_relaxed); }
 const char* dsa_last_error(void) { return g_last_error.c_str(); }
 const char* dsa_build_info(void) {
     return "dsa_b200 sm_100a, CUDA runtime " DSA_STR(CUDART_VERSION);

@@ -143,6 +143,7 @@ void dispatch(const AttnArgs& a, cudaStream_t st) {
 void run_attention(const AttnArgs& a, cudaStream_t st) {
     if (a.bf16) dispatch<__nv_bfloat16>(a, st);
     else dispatch<float>(a, st);
+    note_launch();
 }
 
 }  // namespace dsa

@@ -11,6 +11,8 @@ namespace dsa {
 
 [[noreturn]] void throw_unsupported(const std::string& what);
 [[noreturn]] void throw_cuda(cudaError_t e, const char* where);
+// Counts kernel launches of this library (dsa_launch_counter()).
+void note_launch(int n = 1);
 
 inline int64_t ceil_div_i(int64_t a, int64_t b) { return (a + b - 1) / b; }
 

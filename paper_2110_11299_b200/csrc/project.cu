@@ -150,6 +150,7 @@ void launch_predict(const PredictArgs& a, cudaStream_t st) {
     if (a.per_row) {
         project_rows_kernel<T, D, KD><<<grid, kRowsPerCta, 0, st>>>(
             q, k, a.p, a.L, a.round_f32, a.qmax, a.lq, a.lk, a.sq, a.sk);
+        note_launch();
     } else {
         cudaMemsetAsync(a.amax, 0, sizeof(unsigned long long) * 2 * a.pairs, st);
         project_tensor_kernel<T, D, KD><<<grid, kRowsPerCta, 0, st>>>(q, k, a.p, a.L, a.round_f32,
@@ -159,6 +160,7 @@ void launch_predict(const PredictArgs& a, cudaStream_t st) {
                       static_cast<unsigned>(a.pairs), 2);
         quantize_tensor_kernel<<<g2, 256, 0, st>>>(a.xws, a.amax, a.L, KD, a.qmax, a.lq, a.lk,
                                                    a.sq, a.sk);
+        note_launch(2);
     }
 }
 

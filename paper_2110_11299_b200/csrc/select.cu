@@ -413,11 +413,13 @@ void launch_select(const SelectArgs& a, cudaStream_t st) {
                 auto kern = topk_rows_generic<uint64_t, KD>;
                 cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
                 kern<<<dim3(static_cast<unsigned>(a.L), P), kNT, sm, st>>>(a);
+                note_launch();
             } else {
                 const size_t sm = static_cast<size_t>(a.L) * 4;
                 auto kern = topk_rows_generic<uint32_t, KD>;
                 cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
                 kern<<<dim3(static_cast<unsigned>(a.L), P), kNT, sm, st>>>(a);
+                note_launch();
             }
             break;
         }
@@ -426,29 +428,35 @@ void launch_select(const SelectArgs& a, cudaStream_t st) {
             auto kern = colvec_generic<KD>;
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
             kern<<<dim3(static_cast<unsigned>(ceil_div_i(a.L, a.vec_v)), P), kNT, sm, st>>>(a);
+                note_launch();
             break;
         }
         case kBlock: {
             const int64_t nb = ceil_div_i(a.L, a.block);
             const int64_t total = a.pairs * 2 * nb * a.KD;
             pool_levels_kernel<<<static_cast<unsigned>(ceil_div_i(total, 256)), 256, 0, st>>>(a, nb);
+            note_launch();
             const size_t sm = static_cast<size_t>(nb) * 8;
             cudaFuncSetAttribute(block_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
             block_generic<<<dim3(static_cast<unsigned>(nb), P), kNT, sm, st>>>(a, nb);
+            note_launch();
             break;
         }
         case kThreshold: {
             exp_table_kernel<<<dim3(static_cast<unsigned>(std::min<int64_t>(ceil_div_i(a.span, 256), 64)), P), 256, 0, st>>>(a);
+            note_launch();
             const size_t sm = static_cast<size_t>(a.L) * 4;
             auto kern = threshold_generic<KD>;
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
             const int64_t n = a.pairs * a.L;
             uint64_t* counts = a.counts;
             kern<<<dim3(static_cast<unsigned>(a.L), P), kNT, sm, st>>>(a, counts, 0);
+                note_launch();
             cudaMemsetAsync(a.rowptr, 0, sizeof(uint64_t), st);
             size_t tb = a.scan_tmp_bytes;
             cub::DeviceScan::InclusiveSum(a.scan_tmp, tb, counts, a.rowptr + 1, static_cast<int64_t>(n), st);
             kern<<<dim3(static_cast<unsigned>(a.L), P), kNT, sm, st>>>(a, counts, 1);
+                note_launch();
             break;
         }
         default: throw_unsupported("unknown mask mode");

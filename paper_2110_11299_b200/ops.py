@@ -208,6 +208,41 @@ class Pipeline:
         return z
 
 
+class Phases:
+    """The three phases as separate, allocation-free calls on preallocated
+    buffers (bench.py times each with CUDA events)."""
+
+    def __init__(self, p: Preset, pairs: int, device="cuda"):
+        self.p, self.pairs = p, pairs
+        self.cfg = config_of(p, pairs)
+        self.ws = _ws(workspace_bytes(p, pairs), device)
+        self.lq = torch.empty((pairs, p.L, p.k), dtype=torch.bfloat16, device=device)
+        self.lk = torch.empty_like(self.lq)
+        ns = (pairs,) if p.quant_scope == "tensor" else (pairs, p.L)
+        self.sq = torch.empty(ns, dtype=torch.float64, device=device)
+        self.sk = torch.empty_like(self.sq)
+        self.mask = alloc_mask(p, pairs, device, empty_rows=False)
+        self._cm = self.mask.as_c()
+
+    def predict(self, q, k, P, stream=None):
+        _abi.check(_abi.lib().dsa_predict(C.byref(self.cfg), _ptr(q), _ptr(k), _ptr(P), _ptr(self.lq),
+                                          _ptr(self.lk), _ptr(self.sq), _ptr(self.sk), _ptr(self.ws),
+                                          self.ws.numel(), _stream(stream)))
+
+    def select(self, stream=None):
+        _abi.check(_abi.lib().dsa_select(C.byref(self.cfg), _ptr(self.lq), _ptr(self.lk),
+                                         _ptr(self.sq), _ptr(self.sk), C.byref(self._cm),
+                                         _ptr(self.ws), self.ws.numel(), _stream(stream)))
+
+    def attend(self, q, k, v, z, stream=None):
+        _abi.check(_abi.lib().dsa_sparse_attention(C.byref(self.cfg), _ptr(q), _ptr(k), _ptr(v),
+                                                   C.byref(self._cm), _ptr(z), _stream(stream)))
+
+
+def launch_counter() -> int:
+    return int(_abi.lib().dsa_launch_counter())
+
+
 def counters(p: Preset, mask: Mask, pairs: int, stream=None) -> dict:
     c = config_of(p, pairs)
     out = _abi.DsaCounts()
