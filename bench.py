@@ -1,0 +1,388 @@
+#!/usr/bin/env python
+"""DSA attention tokens/s (predict + select + sparse attention) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2_vector]
+    python bench.py --impl reference ...      # the reference CPU path
+
+One JSON line on rank 0.  A "step" is one pass of the hot path over the
+config's full batch: all B*H (b,h) pairs, phases 1 -> 2 -> 3, inputs resident
+in HBM (`value`), or through the C-ABI with host buffers and H2D/D2H copies
+inside the timed region (`e2e`).  Under torchrun every rank runs the config's
+pairs (its own seeded pair range: weak scaling, no collective on the hot
+path); checksums are all-reduced over NCCL after timing stops.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "DSA attention tokens/s (predict+sparse attn) at L=4096, 95% sparsity; % roofline"
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def load_peaks():
+    f = ROOT / "MEASURED_PEAKS.json"
+    if f.exists():
+        d = json.loads(f.read_text())
+        return d, "measured (MEASURED_PEAKS.json)"
+    return dict(PEAKS_FALLBACK), "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl" if os.environ.get("DSA_BENCH_BACKEND") != "gloo" else "gloo")
+    return rank, local, world
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int, device) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------- CPU arms
+def reference_sample(p, npairs: int, threads: int, rng_pair0: int = 0):
+    """Time the reference implementation (oracle/_ref, the unmodified
+    reference sources) on `npairs` pairs over `threads` host threads."""
+    from oracle.oracle import REF_SO, Oracle, Reference
+    from paper_2110_11299_b200 import ops
+
+    sub = p.replace(batch=npairs, heads=1)
+    q, k, v, P = ops.generate(sub, pair0=rng_pair0, npairs=npairs)
+    qn, kn, vn, Pn = (t.double().numpy() for t in (q, k, v, P))
+    mode = {"row_topk": 0, "colvec": 1, "block": 2}.get(p.mask_mode)
+    if REF_SO.exists() and mode is not None and p.quant_scope == "tensor":
+        ref = Reference()
+        t0 = time.perf_counter()
+        ref.pipeline(qn, kn, vn, Pn, p.bits, p.dtype == "f32", mode, p.keep, p.vec_v, p.block,
+                     p.force_diag, threads=threads)
+        dt = time.perf_counter() - t0
+        return dt, "reference", f"oracle/_ref (reference sources, isa={ref.isa()})"
+    # modes without a reference composition: the oracle restatement ("port")
+    o = Oracle()
+    t0 = time.perf_counter()
+    from concurrent.futures import ThreadPoolExecutor
+
+    def one(i):
+        lq, sq = o.levels(qn[i], Pn, p.bits, per_row=p.quant_scope == "row", round_f32=p.round_proj_f32)
+        lk, sk = o.levels(kn[i], Pn, p.bits, per_row=p.quant_scope == "row", round_f32=p.round_proj_f32)
+        import numpy as np
+        if p.mask_mode == "threshold":
+            c = sq * sk / np.sqrt(float(p.d))
+            rp, cols, _ = o.mask_threshold(lq, lk, c, p.frac_num, p.frac_den, p.cap, p.causal)
+        else:
+            m = o.mask_topk(lq, lk, p.keep, sk=sk)
+            rp = np.arange(0, p.L * p.keep + 1, p.keep, dtype=np.uint64)
+            cols = m.ravel()
+        o.sparse_attention(qn[i], kn[i], vn[i], rp, cols, p.scale, p.dtype == "f32")
+
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(one, range(npairs)))
+    return time.perf_counter() - t0, "port", "oracle/dsa_oracle.c restatement"
+
+
+def run_reference_arm(args, p, rank, world):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    npairs = min(p.pairs, max(1, args.ref_pairs or 2 * threads))
+    tokens = npairs * p.L / p.heads
+    for _ in range(args.warmup):
+        reference_sample(p, npairs, threads)
+    times = []
+    kind = sample = None
+    for _ in range(args.steps):
+        dt, kind, sample = reference_sample(p, npairs, threads)
+        times.append(dt)
+    mean = statistics.mean(times)
+    value = tokens / mean
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded BASELINE generator)",
+        "config": {**p.summary(), "sample_pairs": npairs},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": kind,
+                         "sample": f"{npairs} of {p.pairs} (b,h) pairs per step via {sample}; "
+                                   f"tokens = pairs*L/heads"},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU arm
+def run_gpu_arm(args, p, rank, local, world):
+    import torch
+    from paper_2110_11299_b200 import ops
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    P_ = p.pairs
+    pair0 = rank * P_  # weak scaling: each rank its own seeded pair range
+    q, k, v, Pm = ops.generate(p, pair0=pair0, npairs=P_, pinned=True)
+    qd, kd, vd, Pd = (t.to(dev) for t in (q, k, v, Pm))
+    zd = torch.empty_like(qd)
+    zh = torch.empty_like(q).pin_memory()
+    stream = torch.cuda.Stream(device=dev)
+    pipe = ops.Pipeline(p, device=dev)
+    ph = ops.Phases(p, P_, device=dev)
+    in_bytes = q.numel() * q.element_size() * 3
+    l2_note = (f"inputs {in_bytes / 1e6:.0f} MB > 126 MB L2 (no flush needed)" if in_bytes > 126e6
+               else "L2 flushed between steps (256 MB write)")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev) if in_bytes <= 126e6 else None
+
+    def step(s):
+        if flush is not None:
+            flush.fill_(1.0)
+        pipe(qd, kd, vd, Pd, out=zd, stream=s)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step(stream)
+    stream.synchronize()
+
+    # ---- device-resident timed region
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n0 = ops.launch_counter()
+    barrier(world)
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        with torch.cuda.stream(stream):
+            ev0.record(stream)
+            for _ in range(args.steps):
+                step(stream)
+            ev1.record(stream)
+        ev1.synchronize()
+        torch.cuda.synchronize(dev)
+    launches = ops.launch_counter() - n0
+    ms = ev0.elapsed_time(ev1) / args.steps
+    ms = max_over_ranks(ms, world, dev)
+    barrier(world)
+
+    # ---- end to end through the C-ABI with host buffers
+    h2d = in_bytes + Pm.numel() * 4
+    d2h = zh.numel() * zh.element_size()
+    with torch.cuda.stream(stream):
+        for _ in range(2):
+            qd.copy_(q, non_blocking=True); kd.copy_(k, non_blocking=True)
+            vd.copy_(v, non_blocking=True); Pd.copy_(Pm, non_blocking=True)
+            pipe(qd, kd, vd, Pd, out=zd, stream=stream)
+            zh.copy_(zd, non_blocking=True)
+    stream.synchronize()
+    barrier(world)
+    torch.cuda.synchronize(dev)
+    with torch.cuda.stream(stream):
+        ev0.record(stream)
+        for _ in range(args.steps):
+            qd.copy_(q, non_blocking=True); kd.copy_(k, non_blocking=True)
+            vd.copy_(v, non_blocking=True); Pd.copy_(Pm, non_blocking=True)
+            pipe(qd, kd, vd, Pd, out=zd, stream=stream)
+            zh.copy_(zd, non_blocking=True)
+        ev1.record(stream)
+    ev1.synchronize()
+    e2e_ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps, world, dev)
+
+    # ---- per-phase timing (same stream, events; for the roofline)
+    phase_ms = {}
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    with torch.cuda.stream(stream):
+        ph.predict(qd, kd, Pd, stream)
+        ph.select(stream)
+        ph.attend(qd, kd, vd, zd, stream)
+    stream.synchronize()
+    acc = {"predict": 0.0, "select": 0.0, "attention": 0.0}
+    reps = max(3, args.steps)
+    for _ in range(reps):
+        with torch.cuda.stream(stream):
+            if flush is not None:
+                flush.fill_(1.0)
+            evs[0].record(stream)
+            ph.predict(qd, kd, Pd, stream)
+            evs[1].record(stream)
+            ph.select(stream)
+            evs[2].record(stream)
+            ph.attend(qd, kd, vd, zd, stream)
+            evs[3].record(stream)
+        evs[3].synchronize()
+        acc["predict"] += evs[0].elapsed_time(evs[1])
+        acc["select"] += evs[1].elapsed_time(evs[2])
+        acc["attention"] += evs[2].elapsed_time(evs[3])
+    for kx in acc:
+        phase_ms[kx] = acc[kx] / reps
+
+    # ---- checksums over NCCL after timing (not on the hot path)
+    import torch.distributed as dist
+    csum = torch.tensor([zd.double().sum().item(), float(zd.abs().max().item())], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(csum)
+
+    if rank != 0:
+        return
+    peaks, peak_src = load_peaks()
+    L, d, k_, e = p.L, p.d, p.k, (2 if p.dtype == "bf16" else 4)
+    pairs = P_
+    cnt = ops.counters(p, ph.mask, pairs, stream=stream)
+    nnz = cnt["nnz"]
+    # algorithmic work per launch of each phase, over all pairs
+    work = {
+        "predict": {"bound": "hbm", "amount": (2 * L * d * e + 2 * L * k_ * 2) * pairs + d * k_ * 4,
+                    "unit": "GB/s", "scale": 1e9},
+        "select": {"bound": "tensor", "amount": (L * (L + 1) if (p.mask_mode == "threshold" and p.causal)
+                                                  else 2 * L * L) * k_ * pairs,
+                   "unit": "TFLOP/s", "scale": 1e12},
+        "attention": {"bound": "hbm", "amount": 4 * L * d * e * pairs, "unit": "GB/s", "scale": 1e9},
+    }
+    dom = max(phase_ms, key=phase_ms.get)
+    w = work[dom]
+    achieved = w["amount"] / (phase_ms[dom] * 1e-3) / w["scale"]
+    peak = peaks["hbm_gbs"] if w["bound"] == "hbm" else peaks["bf16_tflops"]
+    traffic = None
+    tf = ROOT / "profiles" / "traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get(f"{p.name}:{dom}")
+    phases = {}
+    for kx, ms_k in phase_ms.items():
+        wk = work[kx]
+        a_k = wk["amount"] / (ms_k * 1e-3) / wk["scale"]
+        pk = peaks["hbm_gbs"] if wk["bound"] == "hbm" else peaks["bf16_tflops"]
+        phases[kx] = {"ms": ms_k, "bound": wk["bound"], "achieved": a_k, "unit": wk["unit"],
+                      "frac": a_k / pk}
+    tokens = p.tokens * world
+    value = tokens / (ms * 1e-3)
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        npairs = min(pairs, max(1, args.ref_pairs or 2 * threads))
+        dt, kind, sample = reference_sample(p, npairs, threads)
+        cpu = {"value": npairs * L / p.heads / dt, "unit": "tokens/s", "cores": threads, "kind": kind,
+               "sample": f"{npairs} of {pairs} (b,h) pairs via {sample}, {dt:.1f} s wall; tokens = pairs*L/heads"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16" if p.dtype == "bf16" else "f32",
+        "data": "synthetic (seeded BASELINE generator, SURVEY 8.0)",
+        "config": {**p.summary(), "pairs_per_gpu": pairs, "parallelism": f"(b,h)-pairs x{world}",
+                   "l2": l2_note},
+        "e2e": {"value": tokens / (e2e_ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "roofline": {"kernel": dom, "bound": w["bound"], "achieved": achieved, "peak": peak,
+                     "unit": w["unit"], "frac": achieved / peak, "traffic": traffic,
+                     "peak_source": peak_src},
+        "phases": phases,
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+        "gpu_launches": int(launches),
+        "counters": {"nnz": nnz, "sddmm_mults": cnt["sddmm_mults"], "spmm_mults": cnt["spmm_mults"],
+                     "softmax_exps": cnt["softmax_exps"]},
+        "checksum": [float(csum[0].item()), float(csum[1].item())],
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c2_vector")
+    ap.add_argument("--ref-pairs", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    from paper_2110_11299_b200 import load_preset
+
+    p = load_preset(args.config)
+    rank, local, world = dist_setup()
+    try:
+        if args.impl == "reference":
+            run_reference_arm(args, p, rank, world)
+        else:
+            run_gpu_arm(args, p, rank, local, world)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
