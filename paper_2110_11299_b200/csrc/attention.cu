@@ -141,6 +141,10 @@ void dispatch(const AttnArgs& a, cudaStream_t st) {
 }  // namespace
 
 void run_attention(const AttnArgs& a, cudaStream_t st) {
+    if (band_attention_supported(a)) {
+        run_band_attention(a, st);
+        return;
+    }
     if (a.bf16) dispatch<__nv_bfloat16>(a, st);
     else dispatch<float>(a, st);
     note_launch();

@@ -1,0 +1,278 @@
+// Phase 3 for vector-wise (COLVEC) masks: every band of 8 query rows shares
+// one ascending list of `keep` key columns (P/src/maskgen.cpp:51-59), so the
+// band is an 8-wide tensor-core tile.  Per band (one warp):
+//
+//   S^T[key, q] = K_sel . Q_band^T      mma m16n8k16 (M = 16 gathered keys,
+//                                        N = the band's 8 queries, K = d)
+//   online softmax over keys per query column (running max / sum in fp32)
+//   Z^T[d, q]  += V_sel^T . P^T         mma m16n8k16 (M = d, K = keys)
+//
+// K/V rows of the band's keys are gathered in chunks with 16-byte cp.async
+// into XOR-swizzled shared memory (conflict-free ldmatrix), double-buffered
+// so the next chunk's gather overlaps this chunk's math.  The gather is the
+// roofline of this phase (each kept key row is fetched once per band, i.e.
+// reused by the band's 8 queries -- SURVEY H6); HBM sees Q, K, V, Z once.
+#include <cuda_bf16.h>
+
+#include "device_common.cuh"
+#include "kernels.h"
+
+namespace dsa {
+namespace {
+
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
+    const int n = valid ? 16 : 0;  // src-size 0 -> zero fill
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(n));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                        uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                          uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+
+__device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                         uint32_t a3, uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+        "{%8,%9}, {%0,%1,%2,%3};\n"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// Row r of a [rows][D] bf16 tile, 16-byte chunk c, XOR-swizzled within 8 chunks.
+template <int D>
+__device__ __forceinline__ uint32_t swz(int r, int c) {
+    constexpr int kChunks = D / 8;  // 16-byte chunks per row
+    return static_cast<uint32_t>(r * D * 2 + (((c & 7) ^ (r & 7)) | (c & ~7)) * 16);
+    (void)kChunks;
+}
+
+template <int D, int CHUNK>
+struct BandSmem {
+    __nv_bfloat16 k[2][CHUNK * D];
+    __nv_bfloat16 v[2][CHUNK * D];
+    __nv_bfloat16 q[8 * D];            // Q band; reused to stage Z
+    __nv_bfloat16 p[8 * (CHUNK + 8)];  // [query][key], padded rows
+};
+
+template <int D, int CHUNK, int kBandWarps>
+__global__ void __launch_bounds__(kBandWarps * 32)
+    attn_band_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __restrict__ K,
+                     const __nv_bfloat16* __restrict__ V, const uint32_t* __restrict__ band_cols,
+                     int64_t pairs, int64_t L, int64_t keep, int scale, __nv_bfloat16* __restrict__ Z) {
+    extern __shared__ __align__(128) unsigned char dsm[];
+    using S = BandSmem<D, CHUNK>;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    S& sm = reinterpret_cast<S*>(dsm)[warp];
+    const int64_t nb = (L + 7) / 8;
+    const int64_t band_global = static_cast<int64_t>(blockIdx.x) * kBandWarps + warp;
+    if (band_global >= pairs * nb) return;
+    const int64_t pair = band_global / nb, band = band_global % nb;
+    const int64_t r0 = band * 8;
+    const __nv_bfloat16* Kp = K + pair * L * D;
+    const __nv_bfloat16* Vp = V + pair * L * D;
+    const uint32_t* cols = band_cols + (pair * nb + band) * keep;
+    const int g = lane >> 2, c4 = lane & 3;
+    constexpr int kChunks16 = D / 8;  // 16-byte chunks per row
+
+    // ---- Q band -> smem (zero rows past L)
+    for (int t = lane; t < 8 * kChunks16; t += 32) {
+        const int r = t / kChunks16, c = t % kChunks16;
+        const bool ok = r0 + r < L;
+        cp_async16(smem_u32(sm.q) + swz<D>(r, c), Q + (pair * L + (ok ? r0 + r : 0)) * D + c * 8, ok);
+    }
+    auto load_chunk = [&](int buf, int base) {
+        for (int t = lane; t < CHUNK * kChunks16; t += 32) {
+            const int r = t / kChunks16, c = t % kChunks16;
+            const bool ok = base + r < keep;
+            const int64_t j = ok ? static_cast<int64_t>(__ldg(cols + base + r)) : 0;
+            cp_async16(smem_u32(sm.k[buf]) + swz<D>(r, c), Kp + j * D + c * 8, ok);
+            cp_async16(smem_u32(sm.v[buf]) + swz<D>(r, c), Vp + j * D + c * 8, ok);
+        }
+    };
+    const int nchunks = static_cast<int>((keep + CHUNK - 1) / CHUNK);
+    load_chunk(0, 0);
+    cp_async_commit();
+
+    const float sl2 = (scale ? rsqrtf(static_cast<float>(D)) : 1.f) * 1.4426950408889634f;
+    float m_run[2] = {-INFINITY, -INFINITY};  // queries 2c, 2c+1 (log2 domain)
+    float l_part[2] = {0.f, 0.f};
+    float zacc[D / 16][4];
+#pragma unroll
+    for (int t = 0; t < D / 16; ++t)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) zacc[t][u] = 0.f;
+    uint32_t qb[D / 16][2];
+
+    for (int ch = 0; ch < nchunks; ++ch) {
+        const int buf = ch & 1;
+        if (ch + 1 < nchunks) load_chunk(buf ^ 1, (ch + 1) * CHUNK);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncwarp();
+        if (ch == 0) {
+            // B fragments of Q^T: b0b1 = Q[g][16ks + 2c..], b2b3 = Q[g][16ks + 8 + 2c..]
+#pragma unroll
+            for (int ks = 0; ks < D / 16; ++ks) {
+                const char* qbase = reinterpret_cast<const char*>(sm.q);
+                qb[ks][0] = *reinterpret_cast<const uint32_t*>(qbase + swz<D>(g, 2 * ks) + c4 * 4);
+                qb[ks][1] = *reinterpret_cast<const uint32_t*>(qbase + swz<D>(g, 2 * ks + 1) + c4 * 4);
+            }
+        }
+        // ---- S^T = K_chunk . Q^T : CHUNK/16 m-tiles
+        float s[CHUNK / 16][4];
+        const uint32_t kb = smem_u32(sm.k[buf]);
+#pragma unroll
+        for (int mt = 0; mt < CHUNK / 16; ++mt) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) s[mt][u] = 0.f;
+#pragma unroll
+            for (int ks = 0; ks < D / 16; ++ks) {
+                const int mi = lane >> 3;
+                const int row = mt * 16 + (mi & 1) * 8 + (lane & 7);
+                const int chk = ks * 2 + (mi >> 1);
+                uint32_t a0, a1, a2, a3;
+                ldsm_x4(kb + swz<D>(row, chk), a0, a1, a2, a3);
+                mma16816(s[mt], a0, a1, a2, a3, qb[ks][0], qb[ks][1]);
+            }
+        }
+        // ---- online softmax over keys (rows g, g+8 of each m-tile)
+        const int base = ch * CHUNK;
+        float cmax[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+        for (int mt = 0; mt < CHUNK / 16; ++mt)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int key = base + mt * 16 + g + (u >> 1) * 8;
+                const float x = key < keep ? s[mt][u] * sl2 : -INFINITY;
+                s[mt][u] = x;
+                cmax[u & 1] = fmaxf(cmax[u & 1], x);
+            }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            cmax[h] = fmaxf(cmax[h], __shfl_xor_sync(0xffffffffu, cmax[h], 4));
+            cmax[h] = fmaxf(cmax[h], __shfl_xor_sync(0xffffffffu, cmax[h], 8));
+            cmax[h] = fmaxf(cmax[h], __shfl_xor_sync(0xffffffffu, cmax[h], 16));
+        }
+        float corr[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const float mn = fmaxf(m_run[h], cmax[h]);
+            corr[h] = m_run[h] == -INFINITY ? 0.f : exp2f(m_run[h] - mn);
+            m_run[h] = mn;
+            l_part[h] *= corr[h];
+        }
+#pragma unroll
+        for (int t = 0; t < D / 16; ++t) {
+            zacc[t][0] *= corr[0];
+            zacc[t][1] *= corr[1];
+            zacc[t][2] *= corr[0];
+            zacc[t][3] *= corr[1];
+        }
+        // p = 2^(x - m) -> bf16 P[query][key] in smem
+        constexpr int PW = CHUNK + 8;
+#pragma unroll
+        for (int mt = 0; mt < CHUNK / 16; ++mt)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const float pv = exp2f(s[mt][u] - m_run[u & 1]);
+                l_part[u & 1] += pv;
+                const int key = mt * 16 + g + (u >> 1) * 8;
+                const int qq = 2 * c4 + (u & 1);
+                sm.p[qq * PW + key] = __float2bfloat16_rn(pv);
+            }
+        __syncwarp();
+        // ---- Z^T += V_chunk^T . P^T
+        const uint32_t vb = smem_u32(sm.v[buf]);
+#pragma unroll
+        for (int ks = 0; ks < CHUNK / 16; ++ks) {
+            const uint32_t b0 = *reinterpret_cast<const uint32_t*>(&sm.p[g * PW + ks * 16 + 2 * c4]);
+            const uint32_t b1 = *reinterpret_cast<const uint32_t*>(&sm.p[g * PW + ks * 16 + 8 + 2 * c4]);
+#pragma unroll
+            for (int mt = 0; mt < D / 16; ++mt) {
+                const int mi = lane >> 3;
+                const int row = ks * 16 + (mi >> 1) * 8 + (lane & 7);
+                const int chk = mt * 2 + (mi & 1);
+                uint32_t a0, a1, a2, a3;
+                ldsm_x4_t(vb + swz<D>(row, chk), a0, a1, a2, a3);
+                mma16816(zacc[mt], a0, a1, a2, a3, b0, b1);
+            }
+        }
+        __syncwarp();
+    }
+    cp_async_wait<0>();
+    // ---- finalize: l over the 8 lanes sharing c4, Z = Z^T / l
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        l_part[h] += __shfl_xor_sync(0xffffffffu, l_part[h], 4);
+        l_part[h] += __shfl_xor_sync(0xffffffffu, l_part[h], 8);
+        l_part[h] += __shfl_xor_sync(0xffffffffu, l_part[h], 16);
+    }
+    const float inv0 = l_part[0] > 0.f ? 1.f / l_part[0] : 0.f;
+    const float inv1 = l_part[1] > 0.f ? 1.f / l_part[1] : 0.f;
+#pragma unroll
+    for (int mt = 0; mt < D / 16; ++mt) {
+        const int d0 = mt * 16 + g;
+        sm.q[(2 * c4) * D + d0] = __float2bfloat16_rn(zacc[mt][0] * inv0);
+        sm.q[(2 * c4 + 1) * D + d0] = __float2bfloat16_rn(zacc[mt][1] * inv1);
+        sm.q[(2 * c4) * D + d0 + 8] = __float2bfloat16_rn(zacc[mt][2] * inv0);
+        sm.q[(2 * c4 + 1) * D + d0 + 8] = __float2bfloat16_rn(zacc[mt][3] * inv1);
+    }
+    __syncwarp();
+    for (int t = lane; t < 8 * kChunks16; t += 32) {
+        const int r = t / kChunks16, c = t % kChunks16;
+        if (r0 + r < L)
+            *reinterpret_cast<uint4*>(Z + (pair * L + r0 + r) * D + c * 8) =
+                *reinterpret_cast<const uint4*>(&sm.q[r * D + c * 8]);
+    }
+}
+
+template <int D, int CHUNK, int kBandWarps>
+void launch_band(const AttnArgs& a, cudaStream_t st) {
+    const int64_t nb = (a.L + 7) / 8;
+    const size_t smem = sizeof(BandSmem<D, CHUNK>) * kBandWarps;
+    auto kern = attn_band_kernel<D, CHUNK, kBandWarps>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    const unsigned grid = static_cast<unsigned>(ceil_div_i(a.pairs * nb, kBandWarps));
+    kern<<<grid, kBandWarps * 32, smem, st>>>(
+        static_cast<const __nv_bfloat16*>(a.q), static_cast<const __nv_bfloat16*>(a.k),
+        static_cast<const __nv_bfloat16*>(a.v), a.cols, a.pairs, a.L, a.keep, a.scale,
+        static_cast<__nv_bfloat16*>(a.z));
+}
+
+}  // namespace
+
+bool band_attention_supported(const AttnArgs& a) {
+    return a.mode == kColvec && a.vec_v == 8 && a.bf16 && (a.D == 64 || a.D == 128);
+}
+
+void run_band_attention(const AttnArgs& a, cudaStream_t st) {
+    if (a.D == 64) launch_band<64, 32, 12>(a, st);
+    else launch_band<128, 32, 6>(a, st);
+    note_launch();
+}
+
+}  // namespace dsa

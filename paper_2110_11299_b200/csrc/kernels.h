@@ -63,6 +63,8 @@ struct SelectArgs {
 };
 void run_select(const SelectArgs& a, cudaStream_t st);
 size_t select_scan_tmp_bytes(int64_t n);
+bool colvec_tc_supported(const SelectArgs& a);
+void run_colvec_tc(const SelectArgs& a, cudaStream_t st);
 
 struct AttnArgs {
     int mode;
@@ -78,5 +80,7 @@ struct AttnArgs {
     uint8_t* empty_rows;
 };
 void run_attention(const AttnArgs& a, cudaStream_t st);
+bool band_attention_supported(const AttnArgs& a);
+void run_band_attention(const AttnArgs& a, cudaStream_t st);
 
 }  // namespace dsa

@@ -473,6 +473,10 @@ size_t select_scan_tmp_bytes(int64_t n) {
 }
 
 void run_select(const SelectArgs& a, cudaStream_t st) {
+    if (colvec_tc_supported(a)) {
+        run_colvec_tc(a, st);
+        return;
+    }
     switch (a.KD) {
         case 16: launch_select<16>(a, st); break;
         case 32: launch_select<32>(a, st); break;
