@@ -21,6 +21,8 @@
 // exists in HBM.
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "device_common.cuh"
 #include "kernels.h"
 #include "tc_sm100.cuh"
@@ -71,18 +73,13 @@ struct ColvecSmem {
     static constexpr int kTileBytes = kMT * KD * 2;
 };
 
-constexpr int kWin = 512;  // histogram window below the band max
+constexpr int kWin = 512;  // histogram scratch per warp (bins)
 
-// Exact selection of one band from pooled[0..L) (int16 scores): threshold T
-// = keep-th largest value, rem = how many values == T to admit (lowest
-// column first).  Counting runs on a window of kWin values below the band
-// max (the keep-th largest almost always lies there); otherwise a
-// binary search over the full integer range settles T.
-__device__ __forceinline__ void band_threshold(const int16_t* __restrict__ pv, int L, int keep,
-                                               int bmax, int M, uint32_t* h, int lane, int& T,
-                                               uint32_t& rem) {
-    const int lo = bmax - (kWin - 1);
-    for (int i = lane; i < kWin; i += 32) h[i] = 0;
+// Counts values >= lo into h[0..W) and returns the count inside the window.
+template <int W>
+__device__ __forceinline__ uint32_t window_hist(const int16_t* __restrict__ pv, int L, int lo,
+                                                uint32_t* h, int lane) {
+    for (int i = lane; i < W; i += 32) h[i] = 0;
     __syncwarp();
     int j = lane;
     for (; j + 96 < L; j += 128) {
@@ -97,7 +94,19 @@ __device__ __forceinline__ void band_threshold(const int16_t* __restrict__ pv, i
         if (v >= lo) atomicAdd(&h[v - lo], 1u);
     }
     __syncwarp();
-    constexpr int per = kWin / 32;
+    uint32_t c = 0;
+    for (int i = lane; i < W; i += 32) c += h[i];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
+    return c;
+}
+
+// T = the keep-th largest value (bins are values lo..lo+W-1), rem = number
+// of values == T admitted.  Requires count(window) >= keep.
+template <int W>
+__device__ __forceinline__ void window_threshold(const uint32_t* h, int lo, uint32_t kk, int lane,
+                                                 int& T, uint32_t& rem) {
+    constexpr int per = W / 32;
     uint32_t c[per], local = 0;
 #pragma unroll
     for (int i = 0; i < per; ++i) {
@@ -110,27 +119,42 @@ __device__ __forceinline__ void band_threshold(const int16_t* __restrict__ pv, i
         const uint32_t y = __shfl_down_sync(0xffffffffu, suf, off);
         if (lane + off < 32) suf += y;
     }
-    const uint32_t total = __shfl_sync(0xffffffffu, suf, 0);
-    const uint32_t kk = static_cast<uint32_t>(keep);
-    if (total >= kk) {
-        const uint32_t excl = suf - local;
-        const bool mine = excl < kk && kk <= suf;
-        const int src = __ffs(__ballot_sync(0xffffffffu, mine)) - 1;
-        int t = 0;
-        uint32_t r = 0;
-        if (mine) {
-            uint32_t cum = excl;
+    const uint32_t excl = suf - local;
+    const bool mine = excl < kk && kk <= suf;
+    const int src = __ffs(__ballot_sync(0xffffffffu, mine)) - 1;
+    int t = 0;
+    uint32_t r = 0;
+    if (mine) {
+        uint32_t cum = excl;
 #pragma unroll
-            for (int i = per - 1; i >= 0; --i) {
-                if (r == 0 && cum + c[i] >= kk) {
-                    t = lo + lane * per + i;
-                    r = kk - cum;
-                }
-                cum += c[i];
+        for (int i = per - 1; i >= 0; --i) {
+            if (r == 0 && cum + c[i] >= kk) {
+                t = lo + lane * per + i;
+                r = kk - cum;
             }
+            cum += c[i];
         }
-        T = __shfl_sync(0xffffffffu, t, src);
-        rem = __shfl_sync(0xffffffffu, r, src);
+    }
+    T = __shfl_sync(0xffffffffu, t, src);
+    rem = __shfl_sync(0xffffffffu, r, src);
+}
+
+// Exact selection of one band from pooled[0..L) (int16 scores): threshold T
+// = keep-th largest value, rem = how many values == T to admit (lowest
+// column first).  The keep-th largest sits a few dozen below the band max,
+// so counting starts on a 64-value window (few shared atomics), widens to
+// 512, and falls back to a binary search over the full integer range.
+__device__ __forceinline__ void band_threshold(const int16_t* __restrict__ pv, int L, int keep,
+                                               int bmax, int M, uint32_t* h, int lane, int& T,
+                                               uint32_t& rem) {
+    const uint32_t kk = static_cast<uint32_t>(keep);
+    if (window_hist<64>(pv, L, bmax - 63, h, lane) >= kk) {
+        window_threshold<64>(h, bmax - 63, kk, lane, T, rem);
+        return;
+    }
+    const int lo = bmax - (kWin - 1);
+    if (window_hist<kWin>(pv, L, lo, h, lane) >= kk) {
+        window_threshold<kWin>(h, lo, kk, lane, T, rem);
         return;
     }
     // rare: keep-th value below the window -> binary search on count(v >= x)
@@ -179,10 +203,57 @@ __device__ __forceinline__ void band_emit(const int16_t* __restrict__ pv, int L,
     }
 }
 
+constexpr int kList = 1024;  // per-warp output staging (column indices)
+
+__device__ __forceinline__ unsigned vote_ballot(bool p) {
+    unsigned r;
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\tvote.sync.ballot.b32 %0, q, 0xffffffff;\n\t}\n"
+                 : "=r"(r)
+                 : "r"(static_cast<unsigned>(p)));
+    return r;
+}
+
+// Exact top-`keep` of one band (pooled[0..Lp), padded columns INT16_MIN):
+// threshold from the windowed histogram, then one ascending pass that
+// stages kept columns in shared memory (unconditional stores; dropped lanes
+// write a trash slot) and a coalesced copy of the list to global memory.
+__device__ __forceinline__ void band_select(const int16_t* __restrict__ pv, int L, int Lp, int keep,
+                                            int bmax, int M, uint32_t* h, uint32_t* obuf,
+                                            uint32_t* __restrict__ o, int lane) {
+    int T;
+    uint32_t rem;
+    band_threshold(pv, L, keep, bmax, M, h, lane, T, rem);
+    if (keep > kList - 32) {
+        band_emit(pv, L, keep, T, rem, o, lane);
+        return;
+    }
+    const unsigned lt = lanemask_lt();
+    const uint32_t trash = static_cast<uint32_t>(kList - 32 + lane);
+    uint32_t taken = 0, eq_seen = 0;
+    for (int j0 = 0; j0 < Lp; j0 += 128) {
+        int v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = pv[j0 + u * 32 + lane];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const bool eq = v[u] == T;
+            const unsigned be = vote_ballot(eq);
+            const bool take = v[u] > T || (eq && eq_seen + __popc(be & lt) < rem);
+            const unsigned bt = vote_ballot(take);
+            obuf[take ? taken + __popc(bt & lt) : trash] = static_cast<uint32_t>(j0 + u * 32 + lane);
+            taken += __popc(bt);
+            eq_seen += __popc(be);
+        }
+    }
+    __syncwarp();
+    for (int i = lane; i < keep; i += 32) o[i] = obuf[i];
+    __syncwarp();
+}
+
 template <int KD>
 __global__ void __launch_bounds__(kThreads, 1)
     colvec_tc_kernel(const uint16_t* __restrict__ lq, const uint16_t* __restrict__ lk, int64_t L,
-                     int64_t keep, int M, uint32_t* __restrict__ out) {
+                     int64_t keep, int M, uint32_t* __restrict__ out, int dbg) {
     extern __shared__ __align__(1024) unsigned char smem[];
     constexpr int kTile = ColvecSmem<KD>::kTileBytes;
     const int nt = static_cast<int>((L + kMT - 1) / kMT);
@@ -192,6 +263,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     unsigned char* ring = p;                    p += kStages * kTile;     // K~ tiles
     int16_t* pooled = reinterpret_cast<int16_t*>(p); p += 16 * Lp * 2;   // [band][key]
     uint32_t* hist = reinterpret_cast<uint32_t*>(p); p += (kThreads / 32) * kWin * 4;
+    uint32_t* obufs = reinterpret_cast<uint32_t*>(p); p += (kThreads / 32) * kList * 4;
     int* bandmax = reinterpret_cast<int*>(p);   p += 16 * 4;
     uint64_t* bars = reinterpret_cast<uint64_t*>(p);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
@@ -265,6 +337,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::ld_32x32b_x32(base, r0);
             tc::ld_32x32b_x32(base + 32, r1);
             tc::wait_ld();
+            if (dbg & 2) {  // profiling switch: TMEM reads only
+                uint32_t x = 0;
+#pragma unroll
+                for (int i = 0; i < 32; ++i) x ^= r0[i] ^ r1[i];
+                pooled[half * 8 * Lp + key] = static_cast<int16_t>(x);
+            } else
 #pragma unroll
             for (int cb = 0; cb < 2; ++cb) {
                 uint32_t* r = cb ? r1 : r0;
@@ -282,7 +360,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     asm("max.f32 %0, %1, %2, %3;" : "=f"(m2) : "f"(m0), "f"(m1), "f"(f[6]));
                     const float mx = fmaxf(m2, f[7]);
                     const int band = half * 8 + cb * 4 + bb;
-                    pooled[band * Lp + key] = static_cast<int16_t>(__float2int_rn(mx));
+                    pooled[band * Lp + key] = kvalid ? static_cast<int16_t>(__float2int_rn(mx)) : INT16_MIN;
                     if (kvalid) bmax[cb * 4 + bb] = fmaxf(bmax[cb * 4 + bb], mx);
                 }
             }
@@ -304,14 +382,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---- exact per-band selection (one warp per band)
     const int64_t nb = (L + 7) / 8;
     uint32_t* h = hist + warp * kWin;
-    for (int b = warp; b < 16; b += kThreads / 32) {
+    for (int b = warp; b < 16 && !(dbg & 1); b += kThreads / 32) {
         const int64_t band = q0 / 8 + b;
         if (band >= nb) break;
         const int16_t* pv = pooled + b * Lp;
-        int T;
-        uint32_t rem;
-        band_threshold(pv, static_cast<int>(L), static_cast<int>(keep), bandmax[b], M, h, lane, T, rem);
-        band_emit(pv, static_cast<int>(L), static_cast<int>(keep), T, rem, out + (pair * nb + band) * keep, lane);
+        band_select(pv, static_cast<int>(L), Lp, static_cast<int>(keep), bandmax[b], M, h,
+                    obufs + warp * kList, out + (pair * nb + band) * keep, lane);
         __syncwarp();
     }
 }
@@ -322,7 +398,7 @@ size_t colvec_smem_bytes(int64_t L, int M) {
     const size_t nbins = static_cast<size_t>(2 * M + 1);
     (void)nbins;
     return ColvecSmem<KD>::kTileBytes * (1 + kStages) + 16 * nt * kMT * 2 +
-           (kThreads / 32) * kWin * 4 + 16 * 4 + 2 * 8 + 8;
+           (kThreads / 32) * kWin * 4 + (kThreads / 32) * kList * 4 + 16 * 4 + 2 * 8 + 8;
 }
 
 }  // namespace
@@ -336,18 +412,23 @@ bool colvec_tc_supported(const SelectArgs& a) {
 }
 
 void run_colvec_tc(const SelectArgs& a, cudaStream_t st) {
+    // DSA_PROFILE_SWITCH: profiling-only ablations (1: skip selection, 2: TMEM reads only)
+    static const int dbg = [] {
+        const char* e = std::getenv("DSA_PROFILE_SWITCH");
+        return e ? std::atoi(e) : 0;
+    }();
     const int M = static_cast<int>(a.KD) * a.qmax * a.qmax;
     const dim3 grid(static_cast<unsigned>(ceil_div_i(a.L, kNQ)), static_cast<unsigned>(a.pairs));
     if (a.KD == 16) {
         const size_t smem = colvec_smem_bytes<16>(a.L, M);
         cudaFuncSetAttribute(colvec_tc_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
-        colvec_tc_kernel<16><<<grid, kThreads, smem, st>>>(a.lq, a.lk, a.L, a.keep, M, a.cols);
+        colvec_tc_kernel<16><<<grid, kThreads, smem, st>>>(a.lq, a.lk, a.L, a.keep, M, a.cols, dbg);
     } else {
         const size_t smem = colvec_smem_bytes<32>(a.L, M);
         cudaFuncSetAttribute(colvec_tc_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
-        colvec_tc_kernel<32><<<grid, kThreads, smem, st>>>(a.lq, a.lk, a.L, a.keep, M, a.cols);
+        colvec_tc_kernel<32><<<grid, kThreads, smem, st>>>(a.lq, a.lk, a.L, a.keep, M, a.cols, dbg);
     }
     note_launch();
 }

@@ -24,6 +24,8 @@ CASES = [
     ("colvec", 1004, 64, 16, 4, "bf16", "tensor", {"keep": 51, "vec_v": 8}),
     ("colvec", 130, 128, 32, 4, "bf16", "tensor", {"keep": 130, "vec_v": 8}),
     ("colvec", 515, 64, 16, 8, "bf16", "tensor", {"keep": 20, "vec_v": 8}),
+    ("colvec", 1000, 64, 32, 4, "bf16", "tensor", {"keep": 999, "vec_v": 8}),
+    ("colvec", 640, 64, 16, 2, "bf16", "tensor", {"keep": 300, "vec_v": 8}),
     ("colvec", 300, 64, 16, 4, "f32", "tensor", {"keep": 17, "vec_v": 5}),
     ("block", 1000, 64, 16, 4, "bf16", "tensor", {"keep": 5, "block": 32, "force_diag": True}),
     ("block", 333, 128, 32, 8, "bf16", "tensor", {"keep": 3, "block": 16, "force_diag": False}),
