@@ -31,6 +31,8 @@ struct PredictArgs {
     unsigned long long* amax;  // per-tensor: [pairs][2]
 };
 void run_predict(const PredictArgs& a, cudaStream_t st);
+bool predict_fast_supported(const PredictArgs& a);
+void run_predict_fast(const PredictArgs& a, cudaStream_t st);
 
 enum SelectMode { kRowTopk = 0, kColvec = 1, kBlock = 2, kThreshold = 3 };
 

@@ -11,6 +11,8 @@
 // f64), levels = [pairs][L][KD] bf16 (exact small integers), scales f64.
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "device_common.cuh"
 #include "kernels.h"
 
@@ -187,6 +189,11 @@ void dispatch_d(const PredictArgs& a, cudaStream_t st) {
 }  // namespace
 
 void run_predict(const PredictArgs& a, cudaStream_t st) {
+    static const bool force_dfma = std::getenv("DSA_PREDICT_DFMA") != nullptr;  // A/B switch
+    if (!force_dfma && predict_fast_supported(a)) {
+        run_predict_fast(a, st);
+        return;
+    }
     if (a.bf16) dispatch_d<__nv_bfloat16>(a, st);
     else dispatch_d<float>(a, st);
 }

@@ -1,6 +1,7 @@
-"""Times each phase of the hot path with CUDA events (median of N)."""
+"""Times each phase of the hot path with CUDA events: every phase is
+enqueued `reps` times back to back between two events, so host launch
+overhead is hidden behind GPU work (device time per launch)."""
 import argparse
-import statistics
 import sys
 from pathlib import Path
 
@@ -12,7 +13,7 @@ from paper_2110_11299_b200 import load_preset, ops  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c2_vector")
 ap.add_argument("--pairs", type=int, default=0)
-ap.add_argument("--reps", type=int, default=10)
+ap.add_argument("--reps", type=int, default=20)
 a = ap.parse_args()
 p = load_preset(a.config)
 n = a.pairs or p.pairs
@@ -21,19 +22,20 @@ q, k, v, P = ops.generate(sub, npairs=n)
 qd, kd, vd, Pd = (t.cuda() for t in (q, k, v, P))
 ph = ops.Phases(sub, n)
 z = torch.empty_like(qd)
-ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-res = {"predict": [], "select": [], "attention": []}
-for i in range(a.reps + 2):
-    ev[0].record()
-    ph.predict(qd, kd, Pd)
-    ev[1].record()
-    ph.select()
-    ev[2].record()
-    ph.attend(qd, kd, vd, z)
-    ev[3].record()
-    ev[3].synchronize()
-    if i >= 2:
-        res["predict"].append(ev[0].elapsed_time(ev[1]))
-        res["select"].append(ev[1].elapsed_time(ev[2]))
-        res["attention"].append(ev[2].elapsed_time(ev[3]))
-print(a.config, {k_: round(statistics.median(v_), 4) for k_, v_ in res.items()}, flush=True)
+fns = {"predict": lambda: ph.predict(qd, kd, Pd), "select": ph.select,
+       "attention": lambda: ph.attend(qd, kd, vd, z)}
+for f in fns.values():  # warm up in pipeline order
+    f()
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+res = {}
+for name, f in fns.items():
+    f()
+    e0.record()
+    for _ in range(a.reps):
+        f()
+    e1.record()
+    e1.synchronize()
+    res[name] = round(e0.elapsed_time(e1) / a.reps, 4)
+res["total"] = round(sum(res.values()), 4)
+print(a.config, res, flush=True)
