@@ -291,10 +291,10 @@ def run_gpu_arm(args, p, rank, local, world):
         phase_ms[kx] = acc[kx] / reps
 
     # ---- checksums over NCCL after timing (not on the hot path)
-    import torch.distributed as dist
-    csum = torch.tensor([zd.double().sum().item(), float(zd.abs().max().item())], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(csum)
+    from paper_2110_11299_b200.shard import gather_checksums, pair_checksums
+    local_cs = pair_checksums(zd)
+    cs_all = gather_checksums(local_cs, P_ * world) if world > 1 else local_cs
+    csum = torch.stack([cs_all[:, 0].sum(), cs_all[:, 1].max()])
 
     if rank != 0:
         return
