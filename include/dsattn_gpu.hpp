@@ -1,0 +1,373 @@
+// dsattn_gpu.hpp -- C++ host mirror of the reference attention-operator API
+// over the B200 C-ABI (dsa_b200.h).  Header-only; drop it into the
+// reference tree next to P/include/dsattn/ and link libdsa_b200.so.
+//
+// Same names, value semantics and exception types as the reference:
+//   dsattn::gpu::predict              <- quantize(matmul(X,P), QuantSpec)   P/include/dsattn/predictor.hpp:31-49
+//   dsattn::gpu::predicted_topk_mask  <- predicted_topk_mask                P/include/dsattn/maskgen.hpp:14
+//   dsattn::gpu::colvec_mask          <- colvec_mask (max-pooled bands)     P/include/dsattn/maskgen.hpp:31
+//   dsattn::gpu::block_mask           <- (block extension)
+//   dsattn::gpu::threshold_mask       <- threshold_mask (causal, fixed-point softmax, O6)
+//   dsattn::gpu::sparse_attention     <- sddmm -> sparse_softmax -> spmm    P/include/dsattn/sparse.hpp:47-55
+// The GPU entry points take the per-head Q and K (the reference's mask
+// generators take the dense S~ they would otherwise materialise; here S~ is
+// computed exactly on the tensor cores and never leaves the GPU).  Status
+// codes are rethrown as ShapeError / ParamError / ConfigError / IoError
+// (P/include/dsattn/errors.hpp:9-31), so CLI exit codes are unchanged.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "dsa_b200.h"
+#include "dsattn/errors.hpp"
+#include "dsattn/mask.hpp"
+#include "dsattn/matrix.hpp"
+#include "dsattn/predictor.hpp"
+
+namespace dsattn::gpu {
+
+[[noreturn]] inline void rethrow(dsa_status s) {
+    const std::string msg = dsa_last_error();
+    switch (s) {
+        case DSA_ERR_SHAPE: throw ShapeError(msg);
+        case DSA_ERR_PARAM: throw ParamError(msg);
+        case DSA_ERR_CONFIG: throw ConfigError(msg);
+        case DSA_ERR_IO: throw IoError(msg);
+        case DSA_ERR_UNSUPPORTED: throw ParamError(msg);
+        default: throw std::runtime_error(msg);
+    }
+}
+inline void check(dsa_status s) {
+    if (s != DSA_OK) rethrow(s);
+}
+inline void check_cuda(cudaError_t e) {
+    if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
+}
+
+// RAII device allocation.
+class DeviceBuffer {
+  public:
+    DeviceBuffer() = default;
+    explicit DeviceBuffer(size_t bytes) : bytes_(bytes) {
+        if (bytes) check_cuda(cudaMalloc(&p_, bytes));
+    }
+    ~DeviceBuffer() {
+        if (p_) cudaFree(p_);
+    }
+    DeviceBuffer(const DeviceBuffer&) = delete;
+    DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+    DeviceBuffer(DeviceBuffer&& o) noexcept : p_(o.p_), bytes_(o.bytes_) {
+        o.p_ = nullptr;
+        o.bytes_ = 0;
+    }
+    DeviceBuffer& operator=(DeviceBuffer&& o) noexcept {
+        if (this != &o) {
+            if (p_) cudaFree(p_);
+            p_ = o.p_;
+            bytes_ = o.bytes_;
+            o.p_ = nullptr;
+            o.bytes_ = 0;
+        }
+        return *this;
+    }
+    void* get() const { return p_; }
+    size_t size() const { return bytes_; }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p_);
+    }
+
+  private:
+    void* p_ = nullptr;
+    size_t bytes_ = 0;
+};
+
+namespace detail {
+
+inline uint16_t bf16_bits(double x) {
+    float f = static_cast<float>(x);
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    return static_cast<uint16_t>(u >> 16);
+}
+inline bool bf16_exact(double x) {
+    const uint16_t b = bf16_bits(x);
+    uint32_t u = static_cast<uint32_t>(b) << 16;
+    float f;
+    std::memcpy(&f, &u, 4);
+    return static_cast<double>(f) == x;
+}
+
+// The device dtype that holds every value of `ms` exactly: f32 Matrices
+// -> F32; f64 Matrices of bf16 values -> BF16 (e.g. bf16 activations held in
+// double); anything else -> F32 if exact, otherwise ParamError.
+inline dsa_dtype pick_dtype(std::initializer_list<const Matrix*> ms) {
+    bool all_bf16 = true, all_f32 = true, any_f32_prec = false;
+    for (const Matrix* m : ms) {
+        any_f32_prec |= m->precision() == Precision::f32;
+        for (size_t i = 0; i < m->size(); ++i) {
+            const double x = m->data()[i];
+            all_bf16 &= bf16_exact(x);
+            all_f32 &= static_cast<double>(static_cast<float>(x)) == x;
+        }
+    }
+    if (!any_f32_prec && all_bf16) return DSA_BF16;
+    if (all_f32) return DSA_F32;
+    throw ParamError("dsattn::gpu: values are not exactly representable in bf16/f32");
+}
+
+inline DeviceBuffer upload(const Matrix& m, dsa_dtype dt) {
+    DeviceBuffer d(m.size() * (dt == DSA_BF16 ? 2 : 4));
+    if (dt == DSA_BF16) {
+        std::vector<uint16_t> h(m.size());
+        for (size_t i = 0; i < m.size(); ++i) h[i] = bf16_bits(m.data()[i]);
+        check_cuda(cudaMemcpy(d.get(), h.data(), d.size(), cudaMemcpyHostToDevice));
+    } else {
+        std::vector<float> h(m.size());
+        for (size_t i = 0; i < m.size(); ++i) h[i] = static_cast<float>(m.data()[i]);
+        check_cuda(cudaMemcpy(d.get(), h.data(), d.size(), cudaMemcpyHostToDevice));
+    }
+    return d;
+}
+
+inline dsa_config base_config(const Matrix& q, const Matrix& p, int bits, dsa_dtype dt) {
+    dsa_config c{};
+    c.batch = 1;
+    c.heads = 1;
+    c.L = static_cast<int64_t>(q.rows());
+    c.d = static_cast<int64_t>(q.cols());
+    c.k = static_cast<int64_t>(p.cols());
+    c.dtype = dt;
+    c.bits = bits;
+    c.quant_scope = DSA_QUANT_PER_TENSOR;
+    c.round_proj_f32 = (q.precision() == Precision::f32 && p.precision() == Precision::f32) ? 1 : 0;
+    c.scale = 1;
+    c.keep = 1;
+    c.vec_v = 8;
+    c.block = 32;
+    c.frac_num = 1;
+    c.frac_den = 20;
+    c.cap = c.L;
+    return c;
+}
+
+struct DeviceLevels {
+    DeviceBuffer lq, lk, sq, sk;
+};
+
+inline DeviceLevels run_predict(const dsa_config& c, const Matrix& q, const Matrix& k,
+                                const Matrix& p) {
+    if (q.cols() != k.cols() || q.rows() != k.rows()) throw ShapeError("predict: Q/K shapes differ");
+    if (p.rows() != q.cols()) throw ShapeError("approx_scores: X feature dim != d");
+    const dsa_dtype dt = static_cast<dsa_dtype>(c.dtype);
+    DeviceBuffer dq = upload(q, dt), dk = upload(k, dt);
+    std::vector<float> hp(p.size());
+    for (size_t i = 0; i < p.size(); ++i) hp[i] = static_cast<float>(p.data()[i]);
+    DeviceBuffer dp(hp.size() * 4);
+    check_cuda(cudaMemcpy(dp.get(), hp.data(), dp.size(), cudaMemcpyHostToDevice));
+    DeviceLevels lv;
+    lv.lq = DeviceBuffer(c.L * c.k * 2);
+    lv.lk = DeviceBuffer(c.L * c.k * 2);
+    const size_t ns = c.quant_scope == DSA_QUANT_PER_ROW ? c.L : 1;
+    lv.sq = DeviceBuffer(ns * 8);
+    lv.sk = DeviceBuffer(ns * 8);
+    DeviceBuffer ws(dsa_workspace_bytes(&c));
+    check(dsa_predict(&c, dq.get(), dk.get(), dp.as<float>(), lv.lq.as<uint16_t>(), lv.lk.as<uint16_t>(),
+                      lv.sq.as<double>(), lv.sk.as<double>(), ws.get(), ws.size(), nullptr));
+    return lv;
+}
+
+inline SparseMask run_select(const dsa_config& c, const DeviceLevels& lv) {
+    const int64_t cap = dsa_mask_capacity(&c);
+    if (cap < 0) check(dsa_config_validate(&c));
+    DeviceBuffer cols(static_cast<size_t>(cap) * 4);
+    DeviceBuffer rowptr(c.mask_mode == DSA_MASK_THRESHOLD ? (c.L + 1) * 8 : 0);
+    DeviceBuffer ws(dsa_workspace_bytes(&c));
+    dsa_mask m{cols.as<uint32_t>(), rowptr.as<uint64_t>(), cap, nullptr};
+    check(dsa_select(&c, lv.lq.as<uint16_t>(), lv.lk.as<uint16_t>(), lv.sq.as<double>(), lv.sk.as<double>(),
+                     &m, ws.get(), ws.size(), nullptr));
+    std::vector<uint32_t> h(static_cast<size_t>(cap));
+    check_cuda(cudaMemcpy(h.data(), cols.get(), h.size() * 4, cudaMemcpyDeviceToHost));
+    const size_t L = static_cast<size_t>(c.L);
+    SparseMask out(L);
+    switch (c.mask_mode) {
+        case DSA_MASK_ROW_TOPK:
+            for (size_t i = 0; i < L; ++i) out.kept[i].assign(h.begin() + i * c.keep, h.begin() + (i + 1) * c.keep);
+            break;
+        case DSA_MASK_COLVEC:
+            for (size_t i = 0; i < L; ++i) {
+                const size_t b = i / c.vec_v;
+                out.kept[i].assign(h.begin() + b * c.keep, h.begin() + (b + 1) * c.keep);
+            }
+            break;
+        case DSA_MASK_BLOCK:
+            for (size_t i = 0; i < L; ++i) {
+                const size_t ib = i / c.block;
+                for (int64_t t = 0; t < c.keep; ++t) {
+                    const size_t jb = h[ib * c.keep + t];
+                    for (size_t j = jb * c.block; j < std::min(L, (jb + 1) * c.block); ++j)
+                        out.kept[i].push_back(static_cast<uint32_t>(j));
+                }
+            }
+            break;
+        default: {
+            std::vector<uint64_t> rp(L + 1);
+            check_cuda(cudaMemcpy(rp.data(), rowptr.get(), rp.size() * 8, cudaMemcpyDeviceToHost));
+            for (size_t i = 0; i < L; ++i) out.kept[i].assign(h.begin() + rp[i], h.begin() + rp[i + 1]);
+        }
+    }
+    return out;
+}
+
+}  // namespace detail
+
+// Integer levels (held exactly in f64 Matrices) and scales of quant(Q.P),
+// quant(K.P).  Per-tensor scope is the reference's (predictor.cpp:37-41).
+struct Levels {
+    Matrix q, k;
+    std::vector<double> scale_q, scale_k;
+};
+
+inline Levels predict(const Matrix& q, const Matrix& k, const Matrix& p, QuantSpec quant,
+                      bool per_row = false) {
+    quant.validate();
+    const dsa_dtype dt = detail::pick_dtype({&q, &k});
+    dsa_config c = detail::base_config(q, p, quant.bits, dt);
+    c.quant_scope = per_row ? DSA_QUANT_PER_ROW : DSA_QUANT_PER_TENSOR;
+    check(dsa_config_validate(&c));
+    detail::DeviceLevels lv = detail::run_predict(c, q, k, p);
+    Levels out{Matrix(q.rows(), p.cols()), Matrix(k.rows(), p.cols()), {}, {}};
+    std::vector<uint16_t> h(q.rows() * p.cols());
+    for (int w = 0; w < 2; ++w) {
+        check_cuda(cudaMemcpy(h.data(), (w ? lv.lk : lv.lq).get(), h.size() * 2, cudaMemcpyDeviceToHost));
+        Matrix& m = w ? out.k : out.q;
+        for (size_t i = 0; i < h.size(); ++i) {
+            uint32_t u = static_cast<uint32_t>(h[i]) << 16;
+            float f;
+            std::memcpy(&f, &u, 4);
+            m.raw()[i] = f;
+        }
+        std::vector<double>& s = w ? out.scale_k : out.scale_q;
+        s.resize(per_row ? q.rows() : 1);
+        check_cuda(cudaMemcpy(s.data(), (w ? lv.sk : lv.sq).get(), s.size() * 8, cudaMemcpyDeviceToHost));
+    }
+    return out;
+}
+
+inline SparseMask predicted_topk_mask(const Matrix& q, const Matrix& k, const Matrix& p,
+                                      QuantSpec quant, size_t keep_per_row, bool per_row = false) {
+    quant.validate();
+    dsa_config c = detail::base_config(q, p, quant.bits, detail::pick_dtype({&q, &k}));
+    c.quant_scope = per_row ? DSA_QUANT_PER_ROW : DSA_QUANT_PER_TENSOR;
+    c.mask_mode = DSA_MASK_ROW_TOPK;
+    c.keep = static_cast<int64_t>(keep_per_row);
+    check(dsa_config_validate(&c));
+    return detail::run_select(c, detail::run_predict(c, q, k, p));
+}
+
+inline SparseMask colvec_mask(const Matrix& q, const Matrix& k, const Matrix& p, QuantSpec quant,
+                              ColVecSpec spec, size_t keep_per_band) {
+    quant.validate();
+    if (spec.orientation != VecOrientation::col)
+        throw ParamError("dsattn::gpu::colvec_mask: only column vectors (v query rows x 1 key)");
+    dsa_config c = detail::base_config(q, p, quant.bits, detail::pick_dtype({&q, &k}));
+    c.mask_mode = DSA_MASK_COLVEC;
+    c.vec_v = static_cast<int32_t>(spec.v);
+    c.keep = static_cast<int64_t>(keep_per_band);
+    check(dsa_config_validate(&c));
+    return detail::run_select(c, detail::run_predict(c, q, k, p));
+}
+
+inline SparseMask block_mask(const Matrix& q, const Matrix& k, const Matrix& p, QuantSpec quant,
+                             size_t block, size_t keep_blocks, bool force_diag) {
+    quant.validate();
+    dsa_config c = detail::base_config(q, p, quant.bits, detail::pick_dtype({&q, &k}));
+    c.mask_mode = DSA_MASK_BLOCK;
+    c.block = static_cast<int32_t>(block);
+    c.keep = static_cast<int64_t>(keep_blocks);
+    c.force_diag = force_diag ? 1 : 0;
+    check(dsa_config_validate(&c));
+    return detail::run_select(c, detail::run_predict(c, q, k, p));
+}
+
+// Keeps p~ >= frac_den / (frac_num * L) of softmax(s_q s_k S_int / sqrt(d))
+// (causal: over j <= i), at most `cap` per row; rows may be empty.
+inline SparseMask threshold_mask(const Matrix& q, const Matrix& k, const Matrix& p, QuantSpec quant,
+                                 int64_t frac_num, int64_t frac_den, size_t cap, bool causal) {
+    quant.validate();
+    dsa_config c = detail::base_config(q, p, quant.bits, detail::pick_dtype({&q, &k}));
+    c.mask_mode = DSA_MASK_THRESHOLD;
+    c.frac_num = frac_num;
+    c.frac_den = frac_den;
+    c.cap = static_cast<int64_t>(cap);
+    c.causal = causal ? 1 : 0;
+    check(dsa_config_validate(&c));
+    return detail::run_select(c, detail::run_predict(c, q, k, p));
+}
+
+// sddmm -> sparse_softmax -> spmm for one head; empty rows give zero rows
+// (flagged in *empty_rows when given).  Output precision follows V.
+inline Matrix sparse_attention(const Matrix& q, const Matrix& k, const Matrix& v,
+                               const SparseMask& mask, bool scale,
+                               std::vector<uint8_t>* empty_rows = nullptr) {
+    if (q.cols() != k.cols()) throw ShapeError("sddmm: Q/K feature dims differ");
+    if (q.rows() != mask.l || k.rows() != mask.l) throw ShapeError("sddmm: mask size != sequence length");
+    if (v.rows() != mask.l) throw ShapeError("spmm: V rows != sequence length");
+    if (v.cols() != q.cols()) throw ShapeError("dsattn::gpu: needs d_v == d_k");
+    mask.validate();
+    const dsa_dtype dt = detail::pick_dtype({&q, &k, &v});
+    dsa_config c{};
+    c.batch = c.heads = 1;
+    c.L = static_cast<int64_t>(q.rows());
+    c.d = static_cast<int64_t>(q.cols());
+    c.k = 16;
+    c.dtype = dt;
+    c.bits = 4;
+    c.mask_mode = DSA_MASK_THRESHOLD;  // general CSR layout
+    c.scale = scale ? 1 : 0;
+    c.frac_num = 1;
+    c.frac_den = 1;
+    c.cap = c.L;
+    check(dsa_config_validate(&c));
+    std::vector<uint64_t> rp(mask.l + 1, 0);
+    std::vector<uint32_t> cols;
+    for (size_t i = 0; i < mask.l; ++i) {
+        rp[i + 1] = rp[i] + mask.kept[i].size();
+        cols.insert(cols.end(), mask.kept[i].begin(), mask.kept[i].end());
+    }
+    DeviceBuffer dq = detail::upload(q, dt), dk = detail::upload(k, dt), dv = detail::upload(v, dt);
+    DeviceBuffer dz(dq.size()), drp(rp.size() * 8), dc(std::max<size_t>(cols.size(), 1) * 4), de(mask.l);
+    check_cuda(cudaMemcpy(drp.get(), rp.data(), rp.size() * 8, cudaMemcpyHostToDevice));
+    if (!cols.empty()) check_cuda(cudaMemcpy(dc.get(), cols.data(), cols.size() * 4, cudaMemcpyHostToDevice));
+    dsa_mask m{dc.as<uint32_t>(), drp.as<uint64_t>(), static_cast<int64_t>(cols.size()), de.as<uint8_t>()};
+    check(dsa_sparse_attention(&c, dq.get(), dk.get(), dv.get(), &m, dz.get(), nullptr));
+    Matrix z(mask.l, v.cols(), v.precision());
+    if (dt == DSA_BF16) {
+        std::vector<uint16_t> h(z.size());
+        check_cuda(cudaMemcpy(h.data(), dz.get(), h.size() * 2, cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < h.size(); ++i) {
+            uint32_t u = static_cast<uint32_t>(h[i]) << 16;
+            float f;
+            std::memcpy(&f, &u, 4);
+            z.raw()[i] = f;
+        }
+    } else {
+        std::vector<float> h(z.size());
+        check_cuda(cudaMemcpy(h.data(), dz.get(), h.size() * 4, cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < h.size(); ++i) z.raw()[i] = h[i];
+    }
+    z.round_to_precision();
+    if (empty_rows) {
+        empty_rows->resize(mask.l);
+        check_cuda(cudaMemcpy(empty_rows->data(), de.get(), mask.l, cudaMemcpyDeviceToHost));
+    }
+    return z;
+}
+
+}  // namespace dsattn::gpu

@@ -1,0 +1,135 @@
+// C++ drop-in checks: include/dsattn_gpu.hpp used exactly as a reference
+// caller would (reference types, value semantics, reference exceptions),
+// compared with the reference implementation linked into the same binary.
+// Built by oracle/Makefile (target shim_test) into oracle/_ref/test_shim;
+// run on a GPU by tests/test_gpu_cpp_shim.py.  Cases mirror the reference's
+// own tests (P/tests/test_linalg.cpp:97-101, test_maskgen.cpp, test_sparse.cpp).
+#include <cmath>
+#include <cstdio>
+#include <vector>
+
+#include "dsattn/linalg.hpp"
+#include "dsattn/maskgen.hpp"
+#include "dsattn/predictor.hpp"
+#include "dsattn/sparse.hpp"
+#include "dsattn_gpu.hpp"
+
+using namespace dsattn;
+
+static int g_fail = 0, g_pass = 0;
+#define CHECK(cond)                                                        \
+    do {                                                                   \
+        if (cond) {                                                        \
+            ++g_pass;                                                      \
+        } else {                                                           \
+            ++g_fail;                                                      \
+            std::printf("FAIL %s:%d  %s\n", __FILE__, __LINE__, #cond);   \
+        }                                                                  \
+    } while (0)
+
+template <class E, class F>
+static bool throws(F&& f) {
+    try {
+        f();
+    } catch (const E&) {
+        return true;
+    } catch (...) {
+        return false;
+    }
+    return false;
+}
+
+static Matrix bf16_normal(size_t r, size_t c, Rng& rng) {
+    Matrix m(r, c);
+    for (size_t i = 0; i < m.size(); ++i) {
+        float f = static_cast<float>(rng.normal());
+        uint32_t u;
+        std::memcpy(&u, &f, 4);
+        u &= 0xffff0000u;
+        std::memcpy(&f, &u, 4);
+        m.raw()[i] = f;
+    }
+    return m;
+}
+
+// Integer levels via the reference: quantize(matmul(X, P)) / s
+static Matrix ref_levels(const Matrix& x, const Matrix& p, int bits) {
+    Matrix xp = matmul(x, p);
+    Matrix qt = quantize(xp, QuantSpec{bits});
+    const double s = max_abs(xp) / ((1 << (bits - 1)) - 1);
+    Matrix lv(qt.rows(), qt.cols());
+    for (size_t i = 0; i < qt.size(); ++i) lv.raw()[i] = s == 0 ? 0 : std::lround(qt.data()[i] / s);
+    return lv;
+}
+
+int main() {
+    Rng rng(2110);
+    const size_t L = 300, d = 64, k = 16;
+    Matrix q = bf16_normal(L, d, rng), kk = bf16_normal(L, d, rng), v = bf16_normal(L, d, rng);
+    Matrix p = random_normal(d, k, 0.0, 0.25, rng, Precision::f32).as_precision(Precision::f64);
+
+    // levels == the reference's quantize (bit-exact)
+    gpu::Levels lv = gpu::predict(q, kk, p, QuantSpec{4});
+    Matrix rq = ref_levels(q, p, 4), rk = ref_levels(kk, p, 4);
+    CHECK(max_abs_diff(lv.q, rq) == 0.0);
+    CHECK(max_abs_diff(lv.k, rk) == 0.0);
+
+    // predicted_topk_mask == reference predicted_topk_mask on exact S~
+    SparseMask g = gpu::predicted_topk_mask(q, kk, p, QuantSpec{4}, 17);
+    SparseMask r = predicted_topk_mask(matmul_nt(rq, rk), 17);
+    CHECK(g == r);
+
+    // colvec (max-pooled) == reference primitives composition
+    SparseMask gc = gpu::colvec_mask(q, kk, p, QuantSpec{4}, ColVecSpec{8, VecOrientation::col}, 9);
+    {
+        Matrix s = matmul_nt(rq, rk);
+        bool ok = true;
+        for (size_t b0 = 0; b0 < L; b0 += 8) {
+            Matrix pooled(1, L);
+            for (size_t j = 0; j < L; ++j) {
+                double m = s(b0, j);
+                for (size_t i = b0 + 1; i < std::min(L, b0 + 8); ++i) m = std::max(m, s(i, j));
+                pooled.raw()[j] = m;
+            }
+            auto cols = row_topk_indices(pooled, 9)[0];
+            for (size_t i = b0; i < std::min(L, b0 + 8); ++i) ok &= gc.kept[i] == cols;
+        }
+        CHECK(ok);
+    }
+
+    // tie known answer: S row [1, 7, 4, 7] -> top-2 {1, 3} (P/tests/test_linalg.cpp:97-101)
+    {
+        Matrix q1(4, 16), k1(4, 16), eye(16, 16, Precision::f32);
+        for (size_t i = 0; i < 16; ++i) eye.set(i, i, 1.0);
+        for (size_t i = 0; i < 4; ++i) q1.set(i, 0, 1.0);
+        const double col0[4] = {1.0, 9.0, 5.0, 9.0};
+        for (size_t i = 0; i < 4; ++i) k1.set(i, 0, col0[i]);
+        SparseMask t = gpu::predicted_topk_mask(q1, k1, eye.as_precision(Precision::f64), QuantSpec{4}, 2);
+        CHECK((t.kept[0] == std::vector<uint32_t>{1, 3}));
+    }
+
+    // sparse attention vs the reference sddmm -> sparse_softmax -> spmm
+    {
+        Matrix qf = q.as_precision(Precision::f32), kf = kk.as_precision(Precision::f32),
+               vf = v.as_precision(Precision::f32);
+        Matrix zg = gpu::sparse_attention(qf, kf, vf, r, true);
+        Matrix zr = spmm(sparse_softmax(sddmm(qf, kf, r, true)), vf);
+        CHECK(max_abs_diff(zg, zr) <= 1e-5 * std::max(1.0, max_abs(zr)));
+        // empty row -> zero, flagged (P/tests/test_sparse.cpp:89-97)
+        SparseMask e = r;
+        e.kept[3].clear();
+        std::vector<uint8_t> flags;
+        Matrix ze = gpu::sparse_attention(qf, kf, vf, e, true, &flags);
+        bool zero = true;
+        for (size_t j = 0; j < d; ++j) zero &= ze(3, j) == 0.0;
+        CHECK(zero && flags[3] == 1 && flags[2] == 0);
+    }
+
+    // reference exception types (P/include/dsattn/errors.hpp)
+    CHECK(throws<ParamError>([&] { gpu::predicted_topk_mask(q, kk, p, QuantSpec{4}, 0); }));
+    CHECK(throws<ParamError>([&] { gpu::predict(q, kk, p, QuantSpec{3}); }));
+    CHECK(throws<ShapeError>([&] { gpu::sparse_attention(q, kk, Matrix(L + 1, d), r, true); }));
+
+    std::printf("shim: %d passed, %d failed\n", g_pass, g_fail);
+    return g_fail == 0 ? 0 : 1;
+}
