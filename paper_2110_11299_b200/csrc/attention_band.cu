@@ -14,6 +14,8 @@
 // reused by the band's 8 queries -- SURVEY H6); HBM sees Q, K, V, Z once.
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "device_common.cuh"
 #include "kernels.h"
 
@@ -250,6 +252,236 @@ __global__ void __launch_bounds__(kBandWarps * 32)
     }
 }
 
+// ---------------------------------------------------------------- v2
+// K fragments straight from global memory into registers: the reduction
+// order over d is permuted so each lane's slots of a k-step are 4 CONSECUTIVE
+// d values of one 32/64-byte row segment (16-byte loads, no shared memory,
+// no ldmatrix); the Q^T B-fragments use the same permutation.  One index
+// load per gathered row (lane = row, shared by shuffles).  V rows still go
+// through cp.async + XOR-swizzled shared memory for ldmatrix.trans.
+template <int D>
+struct BandSmemV2 {
+    __nv_bfloat16 v[2][32 * D];
+    __nv_bfloat16 p[8 * 40];  // [query][key], padded rows
+    __nv_bfloat16 z[8 * D];
+};
+
+template <int D>
+__device__ __forceinline__ void load_k_frag(const __nv_bfloat16* __restrict__ Kp, uint32_t idx,
+                                            int g, int c4, uint4 (&kw)[2][2][D / 64 * 2]) {
+    // two m-tiles x rows (g, g+8): this lane's D/4-wide segment [c4*D/4, ...)
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t j = __shfl_sync(0xffffffffu, idx, mt * 16 + g + h * 8);
+            const uint4* src = reinterpret_cast<const uint4*>(Kp + static_cast<int64_t>(j) * D + c4 * (D / 4));
+#pragma unroll
+            for (int v = 0; v < D / 32; ++v) kw[mt][h][v] = __ldg(src + v);
+        }
+}
+
+template <int D, int kWarps>
+__global__ void __launch_bounds__(kWarps * 32)
+    attn_band_v2_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __restrict__ K,
+                        const __nv_bfloat16* __restrict__ V, const uint32_t* __restrict__ band_cols,
+                        int64_t pairs, int64_t L, int64_t keep, int scale, __nv_bfloat16* __restrict__ Z) {
+    constexpr int CH = 32;
+    constexpr int NW = D / 32;        // uint4 per lane per K row segment (D/4 bf16)
+    extern __shared__ __align__(128) unsigned char dsm[];
+    using S = BandSmemV2<D>;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    S& sm = reinterpret_cast<S*>(dsm)[warp];
+    const int64_t nb = (L + 7) / 8;
+    const int64_t band_global = static_cast<int64_t>(blockIdx.x) * kWarps + warp;
+    if (band_global >= pairs * nb) return;
+    const int64_t pair = band_global / nb, band = band_global % nb;
+    const int64_t r0 = band * 8;
+    const __nv_bfloat16* Kp = K + pair * L * D;
+    const __nv_bfloat16* Vp = V + pair * L * D;
+    const uint32_t* cols = band_cols + (pair * nb + band) * keep;
+    const int g = lane >> 2, c4 = lane & 3;
+    constexpr int kChunks16 = D / 8;
+
+    // Q^T B-fragments (same d permutation as K): row g, segment [c4*D/4, +D/4)
+    uint32_t qw[D / 8];
+    {
+        const bool ok = r0 + g < L;
+        const uint4* src = reinterpret_cast<const uint4*>(Q + (pair * L + (ok ? r0 + g : 0)) * D + c4 * (D / 4));
+#pragma unroll
+        for (int v = 0; v < NW; ++v) {
+            const uint4 x = ok ? __ldg(src + v) : make_uint4(0, 0, 0, 0);
+            qw[4 * v + 0] = x.x;
+            qw[4 * v + 1] = x.y;
+            qw[4 * v + 2] = x.z;
+            qw[4 * v + 3] = x.w;
+        }
+    }
+    const int nchunks = static_cast<int>((keep + CH - 1) / CH);
+    auto chunk_idx = [&](int ch) -> uint32_t {
+        const int64_t p = static_cast<int64_t>(ch) * CH + lane;
+        return p < keep ? __ldg(cols + p) : 0u;
+    };
+    auto load_v = [&](int buf, uint32_t idx, int ch) {
+#pragma unroll
+        for (int t = lane; t < CH * kChunks16; t += 32) {
+            const int r = t / kChunks16, c = t % kChunks16;
+            const uint32_t j = __shfl_sync(0xffffffffu, idx, r);
+            const bool ok = static_cast<int64_t>(ch) * CH + r < keep;
+            cp_async16(smem_u32(sm.v[buf]) + swz<D>(r, c), Vp + static_cast<int64_t>(j) * D + c * 8, ok);
+        }
+    };
+    uint32_t idx = chunk_idx(0);
+    uint4 kw[2][2][NW];
+    load_k_frag<D>(Kp, idx, g, c4, kw);
+    load_v(0, idx, 0);
+    cp_async_commit();
+
+    const float sl2 = (scale ? rsqrtf(static_cast<float>(D)) : 1.f) * 1.4426950408889634f;
+    float m_run[2] = {-INFINITY, -INFINITY};
+    float l_part[2] = {0.f, 0.f};
+    float zacc[D / 16][4];
+#pragma unroll
+    for (int t = 0; t < D / 16; ++t)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) zacc[t][u] = 0.f;
+
+    for (int ch = 0; ch < nchunks; ++ch) {
+        const int buf = ch & 1;
+        // prefetch the next chunk: indices, K fragments (registers), V (cp.async)
+        uint4 kn[2][2][NW];
+        uint32_t idx_n = 0;
+        if (ch + 1 < nchunks) {
+            idx_n = chunk_idx(ch + 1);
+            load_k_frag<D>(Kp, idx_n, g, c4, kn);
+            load_v(buf ^ 1, idx_n, ch + 1);
+        }
+        cp_async_commit();
+        // ---- S^T = K_chunk . Q^T (2 m-tiles of 16 keys)
+        float s[2][4];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) s[mt][u] = 0.f;
+            const uint32_t* ka = reinterpret_cast<const uint32_t*>(kw[mt][0]);
+            const uint32_t* kb = reinterpret_cast<const uint32_t*>(kw[mt][1]);
+#pragma unroll
+            for (int ks = 0; ks < D / 16; ++ks)
+                mma16816(s[mt], ka[2 * ks], kb[2 * ks], ka[2 * ks + 1], kb[2 * ks + 1], qw[2 * ks], qw[2 * ks + 1]);
+        }
+        // ---- online softmax over keys
+        const int base = ch * CH;
+        float cmax[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int key = base + mt * 16 + g + (u >> 1) * 8;
+                const float x = key < keep ? s[mt][u] * sl2 : -INFINITY;
+                s[mt][u] = x;
+                cmax[u & 1] = fmaxf(cmax[u & 1], x);
+            }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            cmax[h] = fmaxf(cmax[h], __shfl_xor_sync(0xffffffffu, cmax[h], 4));
+            cmax[h] = fmaxf(cmax[h], __shfl_xor_sync(0xffffffffu, cmax[h], 8));
+            cmax[h] = fmaxf(cmax[h], __shfl_xor_sync(0xffffffffu, cmax[h], 16));
+        }
+        float corr[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const float mn = fmaxf(m_run[h], cmax[h]);
+            corr[h] = m_run[h] == -INFINITY ? 0.f : exp2f(m_run[h] - mn);
+            m_run[h] = mn;
+            l_part[h] *= corr[h];
+        }
+#pragma unroll
+        for (int t = 0; t < D / 16; ++t) {
+            zacc[t][0] *= corr[0];
+            zacc[t][1] *= corr[1];
+            zacc[t][2] *= corr[0];
+            zacc[t][3] *= corr[1];
+        }
+        constexpr int PW = CH + 8;
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const float pv = exp2f(s[mt][u] - m_run[u & 1]);
+                l_part[u & 1] += pv;
+                sm.p[(2 * c4 + (u & 1)) * PW + mt * 16 + g + (u >> 1) * 8] = __float2bfloat16_rn(pv);
+            }
+        cp_async_wait<1>();
+        __syncwarp();
+        // ---- Z^T += V_chunk^T . P^T
+        const uint32_t vb = smem_u32(sm.v[buf]);
+#pragma unroll
+        for (int ks = 0; ks < CH / 16; ++ks) {
+            const uint32_t b0 = *reinterpret_cast<const uint32_t*>(&sm.p[g * PW + ks * 16 + 2 * c4]);
+            const uint32_t b1 = *reinterpret_cast<const uint32_t*>(&sm.p[g * PW + ks * 16 + 8 + 2 * c4]);
+#pragma unroll
+            for (int mt = 0; mt < D / 16; ++mt) {
+                const int mi = lane >> 3;
+                const int row = ks * 16 + (mi >> 1) * 8 + (lane & 7);
+                const int chk = mt * 2 + (mi & 1);
+                uint32_t a0, a1, a2, a3;
+                ldsm_x4_t(vb + swz<D>(row, chk), a0, a1, a2, a3);
+                mma16816(zacc[mt], a0, a1, a2, a3, b0, b1);
+            }
+        }
+        __syncwarp();
+        if (ch + 1 < nchunks) {
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int v = 0; v < NW; ++v) kw[mt][h][v] = kn[mt][h][v];
+        }
+    }
+    cp_async_wait<0>();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        l_part[h] += __shfl_xor_sync(0xffffffffu, l_part[h], 4);
+        l_part[h] += __shfl_xor_sync(0xffffffffu, l_part[h], 8);
+        l_part[h] += __shfl_xor_sync(0xffffffffu, l_part[h], 16);
+    }
+    const float inv0 = l_part[0] > 0.f ? 1.f / l_part[0] : 0.f;
+    const float inv1 = l_part[1] > 0.f ? 1.f / l_part[1] : 0.f;
+#pragma unroll
+    for (int mt = 0; mt < D / 16; ++mt) {
+        const int d0 = mt * 16 + g;
+        sm.z[(2 * c4) * D + d0] = __float2bfloat16_rn(zacc[mt][0] * inv0);
+        sm.z[(2 * c4 + 1) * D + d0] = __float2bfloat16_rn(zacc[mt][1] * inv1);
+        sm.z[(2 * c4) * D + d0 + 8] = __float2bfloat16_rn(zacc[mt][2] * inv0);
+        sm.z[(2 * c4 + 1) * D + d0 + 8] = __float2bfloat16_rn(zacc[mt][3] * inv1);
+    }
+    __syncwarp();
+    for (int t = lane; t < 8 * kChunks16; t += 32) {
+        const int r = t / kChunks16, c = t % kChunks16;
+        if (r0 + r < L)
+            *reinterpret_cast<uint4*>(Z + (pair * L + r0 + r) * D + c * 8) =
+                *reinterpret_cast<const uint4*>(&sm.z[r * D + c * 8]);
+    }
+}
+
+template <int D, int kWarps>
+void launch_band_v2(const AttnArgs& a, cudaStream_t st) {
+    const int64_t nb = (a.L + 7) / 8;
+    const size_t smem = sizeof(BandSmemV2<D>) * kWarps;
+    auto kern = attn_band_v2_kernel<D, kWarps>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        attr = true;
+    }
+    const unsigned grid = static_cast<unsigned>(ceil_div_i(a.pairs * nb, kWarps));
+    kern<<<grid, kWarps * 32, smem, st>>>(
+        static_cast<const __nv_bfloat16*>(a.q), static_cast<const __nv_bfloat16*>(a.k),
+        static_cast<const __nv_bfloat16*>(a.v), a.cols, a.pairs, a.L, a.keep, a.scale,
+        static_cast<__nv_bfloat16*>(a.z));
+}
+
 template <int D, int CHUNK, int kBandWarps>
 void launch_band(const AttnArgs& a, cudaStream_t st) {
     const int64_t nb = (a.L + 7) / 8;
@@ -270,8 +502,14 @@ bool band_attention_supported(const AttnArgs& a) {
 }
 
 void run_band_attention(const AttnArgs& a, cudaStream_t st) {
-    if (a.D == 64) launch_band<64, 32, 12>(a, st);
-    else launch_band<128, 32, 6>(a, st);
+    static const bool v1 = std::getenv("DSA_BAND_V1") != nullptr;  // A/B switch
+    if (v1) {
+        if (a.D == 64) launch_band<64, 32, 12>(a, st);
+        else launch_band<128, 32, 6>(a, st);
+    } else {
+        if (a.D == 64) launch_band_v2<64, 16>(a, st);
+        else launch_band_v2<128, 8>(a, st);
+    }
     note_launch();
 }
 
