@@ -118,9 +118,12 @@ size_t dsa_workspace_bytes(const dsa_config* cfg);
 int64_t dsa_mask_capacity(const dsa_config* cfg);
 
 /* ------------------------------------------------------------ hot path */
-/* (1) projection + quantisation.  levels_q/levels_k: [pairs][L][k] integer
- * levels held exactly in bf16 (uint16 bits); scale_q/scale_k: [pairs]
- * (PER_TENSOR) or [pairs][L] (PER_ROW) doubles. */
+/* (1) projection + quantisation.  levels_q/levels_k: integer levels held
+ * exactly in bf16 (uint16 bits), chunk-planar per pair: [pairs][k/8][L][8]
+ * (element (r, c) of a pair at ((c/8)*L + r)*8 + c%8 -- a run of rows of one
+ * 8-column chunk is contiguous, which makes tensor-core tiles single bulk
+ * copies); scale_q/scale_k: [pairs] (PER_TENSOR) or [pairs][L] (PER_ROW)
+ * doubles. */
 dsa_status dsa_predict(const dsa_config* cfg, const void* q, const void* k, const float* p,
                        uint16_t* levels_q, uint16_t* levels_k, double* scale_q, double* scale_k,
                        void* workspace, size_t workspace_bytes, void* stream);

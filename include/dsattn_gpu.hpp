@@ -247,12 +247,14 @@ inline Levels predict(const Matrix& q, const Matrix& k, const Matrix& p, QuantSp
     for (int w = 0; w < 2; ++w) {
         check_cuda(cudaMemcpy(h.data(), (w ? lv.lk : lv.lq).get(), h.size() * 2, cudaMemcpyDeviceToHost));
         Matrix& m = w ? out.k : out.q;
-        for (size_t i = 0; i < h.size(); ++i) {
-            uint32_t u = static_cast<uint32_t>(h[i]) << 16;
-            float f;
-            std::memcpy(&f, &u, 4);
-            m.raw()[i] = f;
-        }
+        const size_t L = q.rows(), K = p.cols();
+        for (size_t r = 0; r < L; ++r)
+            for (size_t c = 0; c < K; ++c) {  // chunk-planar [K/8][L][8] -> row-major
+                uint32_t u = static_cast<uint32_t>(h[((c / 8) * L + r) * 8 + c % 8]) << 16;
+                float f;
+                std::memcpy(&f, &u, 4);
+                m.raw()[r * K + c] = f;
+            }
         std::vector<double>& s = w ? out.scale_k : out.scale_q;
         s.resize(per_row ? q.rows() : 1);
         check_cuda(cudaMemcpy(s.data(), (w ? lv.sk : lv.sq).get(), s.size() * 8, cudaMemcpyDeviceToHost));

@@ -23,6 +23,14 @@ __device__ __forceinline__ __nv_bfloat16 from_float<__nv_bfloat16>(float x) {
     return __float2bfloat16_rn(x);
 }
 
+// Levels layout ("chunk-planar"): per (b,h) pair [KD/8][L][8] bf16, i.e.
+// element (row r, column c) at ((c/8) * L + r) * 8 + c % 8.  A run of rows of
+// one 8-column chunk is contiguous, so a 128-row tile of the K-major
+// no-swizzle UMMA layout is KD/8 contiguous bulk copies.
+__host__ __device__ __forceinline__ int64_t lvl_index(int64_t L, int64_t r, int c) {
+    return ((static_cast<int64_t>(c >> 3) * L + r) << 3) + (c & 7);
+}
+
 // bf16 bits holding a small integer level -> int (exact for |v| <= 256).
 __device__ __forceinline__ int level_to_int(uint16_t b) {
     return static_cast<int>(__uint_as_float(static_cast<uint32_t>(b) << 16));

@@ -66,6 +66,8 @@ struct SelectArgs {
 void run_select(const SelectArgs& a, cudaStream_t st);
 size_t select_scan_tmp_bytes(int64_t n);
 bool colvec_tc_supported(const SelectArgs& a);
+bool colvec_ws_supported(const SelectArgs& a);
+void run_colvec_ws(const SelectArgs& a, cudaStream_t st);
 void run_colvec_tc(const SelectArgs& a, cudaStream_t st);
 
 struct AttnArgs {

@@ -110,7 +110,7 @@ __global__ void quantize_tensor_kernel(const double* __restrict__ x,
             r = round_half_away(xs[i] / s);
             r = fmin(fmax(r, -qmax), qmax);
         }
-        out[i] = level_bits(r);
+        out[lvl_index(L, i / KD, static_cast<int>(i % KD))] = level_bits(r);
     }
 }
 
@@ -134,12 +134,12 @@ __global__ void __launch_bounds__(kRowsPerCta)
 #pragma unroll
     for (int j = 0; j < KD; ++j) am = fmax(am, fabs(acc[j]));
     const double s = am / qmax;
-    uint16_t* o = (which ? lk : lq) + (pair * L + row) * KD;
+    uint16_t* o = (which ? lk : lq) + pair * L * KD;
 #pragma unroll
     for (int j = 0; j < KD; ++j) {
         double r = 0.0;
         if (am != 0.0) r = fmin(fmax(round_half_away(acc[j] / s), -qmax), qmax);
-        o[j] = level_bits(r);
+        o[lvl_index(L, row, j)] = level_bits(r);
     }
     (which ? sk : sq)[pair * L + row] = am == 0.0 ? 0.0 : s;
 }

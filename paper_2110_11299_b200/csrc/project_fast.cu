@@ -184,8 +184,8 @@ template <class T, int D, int KD>
 __device__ __forceinline__ void quantize_group(const float* xv, float abs_e_row, const float* pn,
                                                double amax, float inv_s, double s, double qmax,
                                                const T* __restrict__ row, const double* pd, int c,
-                                               int round_f32, uint16_t* __restrict__ out_row,
-                                               bool valid) {
+                                               int round_f32, uint16_t* __restrict__ out_pair,
+                                               int64_t L, int64_t r_out, bool valid) {
     uint32_t w[KD / 8];
 #pragma unroll
     for (int nt = 0; nt < KD / 8; ++nt) {
@@ -210,7 +210,7 @@ __device__ __forceinline__ void quantize_group(const float* xv, float abs_e_row,
     if (valid) {
 #pragma unroll
         for (int nt = 0; nt < KD / 8; ++nt)
-            *reinterpret_cast<uint32_t*>(out_row + nt * 8 + 2 * c) = w[nt];
+            *reinterpret_cast<uint32_t*>(out_pair + lvl_index(L, r_out, nt * 8 + 2 * c)) = w[nt];
     }
 }
 
@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(kThreads)
         quantize_group<T, D, KD>(xs + (static_cast<size_t>(gi) * 32 + lane) * (KD / 4),
                                  re[gi * 8 + g], pn, amax[w], inv_s[w], s[w], qmax,
                                  base[w] + (valid ? r : 0) * D, pd, c, round_f32,
-                                 outp[w] + (valid ? r : 0) * KD, valid);
+                                 outp[w], L, valid ? r : 0, valid);
     }
     if (rank == 0 && tid < 2) (tid ? sk : sq)[pair] = amax[tid] == 0.0 ? 0.0 : s[tid];
     cluster.sync();  // rank 0's shared memory stays alive until every CTA is done with it
@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(kThreads)
     am = fmax(am, __shfl_xor_sync(0xffffffffu, am, 2));
     const double s = am / qmax;
     quantize_group<T, D, KD>(xf, abs_e, pn, am, static_cast<float>(qmax / am), s, qmax, row, pd, c,
-                             round_f32, (w ? lk : lq) + (pair * L + (valid ? r : 0)) * KD, valid);
+                             round_f32, (w ? lk : lq) + pair * L * KD, L, valid ? r : 0, valid);
     if (valid && c == 0) (w ? sk : sq)[pair * L + r] = am == 0.0 ? 0.0 : s;
 }
 

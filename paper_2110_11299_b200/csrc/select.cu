@@ -12,6 +12,7 @@
 // and shape; the tensor-core fast paths (select_tc.cu) take over the
 // configurations they are specialised for.
 #include <cub/cub.cuh>
+#include <cstdlib>
 #include <cuda_bf16.h>
 
 #include "device_common.cuh"
@@ -175,12 +176,13 @@ __device__ uint32_t block_emit(int n, uint32_t rem, Flags flags, uint32_t* out, 
     return base_out;
 }
 
+// row r of one pair's chunk-planar levels ([KD/8][L][8]) as floats
 template <int KD>
-__device__ __forceinline__ void load_levels(const uint16_t* __restrict__ row, float (&x)[KD]) {
-    const uint4* src = reinterpret_cast<const uint4*>(row);
+__device__ __forceinline__ void load_levels(const uint16_t* __restrict__ pairbase, int64_t L, int64_t row,
+                                            float (&x)[KD]) {
 #pragma unroll
     for (int v = 0; v < KD / 8; ++v) {
-        uint4 r = __ldg(src + v);
+        uint4 r = __ldg(reinterpret_cast<const uint4*>(pairbase + lvl_index(L, row, v * 8)));
         const uint32_t w[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -192,9 +194,10 @@ __device__ __forceinline__ void load_levels(const uint16_t* __restrict__ row, fl
 
 // Exact: |products| <= 127^2 and |sums| < 2^24, so fp32 FMA is exact.
 template <int KD>
-__device__ __forceinline__ int score_with(const float (&q)[KD], const uint16_t* __restrict__ krow) {
+__device__ __forceinline__ int score_with(const float (&q)[KD], const uint16_t* __restrict__ kbase, int64_t L,
+                                          int64_t j) {
     float kk[KD];
-    load_levels<KD>(krow, kk);
+    load_levels<KD>(kbase, L, j, kk);
     float acc = 0.f;
 #pragma unroll
     for (int t = 0; t < KD; ++t) acc = fmaf(q[t], kk[t], acc);
@@ -210,10 +213,10 @@ __global__ void __launch_bounds__(kNT) topk_rows_generic(SelectArgs a) {
     const int64_t i = blockIdx.x, pair = blockIdx.y;
     const int L = static_cast<int>(a.L);
     float q[KD];
-    load_levels<KD>(a.lq + (pair * a.L + i) * KD, q);
+    load_levels<KD>(a.lq + pair * a.L * KD, a.L, i, q);
     const uint16_t* lk = a.lk + pair * a.L * KD;
     for (int j = threadIdx.x; j < L; j += kNT) {
-        const int sc = score_with<KD>(q, lk + static_cast<int64_t>(j) * KD);
+        const int sc = score_with<KD>(q, lk, a.L, j);
         if constexpr (sizeof(KeyT) == 8)
             keys[j] = rank_key_f64(static_cast<double>(sc) * a.sk[pair * a.L + j]);
         else
@@ -243,11 +246,11 @@ __global__ void __launch_bounds__(kNT) colvec_generic(SelectArgs a) {
     const uint16_t* lq = a.lq + pair * a.L * KD;
     for (int j = threadIdx.x; j < L; j += kNT) {
         float kk[KD];
-        load_levels<KD>(lk + static_cast<int64_t>(j) * KD, kk);
+        load_levels<KD>(lk, a.L, j, kk);
         int best = INT32_MIN;
         for (int64_t r = r0; r < r1; ++r) {
             float q[KD];
-            load_levels<KD>(lq + r * KD, q);
+            load_levels<KD>(lq, a.L, r, q);
             float acc = 0.f;
 #pragma unroll
             for (int t = 0; t < KD; ++t) acc = fmaf(q[t], kk[t], acc);
@@ -276,7 +279,7 @@ __global__ void pool_levels_kernel(SelectArgs a, int64_t nb) {
     const uint16_t* lv = (which ? a.lk : a.lq) + pair * a.L * a.KD;
     int acc = 0;
     for (int64_t r = blk * a.block; r < min((blk + 1) * a.block, a.L); ++r)
-        acc += level_to_int(lv[r * a.KD + t]);
+        acc += level_to_int(lv[lvl_index(a.L, r, static_cast<int>(t))]);
     a.pooled[idx] = acc;
 }
 
@@ -337,11 +340,11 @@ __global__ void __launch_bounds__(kNT) threshold_generic(SelectArgs a, uint64_t*
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n = a.causal ? static_cast<int>(i) + 1 : static_cast<int>(a.L);
     float q[KD];
-    load_levels<KD>(a.lq + (pair * a.L + i) * KD, q);
+    load_levels<KD>(a.lq + pair * a.L * KD, a.L, i, q);
     const uint16_t* lk = a.lk + pair * a.L * KD;
     int mx = INT32_MIN;
     for (int j = tid; j < n; j += kNT) {
-        const int sc = score_with<KD>(q, lk + static_cast<int64_t>(j) * KD);
+        const int sc = score_with<KD>(q, lk, a.L, j);
         keys[j] = static_cast<uint32_t>(sc);
         mx = max(mx, sc);
     }
@@ -473,6 +476,11 @@ size_t select_scan_tmp_bytes(int64_t n) {
 }
 
 void run_select(const SelectArgs& a, cudaStream_t st) {
+    static const bool ws = std::getenv("DSA_SELECT_WS") != nullptr;  // experimental warp-specialised variant
+    if (ws && colvec_ws_supported(a)) {
+        run_colvec_ws(a, st);
+        return;
+    }
     if (colvec_tc_supported(a)) {
         run_colvec_tc(a, st);
         return;

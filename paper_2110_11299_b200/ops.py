@@ -99,9 +99,15 @@ def generate(p: Preset, pair0: int = 0, npairs: int | None = None, threads: int 
 
 
 # ------------------------------------------------------------------ phases
+def levels_rows(t: torch.Tensor) -> torch.Tensor:
+    """Chunk-planar levels [pairs, k/8, L, 8] -> row-major [pairs, L, k]."""
+    pairs, kc, L, _ = t.shape
+    return t.permute(0, 2, 1, 3).reshape(pairs, L, kc * 8)
+
+
 @dataclass
 class Levels:
-    lq: torch.Tensor   # [pairs, L, k] bf16 (exact integer levels)
+    lq: torch.Tensor   # [pairs, k/8, L, 8] bf16 chunk-planar (exact integer levels)
     lk: torch.Tensor
     sq: torch.Tensor   # f64 [pairs] or [pairs, L]
     sk: torch.Tensor
@@ -142,7 +148,7 @@ def predict(p: Preset, q: torch.Tensor, k: torch.Tensor, P: torch.Tensor, stream
     _check_inputs(p, pairs, q, k)
     c = config_of(p, pairs)
     dev = q.device
-    lq = torch.empty((pairs, p.L, p.k), dtype=torch.bfloat16, device=dev)
+    lq = torch.empty((pairs, p.k // 8, p.L, 8), dtype=torch.bfloat16, device=dev)
     lk = torch.empty_like(lq)
     ns = (pairs,) if p.quant_scope == "tensor" else (pairs, p.L)
     sq = torch.empty(ns, dtype=torch.float64, device=dev)
@@ -216,7 +222,7 @@ class Phases:
         self.p, self.pairs = p, pairs
         self.cfg = config_of(p, pairs)
         self.ws = _ws(workspace_bytes(p, pairs), device)
-        self.lq = torch.empty((pairs, p.L, p.k), dtype=torch.bfloat16, device=device)
+        self.lq = torch.empty((pairs, p.k // 8, p.L, 8), dtype=torch.bfloat16, device=device)
         self.lk = torch.empty_like(self.lq)
         ns = (pairs,) if p.quant_scope == "tensor" else (pairs, p.L)
         self.sq = torch.empty(ns, dtype=torch.float64, device=device)

@@ -73,8 +73,8 @@ def test_parity(name, npairs, oracle):
     for pr in range(npairs):
         lq, sq = oracle_levels(oracle, sub, q[pr], P)
         lk, sk = oracle_levels(oracle, sub, k[pr], P)
-        glq = lv.lq[pr].float().cpu().numpy().astype(np.int32)
-        glk = lv.lk[pr].float().cpu().numpy().astype(np.int32)
+        glq = ops.levels_rows(lv.lq)[pr].float().cpu().numpy().astype(np.int32)
+        glk = ops.levels_rows(lv.lk)[pr].float().cpu().numpy().astype(np.int32)
         assert np.array_equal(glq, lq), f"{name} pair {pr}: Q levels differ"
         assert np.array_equal(glk, lk), f"{name} pair {pr}: K levels differ"
         assert np.array_equal(lv.sq[pr].cpu().numpy(), np.asarray(sq)), "scale_q differs"

@@ -45,8 +45,8 @@ def test_shape(mode, L, d, k, bits, dtype, scope, extra, oracle):
     for pr in range(npairs):
         lq, sq = oracle_levels(oracle, sub, q[pr], P)
         lk, sk = oracle_levels(oracle, sub, k_[pr], P)
-        assert np.array_equal(lv.lq[pr].float().cpu().numpy().astype(np.int32), lq)
-        assert np.array_equal(lv.lk[pr].float().cpu().numpy().astype(np.int32), lk)
+        assert np.array_equal(ops.levels_rows(lv.lq)[pr].float().cpu().numpy().astype(np.int32), lq)
+        assert np.array_equal(ops.levels_rows(lv.lk)[pr].float().cpu().numpy().astype(np.int32), lk)
         rows = oracle_mask_rows(oracle, sub, lq, lk, sq, sk)
         bad = [i for i in range(L) if not np.array_equal(rows_g[pr][i], rows[i])]
         assert not bad, f"{len(bad)} rows differ, first {bad[:4]}"
