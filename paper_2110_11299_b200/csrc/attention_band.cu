@@ -281,7 +281,10 @@ __device__ __forceinline__ void load_k_frag(const __nv_bfloat16* __restrict__ Kp
         }
 }
 
-template <int D, int kWarps>
+// BLK: block-sparse masks with 32x32 blocks -- the 8-row band's key list is
+// its block row's kept blocks, each expanding to 32 consecutive keys (one
+// 32-key chunk per kept block, so the chunk index is blocks[ch] * 32 + lane).
+template <int D, int kWarps, bool BLK>
 __global__ void __launch_bounds__(kWarps * 32)
     attn_band_v2_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __restrict__ K,
                         const __nv_bfloat16* __restrict__ V, const uint32_t* __restrict__ band_cols,
@@ -299,7 +302,9 @@ __global__ void __launch_bounds__(kWarps * 32)
     const int64_t r0 = band * 8;
     const __nv_bfloat16* Kp = K + pair * L * D;
     const __nv_bfloat16* Vp = V + pair * L * D;
-    const uint32_t* cols = band_cols + (pair * nb + band) * keep;
+    const int64_t nbr = (L + 31) / 32;
+    const uint32_t* cols = BLK ? band_cols + (pair * nbr + (r0 >> 5)) * keep : band_cols + (pair * nb + band) * keep;
+    const int64_t nkeys = BLK ? keep * 32 : keep;
     const int g = lane >> 2, c4 = lane & 3;
     constexpr int kChunks16 = D / 8;
 
@@ -317,8 +322,9 @@ __global__ void __launch_bounds__(kWarps * 32)
             qw[4 * v + 3] = x.w;
         }
     }
-    const int nchunks = static_cast<int>((keep + CH - 1) / CH);
+    const int nchunks = static_cast<int>((nkeys + CH - 1) / CH);
     auto chunk_idx = [&](int ch) -> uint32_t {
+        if (BLK) return __ldg(cols + ch) * 32u + static_cast<uint32_t>(lane);
         const int64_t p = static_cast<int64_t>(ch) * CH + lane;
         return p < keep ? __ldg(cols + p) : 0u;
     };
@@ -327,7 +333,7 @@ __global__ void __launch_bounds__(kWarps * 32)
         for (int t = lane; t < CH * kChunks16; t += 32) {
             const int r = t / kChunks16, c = t % kChunks16;
             const uint32_t j = __shfl_sync(0xffffffffu, idx, r);
-            const bool ok = static_cast<int64_t>(ch) * CH + r < keep;
+            const bool ok = static_cast<int64_t>(ch) * CH + r < nkeys;
             cp_async16(smem_u32(sm.v[buf]) + swz<D>(r, c), Vp + static_cast<int64_t>(j) * D + c * 8, ok);
         }
     };
@@ -377,7 +383,7 @@ __global__ void __launch_bounds__(kWarps * 32)
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int key = base + mt * 16 + g + (u >> 1) * 8;
-                const float x = key < keep ? s[mt][u] * sl2 : -INFINITY;
+                const float x = key < nkeys ? s[mt][u] * sl2 : -INFINITY;
                 s[mt][u] = x;
                 cmax[u & 1] = fmaxf(cmax[u & 1], x);
             }
@@ -465,11 +471,11 @@ __global__ void __launch_bounds__(kWarps * 32)
     }
 }
 
-template <int D, int kWarps>
+template <int D, int kWarps, bool BLK = false>
 void launch_band_v2(const AttnArgs& a, cudaStream_t st) {
     const int64_t nb = (a.L + 7) / 8;
     const size_t smem = sizeof(BandSmemV2<D>) * kWarps;
-    auto kern = attn_band_v2_kernel<D, kWarps>;
+    auto kern = attn_band_v2_kernel<D, kWarps, BLK>;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -498,14 +504,19 @@ void launch_band(const AttnArgs& a, cudaStream_t st) {
 }  // namespace
 
 bool band_attention_supported(const AttnArgs& a) {
-    return a.mode == kColvec && a.vec_v == 8 && a.bf16 && (a.D == 64 || a.D == 128);
+    if (!a.bf16 || (a.D != 64 && a.D != 128)) return false;
+    if (a.mode == kColvec) return a.vec_v == 8;
+    return a.mode == kBlock && a.block == 32 && a.L % 32 == 0;  // block rows = 4 bands
 }
 
 void run_band_attention(const AttnArgs& a, cudaStream_t st) {
     static const bool v1 = std::getenv("DSA_BAND_V1") != nullptr;  // A/B switch
-    if (v1) {
+    if (v1 && a.mode == kColvec) {
         if (a.D == 64) launch_band<64, 32, 12>(a, st);
         else launch_band<128, 32, 6>(a, st);
+    } else if (a.mode == kBlock) {
+        if (a.D == 64) launch_band_v2<64, 16, true>(a, st);
+        else launch_band_v2<128, 8, true>(a, st);
     } else {
         if (a.D == 64) launch_band_v2<64, 16>(a, st);
         else launch_band_v2<128, 8>(a, st);

@@ -28,6 +28,8 @@ CASES = [
     ("colvec", 640, 64, 16, 2, "bf16", "tensor", {"keep": 300, "vec_v": 8}),
     ("colvec", 300, 64, 16, 4, "f32", "tensor", {"keep": 17, "vec_v": 5}),
     ("block", 1000, 64, 16, 4, "bf16", "tensor", {"keep": 5, "block": 32, "force_diag": True}),
+    ("block", 1024, 64, 16, 4, "bf16", "tensor", {"keep": 5, "block": 32, "force_diag": True}),
+    ("block", 96, 128, 32, 4, "bf16", "tensor", {"keep": 3, "block": 32, "force_diag": False}),
     ("block", 333, 128, 32, 8, "bf16", "tensor", {"keep": 3, "block": 16, "force_diag": False}),
     ("threshold", 700, 64, 16, 4, "bf16", "tensor", {"cap": 5, "causal": True}),
     ("threshold", 513, 64, 32, 4, "f32", "tensor", {"cap": 513, "causal": False}),
