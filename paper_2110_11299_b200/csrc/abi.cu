@@ -114,7 +114,7 @@ int64_t capacity_of(const dsa_config& c) {
 
 // Workspace: [x64 | amax | pooled | etab | counts | scan | levels | scales | mask]
 struct Plan {
-    size_t x64 = 0, amax = 0, pooled = 0, etab = 0, counts = 0, scan = 0, lq = 0, lk = 0, sq = 0,
+    size_t x64 = 0, amax = 0, pooled = 0, etab = 0, counts = 0, cut = 0, scan = 0, lq = 0, lk = 0, sq = 0,
            sk = 0, cols = 0, rowptr = 0, total = 0;
     size_t scan_bytes = 0;
 };
@@ -134,6 +134,7 @@ Plan plan(const dsa_config& c, bool pipeline, bool own_mask) {
     p.pooled = take(c.mask_mode == DSA_MASK_BLOCK ? sizeof(int32_t) * P * 2 * ceil_div(c.L, c.block) * c.k : 0);
     p.etab = take(c.mask_mode == DSA_MASK_THRESHOLD ? sizeof(int64_t) * P * span_of(c) : 0);
     p.counts = take(c.mask_mode == DSA_MASK_THRESHOLD ? sizeof(uint64_t) * P * c.L : 0);
+    p.cut = take(c.mask_mode == DSA_MASK_THRESHOLD ? sizeof(int2) * P * c.L : 0);
     if (c.mask_mode == DSA_MASK_THRESHOLD) p.scan_bytes = select_scan_tmp_bytes(P * c.L);
     p.scan = take(p.scan_bytes);
     if (pipeline) {
@@ -220,6 +221,7 @@ void do_select(const dsa_config& c, const uint16_t* lq, const uint16_t* lk, cons
     a.pooled = at<int32_t>(ws, pl.pooled);
     a.etab = at<int64_t>(ws, pl.etab);
     a.counts = at<uint64_t>(ws, pl.counts);
+    a.cut = c.mask_mode == DSA_MASK_THRESHOLD ? at<int2>(ws, pl.cut) : nullptr;
     a.span = span_of(c);
     a.scan_tmp = at<void>(ws, pl.scan);
     a.scan_tmp_bytes = pl.scan_bytes;

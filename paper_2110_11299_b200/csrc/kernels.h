@@ -59,6 +59,7 @@ struct SelectArgs {
     int32_t* pooled;    // block: [pairs][2][nb][KD]
     int64_t* etab;      // threshold: [pairs][span]
     uint64_t* counts;   // threshold: [pairs*L]
+    int2* cut;          // threshold: [pairs*L] {v_cut, tie quota}
     int64_t span;
     void* scan_tmp;
     size_t scan_tmp_bytes;
@@ -69,6 +70,10 @@ bool colvec_tc_supported(const SelectArgs& a);
 bool colvec_ws_supported(const SelectArgs& a);
 void run_colvec_ws(const SelectArgs& a, cudaStream_t st);
 void run_colvec_tc(const SelectArgs& a, cudaStream_t st);
+bool threshold_tc_supported(const SelectArgs& a);
+void run_threshold_tc(const SelectArgs& a, cudaStream_t st);
+void launch_exp_table(const SelectArgs& a, cudaStream_t st);
+void scan_counts(const SelectArgs& a, cudaStream_t st);
 
 struct AttnArgs {
     int mode;

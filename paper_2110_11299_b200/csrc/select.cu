@@ -446,20 +446,15 @@ void launch_select(const SelectArgs& a, cudaStream_t st) {
             break;
         }
         case kThreshold: {
-            exp_table_kernel<<<dim3(static_cast<unsigned>(std::min<int64_t>(ceil_div_i(a.span, 256), 64)), P), 256, 0, st>>>(a);
-            note_launch();
+            launch_exp_table(a, st);
             const size_t sm = static_cast<size_t>(a.L) * 4;
             auto kern = threshold_generic<KD>;
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
-            const int64_t n = a.pairs * a.L;
-            uint64_t* counts = a.counts;
-            kern<<<dim3(static_cast<unsigned>(a.L), P), kNT, sm, st>>>(a, counts, 0);
-                note_launch();
-            cudaMemsetAsync(a.rowptr, 0, sizeof(uint64_t), st);
-            size_t tb = a.scan_tmp_bytes;
-            cub::DeviceScan::InclusiveSum(a.scan_tmp, tb, counts, a.rowptr + 1, static_cast<int64_t>(n), st);
-            kern<<<dim3(static_cast<unsigned>(a.L), P), kNT, sm, st>>>(a, counts, 1);
-                note_launch();
+            kern<<<dim3(static_cast<unsigned>(a.L), P), kNT, sm, st>>>(a, a.counts, 0);
+            note_launch();
+            scan_counts(a, st);
+            kern<<<dim3(static_cast<unsigned>(a.L), P), kNT, sm, st>>>(a, a.counts, 1);
+            note_launch();
             break;
         }
         default: throw_unsupported("unknown mask mode");
@@ -467,6 +462,19 @@ void launch_select(const SelectArgs& a, cudaStream_t st) {
 }
 
 }  // namespace
+
+void launch_exp_table(const SelectArgs& a, cudaStream_t st) {
+    exp_table_kernel<<<dim3(static_cast<unsigned>(std::min<int64_t>(ceil_div_i(a.span, 256), 64)),
+                            static_cast<unsigned>(a.pairs)), 256, 0, st>>>(a);
+    note_launch();
+}
+
+// rowptr[0] = 0, rowptr[1..] = inclusive scan of the per-row kept counts
+void scan_counts(const SelectArgs& a, cudaStream_t st) {
+    cudaMemsetAsync(a.rowptr, 0, sizeof(uint64_t), st);
+    size_t tb = a.scan_tmp_bytes;
+    cub::DeviceScan::InclusiveSum(a.scan_tmp, tb, a.counts, a.rowptr + 1, static_cast<int64_t>(a.pairs * a.L), st);
+}
 
 size_t select_scan_tmp_bytes(int64_t n) {
     size_t b = 0;
@@ -483,6 +491,10 @@ void run_select(const SelectArgs& a, cudaStream_t st) {
     }
     if (colvec_tc_supported(a)) {
         run_colvec_tc(a, st);
+        return;
+    }
+    if (threshold_tc_supported(a)) {
+        run_threshold_tc(a, st);
         return;
     }
     switch (a.KD) {

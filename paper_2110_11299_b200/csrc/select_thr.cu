@@ -1,0 +1,489 @@
+// Phase 2 fast path for threshold masks (SURVEY 8(a) O4 / maskgen.cpp:22-31):
+// tcgen05 score GEMM fused with the exact integer threshold rule.
+//
+// One CTA owns 128 query rows of one (b,h) pair; the 5th-gen tensor core
+// produces the exact integer scores
+//
+//   D[q, key] = sum_c Q~[q, c] * K~[key, c]     tcgen05.mma kind::f16, M = 128
+//                                               queries, N = 64 keys, K = 16
+//
+// into TMEM (double-buffered, 2 x 64 columns; three count / four emit CTAs
+// per SM).  Every
+// thread owns one TMEM lane = one query row, so all per-row reductions are
+// in-thread.  The rule (keep j iff E[m - s_j] * L * num >= Z * den, with
+// E[t] = rint(exp(-c t) 2^40), Z = sum_j E[m - s_j], then the `cap` highest
+// scores, ties to the lowest index; oracle dsa_oracle_mask_threshold) needs
+// the row max before anything else, so the key tiles are streamed in passes:
+//
+//   count kernel:  pass 1  row max m                          (FMNMX3)
+//                  pass 2  per-thread histogram of t = m - s over the first
+//                          kW bins (exact Z from it + direct E lookups for
+//                          the rare t >= kW with E[t] > 0)
+//                  -> t* (largest kept t, binary search on E), kept count,
+//                     cap cut and tie quota from the histogram prefix sums;
+//                     rows whose cut lies beyond kW bins run extra counting
+//                     passes (binary search on the cut) -- exact, rare
+//   scan           rowptr = exclusive scan of the kept counts (cub)
+//   emit kernel:   pass 3  keys with s > v_cut, then the first `quota` keys
+//                          with s == v_cut, in ascending key order (each
+//                          thread writes its own row's list)
+//
+// The L x L score matrix never exists in HBM; K~ tiles are the only
+// streamed operand (bulk cp.async into a 3-stage ring).
+#include <cuda_bf16.h>
+
+#include <cstdlib>
+#include <type_traits>
+
+#include "device_common.cuh"
+#include "kernels.h"
+#include "tc_sm100.cuh"
+
+namespace dsa {
+namespace {
+
+constexpr int kTQ = 128;  // query rows per CTA (UMMA M) = threads
+constexpr int kTN = 64;   // keys per tile (UMMA N)
+constexpr int kSt = 3;    // K~ tile ring
+constexpr int kW = 119;   // histogram bins per row (t = m - s in [0, kW)); 60 KB -> 3 CTAs/SM
+constexpr uint32_t kAll = 0xffffffffu;
+constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: float -> int by addition
+constexpr int kMagicBits = 0x4B400000;
+
+__device__ __forceinline__ void cp16(uint32_t dst, const void* src, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src),
+                 "r"(valid ? 16 : 0));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// K-major no-swizzle canonical layout (8-row x 16-byte cores, LBO = 128,
+// SBO = KD * 16), filled from the chunk-planar levels: consecutive threads
+// copy consecutive rows of one 8-column chunk (contiguous in HBM).
+template <int KD>
+__device__ __forceinline__ uint32_t toff(int r, int c) {
+    return static_cast<uint32_t>((r >> 3) * (KD * 16) + c * 128 + (r & 7) * 16);
+}
+template <int KD, int ROWS>
+__device__ __forceinline__ void load_rows(uint32_t sbase, const uint16_t* __restrict__ src, int64_t row0,
+                                          int64_t L, int tid) {
+    constexpr int kCh = KD / 8;
+    for (int t = tid; t < ROWS * kCh; t += kTQ) {
+        const int c = t / ROWS, r = t % ROWS;
+        const bool ok = row0 + r < L;
+        cp16(sbase + toff<KD>(r, c), src + lvl_index(L, ok ? (row0 + r) : 0, c * 8), ok);
+    }
+}
+
+__device__ __forceinline__ bool keep_rule(uint64_t e, uint64_t z, uint64_t ln, uint64_t den) {
+    const uint64_t lh = __umul64hi(e, ln), ll = e * ln;
+    const uint64_t rh = __umul64hi(z, den), rl = z * den;
+    return lh != rh ? lh > rh : ll >= rl;
+}
+
+struct ThrParams {
+    const uint16_t* lq;
+    const uint16_t* lk;
+    const int64_t* etab;  // [pairs][span]
+    int64_t span, L, cap;
+    int causal;
+    uint64_t ln, den;     // L * frac_num, frac_den
+    uint64_t* counts;     // [pairs * L]
+    int2* cut;            // [pairs * L]: {v_cut, quota}
+    uint8_t* empty_rows;
+    const uint64_t* rowptr;
+    uint32_t* cols;
+};
+
+template <int KD>
+struct ThrLayout {
+    static constexpr int kQ = kTQ * KD * 2;
+    static constexpr int kTile = kTN * KD * 2;
+    static constexpr int kHist = (kW + 1) * kTQ * 4;  // [bin][row] + trash bin: each thread its own bank
+    static constexpr int kE = kW * 8;
+    static constexpr int bytes(bool emit) { return kQ + kSt * kTile + (emit ? 0 : kHist + kE) + 64; }
+};
+
+struct PassCtx {
+    unsigned char* ring;
+    uint64_t* bars;
+    uint32_t tmem;
+    uint64_t qdesc;
+    const uint16_t* lkp;
+    int64_t L;
+    int nkt;
+    int tid, warp;
+};
+
+// Streams key tiles 0..nkt-1 through the tensor core and calls
+// f(tile, regs, col0) with 32 score columns of this thread's row.  `g`
+// counts tiles over all passes (TMEM buffer + mbarrier phase).
+template <int KD, class F>
+__device__ __forceinline__ void score_pass(const PassCtx& c, uint32_t& g, F&& f) {
+    constexpr int kTile = ThrLayout<KD>::kTile;
+    constexpr uint32_t idesc = tc::idesc_bf16_f32(kTQ, kTN);
+    for (int s = 0; s < kSt; ++s) {
+        if (s < c.nkt) load_rows<KD, kTN>(tc::smem_addr(c.ring + s * kTile), c.lkp, static_cast<int64_t>(s) * kTN, c.L, c.tid);
+        cp_commit();
+    }
+    for (int t = 0; t <= c.nkt; ++t) {
+        if (t >= 1) {
+            const uint32_t u = g + t - 1;
+            tc::mbar_wait(&c.bars[u & 1], (u >> 1) & 1);
+            tc::fence_after_sync();
+            const int nxt = t - 1 + kSt;
+            if (nxt < c.nkt)
+                load_rows<KD, kTN>(tc::smem_addr(c.ring + ((t - 1) % kSt) * kTile), c.lkp,
+                                   static_cast<int64_t>(nxt) * kTN, c.L, c.tid);
+            cp_commit();
+        }
+        if (t < c.nkt) {
+            cp_wait<kSt - 1>();
+            tc::fence_proxy_async();
+            __syncthreads();
+            if (c.tid == 0) {
+                tc::fence_after_sync();
+                const uint32_t bbase = tc::smem_addr(c.ring + (t % kSt) * kTile);
+#pragma unroll
+                for (int ks = 0; ks < KD / 16; ++ks) {
+                    const uint64_t bd = tc::desc_kmajor_nosw(bbase + ks * 256, 128, KD * 16);
+                    const uint64_t ad = c.qdesc + static_cast<uint64_t>((ks * 256) >> 4);
+                    tc::mma_bf16(c.tmem + ((g + t) & 1) * kTN, ad, bd, idesc, ks > 0);
+                }
+                tc::commit(&c.bars[(g + t) & 1]);
+            }
+        }
+        if (t >= 1) {
+            const int u = t - 1;
+            const uint32_t base = c.tmem + (static_cast<uint32_t>(c.warp * 32) << 16) + ((g + u) & 1) * kTN;
+            uint32_t r0[32], r1[32];
+            tc::ld_32x32b_x32(base, r0);
+            tc::ld_32x32b_x32(base + 32, r1);
+            tc::wait_ld();
+            f(u, r0, 0);
+            f(u, r1, 32);
+            tc::fence_before_sync();
+        }
+        __syncthreads();
+    }
+    cp_wait<0>();
+    g += static_cast<uint32_t>(c.nkt);
+}
+
+template <int KD, bool EMIT>
+__global__ void __launch_bounds__(kTQ, 3) threshold_tc_kernel(ThrParams a) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    using Ly = ThrLayout<KD>;
+    unsigned char* bq = smem;
+    unsigned char* ring = bq + Ly::kQ;
+    unsigned char* p = ring + kSt * Ly::kTile;
+    uint32_t* hist = reinterpret_cast<uint32_t*>(p);
+    uint64_t* es = reinterpret_cast<uint64_t*>(p + (EMIT ? 0 : Ly::kHist));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(p + (EMIT ? 0 : Ly::kHist + Ly::kE));
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2);
+    int* tz_s = reinterpret_cast<int*>(bars + 3);
+
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int64_t L = a.L;
+    const int nqt = static_cast<int>((L + kTQ - 1) / kTQ);
+    const int64_t q0 = static_cast<int64_t>(nqt - 1 - static_cast<int>(blockIdx.x)) * kTQ;  // heavy tiles first
+    const int64_t pair = blockIdx.y;
+    const int64_t row = q0 + tid;
+    const bool rvalid = row < L;
+    const int64_t kend = a.causal ? (q0 + kTQ < L ? q0 + kTQ : L) : L;
+    // keys up to this bound are valid for every row of the CTA
+    const int64_t kfree = a.causal ? q0 + 1 : L;
+
+    if (tid == 0) {
+        tc::mbar_init(&bars[0], 1);
+        tc::mbar_init(&bars[1], 1);
+        tc::fence_barrier_init();
+    }
+    if (warp == 0) tc::tmem_alloc<2 * kTN>(tslot);
+    const int64_t* E = a.etab + pair * a.span;
+    if (!EMIT) {
+        for (int t = tid; t < kW; t += kTQ) es[t] = t < a.span ? static_cast<uint64_t>(__ldg(E + t)) : 0ull;
+        for (int t = tid; t < (kW + 1) * kTQ; t += kTQ) hist[t] = 0u;
+        if (tid == 0) {  // tz = first t with E[t] == 0 (E is non-increasing), or span
+            int64_t lo = 0, hi = a.span;
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (__ldg(E + mid) == 0) hi = mid;
+                else lo = mid + 1;
+            }
+            *tz_s = static_cast<int>(lo);
+        }
+    }
+    load_rows<KD, kTQ>(tc::smem_addr(bq), a.lq + pair * L * KD, q0, L, tid);
+    cp_commit();
+    cp_wait<0>();
+    tc::fence_proxy_async();
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+
+    PassCtx c;
+    c.ring = ring;
+    c.bars = bars;
+    c.tmem = *tslot;
+    c.qdesc = tc::desc_kmajor_nosw(tc::smem_addr(bq), 128, KD * 16);
+    c.lkp = a.lk + pair * L * KD;
+    c.L = L;
+    c.nkt = static_cast<int>((kend + kTN - 1) / kTN);
+    c.tid = tid;
+    c.warp = warp;
+    uint32_t g = 0;
+    const int64_t gi = pair * L + row;
+
+    // valid(key) for this thread's row: key < kend and (causal: key <= row)
+    const int64_t klim = a.causal ? row + 1 : L;  // keys < klim are candidates
+
+    if (!EMIT) {
+        // ---- pass 1: row max
+        float m = -INFINITY;
+        score_pass<KD>(c, g, [&](int u, const uint32_t* r, int col0) {
+            const float* f = reinterpret_cast<const float*>(r);
+            const int64_t k0 = static_cast<int64_t>(u) * kTN + col0;
+            if (k0 + 32 <= kfree) {
+#pragma unroll
+                for (int x = 0; x < 32; x += 2) {
+                    float y;
+                    asm("max.f32 %0, %1, %2, %3;" : "=f"(y) : "f"(m), "f"(f[x]), "f"(f[x + 1]));
+                    m = y;
+                }
+            } else {
+#pragma unroll
+                for (int x = 0; x < 32; ++x)
+                    if (k0 + x < klim) m = fmaxf(m, f[x]);
+            }
+        });
+        // ---- pass 2: histogram of t = m - s (bins [0, kW)); the tail
+        // t in [kW, tz) (E[t] > 0 beyond the bins; uniform per pair, rare)
+        // adds E[t] to Z directly
+        const int tz = *tz_s;
+        const int wh = tz < kW ? tz : kW;
+        const float mb = m + kMagic;
+        uint64_t zx = 0;
+        uint32_t* hcol = hist + tid;
+        auto hist_pass = [&](auto tail_tag) {
+            constexpr bool kTail = decltype(tail_tag)::value;
+            score_pass<KD>(c, g, [&](int u, const uint32_t* r, int col0) {
+                const float* f = reinterpret_cast<const float*>(r);
+                const int64_t k0 = static_cast<int64_t>(u) * kTN + col0;
+                // branch-free: out-of-window t lands in the trash bin kW
+                auto one = [&](float v) {
+                    const int t = __float_as_int(fmaf(v, -1.0f, mb)) - kMagicBits;
+                    const bool in = static_cast<unsigned>(t) < static_cast<unsigned>(wh);
+                    if (kTail && !in && static_cast<unsigned>(t) < static_cast<unsigned>(tz))
+                        zx += static_cast<uint64_t>(__ldg(E + t));
+                    // shared-memory reduction without return value: no
+                    // load -> add -> store chain between consecutive keys
+                    atomicAdd(hcol + (in ? t : kW) * kTQ, 1u);
+                };
+                if (k0 + 32 <= kfree) {
+#pragma unroll
+                    for (int x = 0; x < 32; ++x) one(f[x]);
+                } else {
+#pragma unroll
+                    for (int x = 0; x < 32; ++x) one(k0 + x < klim ? f[x] : -INFINITY);
+                }
+            });
+        };
+        if (tz > kW) hist_pass(std::true_type{});
+        else hist_pass(std::false_type{});
+        // ---- per-row rule from the histogram
+        auto bin = [&](int t) -> uint32_t { return hcol[t * kTQ]; };
+        uint64_t Z = zx;
+        uint32_t htot = 0;
+        for (int t = 0; t < wh; ++t) {
+            const uint32_t h = bin(t);
+            Z += static_cast<uint64_t>(h) * es[t];
+            htot += h;
+        }
+        // t* = largest t with E[t] kept (E non-increasing); -1: nothing kept
+        int tstar = -1;
+        if (rvalid && keep_rule(es[0], Z, a.ln, a.den)) {
+            int lo = 0, hi = tz - 1;  // keep_rule(E[lo]) holds; E[tz] == 0 never kept
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                const uint64_t e = mid < kW ? es[mid] : static_cast<uint64_t>(__ldg(E + mid));
+                if (keep_rule(e, Z, a.ln, a.den)) lo = mid;
+                else hi = mid - 1;
+            }
+            tstar = lo;
+        }
+        const uint32_t cap = static_cast<uint32_t>(a.cap);
+        uint32_t take = 0, quota = kAll;
+        int cut = -1;  // keep t < cut, plus `quota` of t == cut (kAll: all of them)
+        int st = 0;    // 1: count(t <= t*) needed, 2: binary search for the cap cut
+        int x = 0, lo = 0, hi = 0;
+        uint32_t clo = 0;
+        if (tstar >= 0) {
+            if (tstar < kW || htot >= cap) {
+                const int lim = tstar < kW ? tstar : kW - 1;
+                uint32_t pre = 0;
+                int t = 0;
+                for (; t <= lim; ++t) {
+                    const uint32_t h = bin(t);
+                    if (pre + h >= cap) break;
+                    pre += h;
+                }
+                if (t > lim) {  // count(t <= t*) = pre <= cap... (tstar < kW here)
+                    take = pre;
+                    cut = tstar;
+                } else if (pre + bin(t) == cap && t == tstar) {
+                    take = cap;
+                    cut = tstar;
+                } else {
+                    take = cap;
+                    cut = t;
+                    quota = cap - pre;
+                }
+            } else {
+                st = 1;
+                x = tstar;
+            }
+        }
+        // rare: the cut lies beyond the histogram -> counting passes
+        while (__syncthreads_or(st != 0)) {
+            uint32_t cnt = 0;
+            score_pass<KD>(c, g, [&](int u, const uint32_t* r, int col0) {
+                if (!st) return;
+                const float* f = reinterpret_cast<const float*>(r);
+                const int64_t k0 = static_cast<int64_t>(u) * kTN + col0;
+#pragma unroll
+                for (int y = 0; y < 32; ++y) {
+                    const int t = __float_as_int(fmaf(f[y], -1.0f, mb)) - kMagicBits;
+                    cnt += (t <= x && k0 + y < klim) ? 1u : 0u;
+                }
+            });
+            if (st == 1) {
+                if (cnt <= cap) {
+                    take = cnt;
+                    cut = tstar;
+                    st = 0;
+                } else {
+                    st = 2;
+                    lo = kW - 1;
+                    clo = htot;
+                    hi = tstar;
+                }
+            } else if (st == 2) {
+                if (cnt >= cap) hi = x;
+                else {
+                    lo = x;
+                    clo = cnt;
+                }
+            }
+            if (st == 2) {
+                if (hi == lo + 1) {
+                    take = cap;
+                    cut = hi;
+                    quota = cap - clo;
+                    st = 0;
+                } else {
+                    x = (lo + hi) >> 1;
+                }
+            }
+        }
+        if (rvalid) {
+            a.counts[gi] = take;
+            // v_cut = m - cut as a score; nothing kept -> above every score
+            const int mi = __float2int_rn(m);
+            a.cut[gi] = make_int2(take == 0 ? INT32_MAX : mi - cut, static_cast<int>(quota));
+            if (a.empty_rows) a.empty_rows[gi] = take == 0;
+        }
+    } else {
+        // ---- emission: s > v_cut, then the first `quota` with s == v_cut
+        int2 ci = make_int2(INT32_MAX, 0);
+        uint32_t* out = a.cols;
+        if (rvalid) {
+            ci = a.cut[gi];
+            out += a.rowptr[gi];
+        }
+        const float vc = ci.x == INT32_MAX ? INFINITY : static_cast<float>(ci.x);
+        uint32_t quota = static_cast<uint32_t>(ci.y);
+        uint32_t n = 0;
+        score_pass<KD>(c, g, [&](int u, const uint32_t* r, int col0) {
+            const float* f = reinterpret_cast<const float*>(r);
+            const int64_t k0 = static_cast<int64_t>(u) * kTN + col0;
+            const int lim = k0 + 32 <= kfree ? 32 : static_cast<int>(klim - k0);
+            uint32_t ge = 0;
+#pragma unroll
+            for (int y = 0; y < 32; ++y) ge |= f[y] >= vc ? (1u << y) : 0u;
+            if (lim < 32) ge &= lim > 0 ? (0xffffffffu >> (32 - lim)) : 0u;
+            if (quota != kAll && ge) {  // capped row: only the first `quota` ties
+                uint32_t eq = 0;
+#pragma unroll
+                for (int y = 0; y < 32; ++y) eq |= f[y] == vc ? (1u << y) : 0u;
+                eq &= ge;
+                uint32_t keq = eq;
+                const uint32_t ne = static_cast<uint32_t>(__popc(eq));
+                if (ne > quota) {  // keep the lowest `quota` set bits
+                    keq = 0;
+                    uint32_t e = eq;
+                    for (uint32_t i = 0; i < quota; ++i) {
+                        keq |= e & (~e + 1u);
+                        e &= e - 1u;
+                    }
+                }
+                quota -= static_cast<uint32_t>(__popc(keq));
+                ge = (ge & ~eq) | keq;
+            }
+            while (ge) {
+                const int y = __ffs(ge) - 1;
+                ge &= ge - 1u;
+                out[n++] = static_cast<uint32_t>(k0 + y);
+            }
+        });
+    }
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc<2 * kTN>(c.tmem);
+}
+
+template <int KD, bool EMIT>
+void launch_thr(const ThrParams& p, int64_t pairs, cudaStream_t st) {
+    // at least 46 KB so no fifth CTA lands on an SM whose TMEM is taken
+    // (the count kernel's 64 KB histogram allows three per SM)
+    const int smem = std::max(ThrLayout<KD>::bytes(EMIT), 46 * 1024);
+    auto kern = threshold_tc_kernel<KD, EMIT>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const dim3 grid(static_cast<unsigned>(ceil_div_i(p.L, kTQ)), static_cast<unsigned>(pairs));
+    kern<<<grid, kTQ, smem, st>>>(p);
+    note_launch();
+}
+
+}  // namespace
+
+bool threshold_tc_supported(const SelectArgs& a) {
+    return a.mode == kThreshold && !a.per_row && (a.KD == 16 || a.KD == 32) && a.L < 65536 &&
+           a.cut != nullptr && std::getenv("DSA_THRESHOLD_GENERIC") == nullptr;
+}
+
+// exp table -> count kernel -> scan -> emit kernel
+void run_threshold_tc(const SelectArgs& a, cudaStream_t st) {
+    ThrParams p{};
+    p.lq = a.lq;
+    p.lk = a.lk;
+    p.etab = a.etab;
+    p.span = a.span;
+    p.L = a.L;
+    p.cap = a.cap;
+    p.causal = a.causal;
+    p.ln = static_cast<uint64_t>(a.L) * static_cast<uint64_t>(a.frac_num);
+    p.den = static_cast<uint64_t>(a.frac_den);
+    p.counts = a.counts;
+    p.cut = a.cut;
+    p.empty_rows = a.empty_rows;
+    p.rowptr = a.rowptr;
+    p.cols = a.cols;
+    launch_exp_table(a, st);
+    if (a.KD == 16) launch_thr<16, false>(p, a.pairs, st);
+    else launch_thr<32, false>(p, a.pairs, st);
+    scan_counts(a, st);
+    if (a.KD == 16) launch_thr<16, true>(p, a.pairs, st);
+    else launch_thr<32, true>(p, a.pairs, st);
+}
+
+}  // namespace dsa

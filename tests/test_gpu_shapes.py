@@ -33,6 +33,11 @@ CASES = [
     ("block", 333, 128, 32, 8, "bf16", "tensor", {"keep": 3, "block": 16, "force_diag": False}),
     ("threshold", 700, 64, 16, 4, "bf16", "tensor", {"cap": 5, "causal": True}),
     ("threshold", 513, 64, 32, 4, "f32", "tensor", {"cap": 513, "causal": False}),
+    # 8-bit levels: small exp scale c, so the cut lies beyond the 128-bin
+    # histogram of the tensor-core threshold kernel (counting-pass path)
+    ("threshold", 600, 64, 16, 8, "bf16", "tensor", {"cap": 600, "causal": False}),
+    ("threshold", 1000, 64, 16, 8, "bf16", "tensor", {"cap": 9, "causal": True}),
+    ("threshold", 384, 64, 16, 2, "bf16", "tensor", {"cap": 2, "causal": True}),
 ]
 
 
