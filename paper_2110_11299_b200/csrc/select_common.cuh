@@ -47,7 +47,7 @@ __device__ __forceinline__ uint32_t window_hist(const int16_t* __restrict__ pv, 
 // of values == T admitted.  Requires count(window) >= keep.
 template <int W>
 __device__ __forceinline__ void window_threshold(const uint32_t* h, int lo, uint32_t kk, int lane,
-                                                 int& T, uint32_t& rem) {
+                                                 int& T, uint32_t& rem, uint32_t& nT) {
     constexpr int per = W / 32;
     uint32_t c[per], local = 0;
 #pragma unroll
@@ -65,7 +65,7 @@ __device__ __forceinline__ void window_threshold(const uint32_t* h, int lo, uint
     const bool mine = excl < kk && kk <= suf;
     const int src = __ffs(__ballot_sync(0xffffffffu, mine)) - 1;
     int t = 0;
-    uint32_t r = 0;
+    uint32_t r = 0, n = 0;
     if (mine) {
         uint32_t cum = excl;
 #pragma unroll
@@ -73,12 +73,14 @@ __device__ __forceinline__ void window_threshold(const uint32_t* h, int lo, uint
             if (r == 0 && cum + c[i] >= kk) {
                 t = lo + lane * per + i;
                 r = kk - cum;
+                n = c[i];
             }
             cum += c[i];
         }
     }
     T = __shfl_sync(0xffffffffu, t, src);
     rem = __shfl_sync(0xffffffffu, r, src);
+    nT = __shfl_sync(0xffffffffu, n, src);
 }
 
 // Exact selection of one band from pooled[0..L) (int16 scores): threshold T
@@ -86,12 +88,16 @@ __device__ __forceinline__ void window_threshold(const uint32_t* h, int lo, uint
 // column first).  The keep-th largest sits a few dozen below the band max,
 // so counting starts on a 64-value window (few shared atomics), widens to
 // 512, and falls back to a binary search over the full integer range.
+// nge = count(v >= T) when known from the histogram, else UINT32_MAX.
 __device__ __forceinline__ void band_threshold(const int16_t* __restrict__ pv, int L, int keep,
                                                int bmax, int M, uint32_t* h, int lane, int& T,
-                                               uint32_t& rem) {
+                                               uint32_t& rem, uint32_t& nge) {
     const uint32_t kk = static_cast<uint32_t>(keep);
+    nge = 0xffffffffu;
     if (window_hist<64>(pv, L, bmax - 63, h, lane) >= kk) {
-        window_threshold<64>(h, bmax - 63, kk, lane, T, rem);
+        uint32_t nT;
+        window_threshold<64>(h, bmax - 63, kk, lane, T, rem, nT);
+        nge = kk - rem + nT;
         return;
     }
     const int lo = bmax - 63;
@@ -153,19 +159,57 @@ __device__ __forceinline__ unsigned vote_ballot(bool p) {
 
 // Exact top-`keep` of one band (pooled[0..Lp), padded columns INT16_MIN):
 // threshold from the windowed histogram, then one ascending pass that
-// stages kept columns in shared memory (unconditional stores; dropped lanes
-// write a trash slot) and a coalesced copy of the list to global memory.
+// stages every column with value >= T in shared memory (one ballot per 32
+// columns), a short pass over that list dropping the ties beyond `rem`
+// (lowest columns first), and the copy of the list to global memory.  When
+// the >= T set does not fit the staging list, the two-ballot emission with
+// a trash slot is used instead.
 __device__ __forceinline__ void band_select(const int16_t* __restrict__ pv, int L, int Lp, int keep,
                                             int bmax, int M, uint32_t* h, uint32_t* obuf,
                                             uint32_t* __restrict__ o, int lane) {
     int T;
-    uint32_t rem;
-    band_threshold(pv, L, keep, bmax, M, h, lane, T, rem);
+    uint32_t rem, nge;
+    band_threshold(pv, L, keep, bmax, M, h, lane, T, rem, nge);
     if (keep > kList - 32) {
         band_emit(pv, L, keep, T, rem, o, lane);
         return;
     }
     const unsigned lt = lanemask_lt();
+    if (nge <= static_cast<uint32_t>(kList)) {
+        uint32_t taken = 0;
+        for (int j0 = 0; j0 < Lp; j0 += 128) {
+            int v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = pv[j0 + u * 32 + lane];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const bool ge = v[u] >= T;
+                const unsigned b = vote_ballot(ge);
+                if (ge) obuf[taken + __popc(b & lt)] = static_cast<uint32_t>(j0 + u * 32 + lane);
+                taken += __popc(b);
+            }
+        }
+        __syncwarp();
+        if (nge == static_cast<uint32_t>(keep)) {
+            for (int i = lane; i < keep; i += 32) o[i] = obuf[i];
+        } else {  // admit only the first `rem` columns equal to T
+            uint32_t eq_seen = 0, outp = 0;
+            for (uint32_t i0 = 0; i0 < nge; i0 += 32) {
+                const uint32_t i = i0 + lane;
+                const bool valid = i < nge;
+                const uint32_t col = valid ? obuf[i] : 0u;
+                const bool eq = valid && pv[col] == T;
+                const unsigned be = vote_ballot(eq);
+                const bool kp = valid && (!eq || eq_seen + __popc(be & lt) < rem);
+                const unsigned bk = vote_ballot(kp);
+                if (kp) o[outp + __popc(bk & lt)] = col;
+                outp += __popc(bk);
+                eq_seen += __popc(be);
+            }
+        }
+        __syncwarp();
+        return;
+    }
     const uint32_t trash = static_cast<uint32_t>(kList - 32 + lane);
     uint32_t taken = 0, eq_seen = 0;
     for (int j0 = 0; j0 < Lp; j0 += 128) {
