@@ -337,10 +337,13 @@ __global__ void __launch_bounds__(kWarps * 32)
             cp_async16(smem_u32(sm.v[buf]) + swz<D>(r, c), Vp + static_cast<int64_t>(j) * D + c * 8, ok);
         }
     };
-    uint32_t idx = chunk_idx(0);
+    // indices run two chunks ahead, so chunk c+1's K/V loads never wait on
+    // its index load
+    const uint32_t idx0 = chunk_idx(0);
+    uint32_t idx_n = nchunks > 1 ? chunk_idx(1) : 0u;
     uint4 kw[2][2][NW];
-    load_k_frag<D>(Kp, idx, g, c4, kw);
-    load_v(0, idx, 0);
+    load_k_frag<D>(Kp, idx0, g, c4, kw);
+    load_v(0, idx0, 0);
     cp_async_commit();
 
     const float sl2 = (scale ? rsqrtf(static_cast<float>(D)) : 1.f) * 1.4426950408889634f;
@@ -356,12 +359,12 @@ __global__ void __launch_bounds__(kWarps * 32)
         const int buf = ch & 1;
         // prefetch the next chunk: indices, K fragments (registers), V (cp.async)
         uint4 kn[2][2][NW];
-        uint32_t idx_n = 0;
+        const uint32_t idx_nn = ch + 2 < nchunks ? chunk_idx(ch + 2) : 0u;
         if (ch + 1 < nchunks) {
-            idx_n = chunk_idx(ch + 1);
             load_k_frag<D>(Kp, idx_n, g, c4, kn);
             load_v(buf ^ 1, idx_n, ch + 1);
         }
+        idx_n = idx_nn;
         cp_async_commit();
         // ---- S^T = K_chunk . Q^T (2 m-tiles of 16 keys)
         float s[2][4];
