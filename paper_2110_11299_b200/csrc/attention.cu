@@ -68,9 +68,39 @@ __device__ __forceinline__ float dot_row(const float* qs, const T* __restrict__ 
     return acc;
 }
 
+// kPer consecutive elements of a row as floats with one vector load
+template <class T, int N>
+__device__ __forceinline__ void load_vec(const T* __restrict__ src, float (&out)[N]) {
+    constexpr int kBytes = N * static_cast<int>(sizeof(T));
+    if constexpr (kBytes == 16) {
+        const uint4 r = __ldg(reinterpret_cast<const uint4*>(src));
+        const T* e = reinterpret_cast<const T*>(&r);
+#pragma unroll
+        for (int u = 0; u < N; ++u) out[u] = to_float(e[u]);
+    } else if constexpr (kBytes == 8) {
+        const uint2 r = __ldg(reinterpret_cast<const uint2*>(src));
+        const T* e = reinterpret_cast<const T*>(&r);
+#pragma unroll
+        for (int u = 0; u < N; ++u) out[u] = to_float(e[u]);
+    } else if constexpr (kBytes == 4) {
+        const uint32_t r = __ldg(reinterpret_cast<const unsigned int*>(src));
+        const T* e = reinterpret_cast<const T*>(&r);
+#pragma unroll
+        for (int u = 0; u < N; ++u) out[u] = to_float(e[u]);
+    } else {
+#pragma unroll
+        for (int u = 0; u < N; ++u) out[u] = to_float(src[u]);
+    }
+}
+
+// One warp per query row.  Scores: lane = kept key (its K row in 16-byte
+// loads).  Output: lane = kPer CONSECUTIVE dims, so a V row is one
+// coalesced warp-wide vector read; the 32 keys of a chunk are unrolled in
+// groups of 8 so eight independent V gathers are in flight per lane.
 template <class T, int D>
 __global__ void __launch_bounds__(kWarpsPerCta * 32) attn_rows_generic(AttnArgs a) {
-    constexpr int kPer = (D + 31) / 32;  // output dims per lane
+    constexpr int kPer = D >= 32 ? D / 32 : 1;  // output dims per lane
+    constexpr int kLanes = D / kPer;            // lanes holding output dims
     __shared__ float qs[kWarpsPerCta][D];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t row_global = static_cast<int64_t>(blockIdx.x) * kWarpsPerCta + warp;
@@ -84,6 +114,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) attn_rows_generic(AttnArgs 
     __syncwarp();
     const RowList rl = row_list(a, pair, i);
     const int total = rl.count * rl.expand;
+    const int dl = lane < kLanes ? lane * kPer : 0;  // this lane's first output dim
     float m = -INFINITY, l = 0.f, acc[kPer];
 #pragma unroll
     for (int u = 0; u < kPer; ++u) acc[u] = 0.f;
@@ -103,25 +134,27 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) attn_rows_generic(AttnArgs 
 #pragma unroll
         for (int u = 0; u < kPer; ++u) acc[u] *= corr;
         m = mnew;
+        const int jj = j >= 0 ? j : 0;  // dropped keys gather row 0 with weight 0
         const int nvalid = min(32, total - p0);
-        for (int t = 0; t < nvalid; ++t) {
-            const float wt = __shfl_sync(0xffffffffu, w, t);
-            const int jt = __shfl_sync(0xffffffffu, j, t);
-            if (jt < 0) continue;
-            const T* vrow = vb + static_cast<int64_t>(jt) * D;
+        for (int t0 = 0; t0 < nvalid; t0 += 8) {
+            float vv[8][kPer], wt[8];
 #pragma unroll
-            for (int u = 0; u < kPer; ++u) {
-                const int c = lane + 32 * u;
-                if (c < D) acc[u] = fmaf(wt, to_float(vrow[c]), acc[u]);
+            for (int t = 0; t < 8; ++t) {
+                wt[t] = __shfl_sync(0xffffffffu, w, t0 + t);
+                const int jt = __shfl_sync(0xffffffffu, jj, t0 + t);
+                load_vec<T, kPer>(vb + static_cast<int64_t>(jt) * D + dl, vv[t]);
             }
+#pragma unroll
+            for (int t = 0; t < 8; ++t)
+#pragma unroll
+                for (int u = 0; u < kPer; ++u) acc[u] = fmaf(wt[t], vv[t][u], acc[u]);
         }
     }
     T* z = static_cast<T*>(a.z) + (pair * a.L + i) * D;
     const float inv = l > 0.f ? 1.f / l : 0.f;
+    if (lane < kLanes) {
 #pragma unroll
-    for (int u = 0; u < kPer; ++u) {
-        const int c = lane + 32 * u;
-        if (c < D) z[c] = from_float<T>(acc[u] * inv);
+        for (int u = 0; u < kPer; ++u) z[dl + u] = from_float<T>(acc[u] * inv);
     }
     if (lane == 0 && a.empty_rows) a.empty_rows[pair * a.L + i] = (l > 0.f) ? 0 : 1;
 }
