@@ -68,6 +68,31 @@ __device__ __forceinline__ float dot_row(const float* qs, const T* __restrict__ 
     return acc;
 }
 
+// <q_seg, k_seg> over D/4 consecutive elements (16-byte loads when possible)
+template <class T, int D>
+__device__ __forceinline__ float dot_seg(const float (&qr)[D / 4], const T* __restrict__ kseg) {
+    constexpr int N = D / 4;
+    constexpr int kBytes = N * static_cast<int>(sizeof(T));
+    float acc = 0.f;
+    if constexpr (kBytes % 16 == 0) {
+        constexpr int kVec = 16 / sizeof(T);
+        const uint4* src = reinterpret_cast<const uint4*>(kseg);
+        uint4 raw[kBytes / 16];
+#pragma unroll
+        for (int v = 0; v < kBytes / 16; ++v) raw[v] = __ldg(src + v);
+#pragma unroll
+        for (int v = 0; v < kBytes / 16; ++v) {
+            const T* e = reinterpret_cast<const T*>(&raw[v]);
+#pragma unroll
+            for (int u = 0; u < kVec; ++u) acc = fmaf(qr[v * kVec + u], to_float(e[u]), acc);
+        }
+    } else {
+#pragma unroll
+        for (int u = 0; u < N; ++u) acc = fmaf(qr[u], to_float(kseg[u]), acc);
+    }
+    return acc;
+}
+
 // kPer consecutive elements of a row as floats with one vector load
 template <class T, int N>
 __device__ __forceinline__ void load_vec(const T* __restrict__ src, float (&out)[N]) {
@@ -115,6 +140,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) attn_rows_generic(AttnArgs 
     const RowList rl = row_list(a, pair, i);
     const int total = rl.count * rl.expand;
     const int dl = lane < kLanes ? lane * kPer : 0;  // this lane's first output dim
+    float qr[D / 4];  // this lane's quarter of q (score segment)
+#pragma unroll
+    for (int u = 0; u < D / 4; ++u) qr[u] = qs[warp][(lane & 3) * (D / 4) + u];
     float m = -INFINITY, l = 0.f, acc[kPer];
 #pragma unroll
     for (int u = 0; u < kPer; ++u) acc[u] = 0.f;
@@ -126,7 +154,24 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) attn_rows_generic(AttnArgs 
                                : static_cast<int>(rl.cols[p / rl.expand]) * rl.expand + p % rl.expand;
             if (j >= a.L) j = -1;  // ragged last block
         }
-        const float s = j >= 0 ? dot_row<T, D>(qs[warp], kb + static_cast<int64_t>(j) * D) : -INFINITY;
+        // scores: four lanes per key (each a D/4 segment, 2 x 16 B for bf16
+        // D = 64), eight keys per round -> a K row is one L1 wavefront per
+        // 4 lanes instead of one per lane; reduce the quarter sums, then move
+        // key t's score to lane t
+        float s = -INFINITY;
+        const int nval = min(32, total - p0);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            if (r * 8 >= nval) break;
+            const int jr = __shfl_sync(0xffffffffu, j, r * 8 + (lane >> 2));
+            float part = 0.f;
+            if (jr >= 0) part = dot_seg<T, D>(qr, kb + static_cast<int64_t>(jr) * D + (lane & 3) * (D / 4));
+            part += __shfl_xor_sync(0xffffffffu, part, 1);
+            part += __shfl_xor_sync(0xffffffffu, part, 2);
+            const float got = __shfl_sync(0xffffffffu, part, 4 * (lane & 7));
+            if ((lane >> 3) == r) s = got;
+        }
+        if (j < 0) s = -INFINITY;
         const float mnew = fmaxf(m, warp_max(s));
         const float w = j >= 0 ? expf(s - mnew) : 0.f;
         const float corr = m == -INFINITY ? 0.f : expf(m - mnew);
@@ -135,8 +180,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) attn_rows_generic(AttnArgs 
         for (int u = 0; u < kPer; ++u) acc[u] *= corr;
         m = mnew;
         const int jj = j >= 0 ? j : 0;  // dropped keys gather row 0 with weight 0
-        const int nvalid = min(32, total - p0);
-        for (int t0 = 0; t0 < nvalid; t0 += 8) {
+        for (int t0 = 0; t0 < nval; t0 += 8) {
             float vv[8][kPer], wt[8];
 #pragma unroll
             for (int t = 0; t < 8; ++t) {
