@@ -281,37 +281,59 @@ __device__ __forceinline__ void load_k_frag(const __nv_bfloat16* __restrict__ Kp
         }
 }
 
-// BLK: block-sparse masks with 32x32 blocks -- the 8-row band's key list is
-// its block row's kept blocks, each expanding to 32 consecutive keys (one
-// 32-key chunk per kept block, so the chunk index is blocks[ch] * 32 + lane).
-template <int D, int kWarps, bool BLK>
+// MODE kBandList: COLVEC -- the warp's 8 query rows share one key list.
+// MODE kBlockList: block-sparse masks with 32x32 blocks -- the 8-row band's
+//   key list is its block row's kept blocks, each expanding to 32
+//   consecutive keys (one 32-key chunk per kept block, so the chunk index is
+//   blocks[ch] * 32 + lane).
+// MODE kRowList / kRowCsr: every query row has its own list (ROW_TOPK rows of
+//   `keep`, THRESHOLD CSR rows): one row per warp, the row's q in the first
+//   of the 8 MMA columns (the other seven are zero and ignored).
+enum BandMode { kBandList = 0, kBlockList = 1, kRowList = 2, kRowCsr = 3 };
+
+template <int D, int kWarps, int MODE>
 __global__ void __launch_bounds__(kWarps * 32)
     attn_band_v2_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __restrict__ K,
                         const __nv_bfloat16* __restrict__ V, const uint32_t* __restrict__ band_cols,
-                        int64_t pairs, int64_t L, int64_t keep, int scale, __nv_bfloat16* __restrict__ Z) {
+                        int64_t pairs, int64_t L, int64_t keep, int scale, __nv_bfloat16* __restrict__ Z,
+                        const uint64_t* __restrict__ rowptr, uint8_t* __restrict__ empty_rows) {
     constexpr int CH = 32;
     constexpr int NW = D / 32;        // uint4 per lane per K row segment (D/4 bf16)
+    constexpr bool BLK = MODE == kBlockList;
+    constexpr bool ROW = MODE == kRowList || MODE == kRowCsr;
+    constexpr int kRows = ROW ? 1 : 8;  // query rows per warp
     extern __shared__ __align__(128) unsigned char dsm[];
     using S = BandSmemV2<D>;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     S& sm = reinterpret_cast<S*>(dsm)[warp];
-    const int64_t nb = (L + 7) / 8;
+    const int64_t nb = ROW ? L : (L + 7) / 8;  // warp work items per pair
     const int64_t band_global = static_cast<int64_t>(blockIdx.x) * kWarps + warp;
     if (band_global >= pairs * nb) return;
     const int64_t pair = band_global / nb, band = band_global % nb;
-    const int64_t r0 = band * 8;
+    const int64_t r0 = band * kRows;
     const __nv_bfloat16* Kp = K + pair * L * D;
     const __nv_bfloat16* Vp = V + pair * L * D;
     const int64_t nbr = (L + 31) / 32;
-    const uint32_t* cols = BLK ? band_cols + (pair * nbr + (r0 >> 5)) * keep : band_cols + (pair * nb + band) * keep;
-    const int64_t nkeys = BLK ? keep * 32 : keep;
+    const uint32_t* cols;
+    int64_t nkeys;
+    if (MODE == kBlockList) {
+        cols = band_cols + (pair * nbr + (r0 >> 5)) * keep;
+        nkeys = keep * 32;
+    } else if (MODE == kBandList || MODE == kRowList) {
+        cols = band_cols + (pair * nb + band) * keep;
+        nkeys = keep;
+    } else {
+        const uint64_t b = rowptr[pair * L + r0];
+        cols = band_cols + b;
+        nkeys = static_cast<int64_t>(rowptr[pair * L + r0 + 1] - b);
+    }
     const int g = lane >> 2, c4 = lane & 3;
     constexpr int kChunks16 = D / 8;
 
     // Q^T B-fragments (same d permutation as K): row g, segment [c4*D/4, +D/4)
     uint32_t qw[D / 8];
     {
-        const bool ok = r0 + g < L;
+        const bool ok = g < kRows && r0 + g < L;
         const uint4* src = reinterpret_cast<const uint4*>(Q + (pair * L + (ok ? r0 + g : 0)) * D + c4 * (D / 4));
 #pragma unroll
         for (int v = 0; v < NW; ++v) {
@@ -326,7 +348,7 @@ __global__ void __launch_bounds__(kWarps * 32)
     auto chunk_idx = [&](int ch) -> uint32_t {
         if (BLK) return __ldg(cols + ch) * 32u + static_cast<uint32_t>(lane);
         const int64_t p = static_cast<int64_t>(ch) * CH + lane;
-        return p < keep ? __ldg(cols + p) : 0u;
+        return p < nkeys ? __ldg(cols + p) : 0u;
     };
     auto load_v = [&](int buf, uint32_t idx, int ch) {
 #pragma unroll
@@ -466,19 +488,20 @@ __global__ void __launch_bounds__(kWarps * 32)
         sm.z[(2 * c4 + 1) * D + d0 + 8] = __float2bfloat16_rn(zacc[mt][3] * inv1);
     }
     __syncwarp();
-    for (int t = lane; t < 8 * kChunks16; t += 32) {
+    for (int t = lane; t < kRows * kChunks16; t += 32) {
         const int r = t / kChunks16, c = t % kChunks16;
         if (r0 + r < L)
             *reinterpret_cast<uint4*>(Z + (pair * L + r0 + r) * D + c * 8) =
                 *reinterpret_cast<const uint4*>(&sm.z[r * D + c * 8]);
     }
+    if (ROW && empty_rows && lane == 0) empty_rows[pair * L + r0] = nkeys == 0;
 }
 
-template <int D, int kWarps, bool BLK = false>
+template <int D, int kWarps, int MODE = kBandList>
 void launch_band_v2(const AttnArgs& a, cudaStream_t st) {
-    const int64_t nb = (a.L + 7) / 8;
+    const int64_t nb = (MODE == kRowList || MODE == kRowCsr) ? a.L : (a.L + 7) / 8;
     const size_t smem = sizeof(BandSmemV2<D>) * kWarps;
-    auto kern = attn_band_v2_kernel<D, kWarps, BLK>;
+    auto kern = attn_band_v2_kernel<D, kWarps, MODE>;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -488,7 +511,7 @@ void launch_band_v2(const AttnArgs& a, cudaStream_t st) {
     kern<<<grid, kWarps * 32, smem, st>>>(
         static_cast<const __nv_bfloat16*>(a.q), static_cast<const __nv_bfloat16*>(a.k),
         static_cast<const __nv_bfloat16*>(a.v), a.cols, a.pairs, a.L, a.keep, a.scale,
-        static_cast<__nv_bfloat16*>(a.z));
+        static_cast<__nv_bfloat16*>(a.z), a.rowptr, a.empty_rows);
 }
 
 template <int D, int CHUNK, int kBandWarps>
@@ -508,7 +531,9 @@ void launch_band(const AttnArgs& a, cudaStream_t st) {
 
 bool band_attention_supported(const AttnArgs& a) {
     if (!a.bf16 || (a.D != 64 && a.D != 128)) return false;
+    if (std::getenv("DSA_ATTN_GENERIC") != nullptr) return false;  // A/B switch
     if (a.mode == kColvec) return a.vec_v == 8;
+    if (a.mode == kRowTopk || a.mode == kThreshold) return true;
     return a.mode == kBlock && a.block == 32 && a.L % 32 == 0;  // block rows = 4 bands
 }
 
@@ -518,8 +543,14 @@ void run_band_attention(const AttnArgs& a, cudaStream_t st) {
         if (a.D == 64) launch_band<64, 32, 12>(a, st);
         else launch_band<128, 32, 6>(a, st);
     } else if (a.mode == kBlock) {
-        if (a.D == 64) launch_band_v2<64, 16, true>(a, st);
-        else launch_band_v2<128, 8, true>(a, st);
+        if (a.D == 64) launch_band_v2<64, 16, kBlockList>(a, st);
+        else launch_band_v2<128, 8, kBlockList>(a, st);
+    } else if (a.mode == kRowTopk) {
+        if (a.D == 64) launch_band_v2<64, 16, kRowList>(a, st);
+        else launch_band_v2<128, 8, kRowList>(a, st);
+    } else if (a.mode == kThreshold) {
+        if (a.D == 64) launch_band_v2<64, 16, kRowCsr>(a, st);
+        else launch_band_v2<128, 8, kRowCsr>(a, st);
     } else {
         if (a.D == 64) launch_band_v2<64, 16>(a, st);
         else launch_band_v2<128, 8>(a, st);
