@@ -5,6 +5,7 @@
 
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -114,7 +115,7 @@ int64_t capacity_of(const dsa_config& c) {
 
 // Workspace: [x64 | amax | pooled | etab | counts | scan | levels | scales | mask]
 struct Plan {
-    size_t x64 = 0, amax = 0, pooled = 0, etab = 0, counts = 0, cut = 0, scan = 0, lq = 0, lk = 0, sq = 0,
+    size_t x64 = 0, amax = 0, pimg = 0, pooled = 0, etab = 0, counts = 0, cut = 0, scan = 0, lq = 0, lk = 0, sq = 0,
            sk = 0, cols = 0, rowptr = 0, total = 0;
     size_t scan_bytes = 0;
 };
@@ -129,8 +130,14 @@ Plan plan(const dsa_config& c, bool pipeline, bool own_mask) {
         return o;
     };
     const bool per_tensor = c.quant_scope == DSA_QUANT_PER_TENSOR;
-    p.x64 = take(per_tensor ? sizeof(double) * P * 2 * c.L * c.k : 0);
+    // the f64 projection scratch only serves the fallback kernels (f32 inputs,
+    // other d, or DSA_PREDICT_DFMA); the tensor-core path needs the P image
+    const bool tc_path = c.dtype == DSA_BF16 && (c.d == 64 || c.d == 128) && (c.k == 16 || c.k == 32);
+    const bool need_x64 = per_tensor && (!tc_path || std::getenv("DSA_PREDICT_DFMA") != nullptr ||
+                                         std::getenv("DSA_PREDICT_CLUSTER") != nullptr);
+    p.x64 = take(need_x64 ? sizeof(double) * P * 2 * c.L * c.k : 0);
     p.amax = take(per_tensor ? sizeof(unsigned long long) * P * 2 : 0);
+    p.pimg = take(per_tensor ? predict_tc_image_bytes(c.d, c.k) : 0);
     p.pooled = take(c.mask_mode == DSA_MASK_BLOCK ? sizeof(int32_t) * P * 2 * ceil_div(c.L, c.block) * c.k : 0);
     p.etab = take(c.mask_mode == DSA_MASK_THRESHOLD ? sizeof(int64_t) * P * span_of(c) : 0);
     p.counts = take(c.mask_mode == DSA_MASK_THRESHOLD ? sizeof(uint64_t) * P * c.L : 0);
@@ -183,6 +190,7 @@ void do_predict(const dsa_config& c, const void* q, const void* k, const float* 
     a.sk = sk;
     a.xws = at<double>(ws, pl.x64);
     a.amax = at<unsigned long long>(ws, pl.amax);
+    a.pimg = c.quant_scope == DSA_QUANT_PER_TENSOR ? at<unsigned char>(ws, pl.pimg) : nullptr;
     run_predict(a, st);
     check_cuda(cudaGetLastError(), "dsa_predict launch");
 }

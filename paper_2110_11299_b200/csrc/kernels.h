@@ -29,10 +29,14 @@ struct PredictArgs {
     double* sk;
     double* xws;                // per-tensor: [pairs][2][L][KD] f64 scratch
     unsigned long long* amax;  // per-tensor: [pairs][2]
+    unsigned char* pimg;       // tensor-core path: P-split operand image
 };
 void run_predict(const PredictArgs& a, cudaStream_t st);
 bool predict_fast_supported(const PredictArgs& a);
 void run_predict_fast(const PredictArgs& a, cudaStream_t st);
+bool predict_tc_supported(const PredictArgs& a);
+size_t predict_tc_image_bytes(int64_t D, int64_t KD);
+void run_predict_tc(const PredictArgs& a, cudaStream_t st);
 
 enum SelectMode { kRowTopk = 0, kColvec = 1, kBlock = 2, kThreshold = 3 };
 

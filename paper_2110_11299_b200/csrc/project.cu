@@ -190,6 +190,10 @@ void dispatch_d(const PredictArgs& a, cudaStream_t st) {
 
 void run_predict(const PredictArgs& a, cudaStream_t st) {
     static const bool force_dfma = std::getenv("DSA_PREDICT_DFMA") != nullptr;  // A/B switch
+    if (!force_dfma && predict_tc_supported(a)) {
+        run_predict_tc(a, st);
+        return;
+    }
     if (!force_dfma && predict_fast_supported(a)) {
         run_predict_fast(a, st);
         return;

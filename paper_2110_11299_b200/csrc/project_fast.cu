@@ -88,28 +88,40 @@ __device__ __forceinline__ void group_dmma(const T* __restrict__ row, bool valid
     }
 }
 
-// The Q and K rows of one 8-row group together: all loads issued first,
-// then 2 tensors x KD/8 column tiles x 2 k-halves = independent DMMA chains
-// (the k split is one more fp64 rounding, inside the bound).
+// The Q and K rows of one 8-row group together: the raw 16-byte loads are
+// issued one group ahead (group_load) so the DMMA chains of group g overlap
+// the HBM latency of group g + 1; then 2 tensors x KD/8 column tiles x 2
+// k-halves = independent DMMA chains (the k split is one more fp64
+// rounding, inside the bound).
+template <class T, int D>
+struct GroupRaw {
+    static constexpr int NV = (D / 4) / (16 / static_cast<int>(sizeof(T)));
+    uint4 v[2][NV];
+};
+
+template <class T, int D>
+__device__ __forceinline__ void group_load(const T* __restrict__ rq, const T* __restrict__ rk, bool valid, int c,
+                                           GroupRaw<T, D>& raw) {
+    constexpr int KS = D / 4;
+#pragma unroll
+    for (int v = 0; v < GroupRaw<T, D>::NV; ++v) {
+        raw.v[0][v] = valid ? __ldg(reinterpret_cast<const uint4*>(rq + c * KS) + v) : make_uint4(0, 0, 0, 0);
+        raw.v[1][v] = valid ? __ldg(reinterpret_cast<const uint4*>(rk + c * KS) + v) : make_uint4(0, 0, 0, 0);
+    }
+}
+
 template <class T, int D, int KD>
-__device__ __forceinline__ void group_dmma2(const T* __restrict__ rq, const T* __restrict__ rk,
-                                            bool valid, const double* pd, int c, int g,
+__device__ __forceinline__ void group_dmma2(const GroupRaw<T, D>& raw, const double* pd, int c, int g,
                                             double (&x)[2][KD / 4], double (&n2)[2]) {
     constexpr int KS = D / 4;
     constexpr int kVec = 16 / sizeof(T);
-    constexpr int NV = KS / kVec;
-    uint4 raw[2][NV];
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-        raw[0][v] = valid ? __ldg(reinterpret_cast<const uint4*>(rq + c * KS) + v) : make_uint4(0, 0, 0, 0);
-        raw[1][v] = valid ? __ldg(reinterpret_cast<const uint4*>(rk + c * KS) + v) : make_uint4(0, 0, 0, 0);
-    }
+    constexpr int NV = GroupRaw<T, D>::NV;
     double a[2][KS];
 #pragma unroll
     for (int w = 0; w < 2; ++w) {
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
-            const T* e = reinterpret_cast<const T*>(&raw[w][v]);
+            const T* e = reinterpret_cast<const T*>(&raw.v[w][v]);
 #pragma unroll
             for (int u = 0; u < kVec; ++u) a[w][v * kVec + u] = to_double(e[u]);
         }
@@ -246,12 +258,23 @@ __global__ void __launch_bounds__(kThreads)
 
     const T* base[2] = {q + pair * L * D, k + pair * L * D};
     float lb[2] = {0.f, 0.f};
+    GroupRaw<T, D> nxt;
+    {
+        const int64_t r = row0 + warp * 8 + g;
+        const bool ok = warp < ngroups && r < L;
+        group_load<T, D>(base[0] + (ok ? r : 0) * D, base[1] + (ok ? r : 0) * D, ok, c, nxt);
+    }
     for (int grp = warp; grp < ngroups; grp += kWarps) {
         const int64_t r = row0 + grp * 8 + g;
         const bool valid = r < L;
+        const GroupRaw<T, D> cur = nxt;
+        {
+            const int64_t rn = r + kWarps * 8;
+            const bool ok = grp + kWarps < ngroups && rn < L;
+            group_load<T, D>(base[0] + (ok ? rn : 0) * D, base[1] + (ok ? rn : 0) * D, ok, c, nxt);
+        }
         double x[2][KD / 4], n2[2];
-        group_dmma2<T, D, KD>(base[0] + (valid ? r : 0) * D, base[1] + (valid ? r : 0) * D, valid, pd,
-                              c, g, x, n2);
+        group_dmma2<T, D, KD>(cur, pd, c, g, x, n2);
 #pragma unroll
         for (int w = 0; w < 2; ++w) {
             const int gi = w * ngroups + grp;

@@ -1,0 +1,369 @@
+// Phase 1 on the 5th-gen tensor cores: projection + quantisation with levels
+// certified bit-identical to the reference's (bf16 inputs).
+//
+// The reference level is clamp(round_half_away(x64 / s)), x64 the double
+// sequential-FMA chain of the row against P (P/src/kernels/scalar.cpp:19-32)
+// and s = max|x64| / qmax over the (b,h) tensor (P/src/predictor.cpp:37-43).
+//
+//   * P (f32) is split EXACTLY into three bf16 parts P = P1 + P2 + P3 (8 + 8 +
+//     8 significant bits), so every product q * Pi is exact and
+//       x^ = X . [P1 | P2 | P3]   (tcgen05.mma kind::f16, M = 128 rows,
+//                                  N = 3 k, K = d, fp32 accumulation in TMEM)
+//     is x up to fp32 accumulation rounding: |x^ - x64| <= e with
+//       e = d 2^-22 |q| |p_j| + |x^| 2^-23 (+ one f32 ulp when the reference
+//           rounds the product through float)  -- twice the worst-case
+//     fp32 accumulation bound, so truncating adders are covered too;
+//   * amax pass: per CTA, only elements with |x^| + e >= max(|x^| - e) can
+//     hold the CTA's maximum; they are recomputed with the reference's own
+//     fp64 chain and the exact maximum is merged per tensor with an atomic
+//     max on its IEEE bits -- the global maximum's element is always a
+//     candidate of its own CTA, so no second candidate pass is needed;
+//   * quantise pass: t = x^ / s is certified when it is farther than the
+//     scaled bound from every .5 rounding boundary, else the level is
+//     recomputed exactly (a few in 10^4).
+//
+// One CTA = 128 rows of one tensor of one pair (thread = row = TMEM lane);
+// X tiles arrive by 16-byte cp.async into the K-major no-swizzle layout, the
+// P-split operand image (built once per call by psplit_kernel) by cp.async
+// from L2, one MMA batch per CTA; many CTAs per SM overlap each other's
+// loads.  Uncertified elements go to a shared list and are recomputed by the
+// whole CTA (the reference chain is sequential, so one element per thread).
+// HBM traffic: Q and K read twice (amax pass, quantise pass), levels
+// written once.
+#include <cuda_bf16.h>
+
+#include <cstdlib>
+
+#include "device_common.cuh"
+#include "kernels.h"
+#include "tc_sm100.cuh"
+
+namespace dsa {
+namespace {
+
+constexpr int kRows = 128;  // rows per CTA = threads = UMMA M
+
+__device__ __forceinline__ void cp16(uint32_t dst, const void* src, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src),
+                 "r"(valid ? 16 : 0));
+}
+
+// K-major no-swizzle canonical layout of a [rows][D] bf16 operand: 8-row x
+// 16-byte core matrices, K-adjacent cores 128 B apart (LBO), 8-row groups
+// D * 16 B apart (SBO).
+template <int D>
+__device__ __forceinline__ uint32_t opnd_off(int r, int c) {
+    return static_cast<uint32_t>((r >> 3) * (D * 16) + (c >> 3) * 128 + (r & 7) * 16 + (c & 7) * 2);
+}
+
+// the reference's fp64 chain (P read as f32 -> f64, exact), the row read
+// from the staged operand tile
+template <int D, int KD>
+__device__ __forceinline__ double ref_chain_s(const unsigned char* xa, int r, const float* __restrict__ p, int j,
+                                              int round_f32) {
+    double acc = 0.0;
+#pragma unroll 8
+    for (int t = 0; t < D; ++t) {
+        const __nv_bfloat16 xv = *reinterpret_cast<const __nv_bfloat16*>(xa + opnd_off<D>(r, t));
+        acc = fma(to_double(xv), static_cast<double>(__ldg(p + t * KD + j)), acc);
+    }
+    return round_f32 ? static_cast<double>(static_cast<float>(acc)) : acc;
+}
+
+constexpr int kMaxList = 1024;  // uncertified (row, column) entries recomputed cooperatively
+
+__device__ __forceinline__ float xbound(float x, float qp, int round_f32, float dscale) {
+    return fmaf(qp, dscale, fabsf(x) * (round_f32 ? 2.4e-7f : 1.2e-7f)) + 1e-30f;
+}
+
+// Certified level, or NaN when t = x/s may round differently from the
+// reference's (fp32 arithmetic; the margin covers the bound and the fp32
+// rounding of x * (1/s)).
+__device__ __forceinline__ float cert_level(float x, float e, float inv_s, float qmax) {
+    const float t = x * inv_s;
+    const float at = fabsf(t);
+    const float frac = at - floorf(at);
+    const float margin = fmaf(at, 1e-6f, e * inv_s * 1.001f) + 1e-30f;
+    if (fabsf(frac - 0.5f) <= margin) return __int_as_float(0x7fc00000);
+    return fminf(fmaxf(copysignf(floorf(at + 0.5f), t), -qmax), qmax);
+}
+
+template <int D, int KD>
+struct ProjSmem {
+    static constexpr int N = 3 * KD;                 // B rows: P1 | P2 | P3 columns
+    static constexpr int kX = kRows * D * 2;         // X tile
+    static constexpr int kB = N * D * 2;             // P-split image
+    static constexpr int kImg = kB + KD * 4;         // image + |p_j| (bound factors)
+    static constexpr int kLvl = kRows * KD * 2;      // staged levels [row][KD] bf16
+    static constexpr int kList = kMaxList * 4;
+    static constexpr int kMisc = 64;
+    static constexpr int bytes() { return kX + kImg + kMisc + kLvl + kList; }
+};
+
+// P -> exact three-way bf16 split in the B-operand layout + |p_j| * 1.001
+// (one CTA; the image is the same for every pair).
+template <int D, int KD>
+__global__ void psplit_kernel(const float* __restrict__ p, unsigned char* __restrict__ img) {
+    using Sm = ProjSmem<D, KD>;
+    for (int i = threadIdx.x; i < D * KD; i += blockDim.x) {
+        const int c = i / KD, j = i % KD;
+        const float v = p[i];
+        const __nv_bfloat16 b1 = __float2bfloat16_rn(v);
+        const float r1 = v - __bfloat162float(b1);
+        const __nv_bfloat16 b2 = __float2bfloat16_rn(r1);
+        const float r2 = r1 - __bfloat162float(b2);
+        const __nv_bfloat16 b3 = __float2bfloat16_rn(r2);
+        *reinterpret_cast<__nv_bfloat16*>(img + opnd_off<D>(j, c)) = b1;
+        *reinterpret_cast<__nv_bfloat16*>(img + opnd_off<D>(KD + j, c)) = b2;
+        *reinterpret_cast<__nv_bfloat16*>(img + opnd_off<D>(2 * KD + j, c)) = b3;
+    }
+    if (threadIdx.x < KD) {
+        double s2 = 0.0;
+        for (int u = 0; u < D; ++u) {
+            const double v = static_cast<double>(p[u * KD + threadIdx.x]);
+            s2 = fma(v, v, s2);
+        }
+        reinterpret_cast<float*>(img + Sm::kB)[threadIdx.x] = static_cast<float>(sqrt(s2) * 1.001);
+    }
+}
+
+// QUANT = false: exact per-tensor amax (atomic max into amax[pair][2]).
+// QUANT = true : levels (chunk-planar) + scales from the exact amax.
+// grid = (row tiles, 2 tensors, pairs)
+template <int D, int KD, bool QUANT>
+__global__ void __launch_bounds__(kRows)
+    project_tc_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k,
+                      const float* __restrict__ p, const unsigned char* __restrict__ img, int64_t L,
+                      int round_f32, double qmax, unsigned long long* __restrict__ amax,
+                      uint16_t* __restrict__ lq, uint16_t* __restrict__ lk, double* __restrict__ sq,
+                      double* __restrict__ sk) {
+    using Sm = ProjSmem<D, KD>;
+    constexpr int N = Sm::N;
+    constexpr int TC = N <= 64 ? 64 : 128;  // TMEM columns
+    extern __shared__ __align__(1024) unsigned char smem[];
+    unsigned char* xa = smem;
+    unsigned char* pb = smem + Sm::kX;
+    const float* pn = reinterpret_cast<const float*>(pb + Sm::kB);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(pb + Sm::kImg);
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
+    unsigned int* red_f = tslot + 1;                                   // CTA max(|x| - e), float bits
+    unsigned long long* red_d = reinterpret_cast<unsigned long long*>(bar + 3);  // CTA exact max
+    unsigned int* lcount = reinterpret_cast<unsigned int*>(bar + 4);
+    uint16_t* lvl_s = reinterpret_cast<uint16_t*>(pb + Sm::kImg + Sm::kMisc);
+    uint32_t* list = reinterpret_cast<uint32_t*>(pb + Sm::kImg + Sm::kMisc + Sm::kLvl);
+
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int which = blockIdx.y;
+    const int64_t pair = blockIdx.z;
+    const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kRows;
+    const __nv_bfloat16* X = (which ? k : q) + pair * L * D;
+
+    if (tid == 0) {
+        tc::mbar_init(bar, 1);
+        tc::fence_barrier_init();
+        *red_f = 0u;
+        *red_d = 0ull;
+        *lcount = 0u;
+    }
+    if (warp == 0) tc::tmem_alloc<TC>(tslot);
+    {
+        // X tile: 16-byte chunks, 8 consecutive threads = 8 rows of one chunk
+        constexpr int kCh = D / 8;
+        const uint32_t xs = tc::smem_addr(xa);
+        for (int i = tid; i < kRows * kCh; i += kRows) {
+            const int r7 = i & 7, ch = (i >> 3) % kCh, rg = (i >> 3) / kCh;
+            const int r = rg * 8 + r7;
+            const bool ok = row0 + r < L;
+            cp16(xs + opnd_off<D>(r, ch * 8), X + (ok ? row0 + r : 0) * D + ch * 8, ok);
+        }
+        // P-split image (+ |p_j|)
+        const uint32_t ps = tc::smem_addr(pb);
+        for (int i = tid; i < Sm::kImg / 16; i += kRows) cp16(ps + i * 16, img + i * 16, true);
+        asm volatile("cp.async.commit_group;\n");
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
+    tc::fence_proxy_async();
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tmem = *tslot;
+    if (tid == 0) {
+        constexpr uint32_t idesc = tc::idesc_bf16_f32(kRows, N);
+        const uint32_t xs = tc::smem_addr(xa), bs = tc::smem_addr(pb);
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) {
+            const uint64_t ad = tc::desc_kmajor_nosw(xs + ks * 256, 128, D * 16);
+            const uint64_t bd = tc::desc_kmajor_nosw(bs + ks * 256, 128, D * 16);
+            tc::mma_bf16(tmem, ad, bd, idesc, ks > 0);
+        }
+        tc::commit(bar);
+    }
+    // |q| of this thread's row (bound factor), from the staged tile
+    const int64_t r = row0 + tid;
+    const bool valid = r < L;
+    float nq;
+    {
+        float s2 = 0.f;
+#pragma unroll
+        for (int ch = 0; ch < D / 8; ++ch) {
+            const uint4 v = *reinterpret_cast<const uint4*>(xa + opnd_off<D>(tid, ch * 8));
+            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const float2 f = __bfloat1622float2(h[u]);
+                s2 = fmaf(f.x, f.x, fmaf(f.y, f.y, s2));
+            }
+        }
+        nq = sqrtf(s2) * 1.001f + 1e-30f;
+    }
+    const float dq = nq * (static_cast<float>(D) * 2.384185791015625e-7f);  // |q| d 2^-22
+    const float rel = round_f32 ? 2.4e-7f : 1.2e-7f;
+    tc::mbar_wait(bar, 0);
+    tc::fence_after_sync();
+    // x^_j = P1 part + (P2 part + P3 part)
+    float xv[KD];
+    {
+        const uint32_t base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+        uint32_t d0[32];
+        if constexpr (N == 48) {
+            uint32_t d1[16];
+            tc::ld_32x32b_x32(base, d0);
+            tc::ld_32x32b_x16(base + 32, d1);
+            tc::wait_ld();
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                xv[j] = __uint_as_float(d0[j]) + (__uint_as_float(d0[16 + j]) + __uint_as_float(d1[j]));
+        } else {
+            uint32_t d1[32], d2[32];
+            tc::ld_32x32b_x32(base, d0);
+            tc::ld_32x32b_x32(base + 32, d1);
+            tc::ld_32x32b_x32(base + 64, d2);
+            tc::wait_ld();
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                xv[j] = __uint_as_float(d0[j]) + (__uint_as_float(d1[j]) + __uint_as_float(d2[j]));
+        }
+    }
+    tc::fence_before_sync();
+    if (!QUANT) {
+        // e_j <= E_row = |q| d 2^-22 max_j |p_j| + rel max_j |x_j|: one bound per
+        // row keeps the candidate test to a compare per element
+        float xm = 0.f, pm = 0.f;
+#pragma unroll
+        for (int j = 0; j < KD; ++j) {
+            xm = fmaxf(xm, fabsf(xv[j]));
+            pm = fmaxf(pm, pn[j]);
+        }
+        const float er = fmaf(dq, pm, xm * rel) + 1e-30f;
+        if (valid) atomicMax(red_f, __float_as_uint(fmaxf(0.f, (xm - er) * 0.999999f)));
+        __syncthreads();
+        const float thr = __uint_as_float(*red_f) - er;  // |x_j| >= LB - E_row
+#pragma unroll
+        for (int j = 0; j < KD; ++j)
+            if (valid && fabsf(xv[j]) >= thr) {
+                const unsigned slot = atomicAdd(lcount, 1u);
+                if (slot < kMaxList) list[slot] = (static_cast<uint32_t>(tid) << 6) | j;
+                else atomicMax(red_d, static_cast<unsigned long long>(__double_as_longlong(
+                                          fabs(ref_chain_s<D, KD>(xa, tid, p, j, round_f32)))));
+            }
+        __syncthreads();
+        const unsigned n = min(*lcount, static_cast<unsigned>(kMaxList));
+        double am = 0.0;
+        for (unsigned e = tid; e < n; e += kRows)
+            am = fmax(am, fabs(ref_chain_s<D, KD>(xa, static_cast<int>(list[e] >> 6), p, list[e] & 63, round_f32)));
+        if (am > 0.0) atomicMax(red_d, static_cast<unsigned long long>(__double_as_longlong(am)));
+        __syncthreads();
+        if (tid == 0 && *red_d) atomicMax(amax + pair * 2 + which, *red_d);
+    } else {
+        const double am = __longlong_as_double(static_cast<long long>(amax[pair * 2 + which]));
+        const double s = am / qmax;
+        const float inv_s = static_cast<float>(qmax / am);
+        const float qm = static_cast<float>(qmax);
+        if (row0 == 0 && tid == 0) (which ? sk : sq)[pair] = am == 0.0 ? 0.0 : s;
+        // certified levels -> staging; the rest -> shared list, recomputed
+        // exactly by the whole CTA, then each thread writes its row
+#pragma unroll
+        for (int j = 0; j < KD; ++j) {
+            float lv = 0.f;
+            if (am != 0.0) {
+                lv = cert_level(xv[j], fmaf(dq, pn[j], fabsf(xv[j]) * rel) + 1e-30f, inv_s, qm);
+                if (lv != lv) {
+                    lv = 0.f;
+                    if (valid) {
+                        const unsigned slot = atomicAdd(lcount, 1u);
+                        if (slot < kMaxList) {
+                            list[slot] = (static_cast<uint32_t>(tid) << 6) | j;
+                        } else {
+                            const double xe = ref_chain_s<D, KD>(xa, tid, p, j, round_f32);
+                            lv = static_cast<float>(fmin(fmax(round_half_away(xe / s), -qmax), qmax));
+                        }
+                    }
+                }
+            }
+            lvl_s[tid * KD + j] = static_cast<uint16_t>(__float_as_uint(lv) >> 16);
+        }
+        __syncthreads();
+        const unsigned n = min(*lcount, static_cast<unsigned>(kMaxList));
+        for (unsigned e = tid; e < n; e += kRows) {
+            const int rr = static_cast<int>(list[e] >> 6), j = static_cast<int>(list[e] & 63);
+            const double xe = ref_chain_s<D, KD>(xa, rr, p, j, round_f32);
+            const float lv = static_cast<float>(fmin(fmax(round_half_away(xe / s), -qmax), qmax));
+            lvl_s[rr * KD + j] = static_cast<uint16_t>(__float_as_uint(lv) >> 16);
+        }
+        __syncthreads();
+        if (valid) {
+            uint16_t* out = (which ? lk : lq) + pair * L * KD;
+            const uint4* src = reinterpret_cast<const uint4*>(lvl_s + tid * KD);
+#pragma unroll
+            for (int c = 0; c < KD / 8; ++c) *reinterpret_cast<uint4*>(out + lvl_index(L, r, c * 8)) = src[c];
+        }
+    }
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc<TC>(tmem);
+}
+
+template <int D, int KD>
+void launch_tc(const PredictArgs& a, cudaStream_t st) {
+    using Sm = ProjSmem<D, KD>;
+    constexpr int TC = 3 * KD <= 64 ? 64 : 128;
+    // no more CTAs per SM than TMEM holds (512 columns)
+    const int smem = std::max(Sm::bytes(), (228 * 1024) / (512 / TC + 1) + 1024);
+    auto ka = project_tc_kernel<D, KD, false>;
+    auto kq = project_tc_kernel<D, KD, true>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr = true;
+    }
+    const auto* q = static_cast<const __nv_bfloat16*>(a.q);
+    const auto* k = static_cast<const __nv_bfloat16*>(a.k);
+    const dim3 grid(static_cast<unsigned>(ceil_div_i(a.L, kRows)), 2, static_cast<unsigned>(a.pairs));
+    psplit_kernel<D, KD><<<1, 256, 0, st>>>(a.p, a.pimg);
+    cudaMemsetAsync(a.amax, 0, sizeof(unsigned long long) * 2 * a.pairs, st);
+    ka<<<grid, kRows, smem, st>>>(q, k, a.p, a.pimg, a.L, a.round_f32, a.qmax, a.amax, a.lq, a.lk, a.sq, a.sk);
+    kq<<<grid, kRows, smem, st>>>(q, k, a.p, a.pimg, a.L, a.round_f32, a.qmax, a.amax, a.lq, a.lk, a.sq, a.sk);
+    note_launch(3);
+}
+
+}  // namespace
+
+size_t predict_tc_image_bytes(int64_t D, int64_t KD) { return static_cast<size_t>(3 * KD * D * 2 + KD * 4); }
+
+bool predict_tc_supported(const PredictArgs& a) {
+    if (!a.bf16 || a.per_row || a.pimg == nullptr) return false;
+    if (std::getenv("DSA_PREDICT_CLUSTER") != nullptr) return false;  // A/B switch
+    return (a.D == 64 || a.D == 128) && (a.KD == 16 || a.KD == 32);
+}
+
+void run_predict_tc(const PredictArgs& a, cudaStream_t st) {
+    if (a.D == 64) {
+        if (a.KD == 16) launch_tc<64, 16>(a, st);
+        else launch_tc<64, 32>(a, st);
+    } else {
+        if (a.KD == 16) launch_tc<128, 16>(a, st);
+        else launch_tc<128, 32>(a, st);
+    }
+}
+
+}  // namespace dsa
