@@ -34,7 +34,9 @@ namespace {
 using namespace sel;
 
 constexpr int kMT = 128;      // keys per tile (UMMA M)
-constexpr int kStages = 4;    // K~ tile ring
+constexpr int kStages = 6;    // K~ tile ring
+constexpr int kAcc = 4;       // TMEM accumulators (tiles in flight between MMA and epilogue)
+constexpr int kLag = 2;       // MMA issue runs kLag tiles ahead of the epilogue
 constexpr int kThreads = 256;
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
@@ -91,8 +93,8 @@ __global__ void __launch_bounds__(kThreads, NQ == 64 ? 2 : 1)
     uint32_t* hist = reinterpret_cast<uint32_t*>(p); p += (kThreads / 32) * 64 * 4;
     uint32_t* obufs = reinterpret_cast<uint32_t*>(p); p += (kThreads / 32) * kList * 4;
     int* bandmax = reinterpret_cast<int*>(p);   p += 16 * 4;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(p);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(p);  // one per TMEM accumulator
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kAcc);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int quarter = warp & 3, half = warp >> 2;  // TMEM lane quarter, column half
@@ -102,12 +104,11 @@ __global__ void __launch_bounds__(kThreads, NQ == 64 ? 2 : 1)
     const uint16_t* lkp = lk + pair * L * KD;
 
     if (tid == 0) {
-        tc::mbar_init(&bars[0], 1);
-        tc::mbar_init(&bars[1], 1);
+        for (int b = 0; b < kAcc; ++b) tc::mbar_init(&bars[b], 1);
         tc::fence_barrier_init();
     }
     if (tid < NB) bandmax[tid] = INT32_MIN;
-    if (warp == 0) tc::tmem_alloc<2 * NQ>(tmem_slot);
+    if (warp == 0) tc::tmem_alloc<kAcc * NQ>(tmem_slot);
 
     // prologue: Q~ block + first kStages K~ tiles (group t <-> tile t)
     load_tile<KD, NQ>(tc::smem_addr(bq), lqp, q0, L, tid);
@@ -126,39 +127,36 @@ __global__ void __launch_bounds__(kThreads, NQ == 64 ? 2 : 1)
 #pragma unroll
     for (int i = 0; i < BPW; ++i) bmax[i] = -INFINITY;
 
-    for (int t = 0; t <= nt; ++t) {
-        if (t >= 1) {
-            tc::mbar_wait(&bars[(t - 1) & 1], ((t - 1) >> 1) & 1);
-            tc::fence_after_sync();
-            const int nxt = t - 1 + kStages;
-            if (nxt < nt)
-                load_tile<KD>(tc::smem_addr(ring + ((t - 1) % kStages) * kTile), lkp,
-                              static_cast<int64_t>(nxt) * kMT, L, tid);
-            cp_commit();
-        }
+    // Software pipeline, MMA kLag tiles ahead of the epilogue: iteration t
+    // issues the MMA of tile t (accumulator t % kAcc) and drains tile t-kLag,
+    // whose MMA finished long ago; its K~ slot is then refilled with tile
+    // t - kLag + kStages.  One __syncthreads per tile.
+    for (int t = 0; t < nt + kLag; ++t) {
         if (t < nt) {
-            cp_wait<kStages - 1>();
+            cp_wait<kStages - 1 - kLag>();
             tc::fence_proxy_async();
-            __syncthreads();
-            if (tid == 0) {
-                tc::fence_after_sync();
-                const uint32_t abase = tc::smem_addr(ring + (t % kStages) * kTile);
-#pragma unroll
-                for (int ks = 0; ks < KD / 16; ++ks) {
-                    const uint64_t ad = tc::desc_kmajor_nosw(abase + ks * 256, 128, KD * 16);
-                    const uint64_t bd = bdesc + static_cast<uint64_t>((ks * 256) >> 4);
-                    tc::mma_bf16(tmem + (t & 1) * NQ, ad, bd, idesc, ks > 0);
-                }
-                tc::commit(&bars[t & 1]);
-            }
         }
-        if (t >= 1) {
-            // epilogue of tile u = t-1: thread = key u*128 + 32*quarter + lane,
-            // query columns [64*half, 64*half + 64) = bands 8*half .. 8*half+7
-            const int u = t - 1;
+        __syncthreads();
+        if (t < nt && tid == 0) {
+            tc::fence_after_sync();
+            const uint32_t abase = tc::smem_addr(ring + (t % kStages) * kTile);
+#pragma unroll
+            for (int ks = 0; ks < KD / 16; ++ks) {
+                const uint64_t ad = tc::desc_kmajor_nosw(abase + ks * 256, 128, KD * 16);
+                const uint64_t bd = bdesc + static_cast<uint64_t>((ks * 256) >> 4);
+                tc::mma_bf16(tmem + (t % kAcc) * NQ, ad, bd, idesc, ks > 0);
+            }
+            tc::commit(&bars[t % kAcc]);
+        }
+        if (t >= kLag) {
+            const int u = t - kLag;
+            tc::mbar_wait(&bars[u % kAcc], (u / kAcc) & 1);
+            tc::fence_after_sync();
+            // epilogue of tile u: thread = key u*128 + 32*quarter + lane,
+            // query columns [CPW*half, CPW*half + CPW)
             const int key = u * kMT + quarter * 32 + lane;
             const bool kvalid = key < L;
-            const uint32_t base = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + (u & 1) * NQ + half * CPW;
+            const uint32_t base = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + (u % kAcc) * NQ + half * CPW;
             uint32_t rr[NLD][32];
 #pragma unroll
             for (int l = 0; l < NLD; ++l) tc::ld_32x32b_x32(base + l * 32, rr[l]);
@@ -185,9 +183,14 @@ __global__ void __launch_bounds__(kThreads, NQ == 64 ? 2 : 1)
                 }
             }
             tc::fence_before_sync();
+            // tile u's K~ slot is free (its MMA completed): refill it
+            const int nxt = u + kStages;
+            if (nxt < nt)
+                load_tile<KD>(tc::smem_addr(ring + (u % kStages) * kTile), lkp, static_cast<int64_t>(nxt) * kMT, L, tid);
         }
-        __syncthreads();
+        cp_commit();
     }
+    __syncthreads();
     // band maxima: warp reduce, then shared atomics across the 4 lane quarters
 #pragma unroll
     for (int i = 0; i < BPW; ++i) {
@@ -197,7 +200,7 @@ __global__ void __launch_bounds__(kThreads, NQ == 64 ? 2 : 1)
         if (lane == 0) atomicMax(&bandmax[half * BPW + i], __float2int_rn(v));
     }
     __syncthreads();
-    if (warp == 0) tc::tmem_dealloc<2 * NQ>(tmem);
+    if (warp == 0) tc::tmem_dealloc<kAcc * NQ>(tmem);
 
     // ---- exact per-band selection (one warp per band)
     const int64_t nb = (L + 7) / 8;
@@ -216,7 +219,7 @@ template <int KD, int NQ>
 size_t colvec_smem_bytes(int64_t L) {
     const int64_t nt = (L + kMT - 1) / kMT;
     return ColvecSmem<KD>::kTileBytes * kStages + NQ * KD * 2 + (NQ / 8) * nt * kMT * 2 +
-           (kThreads / 32) * 64 * 4 + (kThreads / 32) * kList * 4 + 16 * 4 + 2 * 8 + 8;
+           (kThreads / 32) * 64 * 4 + (kThreads / 32) * kList * 4 + 16 * 4 + kAcc * 8 + 8;
 }
 
 }  // namespace
