@@ -252,6 +252,196 @@ __global__ void __launch_bounds__(kBandWarps * 32)
     }
 }
 
+// ----------------------------------------------------------- block rows
+// BLOCK masks with 32x32 blocks: the four 8-row bands of a 32-row block row
+// share one key list (its kept blocks), so one CTA of four warps owns the
+// block row and stages each kept block's 32 K and V rows ONCE in shared
+// memory (contiguous rows -> fully coalesced 16-byte cp.async, XOR-swizzled
+// for conflict-free ldmatrix), double buffered; every warp then runs the
+// band computation of attn_band_kernel (S^T = K_blk . Q_band^T, online
+// softmax, Z^T += V_blk^T . P^T) on the shared tiles.  L2 -> SM traffic is a
+// quarter of the per-band kernels'.
+template <int D>
+struct BlockSmem {
+    __nv_bfloat16 k[2][32 * D];
+    __nv_bfloat16 v[2][32 * D];
+    __nv_bfloat16 q[4][8 * D];   // per warp: Q band, reused to stage Z
+    __nv_bfloat16 p[4][8 * 40];  // per warp: [query][key], padded rows
+};
+
+template <int D>
+__global__ void __launch_bounds__(128)
+    attn_block_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __restrict__ K,
+                      const __nv_bfloat16* __restrict__ V, const uint32_t* __restrict__ block_cols,
+                      int64_t L, int64_t keep, int scale, __nv_bfloat16* __restrict__ Z) {
+    constexpr int CHUNK = 32;
+    extern __shared__ __align__(128) unsigned char dsm[];
+    BlockSmem<D>& sm = *reinterpret_cast<BlockSmem<D>*>(dsm);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t nbr = L / 32;
+    const int64_t pair = blockIdx.y, br = blockIdx.x;
+    const int64_t r0 = br * 32 + warp * 8;  // this warp's band
+    const __nv_bfloat16* Kp = K + pair * L * D;
+    const __nv_bfloat16* Vp = V + pair * L * D;
+    const uint32_t* cols = block_cols + (pair * nbr + br) * keep;
+    const int g = lane >> 2, c4 = lane & 3;
+    constexpr int kChunks16 = D / 8;
+    __nv_bfloat16* sq = sm.q[warp];
+    __nv_bfloat16* sp = sm.p[warp];
+
+    for (int t = lane; t < 8 * kChunks16; t += 32) {
+        const int r = t / kChunks16, c = t % kChunks16;
+        cp_async16(smem_u32(sq) + swz<D>(r, c), Q + (pair * L + r0 + r) * D + c * 8, true);
+    }
+    auto load_block = [&](int buf, int ch) {
+        const int64_t j0 = static_cast<int64_t>(__ldg(cols + ch)) * 32;
+        for (int t = tid; t < CHUNK * kChunks16; t += 128) {
+            const int r = t / kChunks16, c = t % kChunks16;
+            cp_async16(smem_u32(sm.k[buf]) + swz<D>(r, c), Kp + (j0 + r) * D + c * 8, true);
+            cp_async16(smem_u32(sm.v[buf]) + swz<D>(r, c), Vp + (j0 + r) * D + c * 8, true);
+        }
+    };
+    const int nchunks = static_cast<int>(keep);
+    load_block(0, 0);
+    cp_async_commit();
+
+    const float sl2 = (scale ? rsqrtf(static_cast<float>(D)) : 1.f) * 1.4426950408889634f;
+    float m_run[2] = {-INFINITY, -INFINITY};
+    float l_part[2] = {0.f, 0.f};
+    float zacc[D / 16][4];
+#pragma unroll
+    for (int t = 0; t < D / 16; ++t)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) zacc[t][u] = 0.f;
+    uint32_t qb[D / 16][2];
+
+    for (int ch = 0; ch < nchunks; ++ch) {
+        const int buf = ch & 1;
+        if (ch + 1 < nchunks) load_block(buf ^ 1, ch + 1);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncthreads();
+        if (ch == 0) {
+#pragma unroll
+            for (int ks = 0; ks < D / 16; ++ks) {
+                const char* qbase = reinterpret_cast<const char*>(sq);
+                qb[ks][0] = *reinterpret_cast<const uint32_t*>(qbase + swz<D>(g, 2 * ks) + c4 * 4);
+                qb[ks][1] = *reinterpret_cast<const uint32_t*>(qbase + swz<D>(g, 2 * ks + 1) + c4 * 4);
+            }
+        }
+        float s[CHUNK / 16][4];
+        const uint32_t kb = smem_u32(sm.k[buf]);
+#pragma unroll
+        for (int mt = 0; mt < CHUNK / 16; ++mt) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) s[mt][u] = 0.f;
+#pragma unroll
+            for (int ks = 0; ks < D / 16; ++ks) {
+                const int mi = lane >> 3;
+                const int row = mt * 16 + (mi & 1) * 8 + (lane & 7);
+                const int chk = ks * 2 + (mi >> 1);
+                uint32_t a0, a1, a2, a3;
+                ldsm_x4(kb + swz<D>(row, chk), a0, a1, a2, a3);
+                mma16816(s[mt], a0, a1, a2, a3, qb[ks][0], qb[ks][1]);
+            }
+        }
+        float cmax[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+        for (int mt = 0; mt < CHUNK / 16; ++mt)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const float x = s[mt][u] * sl2;
+                s[mt][u] = x;
+                cmax[u & 1] = fmaxf(cmax[u & 1], x);
+            }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            cmax[h] = fmaxf(cmax[h], __shfl_xor_sync(0xffffffffu, cmax[h], 4));
+            cmax[h] = fmaxf(cmax[h], __shfl_xor_sync(0xffffffffu, cmax[h], 8));
+            cmax[h] = fmaxf(cmax[h], __shfl_xor_sync(0xffffffffu, cmax[h], 16));
+        }
+        float corr[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const float mn = fmaxf(m_run[h], cmax[h]);
+            corr[h] = m_run[h] == -INFINITY ? 0.f : exp2f(m_run[h] - mn);
+            m_run[h] = mn;
+            l_part[h] *= corr[h];
+        }
+#pragma unroll
+        for (int t = 0; t < D / 16; ++t) {
+            zacc[t][0] *= corr[0];
+            zacc[t][1] *= corr[1];
+            zacc[t][2] *= corr[0];
+            zacc[t][3] *= corr[1];
+        }
+        constexpr int PW = CHUNK + 8;
+#pragma unroll
+        for (int mt = 0; mt < CHUNK / 16; ++mt)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const float pv = exp2f(s[mt][u] - m_run[u & 1]);
+                l_part[u & 1] += pv;
+                sp[(2 * c4 + (u & 1)) * PW + mt * 16 + g + (u >> 1) * 8] = __float2bfloat16_rn(pv);
+            }
+        __syncwarp();
+        const uint32_t vb = smem_u32(sm.v[buf]);
+#pragma unroll
+        for (int ks = 0; ks < CHUNK / 16; ++ks) {
+            const uint32_t b0 = *reinterpret_cast<const uint32_t*>(&sp[g * PW + ks * 16 + 2 * c4]);
+            const uint32_t b1 = *reinterpret_cast<const uint32_t*>(&sp[g * PW + ks * 16 + 8 + 2 * c4]);
+#pragma unroll
+            for (int mt = 0; mt < D / 16; ++mt) {
+                const int mi = lane >> 3;
+                const int row = ks * 16 + (mi >> 1) * 8 + (lane & 7);
+                const int chk = mt * 2 + (mi & 1);
+                uint32_t a0, a1, a2, a3;
+                ldsm_x4_t(vb + swz<D>(row, chk), a0, a1, a2, a3);
+                mma16816(zacc[mt], a0, a1, a2, a3, b0, b1);
+            }
+        }
+        __syncthreads();  // every warp done with `buf` before it is refilled
+    }
+    cp_async_wait<0>();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        l_part[h] += __shfl_xor_sync(0xffffffffu, l_part[h], 4);
+        l_part[h] += __shfl_xor_sync(0xffffffffu, l_part[h], 8);
+        l_part[h] += __shfl_xor_sync(0xffffffffu, l_part[h], 16);
+    }
+    const float inv0 = l_part[0] > 0.f ? 1.f / l_part[0] : 0.f;
+    const float inv1 = l_part[1] > 0.f ? 1.f / l_part[1] : 0.f;
+#pragma unroll
+    for (int mt = 0; mt < D / 16; ++mt) {
+        const int d0 = mt * 16 + g;
+        sq[(2 * c4) * D + d0] = __float2bfloat16_rn(zacc[mt][0] * inv0);
+        sq[(2 * c4 + 1) * D + d0] = __float2bfloat16_rn(zacc[mt][1] * inv1);
+        sq[(2 * c4) * D + d0 + 8] = __float2bfloat16_rn(zacc[mt][2] * inv0);
+        sq[(2 * c4 + 1) * D + d0 + 8] = __float2bfloat16_rn(zacc[mt][3] * inv1);
+    }
+    __syncwarp();
+    for (int t = lane; t < 8 * kChunks16; t += 32) {
+        const int r = t / kChunks16, c = t % kChunks16;
+        *reinterpret_cast<uint4*>(Z + (pair * L + r0 + r) * D + c * 8) =
+            *reinterpret_cast<const uint4*>(&sq[r * D + c * 8]);
+    }
+}
+
+template <int D>
+void launch_block(const AttnArgs& a, cudaStream_t st) {
+    const size_t smem = sizeof(BlockSmem<D>);
+    auto kern = attn_block_kernel<D>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        attr = true;
+    }
+    const dim3 grid(static_cast<unsigned>(a.L / 32), static_cast<unsigned>(a.pairs));
+    kern<<<grid, 128, smem, st>>>(static_cast<const __nv_bfloat16*>(a.q), static_cast<const __nv_bfloat16*>(a.k),
+                                  static_cast<const __nv_bfloat16*>(a.v), a.cols, a.L, a.keep, a.scale,
+                                  static_cast<__nv_bfloat16*>(a.z));
+}
+
 // ---------------------------------------------------------------- v2
 // K fragments straight from global memory into registers: the reduction
 // order over d is permuted so each lane's slots of a k-step are 4 CONSECUTIVE
@@ -543,8 +733,14 @@ void run_band_attention(const AttnArgs& a, cudaStream_t st) {
         if (a.D == 64) launch_band<64, 32, 12>(a, st);
         else launch_band<128, 32, 6>(a, st);
     } else if (a.mode == kBlock) {
-        if (a.D == 64) launch_band_v2<64, 16, kBlockList>(a, st);
-        else launch_band_v2<128, 8, kBlockList>(a, st);
+        static const bool per_band = std::getenv("DSA_BLOCK_PER_BAND") != nullptr;  // A/B switch
+        if (per_band) {
+            if (a.D == 64) launch_band_v2<64, 16, kBlockList>(a, st);
+            else launch_band_v2<128, 8, kBlockList>(a, st);
+        } else {
+            if (a.D == 64) launch_block<64>(a, st);
+            else launch_block<128>(a, st);
+        }
     } else if (a.mode == kRowTopk) {
         if (a.D == 64) launch_band_v2<64, 16, kRowList>(a, st);
         else launch_band_v2<128, 8, kRowList>(a, st);
