@@ -12,6 +12,7 @@
 // and shape; the tensor-core fast paths (select_tc.cu) take over the
 // configurations they are specialised for.
 #include <cub/cub.cuh>
+#include <climits>
 #include <cstdlib>
 #include <cuda_bf16.h>
 
@@ -270,17 +271,32 @@ __global__ void __launch_bounds__(kNT) colvec_generic(SelectArgs a) {
 
 // --------------------------------------------------------------- block
 // pooled[pair][0|1][nb][KD] = sum of the block's rows of levels (exact int).
+// Block sums of the levels: one thread per (pair, tensor, block, 8-column
+// chunk); the chunk-planar layout makes a block's rows of one chunk a
+// contiguous run, read as 16-byte vectors (8 independent sums).
 __global__ void pool_levels_kernel(SelectArgs a, int64_t nb) {
     const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int64_t total = a.pairs * 2 * nb * a.KD;
+    const int64_t nch = a.KD / 8;
+    const int64_t total = a.pairs * 2 * nb * nch;
     if (idx >= total) return;
-    const int64_t t = idx % a.KD, blk = (idx / a.KD) % nb, which = (idx / (a.KD * nb)) % 2,
-                  pair = idx / (a.KD * nb * 2);
-    const uint16_t* lv = (which ? a.lk : a.lq) + pair * a.L * a.KD;
-    int acc = 0;
-    for (int64_t r = blk * a.block; r < min((blk + 1) * a.block, a.L); ++r)
-        acc += level_to_int(lv[lvl_index(a.L, r, static_cast<int>(t))]);
-    a.pooled[idx] = acc;
+    const int64_t c = idx % nch, blk = (idx / nch) % nb, which = (idx / (nch * nb)) % 2,
+                  pair = idx / (nch * nb * 2);
+    const uint16_t* lv = (which ? a.lk : a.lq) + pair * a.L * a.KD + lvl_index(a.L, 0, static_cast<int>(c * 8));
+    int acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const int64_t r1 = min((blk + 1) * a.block, a.L);
+#pragma unroll 8
+    for (int64_t r = blk * a.block; r < r1; ++r) {
+        const uint4 w = __ldg(reinterpret_cast<const uint4*>(lv + r * 8));
+        const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            acc[2 * h] += static_cast<int>(__uint_as_float(ww[h] << 16));
+            acc[2 * h + 1] += static_cast<int>(__uint_as_float(ww[h] & 0xffff0000u));
+        }
+    }
+    int32_t* out = a.pooled + ((pair * 2 + which) * nb + blk) * a.KD + c * 8;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) out[u] = acc[u];
 }
 
 __global__ void __launch_bounds__(kNT) block_generic(SelectArgs a, int64_t nb) {
@@ -308,6 +324,92 @@ __global__ void __launch_bounds__(kNT) block_generic(SelectArgs a, int64_t nb) {
         lt = keys[j] < T;
         eq = keys[j] == T;
     }, out, s);
+}
+
+// Warp-per-block-row BLOCK selection (nb <= 32 * kBlkPerLane, keep <= 32):
+// the pooled K levels of the pair are staged once per CTA, each lane scores
+// kBlkPerLane block columns exactly (int32 dot, int64 mean weighting), then
+// `keep` rounds of a warp arg-max (value desc, lowest block first; the
+// forced diagonal ranks above everything) and a 32-lane bitonic sort give
+// the ascending block list.  Same ranking as block_generic / the oracle.
+constexpr int kBlkPerLane = 16;
+
+__device__ __forceinline__ bool blk_before(long long va, int ia, long long vb, int ib) {
+    return va > vb || (va == vb && ia < ib);
+}
+
+template <int KD>
+__global__ void __launch_bounds__(256) block_select_warp(SelectArgs a, int64_t nb) {
+    extern __shared__ __align__(16) int32_t pks[];  // [nb][KD]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t pair = blockIdx.y;
+    const int32_t* pk = a.pooled + (pair * 2 + 1) * nb * KD;
+    for (int64_t i = threadIdx.x; i < nb * KD; i += 256) pks[i] = pk[i];
+    __syncthreads();
+    const int64_t ib = static_cast<int64_t>(blockIdx.x) * 8 + warp;
+    if (ib >= nb) return;
+    const int32_t* pq = a.pooled + ((pair * 2 + 0) * nb + ib) * KD;
+    int32_t qv[KD];
+#pragma unroll
+    for (int t = 0; t < KD; ++t) qv[t] = __ldg(pq + t);
+    const int64_t r = a.L - (nb - 1) * a.block;  // width of the last (possibly ragged) block
+    long long val[kBlkPerLane];
+#pragma unroll
+    for (int u = 0; u < kBlkPerLane; ++u) {
+        const int64_t jb = static_cast<int64_t>(u) * 32 + lane;
+        if (jb < nb) {
+            int32_t sum = 0;
+            const int4* row = reinterpret_cast<const int4*>(pks + jb * KD);
+#pragma unroll
+            for (int t4 = 0; t4 < KD / 4; ++t4) {
+                const int4 w = row[t4];
+                sum += qv[4 * t4] * w.x + qv[4 * t4 + 1] * w.y + qv[4 * t4 + 2] * w.z + qv[4 * t4 + 3] * w.w;
+            }
+            const int64_t width = jb == nb - 1 ? r : a.block;
+            long long v = width == a.block ? static_cast<long long>(sum) * r : static_cast<long long>(sum) * a.block;
+            if (a.force_diag && jb == ib) v = LLONG_MAX;
+            val[u] = v;
+        } else {
+            val[u] = LLONG_MIN;
+        }
+    }
+    int mine = INT32_MAX;  // lane t keeps the t-th selected block
+    uint32_t taken = 0;    // bit u: block u*32 + lane already selected
+    for (int k = 0; k < static_cast<int>(a.keep); ++k) {
+        long long bv = LLONG_MIN;
+        int bi = INT32_MAX;
+#pragma unroll
+        for (int u = 0; u < kBlkPerLane; ++u) {
+            const int jb = u * 32 + lane;
+            if (jb < nb && !((taken >> u) & 1u) && (bi == INT32_MAX || blk_before(val[u], jb, bv, bi))) {
+                bv = val[u];
+                bi = jb;
+            }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const long long ov = __shfl_xor_sync(0xffffffffu, bv, off);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+            if (oi != INT32_MAX && (bi == INT32_MAX || blk_before(ov, oi, bv, bi))) {
+                bv = ov;
+                bi = oi;
+            }
+        }
+        if (lane == k) mine = bi;
+        if ((bi & 31) == lane) taken |= 1u << (bi >> 5);  // the owner retires the winner
+    }
+    // ascending order: bitonic sort across the 32 lanes
+#pragma unroll
+    for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            const int other = __shfl_xor_sync(0xffffffffu, mine, stride);
+            const bool up = (lane & size) == 0;
+            const bool lower = (lane & stride) == 0;
+            mine = (lower == up) ? min(mine, other) : max(mine, other);
+        }
+    }
+    if (lane < a.keep) a.cols[(pair * nb + ib) * a.keep + lane] = static_cast<uint32_t>(mine);
 }
 
 // ----------------------------------------------------------- threshold
@@ -436,12 +538,19 @@ void launch_select(const SelectArgs& a, cudaStream_t st) {
         }
         case kBlock: {
             const int64_t nb = ceil_div_i(a.L, a.block);
-            const int64_t total = a.pairs * 2 * nb * a.KD;
+            const int64_t total = a.pairs * 2 * nb * (a.KD / 8);
             pool_levels_kernel<<<static_cast<unsigned>(ceil_div_i(total, 256)), 256, 0, st>>>(a, nb);
             note_launch();
-            const size_t sm = static_cast<size_t>(nb) * 8;
-            cudaFuncSetAttribute(block_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
-            block_generic<<<dim3(static_cast<unsigned>(nb), P), kNT, sm, st>>>(a, nb);
+            if (a.keep <= 32 && nb <= 32 * kBlkPerLane && nb * KD * 4 <= 200 * 1024 &&
+                std::getenv("DSA_BLOCK_GENERIC") == nullptr) {
+                const size_t sm = static_cast<size_t>(nb) * KD * 4;
+                cudaFuncSetAttribute(block_select_warp<KD>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+                block_select_warp<KD><<<dim3(static_cast<unsigned>(ceil_div_i(nb, 8)), P), 256, sm, st>>>(a, nb);
+            } else {
+                const size_t sm = static_cast<size_t>(nb) * 8;
+                cudaFuncSetAttribute(block_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+                block_generic<<<dim3(static_cast<unsigned>(nb), P), kNT, sm, st>>>(a, nb);
+            }
             note_launch();
             break;
         }
