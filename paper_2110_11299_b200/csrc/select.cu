@@ -326,77 +326,55 @@ __global__ void __launch_bounds__(kNT) block_generic(SelectArgs a, int64_t nb) {
     }, out, s);
 }
 
-// Warp-per-block-row BLOCK selection (nb <= 32 * kBlkPerLane, keep <= 32):
-// the pooled K levels of the pair are staged once per CTA, each lane scores
-// kBlkPerLane block columns exactly (int32 dot, int64 mean weighting), then
-// `keep` rounds of a warp arg-max (value desc, lowest block first; the
+// Warp-per-block-row BLOCK selection (L % block == 0, nb <= 32 * NPL,
+// keep <= 32): each lane scores NPL block columns exactly (int32 dot of the
+// pooled levels -- with equal block widths the mean ranks like the sum),
+// packed as (biased score << 32 | ~block) so one unsigned 64-bit max is
+// "value desc, lowest block first"; `keep` rounds of a warp arg-max (the
 // forced diagonal ranks above everything) and a 32-lane bitonic sort give
 // the ascending block list.  Same ranking as block_generic / the oracle.
-constexpr int kBlkPerLane = 16;
-
-__device__ __forceinline__ bool blk_before(long long va, int ia, long long vb, int ib) {
-    return va > vb || (va == vb && ia < ib);
-}
-
-template <int KD>
+template <int KD, int NPL>
 __global__ void __launch_bounds__(256) block_select_warp(SelectArgs a, int64_t nb) {
-    extern __shared__ __align__(16) int32_t pks[];  // [nb][KD]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t pair = blockIdx.y;
-    const int32_t* pk = a.pooled + (pair * 2 + 1) * nb * KD;
-    for (int64_t i = threadIdx.x; i < nb * KD; i += 256) pks[i] = pk[i];
-    __syncthreads();
+    const int32_t* pks = a.pooled + (pair * 2 + 1) * nb * KD;  // pooled K (L1/L2 resident)
     const int64_t ib = static_cast<int64_t>(blockIdx.x) * 8 + warp;
     if (ib >= nb) return;
     const int32_t* pq = a.pooled + ((pair * 2 + 0) * nb + ib) * KD;
     int32_t qv[KD];
 #pragma unroll
     for (int t = 0; t < KD; ++t) qv[t] = __ldg(pq + t);
-    const int64_t r = a.L - (nb - 1) * a.block;  // width of the last (possibly ragged) block
-    long long val[kBlkPerLane];
+    unsigned long long key[NPL];
 #pragma unroll
-    for (int u = 0; u < kBlkPerLane; ++u) {
-        const int64_t jb = static_cast<int64_t>(u) * 32 + lane;
+    for (int u = 0; u < NPL; ++u) {
+        const int jb = u * 32 + lane;
+        key[u] = 0ull;
         if (jb < nb) {
             int32_t sum = 0;
-            const int4* row = reinterpret_cast<const int4*>(pks + jb * KD);
+            const int4* row = reinterpret_cast<const int4*>(pks + static_cast<int64_t>(jb) * KD);
 #pragma unroll
             for (int t4 = 0; t4 < KD / 4; ++t4) {
-                const int4 w = row[t4];
+                const int4 w = __ldg(row + t4);
                 sum += qv[4 * t4] * w.x + qv[4 * t4 + 1] * w.y + qv[4 * t4 + 2] * w.z + qv[4 * t4 + 3] * w.w;
             }
-            const int64_t width = jb == nb - 1 ? r : a.block;
-            long long v = width == a.block ? static_cast<long long>(sum) * r : static_cast<long long>(sum) * a.block;
-            if (a.force_diag && jb == ib) v = LLONG_MAX;
-            val[u] = v;
-        } else {
-            val[u] = LLONG_MIN;
+            const uint32_t hi = (a.force_diag && jb == ib) ? 0xffffffffu : (static_cast<uint32_t>(sum) ^ 0x80000000u);
+            key[u] = (static_cast<unsigned long long>(hi) << 32) | (0xffffffffu - static_cast<uint32_t>(jb));
         }
     }
     int mine = INT32_MAX;  // lane t keeps the t-th selected block
-    uint32_t taken = 0;    // bit u: block u*32 + lane already selected
     for (int k = 0; k < static_cast<int>(a.keep); ++k) {
-        long long bv = LLONG_MIN;
-        int bi = INT32_MAX;
+        unsigned long long best = key[0];
 #pragma unroll
-        for (int u = 0; u < kBlkPerLane; ++u) {
-            const int jb = u * 32 + lane;
-            if (jb < nb && !((taken >> u) & 1u) && (bi == INT32_MAX || blk_before(val[u], jb, bv, bi))) {
-                bv = val[u];
-                bi = jb;
-            }
-        }
+        for (int u = 1; u < NPL; ++u) best = key[u] > best ? key[u] : best;
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) {
-            const long long ov = __shfl_xor_sync(0xffffffffu, bv, off);
-            const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-            if (oi != INT32_MAX && (bi == INT32_MAX || blk_before(ov, oi, bv, bi))) {
-                bv = ov;
-                bi = oi;
-            }
+            const unsigned long long o = __shfl_xor_sync(0xffffffffu, best, off);
+            best = o > best ? o : best;
         }
-        if (lane == k) mine = bi;
-        if ((bi & 31) == lane) taken |= 1u << (bi >> 5);  // the owner retires the winner
+        if (lane == k) mine = static_cast<int>(0xffffffffu - static_cast<uint32_t>(best));
+#pragma unroll
+        for (int u = 0; u < NPL; ++u)
+            if (key[u] == best) key[u] = 0ull;  // unique: only the owner's slot matches
     }
     // ascending order: bitonic sort across the 32 lanes
 #pragma unroll
@@ -541,11 +519,17 @@ void launch_select(const SelectArgs& a, cudaStream_t st) {
             const int64_t total = a.pairs * 2 * nb * (a.KD / 8);
             pool_levels_kernel<<<static_cast<unsigned>(ceil_div_i(total, 256)), 256, 0, st>>>(a, nb);
             note_launch();
-            if (a.keep <= 32 && nb <= 32 * kBlkPerLane && nb * KD * 4 <= 200 * 1024 &&
-                std::getenv("DSA_BLOCK_GENERIC") == nullptr) {
-                const size_t sm = static_cast<size_t>(nb) * KD * 4;
-                cudaFuncSetAttribute(block_select_warp<KD>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
-                block_select_warp<KD><<<dim3(static_cast<unsigned>(ceil_div_i(nb, 8)), P), 256, sm, st>>>(a, nb);
+            const double bq = static_cast<double>(a.block) * a.qmax;  // |pooled level| bound
+            const bool warp_ok = a.keep <= 32 && a.L % a.block == 0 && nb <= 512 &&
+                                 static_cast<double>(a.KD) * bq * bq < 2147483647.0 &&  // int32 dot exact
+                                 std::getenv("DSA_BLOCK_GENERIC") == nullptr;
+            const dim3 gw(static_cast<unsigned>(ceil_div_i(nb, 8)), P);
+            if (warp_ok && nb <= 128) {
+                block_select_warp<KD, 4><<<gw, 256, 0, st>>>(a, nb);
+            } else if (warp_ok && nb <= 256) {
+                block_select_warp<KD, 8><<<gw, 256, 0, st>>>(a, nb);
+            } else if (warp_ok) {
+                block_select_warp<KD, 16><<<gw, 256, 0, st>>>(a, nb);
             } else {
                 const size_t sm = static_cast<size_t>(nb) * 8;
                 cudaFuncSetAttribute(block_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
