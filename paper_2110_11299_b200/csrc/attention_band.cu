@@ -479,7 +479,13 @@ __device__ __forceinline__ void load_k_frag(const __nv_bfloat16* __restrict__ Kp
 // MODE kRowList / kRowCsr: every query row has its own list (ROW_TOPK rows of
 //   `keep`, THRESHOLD CSR rows): one row per warp, the row's q in the first
 //   of the 8 MMA columns (the other seven are zero and ignored).
-enum BandMode { kBandList = 0, kBlockList = 1, kRowList = 2, kRowCsr = 3 };
+// MODE kRowsBand: per-row lists again, but a warp takes 8 consecutive rows
+//   and streams the CONCATENATION of their lists (contiguous in the CSR /
+//   row-list layout) in 32-key chunks, each row in its own MMA column; an
+//   entry (key, column) is live only when the key's stream position lies in
+//   that row's segment.  No per-row latency chain: one long prefetched
+//   gather stream per warp (the MMA does 8x the useful work, which is free).
+enum BandMode { kBandList = 0, kBlockList = 1, kRowList = 2, kRowCsr = 3, kRowsBand = 4 };
 
 template <int D, int kWarps, int MODE>
 __global__ void __launch_bounds__(kWarps * 32)
@@ -496,6 +502,7 @@ __global__ void __launch_bounds__(kWarps * 32)
     using S = BandSmemV2<D>;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     S& sm = reinterpret_cast<S*>(dsm)[warp];
+    constexpr bool SEG = MODE == kRowsBand;
     const int64_t nb = ROW ? L : (L + 7) / 8;  // warp work items per pair
     const int64_t band_global = static_cast<int64_t>(blockIdx.x) * kWarps + warp;
     if (band_global >= pairs * nb) return;
@@ -512,12 +519,28 @@ __global__ void __launch_bounds__(kWarps * 32)
     } else if (MODE == kBandList || MODE == kRowList) {
         cols = band_cols + (pair * nb + band) * keep;
         nkeys = keep;
-    } else {
+    } else if (MODE == kRowCsr) {
         const uint64_t b = rowptr[pair * L + r0];
         cols = band_cols + b;
         nkeys = static_cast<int64_t>(rowptr[pair * L + r0 + 1] - b);
     }
     const int g = lane >> 2, c4 = lane & 3;
+    // kRowsBand: stream segment bounds of this thread's two columns (rows
+    // 2c4, 2c4+1): [sb0, sb1) and [sb1, sb2)
+    int64_t sb0 = 0, sb1 = 0, sb2 = 0;
+    if (SEG) {
+        const int64_t e = r0 + 8 < L ? r0 + 8 : L;
+        auto bound = [&](int c) -> int64_t {
+            const int64_t r = r0 + c < e ? r0 + c : e;
+            return rowptr ? static_cast<int64_t>(rowptr[pair * L + r]) : (pair * L + r) * keep;
+        };
+        const int64_t b0 = bound(0);
+        cols = band_cols + b0;
+        nkeys = bound(8) - b0;
+        sb0 = bound(2 * c4) - b0;
+        sb1 = bound(2 * c4 + 1) - b0;
+        sb2 = bound(2 * c4 + 2) - b0;
+    }
     constexpr int kChunks16 = D / 8;
 
     // Q^T B-fragments (same d permutation as K): row g, segment [c4*D/4, +D/4)
@@ -598,7 +621,9 @@ __global__ void __launch_bounds__(kWarps * 32)
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int key = base + mt * 16 + g + (u >> 1) * 8;
-                const float x = key < nkeys ? s[mt][u] * sl2 : -INFINITY;
+                bool live = key < nkeys;
+                if (SEG) live = (u & 1) ? (key >= sb1 && key < sb2) : (key >= sb0 && key < sb1);
+                const float x = live ? s[mt][u] * sl2 : -INFINITY;
                 s[mt][u] = x;
                 cmax[u & 1] = fmaxf(cmax[u & 1], x);
             }
@@ -628,7 +653,8 @@ __global__ void __launch_bounds__(kWarps * 32)
         for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const float pv = exp2f(s[mt][u] - m_run[u & 1]);
+                // a column may have no live key yet (m_run = -inf): weight 0
+                const float pv = s[mt][u] == -INFINITY ? 0.f : exp2f(s[mt][u] - m_run[u & 1]);
                 l_part[u & 1] += pv;
                 sm.p[(2 * c4 + (u & 1)) * PW + mt * 16 + g + (u >> 1) * 8] = __float2bfloat16_rn(pv);
             }
@@ -685,6 +711,10 @@ __global__ void __launch_bounds__(kWarps * 32)
                 *reinterpret_cast<const uint4*>(&sm.z[r * D + c * 8]);
     }
     if (ROW && empty_rows && lane == 0) empty_rows[pair * L + r0] = nkeys == 0;
+    if (SEG && empty_rows && g == 0) {
+        if (r0 + 2 * c4 < L) empty_rows[pair * L + r0 + 2 * c4] = sb1 == sb0;
+        if (r0 + 2 * c4 + 1 < L) empty_rows[pair * L + r0 + 2 * c4 + 1] = sb2 == sb1;
+    }
 }
 
 template <int D, int kWarps, int MODE = kBandList>
@@ -741,12 +771,22 @@ void run_band_attention(const AttnArgs& a, cudaStream_t st) {
             if (a.D == 64) launch_block<64>(a, st);
             else launch_block<128>(a, st);
         }
-    } else if (a.mode == kRowTopk) {
-        if (a.D == 64) launch_band_v2<64, 16, kRowList>(a, st);
-        else launch_band_v2<128, 8, kRowList>(a, st);
-    } else if (a.mode == kThreshold) {
-        if (a.D == 64) launch_band_v2<64, 16, kRowCsr>(a, st);
-        else launch_band_v2<128, 8, kRowCsr>(a, st);
+    } else if (a.mode == kRowTopk || a.mode == kThreshold) {
+        static const bool per_row = std::getenv("DSA_ATTN_ROW_PER_WARP") != nullptr;  // A/B switch
+        AttnArgs b = a;
+        if (a.mode == kRowTopk) b.rowptr = nullptr;  // fixed-length row lists
+        if (per_row) {
+            if (a.mode == kRowTopk) {
+                if (a.D == 64) launch_band_v2<64, 16, kRowList>(a, st);
+                else launch_band_v2<128, 8, kRowList>(a, st);
+            } else {
+                if (a.D == 64) launch_band_v2<64, 16, kRowCsr>(a, st);
+                else launch_band_v2<128, 8, kRowCsr>(a, st);
+            }
+        } else {
+            if (a.D == 64) launch_band_v2<64, 16, kRowsBand>(b, st);
+            else launch_band_v2<128, 8, kRowsBand>(b, st);
+        }
     } else {
         if (a.D == 64) launch_band_v2<64, 16>(a, st);
         else launch_band_v2<128, 8>(a, st);

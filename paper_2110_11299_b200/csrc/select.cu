@@ -234,6 +234,69 @@ __global__ void __launch_bounds__(kNT) topk_rows_generic(SelectArgs a) {
     }, out, s);
 }
 
+// Per-row-scaled top-k (quant_scope = row): the ranking key is
+// the double product s_ij * sk_j.  Selection runs on 32-bit keys f =
+// fl32(s * sk) (rounding is monotone, so f orders the products except
+// inside groups of equal f), then the threshold group is resolved exactly:
+// if only part of the f == T group is kept, its members are ranked by the
+// double product (ties: lowest column) -- half the radix passes of a 64-bit
+// select and the same result.
+template <int KD>
+__global__ void __launch_bounds__(kNT) topk_rows_scaled(SelectArgs a) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    const int L = static_cast<int>(a.L);
+    uint32_t* keys = reinterpret_cast<uint32_t*>(dsm);            // [L]
+    int32_t* ties = reinterpret_cast<int32_t*>(keys + L);          // [L]
+    int16_t* sv = reinterpret_cast<int16_t*>(ties + L);            // [L] exact scores
+    uint8_t* take = reinterpret_cast<uint8_t*>(sv + L);            // [L]
+    __shared__ SelSmem s;
+    __shared__ unsigned tie_count;
+    const int64_t i = blockIdx.x, pair = blockIdx.y;
+    const int tid = threadIdx.x;
+    const double* skp = a.sk + pair * a.L;
+    float q[KD];
+    load_levels<KD>(a.lq + pair * a.L * KD, a.L, i, q);
+    const uint16_t* lk = a.lk + pair * a.L * KD;
+    if (tid == 0) tie_count = 0u;
+    for (int j = tid; j < L; j += kNT) {
+        const int sc = score_with<KD>(q, lk, a.L, j);
+        sv[j] = static_cast<int16_t>(sc);
+        take[j] = 0;
+        const float f = static_cast<float>(static_cast<double>(sc) * __ldg(skp + j));
+        const uint32_t b = __float_as_uint(f == 0.f ? 0.f : f);
+        const uint32_t o = (b >> 31) ? ~b : (b | 0x80000000u);  // ascending with f
+        keys[j] = ~o;                                           // smaller = better
+    }
+    __syncthreads();
+    uint32_t T, rem;
+    block_radix_select<uint32_t>(keys, L, static_cast<int>(a.keep), s, T, rem);
+    for (int j = tid; j < L; j += kNT)
+        if (keys[j] == T) ties[atomicAdd(&tie_count, 1u)] = j;
+    __syncthreads();
+    const int m = static_cast<int>(tie_count);
+    for (int c = tid; c < m; c += kNT) {
+        const int j = ties[c];
+        if (static_cast<uint32_t>(m) == rem) {
+            take[j] = 1;
+            continue;
+        }
+        const double d = static_cast<double>(sv[j]) * __ldg(skp + j);
+        uint32_t rank = 0;
+        for (int c2 = 0; c2 < m; ++c2) {
+            const int j2 = ties[c2];
+            const double d2 = static_cast<double>(sv[j2]) * __ldg(skp + j2);
+            rank += (d2 > d || (d2 == d && j2 < j)) ? 1u : 0u;
+        }
+        take[j] = rank < rem;
+    }
+    __syncthreads();
+    uint32_t* out = a.cols + (pair * a.L + i) * a.keep;
+    block_emit(L, 0u, [&](int j, bool& lt, bool& eq) {
+        lt = keys[j] < T || (keys[j] == T && take[j]);
+        eq = false;
+    }, out, s);
+}
+
 // -------------------------------------------------------------- colvec
 template <int KD>
 __global__ void __launch_bounds__(kNT) colvec_generic(SelectArgs a) {
@@ -491,7 +554,14 @@ void launch_select(const SelectArgs& a, cudaStream_t st) {
     const unsigned P = static_cast<unsigned>(a.pairs);
     switch (a.mode) {
         case kRowTopk: {
-            if (a.per_row) {
+            if (a.per_row && a.L <= 8192 && a.qmax * a.qmax * KD < 32768 &&
+                std::getenv("DSA_TOPK64") == nullptr) {  // int16 exact scores
+                const size_t sm = static_cast<size_t>(a.L) * 11;
+                auto kern = topk_rows_scaled<KD>;
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+                kern<<<dim3(static_cast<unsigned>(a.L), P), kNT, sm, st>>>(a);
+                note_launch();
+            } else if (a.per_row) {
                 const size_t sm = static_cast<size_t>(a.L) * 8;
                 auto kern = topk_rows_generic<uint64_t, KD>;
                 cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
