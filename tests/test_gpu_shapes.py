@@ -31,7 +31,15 @@ CASES = [
     ("block", 1024, 64, 16, 4, "bf16", "tensor", {"keep": 5, "block": 32, "force_diag": True}),
     ("block", 96, 128, 32, 4, "bf16", "tensor", {"keep": 3, "block": 32, "force_diag": False}),
     ("block", 333, 128, 32, 8, "bf16", "tensor", {"keep": 3, "block": 16, "force_diag": False}),
+    ("block", 1024, 128, 32, 8, "bf16", "tensor", {"keep": 7, "block": 32, "force_diag": False}),
+    ("block", 512, 64, 16, 4, "bf16", "tensor", {"keep": 16, "block": 16, "force_diag": True}),
+    ("row_topk", 512, 64, 16, 8, "bf16", "row", {"keep": 40}),
+    ("row_topk", 640, 128, 32, 4, "bf16", "row", {"keep": 3}),
+    ("row_topk", 1024, 64, 16, 4, "bf16", "tensor", {"keep": 64}),
     ("threshold", 700, 64, 16, 4, "bf16", "tensor", {"cap": 5, "causal": True}),
+    # theta = 400 / L: most rows keep one key or none (empty-row flags)
+    ("threshold", 700, 64, 16, 4, "bf16", "tensor", {"cap": 50, "causal": True, "frac_num": 1, "frac_den": 400}),
+    ("threshold", 640, 128, 32, 4, "bf16", "tensor", {"cap": 64, "causal": False}),
     ("threshold", 513, 64, 32, 4, "f32", "tensor", {"cap": 513, "causal": False}),
     # 8-bit levels: small exp scale c, so the cut lies beyond the 128-bin
     # histogram of the tensor-core threshold kernel (counting-pass path)
@@ -58,8 +66,11 @@ def test_shape(mode, L, d, k, bits, dtype, scope, extra, oracle):
         bad = [i for i in range(L) if not np.array_equal(rows_g[pr][i], rows[i])]
         assert not bad, f"{len(bad)} rows differ, first {bad[:4]}"
         rp, cols = ops.to_csr(rows)
-        zr, _ = oracle.sparse_attention(q[pr].double().numpy(), k_[pr].double().numpy(),
-                                        v[pr].double().numpy(), rp, cols, True, dtype == "f32")
+        zr, er = oracle.sparse_attention(q[pr].double().numpy(), k_[pr].double().numpy(),
+                                         v[pr].double().numpy(), rp, cols, True, dtype == "f32")
         zg = z[pr].double().cpu().numpy()
+        if mask.empty_rows is not None:
+            ge = mask.empty_rows[pr * L:(pr + 1) * L].cpu().numpy()
+            assert np.array_equal(ge.astype(bool), er.astype(bool)), "empty-row flags differ"
         worst = max(worst, np.abs(zg - zr).max() / max(np.abs(zr).max(), 1e-30))
     assert worst <= TOL[dtype], worst
