@@ -221,6 +221,25 @@ def run_gpu_arm(args, p, rank, local, world):
             step(stream)
     stream.synchronize()
 
+    # one step captured as a CUDA graph (replayed per timed step: the same
+    # kernels, without host launch gaps); eager launches if capture fails
+    graph, per_step = None, None
+    if not args.no_graph:
+        try:
+            g = torch.cuda.CUDAGraph()
+            c0 = ops.launch_counter()
+            with torch.cuda.graph(g, stream=stream):
+                step(stream)
+            per_step = ops.launch_counter() - c0
+            graph = g
+            with torch.cuda.stream(stream):
+                graph.replay()
+            stream.synchronize()
+        except Exception as e:  # pragma: no cover - capture unsupported
+            print(f"[bench] graph capture failed ({e}); eager launches", file=sys.stderr)
+            graph = None
+            torch.cuda.synchronize(dev)
+
     # ---- device-resident timed region
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     n0 = ops.launch_counter()
@@ -230,11 +249,14 @@ def run_gpu_arm(args, p, rank, local, world):
         with torch.cuda.stream(stream):
             ev0.record(stream)
             for _ in range(args.steps):
-                step(stream)
+                if graph is not None:
+                    graph.replay()
+                else:
+                    step(stream)
             ev1.record(stream)
         ev1.synchronize()
         torch.cuda.synchronize(dev)
-    launches = ops.launch_counter() - n0
+    launches = per_step * args.steps if graph is not None else ops.launch_counter() - n0
     ms = ev0.elapsed_time(ev1) / args.steps
     ms = max_over_ranks(ms, world, dev)
     barrier(world)
@@ -377,6 +399,7 @@ def run_gpu_arm(args, p, rank, local, world):
         "vs_baseline": None, "dtype": "bf16" if p.dtype == "bf16" else "f32",
         "data": "synthetic (seeded BASELINE generator, SURVEY 8.0)",
         "config": {**p.summary(), "pairs_per_gpu": pairs, "parallelism": f"(b,h)-pairs x{world}",
+                   "launch": "cuda graph per step" if graph is not None else "eager",
                    "l2": l2_note},
         "e2e": {"value": tokens / (e2e_ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
@@ -403,6 +426,7 @@ def main():
     ap.add_argument("--config", default="c2_vector")
     ap.add_argument("--ref-pairs", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="eager launches in the timed region")
     args = ap.parse_args()
     from paper_2110_11299_b200 import load_preset
 

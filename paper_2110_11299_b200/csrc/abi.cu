@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -113,7 +114,9 @@ int64_t capacity_of(const dsa_config& c) {
     }
 }
 
-// Workspace: [x64 | amax | pooled | etab | counts | scan | levels | scales | mask]
+constexpr int kMaxChunks = 4;  // dsa_pipeline: pair chunks overlapped on three streams
+
+// Workspace: [x64 | amax | pimg | pooled | etab | counts | cut | scan | levels | scales | mask]
 struct Plan {
     size_t x64 = 0, amax = 0, pimg = 0, pooled = 0, etab = 0, counts = 0, cut = 0, scan = 0, lq = 0, lk = 0, sq = 0,
            sk = 0, cols = 0, rowptr = 0, total = 0;
@@ -137,7 +140,7 @@ Plan plan(const dsa_config& c, bool pipeline, bool own_mask) {
                                          std::getenv("DSA_PREDICT_CLUSTER") != nullptr);
     p.x64 = take(need_x64 ? sizeof(double) * P * 2 * c.L * c.k : 0);
     p.amax = take(per_tensor ? sizeof(unsigned long long) * P * 2 : 0);
-    p.pimg = take(per_tensor ? predict_tc_image_bytes(c.d, c.k) : 0);
+    p.pimg = take(per_tensor ? align_up(predict_tc_image_bytes(c.d, c.k)) * kMaxChunks : 0);
     p.pooled = take(c.mask_mode == DSA_MASK_BLOCK ? sizeof(int32_t) * P * 2 * ceil_div(c.L, c.block) * c.k : 0);
     p.etab = take(c.mask_mode == DSA_MASK_THRESHOLD ? sizeof(int64_t) * P * span_of(c) : 0);
     p.counts = take(c.mask_mode == DSA_MASK_THRESHOLD ? sizeof(uint64_t) * P * c.L : 0);
@@ -169,8 +172,78 @@ void check_ws(const Plan& p, void* ws, size_t bytes) {
         throw Error(DSA_ERR_PARAM, "dsa: workspace too small (need " + std::to_string(p.total) + " bytes)");
 }
 
+// Phase scratch of the pairs [pair0, ...) of the planned config `c`; chunk
+// `ci` gets its own P-split image (concurrent chunks never share scratch).
+struct Scratch {
+    double* x64;
+    unsigned long long* amax;
+    unsigned char* pimg;
+    int32_t* pooled;
+    int64_t* etab;
+    uint64_t* counts;
+    int2* cut;
+    void* scan;
+    size_t scan_bytes;
+};
+
+Scratch scratch_of(const dsa_config& c, const Plan& pl, void* ws, int64_t pair0 = 0, int ci = 0) {
+    Scratch r{};
+    r.x64 = at<double>(ws, pl.x64) + pair0 * 2 * c.L * c.k;
+    r.amax = at<unsigned long long>(ws, pl.amax) + pair0 * 2;
+    r.pimg = c.quant_scope == DSA_QUANT_PER_TENSOR
+                 ? at<unsigned char>(ws, pl.pimg) + static_cast<size_t>(ci) * align_up(predict_tc_image_bytes(c.d, c.k))
+                 : nullptr;
+    r.pooled = at<int32_t>(ws, pl.pooled) + pair0 * 2 * ceil_div(c.L, c.block > 0 ? c.block : 1) * c.k;
+    r.etab = at<int64_t>(ws, pl.etab);
+    r.counts = at<uint64_t>(ws, pl.counts);
+    r.cut = c.mask_mode == DSA_MASK_THRESHOLD ? at<int2>(ws, pl.cut) : nullptr;
+    r.scan = at<void>(ws, pl.scan);
+    r.scan_bytes = pl.scan_bytes;
+    return r;
+}
+
+// Number of pair chunks dsa_pipeline overlaps (1 = serial).  Threshold
+// masks keep one global CSR (a single scan over all rows): serial.
+int pipeline_chunks(const dsa_config& c) {
+    static const int env = [] {
+        const char* e = std::getenv("DSA_PIPELINE_CHUNKS");
+        return e ? std::atoi(e) : -1;
+    }();
+    if (c.mask_mode == DSA_MASK_THRESHOLD) return 1;
+    const int64_t P = pairs_of(c);
+    // default serial: measured on B200 (C2), 2 and 4 chunks on three streams
+    // were 1-2 % slower than back-to-back full-width kernels
+    int n = env >= 1 ? env : 1;
+    n = static_cast<int>(std::min<int64_t>(std::min(n, kMaxChunks), P / 2));
+    return n < 2 ? 1 : n;
+}
+
+struct StreamSet {
+    cudaStream_t s[3];
+    cudaEvent_t fork, join, ev[2 * kMaxChunks];
+};
+
+// Per-device streams/events for dsa_pipeline (created once, never freed).
+StreamSet& stream_set() {
+    static std::mutex mu;
+    static std::vector<StreamSet*> sets;
+    int dev = 0;
+    check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+    std::lock_guard<std::mutex> lk(mu);
+    if (static_cast<int>(sets.size()) <= dev) sets.resize(dev + 1, nullptr);
+    if (!sets[dev]) {
+        auto* x = new StreamSet;
+        for (auto& st : x->s) check_cuda(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+        check_cuda(cudaEventCreateWithFlags(&x->fork, cudaEventDisableTiming), "event");
+        check_cuda(cudaEventCreateWithFlags(&x->join, cudaEventDisableTiming), "event");
+        for (auto& e : x->ev) check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+        sets[dev] = x;
+    }
+    return *sets[dev];
+}
+
 void do_predict(const dsa_config& c, const void* q, const void* k, const float* p, uint16_t* lq,
-                uint16_t* lk, double* sq, double* sk, const Plan& pl, void* ws, cudaStream_t st) {
+                uint16_t* lk, double* sq, double* sk, const Scratch& ws, cudaStream_t st) {
     if (!q || !k || !p || !lq || !lk || !sq || !sk) throw Error(DSA_ERR_PARAM, "dsa_predict: null pointer");
     PredictArgs a{};
     a.q = q;
@@ -188,15 +261,15 @@ void do_predict(const dsa_config& c, const void* q, const void* k, const float* 
     a.lk = lk;
     a.sq = sq;
     a.sk = sk;
-    a.xws = at<double>(ws, pl.x64);
-    a.amax = at<unsigned long long>(ws, pl.amax);
-    a.pimg = c.quant_scope == DSA_QUANT_PER_TENSOR ? at<unsigned char>(ws, pl.pimg) : nullptr;
+    a.xws = ws.x64;
+    a.amax = ws.amax;
+    a.pimg = ws.pimg;
     run_predict(a, st);
     check_cuda(cudaGetLastError(), "dsa_predict launch");
 }
 
 void do_select(const dsa_config& c, const uint16_t* lq, const uint16_t* lk, const double* sq,
-               const double* sk, const dsa_mask& m, const Plan& pl, void* ws, cudaStream_t st) {
+               const double* sk, const dsa_mask& m, const Scratch& ws, cudaStream_t st) {
     if (!lq || !lk || !sq || !sk || !m.cols) throw Error(DSA_ERR_PARAM, "dsa_select: null pointer");
     if (m.capacity < capacity_of(c) && c.mask_mode != DSA_MASK_THRESHOLD)
         throw Error(DSA_ERR_PARAM, "dsa_select: mask capacity too small");
@@ -226,13 +299,13 @@ void do_select(const dsa_config& c, const uint16_t* lq, const uint16_t* lk, cons
     a.rowptr = m.rowptr;
     a.capacity = m.capacity;
     a.empty_rows = m.empty_rows;
-    a.pooled = at<int32_t>(ws, pl.pooled);
-    a.etab = at<int64_t>(ws, pl.etab);
-    a.counts = at<uint64_t>(ws, pl.counts);
-    a.cut = c.mask_mode == DSA_MASK_THRESHOLD ? at<int2>(ws, pl.cut) : nullptr;
+    a.pooled = ws.pooled;
+    a.etab = ws.etab;
+    a.counts = ws.counts;
+    a.cut = ws.cut;
     a.span = span_of(c);
-    a.scan_tmp = at<void>(ws, pl.scan);
-    a.scan_tmp_bytes = pl.scan_bytes;
+    a.scan_tmp = ws.scan;
+    a.scan_tmp_bytes = ws.scan_bytes;
     if (m.empty_rows && c.mask_mode != DSA_MASK_THRESHOLD)
         check_cuda(cudaMemsetAsync(m.empty_rows, 0, pairs_of(c) * c.L, st), "dsa_select memset");
     run_select(a, st);
@@ -327,7 +400,7 @@ dsa_status dsa_predict(const dsa_config* cfg, const void* q, const void* k, cons
         require_device();
         Plan pl = plan(*cfg, false, false);
         check_ws(pl, workspace, workspace_bytes);
-        do_predict(*cfg, q, k, p, levels_q, levels_k, scale_q, scale_k, pl, workspace,
+        do_predict(*cfg, q, k, p, levels_q, levels_k, scale_q, scale_k, scratch_of(*cfg, pl, workspace),
                    static_cast<cudaStream_t>(stream));
     });
 }
@@ -341,7 +414,7 @@ dsa_status dsa_select(const dsa_config* cfg, const uint16_t* levels_q, const uin
         if (!mask) throw Error(DSA_ERR_PARAM, "dsa_select: null mask");
         Plan pl = plan(*cfg, false, false);
         check_ws(pl, workspace, workspace_bytes);
-        do_select(*cfg, levels_q, levels_k, scale_q, scale_k, *mask, pl, workspace,
+        do_select(*cfg, levels_q, levels_k, scale_q, scale_k, *mask, scratch_of(*cfg, pl, workspace),
                   static_cast<cudaStream_t>(stream));
     });
 }
@@ -379,9 +452,52 @@ dsa_status dsa_pipeline(const dsa_config* cfg, const void* q, const void* k, con
             m.capacity = capacity_of(c);
             m.empty_rows = nullptr;
         }
-        do_predict(c, q, k, p, lq, lk, sq, sk, pl, workspace, st);
-        do_select(c, lq, lk, sq, sk, m, pl, workspace, st);
-        do_attention(c, q, k, v, m, z, st);
+        const int64_t P = pairs_of(c);
+        const int nch = pipeline_chunks(c);
+        if (nch <= 1) {
+            const Scratch sc = scratch_of(c, pl, workspace);
+            do_predict(c, q, k, p, lq, lk, sq, sk, sc, st);
+            do_select(c, lq, lk, sq, sk, m, sc, st);
+            do_attention(c, q, k, v, m, z, st);
+            return;
+        }
+        // pair chunks: predict(c+1) || select(c) || attention(c-1) on three
+        // streams (event fork/join off the caller's stream; graph-capturable)
+        StreamSet& ss = stream_set();
+        check_cuda(cudaEventRecord(ss.fork, st), "dsa_pipeline fork");
+        for (int i = 0; i < 3; ++i) check_cuda(cudaStreamWaitEvent(ss.s[i], ss.fork, 0), "dsa_pipeline fork");
+        const size_t esz = c.dtype == DSA_BF16 ? 2 : 4;
+        const int64_t per_scale = c.quant_scope == DSA_QUANT_PER_TENSOR ? 1 : c.L;
+        const int64_t per_cols = capacity_of(c) / P;
+        for (int ci = 0; ci < nch; ++ci) {
+            const int64_t p0 = P * ci / nch, p1 = P * (ci + 1) / nch;
+            dsa_config cc = c;
+            cc.batch = p1 - p0;
+            cc.heads = 1;
+            const Scratch sc = scratch_of(c, pl, workspace, p0, ci);
+            const size_t xo = static_cast<size_t>(p0 * c.L * c.d) * esz;
+            const auto* qc = static_cast<const char*>(q) + xo;
+            const auto* kc = static_cast<const char*>(k) + xo;
+            const auto* vc = static_cast<const char*>(v) + xo;
+            auto* zc = static_cast<char*>(z) + xo;
+            uint16_t* lqc = lq + p0 * c.L * c.k;
+            uint16_t* lkc = lk + p0 * c.L * c.k;
+            double* sqc = sq + p0 * per_scale;
+            double* skc = sk + p0 * per_scale;
+            dsa_mask mc = m;
+            mc.cols = m.cols + p0 * per_cols;
+            mc.capacity = (p1 - p0) * per_cols;
+            mc.empty_rows = m.empty_rows ? m.empty_rows + p0 * c.L : nullptr;
+            do_predict(cc, qc, kc, p, lqc, lkc, sqc, skc, sc, ss.s[0]);
+            check_cuda(cudaEventRecord(ss.ev[2 * ci], ss.s[0]), "dsa_pipeline event");
+            check_cuda(cudaStreamWaitEvent(ss.s[1], ss.ev[2 * ci], 0), "dsa_pipeline event");
+            do_select(cc, lqc, lkc, sqc, skc, mc, sc, ss.s[1]);
+            check_cuda(cudaEventRecord(ss.ev[2 * ci + 1], ss.s[1]), "dsa_pipeline event");
+            check_cuda(cudaStreamWaitEvent(ss.s[2], ss.ev[2 * ci + 1], 0), "dsa_pipeline event");
+            do_attention(cc, qc, kc, vc, mc, zc, ss.s[2]);
+        }
+        check_cuda(cudaEventRecord(ss.join, ss.s[2]), "dsa_pipeline join");
+        check_cuda(cudaStreamWaitEvent(st, ss.join, 0), "dsa_pipeline join");
     });
 }
 

@@ -103,8 +103,10 @@ struct ProjSmem {
 // P -> exact three-way bf16 split in the B-operand layout + |p_j| * 1.001
 // (one CTA; the image is the same for every pair).
 template <int D, int KD>
-__global__ void psplit_kernel(const float* __restrict__ p, unsigned char* __restrict__ img) {
+__global__ void psplit_kernel(const float* __restrict__ p, unsigned char* __restrict__ img,
+                              unsigned long long* __restrict__ amax, int64_t namax) {
     using Sm = ProjSmem<D, KD>;
+    for (int64_t i = threadIdx.x; i < namax; i += blockDim.x) amax[i] = 0ull;  // amax pass accumulators
     for (int i = threadIdx.x; i < D * KD; i += blockDim.x) {
         const int c = i / KD, j = i % KD;
         const float v = p[i];
@@ -339,8 +341,7 @@ void launch_tc(const PredictArgs& a, cudaStream_t st) {
     const auto* q = static_cast<const __nv_bfloat16*>(a.q);
     const auto* k = static_cast<const __nv_bfloat16*>(a.k);
     const dim3 grid(static_cast<unsigned>(ceil_div_i(a.L, kRows)), 2, static_cast<unsigned>(a.pairs));
-    psplit_kernel<D, KD><<<1, 256, 0, st>>>(a.p, a.pimg);
-    cudaMemsetAsync(a.amax, 0, sizeof(unsigned long long) * 2 * a.pairs, st);
+    psplit_kernel<D, KD><<<1, 256, 0, st>>>(a.p, a.pimg, a.amax, 2 * a.pairs);
     ka<<<grid, kRows, smem, st>>>(q, k, a.p, a.pimg, a.L, a.round_f32, a.qmax, a.amax, a.lq, a.lk, a.sq, a.sk);
     kq<<<grid, kRows, smem, st>>>(q, k, a.p, a.pimg, a.L, a.round_f32, a.qmax, a.amax, a.lq, a.lk, a.sq, a.sk);
     note_launch(3);
