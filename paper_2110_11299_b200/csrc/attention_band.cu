@@ -654,7 +654,7 @@ __global__ void __launch_bounds__(kWarps * 32)
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 // a column may have no live key yet (m_run = -inf): weight 0
-                const float pv = s[mt][u] == -INFINITY ? 0.f : exp2f(s[mt][u] - m_run[u & 1]);
+                const float pv = (SEG && s[mt][u] == -INFINITY) ? 0.f : exp2f(s[mt][u] - m_run[u & 1]);
                 l_part[u & 1] += pv;
                 sm.p[(2 * c4 + (u & 1)) * PW + mt * 16 + g + (u >> 1) * 8] = __float2bfloat16_rn(pv);
             }
