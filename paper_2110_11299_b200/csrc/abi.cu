@@ -118,7 +118,7 @@ constexpr int kMaxChunks = 4;  // dsa_pipeline: pair chunks overlapped on three 
 
 // Workspace: [x64 | amax | pimg | pooled | etab | counts | cut | scan | levels | scales | mask]
 struct Plan {
-    size_t x64 = 0, amax = 0, pimg = 0, pooled = 0, etab = 0, counts = 0, cut = 0, scan = 0, lq = 0, lk = 0, sq = 0,
+    size_t x64 = 0, amax = 0, pimg = 0, ovf = 0, pooled = 0, etab = 0, counts = 0, cut = 0, scan = 0, lq = 0, lk = 0, sq = 0,
            sk = 0, cols = 0, rowptr = 0, total = 0;
     size_t scan_bytes = 0;
 };
@@ -141,6 +141,8 @@ Plan plan(const dsa_config& c, bool pipeline, bool own_mask) {
     p.x64 = take(need_x64 ? sizeof(double) * P * 2 * c.L * c.k : 0);
     p.amax = take(per_tensor ? sizeof(unsigned long long) * P * 2 : 0);
     p.pimg = take(per_tensor ? align_up(predict_tc_image_bytes(c.d, c.k)) * kMaxChunks : 0);
+    const bool row_scaled = c.mask_mode == DSA_MASK_ROW_TOPK && !per_tensor;
+    p.ovf = take(row_scaled ? 16 + sizeof(int64_t) * P * c.L : 0);  // overflow count + row list
     p.pooled = take(c.mask_mode == DSA_MASK_BLOCK ? sizeof(int32_t) * P * 2 * ceil_div(c.L, c.block) * c.k : 0);
     p.etab = take(c.mask_mode == DSA_MASK_THRESHOLD ? sizeof(int64_t) * P * span_of(c) : 0);
     p.counts = take(c.mask_mode == DSA_MASK_THRESHOLD ? sizeof(uint64_t) * P * c.L : 0);
@@ -184,6 +186,8 @@ struct Scratch {
     int2* cut;
     void* scan;
     size_t scan_bytes;
+    unsigned* ovf_n;
+    int64_t* ovf_list;
 };
 
 Scratch scratch_of(const dsa_config& c, const Plan& pl, void* ws, int64_t pair0 = 0, int ci = 0) {
@@ -199,6 +203,9 @@ Scratch scratch_of(const dsa_config& c, const Plan& pl, void* ws, int64_t pair0 
     r.cut = c.mask_mode == DSA_MASK_THRESHOLD ? at<int2>(ws, pl.cut) : nullptr;
     r.scan = at<void>(ws, pl.scan);
     r.scan_bytes = pl.scan_bytes;
+    const bool row_scaled = c.mask_mode == DSA_MASK_ROW_TOPK && c.quant_scope != DSA_QUANT_PER_TENSOR;
+    r.ovf_n = row_scaled ? at<unsigned>(ws, pl.ovf) + pair0 * 0 : nullptr;
+    r.ovf_list = row_scaled ? reinterpret_cast<int64_t*>(at<char>(ws, pl.ovf) + 16) : nullptr;
     return r;
 }
 
@@ -306,6 +313,8 @@ void do_select(const dsa_config& c, const uint16_t* lq, const uint16_t* lk, cons
     a.span = span_of(c);
     a.scan_tmp = ws.scan;
     a.scan_tmp_bytes = ws.scan_bytes;
+    a.ovf_n = ws.ovf_n;
+    a.ovf_list = ws.ovf_list;
     if (m.empty_rows && c.mask_mode != DSA_MASK_THRESHOLD)
         check_cuda(cudaMemsetAsync(m.empty_rows, 0, pairs_of(c) * c.L, st), "dsa_select memset");
     run_select(a, st);

@@ -64,6 +64,8 @@ struct SelectArgs {
     int64_t* etab;      // threshold: [pairs][span]
     uint64_t* counts;   // threshold: [pairs*L]
     int2* cut;          // threshold: [pairs*L] {v_cut, tie quota}
+    unsigned* ovf_n;    // per-row top-k: overflow row count
+    int64_t* ovf_list;  // per-row top-k: overflow rows [pairs*L]
     int64_t span;
     void* scan_tmp;
     size_t scan_tmp_bytes;
@@ -75,6 +77,9 @@ bool colvec_ws_supported(const SelectArgs& a);
 void run_colvec_ws(const SelectArgs& a, cudaStream_t st);
 void run_colvec_tc(const SelectArgs& a, cudaStream_t st);
 bool threshold_tc_supported(const SelectArgs& a);
+bool topk_tc_supported(const SelectArgs& a);
+void run_topk_tc(const SelectArgs& a, cudaStream_t st);
+void launch_topk_scaled_list(const SelectArgs& a, const int64_t* list, const unsigned* nlist, cudaStream_t st);
 void run_threshold_tc(const SelectArgs& a, cudaStream_t st);
 void launch_exp_table(const SelectArgs& a, cudaStream_t st);
 void scan_counts(const SelectArgs& a, cudaStream_t st);

@@ -242,8 +242,7 @@ __global__ void __launch_bounds__(kNT) topk_rows_generic(SelectArgs a) {
 // double product (ties: lowest column) -- half the radix passes of a 64-bit
 // select and the same result.
 template <int KD>
-__global__ void __launch_bounds__(kNT) topk_rows_scaled(SelectArgs a) {
-    extern __shared__ __align__(16) unsigned char dsm[];
+__device__ __forceinline__ void topk_row_scaled(const SelectArgs& a, int64_t pair, int64_t i, unsigned char* dsm) {
     const int L = static_cast<int>(a.L);
     uint32_t* keys = reinterpret_cast<uint32_t*>(dsm);            // [L]
     int32_t* ties = reinterpret_cast<int32_t*>(keys + L);          // [L]
@@ -251,7 +250,6 @@ __global__ void __launch_bounds__(kNT) topk_rows_scaled(SelectArgs a) {
     uint8_t* take = reinterpret_cast<uint8_t*>(sv + L);            // [L]
     __shared__ SelSmem s;
     __shared__ unsigned tie_count;
-    const int64_t i = blockIdx.x, pair = blockIdx.y;
     const int tid = threadIdx.x;
     const double* skp = a.sk + pair * a.L;
     float q[KD];
@@ -295,6 +293,23 @@ __global__ void __launch_bounds__(kNT) topk_rows_scaled(SelectArgs a) {
         lt = keys[j] < T || (keys[j] == T && take[j]);
         eq = false;
     }, out, s);
+}
+
+// rows = blockIdx (grid L x pairs), or the rows listed in `list` (pair * L +
+// row, count *nlist; grid-stride) -- the overflow fallback of topk_tc.
+template <int KD>
+__global__ void __launch_bounds__(kNT) topk_rows_scaled(SelectArgs a, const int64_t* list, const unsigned* nlist) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    if (list == nullptr) {
+        topk_row_scaled<KD>(a, blockIdx.y, blockIdx.x, dsm);
+        return;
+    }
+    const unsigned n = *nlist;
+    for (unsigned idx = blockIdx.x; idx < n; idx += gridDim.x) {
+        const int64_t g = list[idx];
+        topk_row_scaled<KD>(a, g / a.L, g % a.L, dsm);
+        __syncthreads();
+    }
 }
 
 // -------------------------------------------------------------- colvec
@@ -559,7 +574,7 @@ void launch_select(const SelectArgs& a, cudaStream_t st) {
                 const size_t sm = static_cast<size_t>(a.L) * 11;
                 auto kern = topk_rows_scaled<KD>;
                 cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
-                kern<<<dim3(static_cast<unsigned>(a.L), P), kNT, sm, st>>>(a);
+                kern<<<dim3(static_cast<unsigned>(a.L), P), kNT, sm, st>>>(a, nullptr, nullptr);
                 note_launch();
             } else if (a.per_row) {
                 const size_t sm = static_cast<size_t>(a.L) * 8;
@@ -639,6 +654,19 @@ void scan_counts(const SelectArgs& a, cudaStream_t st) {
     cub::DeviceScan::InclusiveSum(a.scan_tmp, tb, a.counts, a.rowptr + 1, static_cast<int64_t>(a.pairs * a.L), st);
 }
 
+void launch_topk_scaled_list(const SelectArgs& a, const int64_t* list, const unsigned* nlist, cudaStream_t st) {
+    const size_t sm = static_cast<size_t>(a.L) * 11;
+    const unsigned grid = 148 * 4;  // grid-stride over the (normally empty) list
+    if (a.KD == 16) {
+        cudaFuncSetAttribute(topk_rows_scaled<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+        topk_rows_scaled<16><<<grid, kNT, sm, st>>>(a, list, nlist);
+    } else {
+        cudaFuncSetAttribute(topk_rows_scaled<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+        topk_rows_scaled<32><<<grid, kNT, sm, st>>>(a, list, nlist);
+    }
+    note_launch();
+}
+
 size_t select_scan_tmp_bytes(int64_t n) {
     size_t b = 0;
     cub::DeviceScan::InclusiveSum(nullptr, b, static_cast<const uint64_t*>(nullptr),
@@ -658,6 +686,10 @@ void run_select(const SelectArgs& a, cudaStream_t st) {
     }
     if (threshold_tc_supported(a)) {
         run_threshold_tc(a, st);
+        return;
+    }
+    if (topk_tc_supported(a)) {
+        run_topk_tc(a, st);
         return;
     }
     switch (a.KD) {
