@@ -118,9 +118,10 @@ constexpr int kMaxChunks = 4;  // dsa_pipeline: pair chunks overlapped on three 
 
 // Workspace: [x64 | amax | pimg | pooled | etab | counts | cut | scan | levels | scales | mask]
 struct Plan {
-    size_t x64 = 0, amax = 0, pimg = 0, ovf = 0, pooled = 0, etab = 0, counts = 0, cut = 0, scan = 0, lq = 0, lk = 0, sq = 0,
+    size_t x64 = 0, xhat = 0, amax = 0, pimg = 0, ovf = 0, pooled = 0, etab = 0, counts = 0, cut = 0, scan = 0, lq = 0, lk = 0, sq = 0,
            sk = 0, cols = 0, rowptr = 0, total = 0;
     size_t scan_bytes = 0;
+    bool has_xhat = false;
 };
 
 Plan plan(const dsa_config& c, bool pipeline, bool own_mask) {
@@ -139,6 +140,12 @@ Plan plan(const dsa_config& c, bool pipeline, bool own_mask) {
     const bool need_x64 = per_tensor && (!tc_path || std::getenv("DSA_PREDICT_DFMA") != nullptr ||
                                          std::getenv("DSA_PREDICT_CLUSTER") != nullptr);
     p.x64 = take(need_x64 ? sizeof(double) * P * 2 * c.L * c.k : 0);
+    // stored x^ for the streaming quantise pass (DSA_PREDICT_TWO_READS=1: the
+    // quantise pass re-reads Q/K and recomputes x^ instead).  8-bit levels
+    // leave ~1 % of the levels uncertified, which the cooperative recompute
+    // of the two-read pass handles far better than a per-thread chain.
+    p.has_xhat = per_tensor && tc_path && c.bits <= 4 && std::getenv("DSA_PREDICT_TWO_READS") == nullptr;
+    p.xhat = take(p.has_xhat ? sizeof(float) * P * 2 * c.L * (c.k + 1) : 0);
     p.amax = take(per_tensor ? sizeof(unsigned long long) * P * 2 : 0);
     p.pimg = take(per_tensor ? align_up(predict_tc_image_bytes(c.d, c.k)) * kMaxChunks : 0);
     const bool row_scaled = c.mask_mode == DSA_MASK_ROW_TOPK && !per_tensor;
@@ -178,6 +185,7 @@ void check_ws(const Plan& p, void* ws, size_t bytes) {
 // `ci` gets its own P-split image (concurrent chunks never share scratch).
 struct Scratch {
     double* x64;
+    float* xhat;
     unsigned long long* amax;
     unsigned char* pimg;
     int32_t* pooled;
@@ -193,6 +201,7 @@ struct Scratch {
 Scratch scratch_of(const dsa_config& c, const Plan& pl, void* ws, int64_t pair0 = 0, int ci = 0) {
     Scratch r{};
     r.x64 = at<double>(ws, pl.x64) + pair0 * 2 * c.L * c.k;
+    r.xhat = pl.has_xhat ? at<float>(ws, pl.xhat) + pair0 * 2 * c.L * (c.k + 1) : nullptr;
     r.amax = at<unsigned long long>(ws, pl.amax) + pair0 * 2;
     r.pimg = c.quant_scope == DSA_QUANT_PER_TENSOR
                  ? at<unsigned char>(ws, pl.pimg) + static_cast<size_t>(ci) * align_up(predict_tc_image_bytes(c.d, c.k))
@@ -269,6 +278,7 @@ void do_predict(const dsa_config& c, const void* q, const void* k, const float* 
     a.sq = sq;
     a.sk = sk;
     a.xws = ws.x64;
+    a.xhat = ws.xhat;
     a.amax = ws.amax;
     a.pimg = ws.pimg;
     run_predict(a, st);

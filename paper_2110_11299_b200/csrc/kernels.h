@@ -30,6 +30,7 @@ struct PredictArgs {
     double* xws;                // per-tensor: [pairs][2][L][KD] f64 scratch
     unsigned long long* amax;  // per-tensor: [pairs][2]
     unsigned char* pimg;       // tensor-core path: P-split operand image
+    float* xhat;               // tensor-core path: x^ [pairs][2][L][KD] + bound factors [pairs][2][L]
 };
 void run_predict(const PredictArgs& a, cudaStream_t st);
 bool predict_fast_supported(const PredictArgs& a);

@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(kRows)
                       const float* __restrict__ p, const unsigned char* __restrict__ img, int64_t L,
                       int round_f32, double qmax, unsigned long long* __restrict__ amax,
                       uint16_t* __restrict__ lq, uint16_t* __restrict__ lk, double* __restrict__ sq,
-                      double* __restrict__ sk) {
+                      double* __restrict__ sk, float* __restrict__ xhat) {
     using Sm = ProjSmem<D, KD>;
     constexpr int N = Sm::N;
     constexpr int TC = N <= 64 ? 64 : 128;  // TMEM columns
@@ -247,6 +247,14 @@ __global__ void __launch_bounds__(kRows)
         }
     }
     tc::fence_before_sync();
+    if (!QUANT && xhat != nullptr && valid) {
+        // x^ and the row's bound factor for the streaming quantise pass:
+        // [pair][tensor][L][KD] floats, then [pair][tensor][L] factors
+        float* xo = xhat + ((pair * 2 + which) * L + r) * KD;
+#pragma unroll
+        for (int j = 0; j < KD; j += 4) *reinterpret_cast<float4*>(xo + j) = make_float4(xv[j], xv[j + 1], xv[j + 2], xv[j + 3]);
+        xhat[gridDim.z * 2 * L * KD + (pair * 2 + which) * L + r] = dq;
+    }
     if (!QUANT) {
         // e_j <= E_row = |q| d 2^-22 max_j |p_j| + rel max_j |x_j|: one bound per
         // row keeps the candidate test to a compare per element
@@ -324,6 +332,62 @@ __global__ void __launch_bounds__(kRows)
     if (warp == 0) tc::tmem_dealloc<TC>(tmem);
 }
 
+// Streaming quantise pass over the stored x^ (thread = row x 8 columns):
+// certified level, or the reference chain from the row in global memory.
+template <int D, int KD>
+__global__ void __launch_bounds__(256)
+    quantize_xhat_kernel(const float* __restrict__ xhat, const __nv_bfloat16* __restrict__ q,
+                         const __nv_bfloat16* __restrict__ k, const float* __restrict__ p,
+                         const unsigned char* __restrict__ img, int64_t pairs, int64_t L, int round_f32,
+                         double qmax, const unsigned long long* __restrict__ amax, uint16_t* __restrict__ lq,
+                         uint16_t* __restrict__ lk, double* __restrict__ sq, double* __restrict__ sk) {
+    using Sm = ProjSmem<D, KD>;
+    constexpr int NC = KD / 8;
+    const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= pairs * 2 * L * NC) return;
+    const int c = static_cast<int>(idx % NC);
+    const int64_t rr = idx / NC;  // (pair * 2 + which) * L + r
+    const int64_t r = rr % L, pw = rr / L;
+    const int which = static_cast<int>(pw & 1);
+    const int64_t pair = pw >> 1;
+    const double am = __longlong_as_double(static_cast<long long>(amax[pw]));
+    const double s = am / qmax;
+    if (r == 0 && c == 0) (which ? sk : sq)[pair] = am == 0.0 ? 0.0 : s;
+    const float inv_s = static_cast<float>(qmax / am);
+    const float qm = static_cast<float>(qmax);
+    const float rel = round_f32 ? 2.4e-7f : 1.2e-7f;
+    const float* pn = reinterpret_cast<const float*>(img + Sm::kB);
+    const float4 a0 = __ldg(reinterpret_cast<const float4*>(xhat + rr * KD + c * 8));
+    const float4 a1 = __ldg(reinterpret_cast<const float4*>(xhat + rr * KD + c * 8 + 4));
+    const float dq = __ldg(xhat + pairs * 2 * L * KD + rr);
+    const float xv[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+    uint32_t w[4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+        float lv2[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int j = c * 8 + 2 * h + u;
+            float lv = 0.f;
+            if (am != 0.0) {
+                lv = cert_level(xv[2 * h + u], fmaf(dq, __ldg(pn + j), fabsf(xv[2 * h + u]) * rel) + 1e-30f, inv_s, qm);
+                if (lv != lv) {  // uncertified: the reference chain
+                    const __nv_bfloat16* row = (which ? k : q) + (pair * L + r) * D;
+                    double acc = 0.0;
+                    for (int t = 0; t < D; ++t)
+                        acc = fma(to_double(row[t]), static_cast<double>(__ldg(p + t * KD + j)), acc);
+                    if (round_f32) acc = static_cast<double>(static_cast<float>(acc));
+                    lv = static_cast<float>(fmin(fmax(round_half_away(acc / s), -qmax), qmax));
+                }
+            }
+            lv2[u] = lv;
+        }
+        w[h] = (__float_as_uint(lv2[0]) >> 16) | ((__float_as_uint(lv2[1]) >> 16) << 16);
+    }
+    uint16_t* out = (which ? lk : lq) + pair * L * KD;
+    *reinterpret_cast<uint4*>(out + lvl_index(L, r, c * 8)) = make_uint4(w[0], w[1], w[2], w[3]);
+}
+
 template <int D, int KD>
 void launch_tc(const PredictArgs& a, cudaStream_t st) {
     using Sm = ProjSmem<D, KD>;
@@ -342,8 +406,19 @@ void launch_tc(const PredictArgs& a, cudaStream_t st) {
     const auto* k = static_cast<const __nv_bfloat16*>(a.k);
     const dim3 grid(static_cast<unsigned>(ceil_div_i(a.L, kRows)), 2, static_cast<unsigned>(a.pairs));
     psplit_kernel<D, KD><<<1, 256, 0, st>>>(a.p, a.pimg, a.amax, 2 * a.pairs);
-    ka<<<grid, kRows, smem, st>>>(q, k, a.p, a.pimg, a.L, a.round_f32, a.qmax, a.amax, a.lq, a.lk, a.sq, a.sk);
-    kq<<<grid, kRows, smem, st>>>(q, k, a.p, a.pimg, a.L, a.round_f32, a.qmax, a.amax, a.lq, a.lk, a.sq, a.sk);
+    if (a.xhat != nullptr) {
+        // amax pass stores x^ (fp32) + bound factors; the quantise pass streams them
+        ka<<<grid, kRows, smem, st>>>(q, k, a.p, a.pimg, a.L, a.round_f32, a.qmax, a.amax, a.lq, a.lk, a.sq, a.sk,
+                                      a.xhat);
+        const int64_t n = a.pairs * 2 * a.L * (KD / 8);
+        quantize_xhat_kernel<D, KD><<<static_cast<unsigned>(ceil_div_i(n, 256)), 256, 0, st>>>(
+            a.xhat, q, k, a.p, a.pimg, a.pairs, a.L, a.round_f32, a.qmax, a.amax, a.lq, a.lk, a.sq, a.sk);
+    } else {
+        ka<<<grid, kRows, smem, st>>>(q, k, a.p, a.pimg, a.L, a.round_f32, a.qmax, a.amax, a.lq, a.lk, a.sq, a.sk,
+                                      nullptr);
+        kq<<<grid, kRows, smem, st>>>(q, k, a.p, a.pimg, a.L, a.round_f32, a.qmax, a.amax, a.lq, a.lk, a.sq, a.sk,
+                                      nullptr);
+    }
     note_launch(3);
 }
 
