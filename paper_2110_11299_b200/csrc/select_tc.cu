@@ -74,7 +74,22 @@ struct ColvecSmem {
 
 // NQ = 64: 8 bands per CTA, ~100 KB of shared memory -> two CTAs per SM, so
 // one CTA's selection overlaps the other's tensor-core / TMEM score loop.
-template <int KD, int NQ>
+// TMA = true: one lane issues every operand copy as TMA-engine bulk copies
+// (the chunk-planar levels make each 8-column plane of a tile one
+// contiguous run; the planes become the K-adjacent core matrices, LBO =
+// rows * 16, SBO = 128) completing on per-slot mbarriers -- no per-thread
+// cp.async address math and no generic->async proxy fence per tile.
+template <int KD>
+__device__ __forceinline__ void bulk_tile(uint32_t sdst, const uint16_t* __restrict__ src, int64_t row0,
+                                          int rows_cap, int64_t L, uint64_t* bar) {
+    const uint32_t rows = static_cast<uint32_t>(L - row0 < rows_cap ? L - row0 : rows_cap);
+    tc::mbar_expect_tx(bar, (KD / 8) * rows * 16);
+#pragma unroll
+    for (int c = 0; c < KD / 8; ++c)
+        tc::bulk_g2s(sdst + c * (rows_cap * 16), src + (c * L + row0) * 8, rows * 16, bar);
+}
+
+template <int KD, int NQ, bool TMA>
 __global__ void __launch_bounds__(kThreads, NQ == 64 ? 2 : 1)
     colvec_tc_kernel(const uint16_t* __restrict__ lq, const uint16_t* __restrict__ lk, int64_t L,
                      int64_t keep, int M, uint32_t* __restrict__ out, int dbg) {
@@ -94,7 +109,8 @@ __global__ void __launch_bounds__(kThreads, NQ == 64 ? 2 : 1)
     uint32_t* obufs = reinterpret_cast<uint32_t*>(p); p += (kThreads / 32) * kList * 4;
     int* bandmax = reinterpret_cast<int*>(p);   p += 16 * 4;
     uint64_t* bars = reinterpret_cast<uint64_t*>(p);  // one per TMEM accumulator
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kAcc);
+    uint64_t* full = bars + kAcc;                     // TMA: one per ring slot, then the Q~ block
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kAcc + kStages + 1);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int quarter = warp & 3, half = warp >> 2;  // TMEM lane quarter, column half
@@ -104,17 +120,24 @@ __global__ void __launch_bounds__(kThreads, NQ == 64 ? 2 : 1)
     const uint16_t* lkp = lk + pair * L * KD;
 
     if (tid == 0) {
-        for (int b = 0; b < kAcc; ++b) tc::mbar_init(&bars[b], 1);
+        for (int b = 0; b < kAcc + (TMA ? kStages + 1 : 0); ++b) tc::mbar_init(&bars[b], 1);
         tc::fence_barrier_init();
+        if (TMA) {
+            bulk_tile<KD>(tc::smem_addr(bq), lqp, q0, NQ, L, &full[kStages]);
+            for (int s = 0; s < kStages && s < nt; ++s)
+                bulk_tile<KD>(tc::smem_addr(ring + s * kTile), lkp, static_cast<int64_t>(s) * kMT, kMT, L, &full[s]);
+        }
     }
     if (tid < NB) bandmax[tid] = INT32_MIN;
     if (warp == 0) tc::tmem_alloc<kAcc * NQ>(tmem_slot);
 
     // prologue: Q~ block + first kStages K~ tiles (group t <-> tile t)
-    load_tile<KD, NQ>(tc::smem_addr(bq), lqp, q0, L, tid);
-    for (int s = 0; s < kStages; ++s) {
-        if (s < nt) load_tile<KD>(tc::smem_addr(ring + s * kTile), lkp, static_cast<int64_t>(s) * kMT, L, tid);
-        cp_commit();
+    if (!TMA) {
+        load_tile<KD, NQ>(tc::smem_addr(bq), lqp, q0, L, tid);
+        for (int s = 0; s < kStages; ++s) {
+            if (s < nt) load_tile<KD>(tc::smem_addr(ring + s * kTile), lkp, static_cast<int64_t>(s) * kMT, L, tid);
+            cp_commit();
+        }
     }
     tc::fence_before_sync();
     __syncthreads();
@@ -132,19 +155,29 @@ __global__ void __launch_bounds__(kThreads, NQ == 64 ? 2 : 1)
     // whose MMA finished long ago; its K~ slot is then refilled with tile
     // t - kLag + kStages.  One __syncthreads per tile.
     for (int t = 0; t < nt + kLag; ++t) {
-        if (t < nt) {
+        if (!TMA && t < nt) {
             cp_wait<kStages - 1 - kLag>();
             tc::fence_proxy_async();
         }
         __syncthreads();
         if (t < nt && tid == 0) {
+            if (TMA) {
+                if (t == 0) tc::mbar_wait(&full[kStages], 0);
+                tc::mbar_wait(&full[t % kStages], (t / kStages) & 1);
+            }
             tc::fence_after_sync();
             const uint32_t abase = tc::smem_addr(ring + (t % kStages) * kTile);
 #pragma unroll
             for (int ks = 0; ks < KD / 16; ++ks) {
-                const uint64_t ad = tc::desc_kmajor_nosw(abase + ks * 256, 128, KD * 16);
-                const uint64_t bd = bdesc + static_cast<uint64_t>((ks * 256) >> 4);
-                tc::mma_bf16(tmem + (t % kAcc) * NQ, ad, bd, idesc, ks > 0);
+                if (TMA) {
+                    const uint64_t ad = tc::desc_kmajor_nosw(abase + ks * 2 * (kMT * 16), kMT * 16, 128);
+                    const uint64_t bd = tc::desc_kmajor_nosw(tc::smem_addr(bq) + ks * 2 * (NQ * 16), NQ * 16, 128);
+                    tc::mma_bf16(tmem + (t % kAcc) * NQ, ad, bd, idesc, ks > 0);
+                } else {
+                    const uint64_t ad = tc::desc_kmajor_nosw(abase + ks * 256, 128, KD * 16);
+                    const uint64_t bd = bdesc + static_cast<uint64_t>((ks * 256) >> 4);
+                    tc::mma_bf16(tmem + (t % kAcc) * NQ, ad, bd, idesc, ks > 0);
+                }
             }
             tc::commit(&bars[t % kAcc]);
         }
@@ -185,10 +218,18 @@ __global__ void __launch_bounds__(kThreads, NQ == 64 ? 2 : 1)
             tc::fence_before_sync();
             // tile u's K~ slot is free (its MMA completed): refill it
             const int nxt = u + kStages;
-            if (nxt < nt)
-                load_tile<KD>(tc::smem_addr(ring + (u % kStages) * kTile), lkp, static_cast<int64_t>(nxt) * kMT, L, tid);
+            if (nxt < nt) {
+                if (TMA) {
+                    if (tid == 0)
+                        bulk_tile<KD>(tc::smem_addr(ring + (u % kStages) * kTile), lkp, static_cast<int64_t>(nxt) * kMT,
+                                      kMT, L, &full[u % kStages]);
+                } else {
+                    load_tile<KD>(tc::smem_addr(ring + (u % kStages) * kTile), lkp, static_cast<int64_t>(nxt) * kMT, L,
+                                  tid);
+                }
+            }
         }
-        cp_commit();
+        if (!TMA) cp_commit();
     }
     __syncthreads();
     // band maxima: warp reduce, then shared atomics across the 4 lane quarters
@@ -387,7 +428,7 @@ template <int KD, int NQ>
 size_t colvec_smem_bytes(int64_t L) {
     const int64_t nt = (L + kMT - 1) / kMT;
     return ColvecSmem<KD>::kTileBytes * kStages + NQ * KD * 2 + (NQ / 8) * nt * kMT * 2 +
-           (kThreads / 32) * 64 * 4 + (kThreads / 32) * kList * 4 + 16 * 4 + 2 * kAcc * 8 + 8;
+           (kThreads / 32) * 64 * 4 + (kThreads / 32) * kList * 4 + 16 * 4 + (2 * kAcc + kStages + 1) * 8 + 8;
 }
 
 }  // namespace
@@ -402,10 +443,13 @@ bool colvec_tc_supported(const SelectArgs& a) {
 
 template <int KD, int NQ>
 void launch_colvec(const SelectArgs& a, int M, int dbg, cudaStream_t st) {
+    // A/B switch: TMA bulk tile copies measured slower on C2 (0.85 vs 0.73 ms)
+    static const bool tma = std::getenv("DSA_COLVEC_TMA") != nullptr;
     const size_t smem = colvec_smem_bytes<KD, NQ>(a.L);
-    cudaFuncSetAttribute(colvec_tc_kernel<KD, NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    auto kern = tma ? colvec_tc_kernel<KD, NQ, true> : colvec_tc_kernel<KD, NQ, false>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     const dim3 grid(static_cast<unsigned>(ceil_div_i(a.L, NQ)), static_cast<unsigned>(a.pairs));
-    colvec_tc_kernel<KD, NQ><<<grid, kThreads, smem, st>>>(a.lq, a.lk, a.L, a.keep, M, a.cols, dbg);
+    kern<<<grid, kThreads, smem, st>>>(a.lq, a.lk, a.L, a.keep, M, a.cols, dbg);
 }
 
 void run_colvec_tc(const SelectArgs& a, cudaStream_t st) {
