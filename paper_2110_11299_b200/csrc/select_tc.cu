@@ -131,11 +131,34 @@ __global__ void __launch_bounds__(kThreads, NQ == 64 ? 2 : 1)
     if (tid < NB) bandmax[tid] = INT32_MIN;
     if (warp == 0) tc::tmem_alloc<kAcc * NQ>(tmem_slot);
 
+    // each thread copies the same 16-byte chunk(s) of every K~ tile: the
+    // chunk-planar levels put tile n's copy of a chunk n * kMT rows further
+    // along the same plane, so the per-tile address math is one add
+    constexpr int kCPT = kMT * (KD / 8) / kThreads;  // chunks per thread per tile
+    uint32_t soff[kCPT];
+    const uint16_t* gsrc[kCPT];
+    int rrow[kCPT];
+#pragma unroll
+    for (int i = 0; i < kCPT; ++i) {
+        const int t = tid + i * kThreads, r = t / (KD / 8), c = t % (KD / 8);
+        soff[i] = tile_off<KD>(r, c);
+        gsrc[i] = lkp + lvl_index(L, r, c * 8);
+        rrow[i] = r;
+    }
+    const uint32_t ring_s = tc::smem_addr(ring);
+    auto load_k = [&](int slot, int tile) {
+        const int64_t row0 = static_cast<int64_t>(tile) * kMT;
+#pragma unroll
+        for (int i = 0; i < kCPT; ++i) {
+            const bool ok = row0 + rrow[i] < L;
+            cp_async16(ring_s + slot * kTile + soff[i], ok ? gsrc[i] + row0 * 8 : gsrc[i], ok);
+        }
+    };
     // prologue: Q~ block + first kStages K~ tiles (group t <-> tile t)
     if (!TMA) {
         load_tile<KD, NQ>(tc::smem_addr(bq), lqp, q0, L, tid);
         for (int s = 0; s < kStages; ++s) {
-            if (s < nt) load_tile<KD>(tc::smem_addr(ring + s * kTile), lkp, static_cast<int64_t>(s) * kMT, L, tid);
+            if (s < nt) load_k(s, s);
             cp_commit();
         }
     }
@@ -224,8 +247,7 @@ __global__ void __launch_bounds__(kThreads, NQ == 64 ? 2 : 1)
                         bulk_tile<KD>(tc::smem_addr(ring + (u % kStages) * kTile), lkp, static_cast<int64_t>(nxt) * kMT,
                                       kMT, L, &full[u % kStages]);
                 } else {
-                    load_tile<KD>(tc::smem_addr(ring + (u % kStages) * kTile), lkp, static_cast<int64_t>(nxt) * kMT, L,
-                                  tid);
+                    load_k(u % kStages, nxt);
                 }
             }
         }
