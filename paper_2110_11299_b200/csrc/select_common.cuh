@@ -18,21 +18,23 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 constexpr int kWin = 512;  // histogram scratch per warp (bins)
 
 // Counts values >= lo into h[0..W) and returns the count inside the window.
-template <int W>
+// S: element stride of the pooled values (1: one band per row; 2: two bands
+// interleaved as int16 pairs)
+template <int W, int S = 1>
 __device__ __forceinline__ uint32_t window_hist(const int16_t* __restrict__ pv, int L, int lo,
                                                 uint32_t* h, int lane) {
     for (int i = lane; i < W; i += 32) h[i] = 0;
     __syncwarp();
     int j = lane;
     for (; j + 96 < L; j += 128) {
-        const int v0 = pv[j], v1 = pv[j + 32], v2 = pv[j + 64], v3 = pv[j + 96];
+        const int v0 = pv[j * S], v1 = pv[(j + 32) * S], v2 = pv[(j + 64) * S], v3 = pv[(j + 96) * S];
         if (v0 >= lo) atomicAdd(&h[v0 - lo], 1u);
         if (v1 >= lo) atomicAdd(&h[v1 - lo], 1u);
         if (v2 >= lo) atomicAdd(&h[v2 - lo], 1u);
         if (v3 >= lo) atomicAdd(&h[v3 - lo], 1u);
     }
     for (; j < L; j += 32) {
-        const int v = pv[j];
+        const int v = pv[j * S];
         if (v >= lo) atomicAdd(&h[v - lo], 1u);
     }
     __syncwarp();
@@ -89,12 +91,13 @@ __device__ __forceinline__ void window_threshold(const uint32_t* h, int lo, uint
 // so counting starts on a 64-value window (few shared atomics), widens to
 // 512, and falls back to a binary search over the full integer range.
 // nge = count(v >= T) when known from the histogram, else UINT32_MAX.
+template <int S = 1>
 __device__ __forceinline__ void band_threshold(const int16_t* __restrict__ pv, int L, int keep,
                                                int bmax, int M, uint32_t* h, int lane, int& T,
                                                uint32_t& rem, uint32_t& nge) {
     const uint32_t kk = static_cast<uint32_t>(keep);
     nge = 0xffffffffu;
-    if (window_hist<64>(pv, L, bmax - 63, h, lane) >= kk) {
+    if (window_hist<64, S>(pv, L, bmax - 63, h, lane) >= kk) {
         uint32_t nT;
         window_threshold<64>(h, bmax - 63, kk, lane, T, rem, nT);
         nge = kk - rem + nT;
@@ -106,7 +109,7 @@ __device__ __forceinline__ void band_threshold(const int16_t* __restrict__ pv, i
     while (a < b) {
         const int mid = a + (b - a + 1) / 2;
         uint32_t cnt = 0;
-        for (int jj = lane; jj < L; jj += 32) cnt += pv[jj] >= mid;
+        for (int jj = lane; jj < L; jj += 32) cnt += pv[jj * S] >= mid;
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
         if (cnt >= kk) a = mid;
@@ -114,7 +117,7 @@ __device__ __forceinline__ void band_threshold(const int16_t* __restrict__ pv, i
     }
     T = a;
     uint32_t above = 0;
-    for (int jj = lane; jj < L; jj += 32) above += pv[jj] > T;
+    for (int jj = lane; jj < L; jj += 32) above += pv[jj * S] > T;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) above += __shfl_xor_sync(0xffffffffu, above, off);
     rem = kk - above;
@@ -122,6 +125,7 @@ __device__ __forceinline__ void band_threshold(const int16_t* __restrict__ pv, i
 
 // Ascending emission: every column with value > T, then values == T in
 // column order until `rem` of them are taken.
+template <int S = 1>
 __device__ __forceinline__ void band_emit(const int16_t* __restrict__ pv, int L, int keep, int T,
                                           uint32_t rem, uint32_t* __restrict__ o, int lane) {
     const uint32_t kk = static_cast<uint32_t>(keep);
@@ -132,7 +136,7 @@ __device__ __forceinline__ void band_emit(const int16_t* __restrict__ pv, int L,
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int j = j0 + u * 32 + lane;
-            v[u] = j < L ? pv[j] : INT32_MIN;
+            v[u] = j < L ? pv[j * S] : INT32_MIN;
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -164,14 +168,15 @@ __device__ __forceinline__ unsigned vote_ballot(bool p) {
 // (lowest columns first), and the copy of the list to global memory.  When
 // the >= T set does not fit the staging list, the two-ballot emission with
 // a trash slot is used instead.
+template <int S = 1>
 __device__ __forceinline__ void band_select(const int16_t* __restrict__ pv, int L, int Lp, int keep,
                                             int bmax, int M, uint32_t* h, uint32_t* obuf,
                                             uint32_t* __restrict__ o, int lane) {
     int T;
     uint32_t rem, nge;
-    band_threshold(pv, L, keep, bmax, M, h, lane, T, rem, nge);
+    band_threshold<S>(pv, L, keep, bmax, M, h, lane, T, rem, nge);
     if (keep > kList - 32) {
-        band_emit(pv, L, keep, T, rem, o, lane);
+        band_emit<S>(pv, L, keep, T, rem, o, lane);
         return;
     }
     const unsigned lt = lanemask_lt();
@@ -180,7 +185,7 @@ __device__ __forceinline__ void band_select(const int16_t* __restrict__ pv, int 
         for (int j0 = 0; j0 < Lp; j0 += 128) {
             int v[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) v[u] = pv[j0 + u * 32 + lane];
+            for (int u = 0; u < 4; ++u) v[u] = pv[(j0 + u * 32 + lane) * S];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const bool ge = v[u] >= T;
@@ -198,7 +203,7 @@ __device__ __forceinline__ void band_select(const int16_t* __restrict__ pv, int 
                 const uint32_t i = i0 + lane;
                 const bool valid = i < nge;
                 const uint32_t col = valid ? obuf[i] : 0u;
-                const bool eq = valid && pv[col] == T;
+                const bool eq = valid && pv[col * S] == T;
                 const unsigned be = vote_ballot(eq);
                 const bool kp = valid && (!eq || eq_seen + __popc(be & lt) < rem);
                 const unsigned bk = vote_ballot(kp);
@@ -215,7 +220,7 @@ __device__ __forceinline__ void band_select(const int16_t* __restrict__ pv, int 
     for (int j0 = 0; j0 < Lp; j0 += 128) {
         int v[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = pv[j0 + u * 32 + lane];
+        for (int u = 0; u < 4; ++u) v[u] = pv[(j0 + u * 32 + lane) * S];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const bool eq = v[u] == T;

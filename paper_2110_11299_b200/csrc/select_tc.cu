@@ -225,6 +225,7 @@ __global__ void __launch_bounds__(kThreads, NQ == 64 ? 2 : 1)
                     for (int x = 0; x < 32; ++x)
                         if (q0 + half * CPW + cb * 32 + x >= L) r[x] = __float_as_uint(-INFINITY);
                 }
+                float m4[4];
 #pragma unroll
                 for (int bb = 0; bb < 4; ++bb) {
                     float m0, m1, m2;
@@ -232,10 +233,19 @@ __global__ void __launch_bounds__(kThreads, NQ == 64 ? 2 : 1)
                     asm("max.f32 %0, %1, %2, %3;" : "=f"(m0) : "f"(f[0]), "f"(f[1]), "f"(f[2]));
                     asm("max.f32 %0, %1, %2, %3;" : "=f"(m1) : "f"(f[3]), "f"(f[4]), "f"(f[5]));
                     asm("max.f32 %0, %1, %2, %3;" : "=f"(m2) : "f"(m0), "f"(m1), "f"(f[6]));
-                    const float mx = fmaxf(m2, f[7]);
-                    const int band = half * BPW + cb * 4 + bb;
-                    pooled[band * Lp + key] = kvalid ? static_cast<int16_t>(__float2int_rn(mx)) : INT16_MIN;
-                    if (kvalid) bmax[cb * 4 + bb] = fmaxf(bmax[cb * 4 + bb], mx);
+                    m4[bb] = fmaxf(m2, f[7]);
+                    if (kvalid) bmax[cb * 4 + bb] = fmaxf(bmax[cb * 4 + bb], m4[bb]);
+                }
+                // two bands per 32-bit store: [band / 2][key][2] int16 (the
+                // exact integer maxima convert by the 1.5 * 2^23 addition)
+#pragma unroll
+                for (int pp = 0; pp < 2; ++pp) {
+                    const int v0 = __float_as_int(m4[2 * pp] + 12582912.0f) - 0x4B400000;
+                    const int v1 = __float_as_int(m4[2 * pp + 1] + 12582912.0f) - 0x4B400000;
+                    const uint32_t packed = kvalid ? __byte_perm(static_cast<uint32_t>(v0), static_cast<uint32_t>(v1), 0x5410)
+                                                   : 0x80008000u;
+                    const int band = half * BPW + cb * 4 + 2 * pp;  // even
+                    *reinterpret_cast<uint32_t*>(pooled + ((band >> 1) * Lp + key) * 2) = packed;
                 }
             }
             tc::fence_before_sync();
@@ -271,9 +281,9 @@ __global__ void __launch_bounds__(kThreads, NQ == 64 ? 2 : 1)
     for (int b = warp; b < NB && !(dbg & 1); b += kThreads / 32) {
         const int64_t band = q0 / 8 + b;
         if (band >= nb) break;
-        const int16_t* pv = pooled + b * Lp;
-        band_select(pv, static_cast<int>(L), Lp, static_cast<int>(keep), bandmax[b], M, h,
-                    obufs + warp * kList, out + (pair * nb + band) * keep, lane);
+        const int16_t* pv = pooled + (b >> 1) * Lp * 2 + (b & 1);
+        band_select<2>(pv, static_cast<int>(L), Lp, static_cast<int>(keep), bandmax[b], M, h,
+                       obufs + warp * kList, out + (pair * nb + band) * keep, lane);
         __syncwarp();
     }
 }
