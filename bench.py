@@ -359,6 +359,8 @@ def run_gpu_arm(args, p, rank, local, world):
                    "unit": "TFLOP/s", "scale": 1e12},
         "attention": {"bound": "hbm", "amount": 4 * L * d * e * pairs, "unit": "GB/s", "scale": 1e9},
     }
+    if p.mask_mode == "block":  # C3: 32x32 blocks put attention near the ridge
+        work["attention"] = {"bound": "tensor", "amount": 4 * nnz * d, "unit": "TFLOP/s", "scale": 1e12}
     dom = max(phase_ms, key=phase_ms.get)
     w = work[dom]
     achieved = w["amount"] / (phase_ms[dom] * 1e-3) / w["scale"]
@@ -374,6 +376,13 @@ def run_gpu_arm(args, p, rank, local, world):
         pk = peaks["hbm_gbs"] if wk["bound"] == "hbm" else peaks["bf16_tflops"]
         phases[kx] = {"ms": ms_k, "bound": wk["bound"], "achieved": a_k, "unit": wk["unit"],
                       "frac": a_k / pk}
+    # explanatory counters: candidates scored per second, and the
+    # K/V row bytes the attention gathers (reuse = query rows sharing a gather)
+    cand = (L * (L + 1) // 2 if (p.mask_mode == "threshold" and p.causal) else L * L) * pairs
+    phases["select"]["candidates_per_s"] = cand / (phase_ms["select"] * 1e-3)
+    reuse = {"colvec": p.vec_v, "block": p.block}.get(p.mask_mode, 1)
+    phases["attention"]["gathered_GBps"] = 2 * nnz * d * e / reuse / (phase_ms["attention"] * 1e-3) / 1e9
+    phases["attention"]["gather_reuse"] = reuse
     tokens = p.tokens * world
     value = tokens / (ms * 1e-3)
     cpu = None
