@@ -205,6 +205,14 @@ class Reference:
             "ref_masked_attention": (I32, [_d, _d, _d, I64, I64, I64, _u64, _u32, I32, _d]),
             "ref_pipeline": (I32, [I64, I32, _d, _d, _d, _d, I64, I64, I64, I32, I32, I32, I64, I64,
                                    I64, I32, _d]),
+            "ref_write_mask": (I32, [C.c_char_p, I64, _u64, _u32]),
+            "ref_read_mask": (I32, [C.c_char_p, C.POINTER(I64), C.POINTER(I64), C.c_void_p, C.c_void_p]),
+            "ref_write_sparse_scores": (I32, [C.c_char_p, I64, _u64, _u32, _d]),
+            "ref_read_sparse_scores": (I32, [C.c_char_p, C.POINTER(I64), C.POINTER(I64), C.c_void_p,
+                                             C.c_void_p, C.c_void_p]),
+            "ref_write_container1": (I32, [C.c_char_p, C.c_char_p, I64, I64, I32, _d, C.c_char_p]),
+            "ref_read_container1": (I32, [C.c_char_p, C.c_char_p, C.POINTER(I64), C.POINTER(I64),
+                                          C.POINTER(I32), C.c_void_p, C.POINTER(I64), C.c_void_p]),
         }
         for n, (r, a) in sig.items():
             f = getattr(L, n)
@@ -214,10 +222,58 @@ class Reference:
     def _chk(self, r):
         if r != 0:
             msg = self.L.ref_last_error().decode()
-            raise {1: ValueError, 2: ValueError}.get(r, RuntimeError)(f"[ref code {r}] {msg}")
+            raise {1: ValueError, 2: ValueError, 5: IOError}.get(r, RuntimeError)(f"[ref code {r}] {msg}")
 
     def isa(self) -> str:
         return self.L.ref_isa_name().decode()
+
+    # ---- the reference's fixture formats (mask.cpp / sparse.cpp / serialize.cpp)
+    def write_mask(self, path, rowptr, cols):
+        rp = np.ascontiguousarray(rowptr, np.uint64)
+        c = np.ascontiguousarray(cols if len(cols) else np.zeros(1), np.uint32)
+        self._chk(self.L.ref_write_mask(str(path).encode(), len(rp) - 1, rp, c))
+
+    def read_mask(self, path):
+        l, nnz = I64(), I64()
+        self._chk(self.L.ref_read_mask(str(path).encode(), C.byref(l), C.byref(nnz), None, None))
+        rp = np.zeros(l.value + 1, np.uint64)
+        cols = np.zeros(max(nnz.value, 1), np.uint32)
+        self._chk(self.L.ref_read_mask(str(path).encode(), C.byref(l), C.byref(nnz),
+                                       rp.ctypes.data_as(C.c_void_p), cols.ctypes.data_as(C.c_void_p)))
+        return rp, cols[: nnz.value]
+
+    def write_sparse_scores(self, path, rowptr, cols, values):
+        rp = np.ascontiguousarray(rowptr, np.uint64)
+        c = np.ascontiguousarray(cols if len(cols) else np.zeros(1), np.uint32)
+        v = np.ascontiguousarray(values if len(values) else np.zeros(1), np.float64)
+        self._chk(self.L.ref_write_sparse_scores(str(path).encode(), len(rp) - 1, rp, c, v))
+
+    def read_sparse_scores(self, path):
+        l, nnz = I64(), I64()
+        self._chk(self.L.ref_read_sparse_scores(str(path).encode(), C.byref(l), C.byref(nnz), None, None, None))
+        rp = np.zeros(l.value + 1, np.uint64)
+        cols = np.zeros(max(nnz.value, 1), np.uint32)
+        vals = np.zeros(max(nnz.value, 1), np.float64)
+        self._chk(self.L.ref_read_sparse_scores(str(path).encode(), C.byref(l), C.byref(nnz),
+                                                rp.ctypes.data_as(C.c_void_p), cols.ctypes.data_as(C.c_void_p),
+                                                vals.ctypes.data_as(C.c_void_p)))
+        return rp, cols[: nnz.value], vals[: nnz.value]
+
+    def write_container1(self, path, name, arr, f32=False, meta=""):
+        a = _f64(arr)
+        self._chk(self.L.ref_write_container1(str(path).encode(), name.encode(), a.shape[0], a.shape[1],
+                                              int(f32), a, meta.encode()))
+
+    def read_container1(self, path, name):
+        r, c, m = I64(), I64(), I64()
+        f32 = I32()
+        self._chk(self.L.ref_read_container1(str(path).encode(), name.encode(), C.byref(r), C.byref(c),
+                                             C.byref(f32), None, C.byref(m), None))
+        out = np.zeros((r.value, c.value))
+        meta = C.create_string_buffer(max(m.value, 1))
+        self._chk(self.L.ref_read_container1(str(path).encode(), name.encode(), C.byref(r), C.byref(c),
+                                             C.byref(f32), out.ctypes.data_as(C.c_void_p), C.byref(m), meta))
+        return out, bool(f32.value), meta.raw[: m.value].decode()
 
     def project(self, x, p, f32=False):
         x, p = _f64(x), _f64(p)

@@ -23,6 +23,8 @@
 #include "dsattn/linalg.hpp"
 #include "dsattn/maskgen.hpp"
 #include "dsattn/predictor.hpp"
+#include "dsattn/mask.hpp"
+#include "dsattn/serialize.hpp"
 #include "dsattn/sparse.hpp"
 
 using namespace dsattn;
@@ -61,6 +63,9 @@ int guarded(F&& f) {
     } catch (const ParamError& e) {
         g_err = e.what();
         return 2;
+    } catch (const IoError& e) {
+        g_err = e.what();
+        return 5;
     } catch (const std::exception& e) {
         g_err = e.what();
         return 9;
@@ -302,6 +307,84 @@ int ref_pipeline(int64_t pairs, int threads, const double* q, const double* k, c
         for (auto& th : pool) th.join();
         for (auto& e : errs)
             if (!e.empty()) throw ParamError(e);
+    });
+}
+
+// ---- fixture / wire formats (P/src/mask.cpp:75-114, P/src/sparse.cpp:122-171,
+// P/src/serialize.cpp:38-95): the reference's own writers and readers, so
+// the GPU harness's files are pinned against them.
+int ref_write_mask(const char* path, int64_t L, const uint64_t* rowptr, const uint32_t* cols) {
+    return guarded([&] { write_mask(path, mask_from_csr(static_cast<size_t>(L), rowptr, cols)); });
+}
+
+// Two calls: cols == NULL returns L (*l_out) and nnz (*nnz_out); then fills
+// rowptr[L+1] and cols[nnz].
+int ref_read_mask(const char* path, int64_t* l_out, int64_t* nnz_out, uint64_t* rowptr, uint32_t* cols) {
+    return guarded([&] {
+        const SparseMask m = read_mask(path);
+        *l_out = static_cast<int64_t>(m.l);
+        *nnz_out = static_cast<int64_t>(m.nnz());
+        if (!cols) return;
+        uint64_t off = 0;
+        rowptr[0] = 0;
+        for (size_t i = 0; i < m.l; ++i) {
+            for (uint32_t c : m.kept[i]) cols[off++] = c;
+            rowptr[i + 1] = off;
+        }
+    });
+}
+
+int ref_write_sparse_scores(const char* path, int64_t L, const uint64_t* rowptr, const uint32_t* cols,
+                            const double* values) {
+    return guarded([&] {
+        SparseScores s;
+        s.mask = mask_from_csr(static_cast<size_t>(L), rowptr, cols);
+        s.row_offsets.assign(rowptr, rowptr + L + 1);
+        s.values.assign(values, values + rowptr[L]);
+        write_sparse_scores(path, s);
+    });
+}
+
+int ref_read_sparse_scores(const char* path, int64_t* l_out, int64_t* nnz_out, uint64_t* rowptr,
+                           uint32_t* cols, double* values) {
+    return guarded([&] {
+        const SparseScores s = read_sparse_scores(path);
+        *l_out = static_cast<int64_t>(s.mask.l);
+        *nnz_out = static_cast<int64_t>(s.values.size());
+        if (!cols) return;
+        uint64_t off = 0;
+        rowptr[0] = 0;
+        for (size_t i = 0; i < s.mask.l; ++i) {
+            for (uint32_t c : s.mask.kept[i]) cols[off++] = c;
+            rowptr[i + 1] = off;
+        }
+        std::memcpy(values, s.values.data(), s.values.size() * sizeof(double));
+    });
+}
+
+// One-entry DSAC container (data: rows*cols doubles, rounded to f32 when
+// f32 != 0, as the reference stores f32 Matrices).
+int ref_write_container1(const char* path, const char* name, int64_t rows, int64_t cols, int f32,
+                         const double* data, const char* meta) {
+    return guarded([&] {
+        write_container(path, {{name, to_matrix(data, static_cast<size_t>(rows), static_cast<size_t>(cols), f32)}},
+                        meta ? meta : "");
+    });
+}
+
+// Entry `name`: first call (out == NULL) reports rows, cols, precision and
+// the meta length; the second copies the data (as doubles) and the meta.
+int ref_read_container1(const char* path, const char* name, int64_t* rows, int64_t* cols, int* f32,
+                        double* out, int64_t* meta_len, char* meta) {
+    return guarded([&] {
+        const Container c = read_container(path);
+        const Matrix& m = c.find(name);
+        *rows = static_cast<int64_t>(m.rows());
+        *cols = static_cast<int64_t>(m.cols());
+        *f32 = m.precision() == Precision::f32 ? 1 : 0;
+        *meta_len = static_cast<int64_t>(c.meta.size());
+        if (out) from_matrix(m, out);
+        if (meta) std::memcpy(meta, c.meta.data(), c.meta.size());
     });
 }
 
