@@ -285,13 +285,8 @@ void do_predict(const dsa_config& c, const void* q, const void* k, const float* 
     check_cuda(cudaGetLastError(), "dsa_predict launch");
 }
 
-void do_select(const dsa_config& c, const uint16_t* lq, const uint16_t* lk, const double* sq,
-               const double* sk, const dsa_mask& m, const Scratch& ws, cudaStream_t st) {
-    if (!lq || !lk || !sq || !sk || !m.cols) throw Error(DSA_ERR_PARAM, "dsa_select: null pointer");
-    if (m.capacity < capacity_of(c) && c.mask_mode != DSA_MASK_THRESHOLD)
-        throw Error(DSA_ERR_PARAM, "dsa_select: mask capacity too small");
-    if (c.mask_mode == DSA_MASK_THRESHOLD && (!m.rowptr || m.capacity < capacity_of(c)))
-        throw Error(DSA_ERR_PARAM, "dsa_select: threshold mode needs rowptr and capacity >= dsa_mask_capacity()");
+SelectArgs select_args(const dsa_config& c, const uint16_t* lq, const uint16_t* lk, const double* sq,
+                       const double* sk, const dsa_mask& m, const Scratch& ws) {
     SelectArgs a{};
     a.mode = c.mask_mode;
     a.pairs = pairs_of(c);
@@ -325,17 +320,24 @@ void do_select(const dsa_config& c, const uint16_t* lq, const uint16_t* lk, cons
     a.scan_tmp_bytes = ws.scan_bytes;
     a.ovf_n = ws.ovf_n;
     a.ovf_list = ws.ovf_list;
+    return a;
+}
+
+void do_select(const dsa_config& c, const uint16_t* lq, const uint16_t* lk, const double* sq,
+               const double* sk, const dsa_mask& m, const Scratch& ws, cudaStream_t st) {
+    if (!lq || !lk || !sq || !sk || !m.cols) throw Error(DSA_ERR_PARAM, "dsa_select: null pointer");
+    if (m.capacity < capacity_of(c) && c.mask_mode != DSA_MASK_THRESHOLD)
+        throw Error(DSA_ERR_PARAM, "dsa_select: mask capacity too small");
+    if (c.mask_mode == DSA_MASK_THRESHOLD && (!m.rowptr || m.capacity < capacity_of(c)))
+        throw Error(DSA_ERR_PARAM, "dsa_select: threshold mode needs rowptr and capacity >= dsa_mask_capacity()");
+    const SelectArgs a = select_args(c, lq, lk, sq, sk, m, ws);
     if (m.empty_rows && c.mask_mode != DSA_MASK_THRESHOLD)
         check_cuda(cudaMemsetAsync(m.empty_rows, 0, pairs_of(c) * c.L, st), "dsa_select memset");
     run_select(a, st);
     check_cuda(cudaGetLastError(), "dsa_select launch");
 }
 
-void do_attention(const dsa_config& c, const void* q, const void* k, const void* v,
-                  const dsa_mask& m, void* z, cudaStream_t st) {
-    if (!q || !k || !v || !z || !m.cols) throw Error(DSA_ERR_PARAM, "dsa_sparse_attention: null pointer");
-    if (c.mask_mode == DSA_MASK_THRESHOLD && !m.rowptr)
-        throw Error(DSA_ERR_PARAM, "dsa_sparse_attention: threshold mask needs rowptr");
+AttnArgs attn_args(const dsa_config& c, const void* q, const void* k, const void* v, const dsa_mask& m, void* z) {
     AttnArgs a{};
     a.mode = c.mask_mode;
     a.pairs = pairs_of(c);
@@ -353,8 +355,32 @@ void do_attention(const dsa_config& c, const void* q, const void* k, const void*
     a.block = c.block;
     a.z = z;
     a.empty_rows = m.empty_rows;
-    run_attention(a, st);
+    return a;
+}
+
+void do_attention(const dsa_config& c, const void* q, const void* k, const void* v,
+                  const dsa_mask& m, void* z, cudaStream_t st) {
+    if (!q || !k || !v || !z || !m.cols) throw Error(DSA_ERR_PARAM, "dsa_sparse_attention: null pointer");
+    if (c.mask_mode == DSA_MASK_THRESHOLD && !m.rowptr)
+        throw Error(DSA_ERR_PARAM, "dsa_sparse_attention: threshold mask needs rowptr");
+    run_attention(attn_args(c, q, k, v, m, z), st);
     check_cuda(cudaGetLastError(), "dsa_sparse_attention launch");
+}
+
+// COLVEC select + attention in one kernel when supported; with no caller
+// mask the selected lists stay on chip (nothing written to HBM).
+bool try_fused(const dsa_config& c, const void* q, const void* k, const void* v, const uint16_t* lq,
+               const uint16_t* lk, const double* sq, const double* sk, const dsa_mask& m, bool mask_wanted,
+               void* z, const Scratch& ws, cudaStream_t st) {
+    if (c.mask_mode != DSA_MASK_COLVEC) return false;
+    SelectArgs sa = select_args(c, lq, lk, sq, sk, m, ws);
+    const AttnArgs aa = attn_args(c, q, k, v, m, z);
+    if (!colvec_fused_supported(sa, aa)) return false;
+    if (!mask_wanted) sa.cols = nullptr;
+    if (m.empty_rows) check_cuda(cudaMemsetAsync(m.empty_rows, 0, pairs_of(c) * c.L, st), "dsa_pipeline memset");
+    run_colvec_fused(sa, aa, st);
+    check_cuda(cudaGetLastError(), "dsa_pipeline fused launch");
+    return true;
 }
 
 void require_device() {
@@ -476,6 +502,7 @@ dsa_status dsa_pipeline(const dsa_config* cfg, const void* q, const void* k, con
         if (nch <= 1) {
             const Scratch sc = scratch_of(c, pl, workspace);
             do_predict(c, q, k, p, lq, lk, sq, sk, sc, st);
+            if (try_fused(c, q, k, v, lq, lk, sq, sk, m, mask_out != nullptr, z, sc, st)) return;
             do_select(c, lq, lk, sq, sk, m, sc, st);
             do_attention(c, q, k, v, m, z, st);
             return;

@@ -101,5 +101,8 @@ struct AttnArgs {
 void run_attention(const AttnArgs& a, cudaStream_t st);
 bool band_attention_supported(const AttnArgs& a);
 void run_band_attention(const AttnArgs& a, cudaStream_t st);
+// fused COLVEC select + band attention (mask optional): dsa_pipeline
+bool colvec_fused_supported(const SelectArgs& s, const AttnArgs& a);
+void run_colvec_fused(const SelectArgs& s, const AttnArgs& a, cudaStream_t st);
 
 }  // namespace dsa

@@ -167,7 +167,8 @@ __device__ __forceinline__ unsigned vote_ballot(bool p) {
 // columns), a short pass over that list dropping the ties beyond `rem`
 // (lowest columns first), and the copy of the list to global memory.  When
 // the >= T set does not fit the staging list, the two-ballot emission with
-// a trash slot is used instead.
+// a trash slot is used instead.  The final list is left in obuf[0, keep)
+// (for a fused consumer); o may be NULL (no global copy).
 template <int S = 1>
 __device__ __forceinline__ void band_select(const int16_t* __restrict__ pv, int L, int Lp, int keep,
                                             int bmax, int M, uint32_t* h, uint32_t* obuf,
@@ -196,8 +197,9 @@ __device__ __forceinline__ void band_select(const int16_t* __restrict__ pv, int 
         }
         __syncwarp();
         if (nge == static_cast<uint32_t>(keep)) {
-            for (int i = lane; i < keep; i += 32) o[i] = obuf[i];
-        } else {  // admit only the first `rem` columns equal to T
+            if (o)
+                for (int i = lane; i < keep; i += 32) o[i] = obuf[i];
+        } else {  // admit only the first `rem` columns equal to T (compacted in place)
             uint32_t eq_seen = 0, outp = 0;
             for (uint32_t i0 = 0; i0 < nge; i0 += 32) {
                 const uint32_t i = i0 + lane;
@@ -207,7 +209,11 @@ __device__ __forceinline__ void band_select(const int16_t* __restrict__ pv, int 
                 const unsigned be = vote_ballot(eq);
                 const bool kp = valid && (!eq || eq_seen + __popc(be & lt) < rem);
                 const unsigned bk = vote_ballot(kp);
-                if (kp) o[outp + __popc(bk & lt)] = col;
+                __syncwarp();  // every lane read its entry before any write below
+                if (kp) {
+                    obuf[outp + __popc(bk & lt)] = col;
+                    if (o) o[outp + __popc(bk & lt)] = col;
+                }
                 outp += __popc(bk);
                 eq_seen += __popc(be);
             }
@@ -233,7 +239,8 @@ __device__ __forceinline__ void band_select(const int16_t* __restrict__ pv, int 
         }
     }
     __syncwarp();
-    for (int i = lane; i < keep; i += 32) o[i] = obuf[i];
+    if (o)
+        for (int i = lane; i < keep; i += 32) o[i] = obuf[i];
     __syncwarp();
 }
 

@@ -25,6 +25,7 @@
 
 #include "device_common.cuh"
 #include "kernels.h"
+#include "band_core.cuh"
 #include "select_common.cuh"
 #include "tc_sm100.cuh"
 
@@ -89,10 +90,23 @@ __device__ __forceinline__ void bulk_tile(uint32_t sdst, const uint16_t* __restr
         tc::bulk_g2s(sdst + c * (rows_cap * 16), src + (c * L + row0) * 8, rows * 16, bar);
 }
 
-template <int KD, int NQ, bool TMA>
+// Fused select + attention (FUSED, NQ = 64, d = 64): after its bands are
+// selected, each warp runs the band attention (band_core.cuh) over its
+// band's list straight from shared memory -- the mask never touches HBM
+// (`out` may be NULL) and one CTA's memory-bound gathers overlap the other
+// resident CTA's ALU-bound score loop / selection.
+struct FusedAttn {
+    const __nv_bfloat16* q;
+    const __nv_bfloat16* k;
+    const __nv_bfloat16* v;
+    __nv_bfloat16* z;
+    int scale;
+};
+
+template <int KD, int NQ, bool TMA, bool FUSED = false>
 __global__ void __launch_bounds__(kThreads, NQ == 64 ? 2 : 1)
     colvec_tc_kernel(const uint16_t* __restrict__ lq, const uint16_t* __restrict__ lk, int64_t L,
-                     int64_t keep, int M, uint32_t* __restrict__ out, int dbg) {
+                     int64_t keep, int M, uint32_t* __restrict__ out, int dbg, FusedAttn fa) {
     extern __shared__ __align__(1024) unsigned char smem[];
     constexpr int NB = NQ / 8;       // bands per CTA
     constexpr int CPW = NQ / 2;      // query columns per epilogue warp (lane quarter x half)
@@ -283,8 +297,25 @@ __global__ void __launch_bounds__(kThreads, NQ == 64 ? 2 : 1)
         if (band >= nb) break;
         const int16_t* pv = pooled + (b >> 1) * Lp * 2 + (b & 1);
         band_select<2>(pv, static_cast<int>(L), Lp, static_cast<int>(keep), bandmax[b], M, h,
-                       obufs + warp * kList, out + (pair * nb + band) * keep, lane);
+                       obufs + warp * kList, out ? out + (pair * nb + band) * keep : nullptr, lane);
         __syncwarp();
+    }
+    if constexpr (FUSED) {
+        static_assert(NQ == 64 && kThreads / 32 == 8, "fused path: one band per warp");
+        // the score-loop buffers (ring, pooled, histograms) are free now
+        __syncthreads();
+        using BS = bc::BandSmemV2<64>;
+        BS& sm = reinterpret_cast<BS*>(ring)[warp];
+        const int64_t band = q0 / 8 + warp;
+        if (band < nb) {
+            const uint32_t* lst = obufs + warp * kList;
+            auto chunk_idx = [&](int ch) -> uint32_t {
+                const int64_t pidx = static_cast<int64_t>(ch) * 32 + lane;
+                return pidx < keep ? lst[pidx] : 0u;
+            };
+            bc::band_core<64, 8, false>(sm, fa.q, fa.k + pair * L * 64, fa.v + pair * L * 64, pair, L, band * 8,
+                                        keep, 0, 0, 0, fa.scale, fa.z, chunk_idx, lane);
+        }
     }
 }
 
@@ -481,7 +512,7 @@ void launch_colvec(const SelectArgs& a, int M, int dbg, cudaStream_t st) {
     auto kern = tma ? colvec_tc_kernel<KD, NQ, true> : colvec_tc_kernel<KD, NQ, false>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     const dim3 grid(static_cast<unsigned>(ceil_div_i(a.L, NQ)), static_cast<unsigned>(a.pairs));
-    kern<<<grid, kThreads, smem, st>>>(a.lq, a.lk, a.L, a.keep, M, a.cols, dbg);
+    kern<<<grid, kThreads, smem, st>>>(a.lq, a.lk, a.L, a.keep, M, a.cols, dbg, FusedAttn{});
 }
 
 void run_colvec_tc(const SelectArgs& a, cudaStream_t st) {
@@ -512,6 +543,29 @@ void run_colvec_tc(const SelectArgs& a, cudaStream_t st) {
         if (two) launch_colvec<32, 64>(a, M, dbg, st);
         else launch_colvec<32, 128>(a, M, dbg, st);
     }
+    note_launch();
+}
+
+bool colvec_fused_supported(const SelectArgs& s, const AttnArgs& a) {
+    if (std::getenv("DSA_NO_FUSE") != nullptr) return false;
+    if (!colvec_tc_supported(s) || s.KD != 16 || !a.bf16 || a.D != 64 || a.vec_v != 8) return false;
+    if (s.keep > kList - 32) return false;  // band list must stay in the staging buffer
+    const size_t smem = colvec_smem_bytes<16, 64>(s.L);
+    // the per-warp attention buffers reuse the ring + pooled + histogram region
+    const size_t reuse = static_cast<size_t>(ColvecSmem<16>::kTileBytes) * kStages +
+                         static_cast<size_t>(8) * ((s.L + kMT - 1) / kMT) * kMT * 2 + (kThreads / 32) * 64 * 4;
+    return smem <= 113 * 1024 && reuse >= sizeof(bc::BandSmemV2<64>) * 8;
+}
+
+void run_colvec_fused(const SelectArgs& s, const AttnArgs& a, cudaStream_t st) {
+    const int M = static_cast<int>(s.KD) * s.qmax * s.qmax;
+    const size_t smem = colvec_smem_bytes<16, 64>(s.L);
+    auto kern = colvec_tc_kernel<16, 64, false, true>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    const dim3 grid(static_cast<unsigned>(ceil_div_i(s.L, 64)), static_cast<unsigned>(s.pairs));
+    FusedAttn fa{static_cast<const __nv_bfloat16*>(a.q), static_cast<const __nv_bfloat16*>(a.k),
+                 static_cast<const __nv_bfloat16*>(a.v), static_cast<__nv_bfloat16*>(a.z), a.scale};
+    kern<<<grid, kThreads, smem, st>>>(s.lq, s.lk, s.L, s.keep, M, s.cols, 0, fa);
     note_launch();
 }
 

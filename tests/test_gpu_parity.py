@@ -93,3 +93,22 @@ def test_parity(name, npairs, oracle):
             ge = mask.empty_rows[pr * sub.L:(pr + 1) * sub.L].cpu().numpy()
             assert np.array_equal(ge.astype(bool), er.astype(bool)), "empty-row flags differ"
     assert worst <= TOL[sub.dtype], f"{name}: rel err {worst:.3e} > {TOL[sub.dtype]}"
+
+
+@pytest.mark.parametrize("L,keep", [(4096, 205), (1004, 51)])
+def test_pipeline_fused_matches_phases(L, keep):
+    """dsa_pipeline (COLVEC: fused select + attention, the mask kept on chip
+    unless requested) gives the same Z bits and mask as the three separate
+    C-ABI phases."""
+    p = load_preset("c2_vector").replace(L=L, keep=keep)
+    sub, (q, k, v, P), lv, mask, z = run_gpu(p, 3)
+    dev = torch.device("cuda:0")
+    qd, kd, vd, Pd = (t.to(dev) for t in (q, k, v, P))
+    for keep_mask in (False, True):
+        pipe = ops.Pipeline(sub, device=dev, keep_mask=keep_mask)
+        zp = pipe(qd, kd, vd, Pd)
+        torch.cuda.synchronize()
+        assert torch.equal(zp, z), "fused pipeline Z differs from the phase-by-phase Z"
+        if keep_mask:
+            n = mask.cols.numel()
+            assert torch.equal(pipe.mask.cols[:n], mask.cols), "fused pipeline mask differs"
