@@ -381,6 +381,216 @@ __global__ void __launch_bounds__(128)
     }
 }
 
+// Same block-row computation with each warp owning NT bands (8 * NT query
+// rows, one MMA n-tile each): the K and V fragments a warp loads from shared
+// memory (ldmatrix) serve all its n-tiles, so the L1 / shared-memory
+// wavefronts per block drop by NT while the CTA (32 / (8 NT) warps) still
+// stages every kept block once.
+template <int D, int NT>
+struct BlockSmemN {
+    static constexpr int kWarps = 4 / NT;
+    __nv_bfloat16 k[2][32 * D];
+    __nv_bfloat16 v[2][32 * D];
+    __nv_bfloat16 q[kWarps][NT][8 * D];   // per warp: Q bands, reused to stage Z
+    __nv_bfloat16 p[kWarps][NT][8 * 40];  // per warp: [query][key], padded rows
+};
+
+template <int D, int NT>
+__global__ void __launch_bounds__(128 / NT)
+    attn_block_nt_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __restrict__ K,
+                         const __nv_bfloat16* __restrict__ V, const uint32_t* __restrict__ block_cols,
+                         int64_t L, int64_t keep, int scale, __nv_bfloat16* __restrict__ Z) {
+    constexpr int CHUNK = 32;
+    constexpr int kT = 128 / NT;  // threads per CTA
+    extern __shared__ __align__(128) unsigned char dsm[];
+    using SM = BlockSmemN<D, NT>;
+    SM& sm = *reinterpret_cast<SM*>(dsm);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t nbr = L / 32;
+    const int64_t pair = blockIdx.y, br = blockIdx.x;
+    const int64_t r0 = br * 32 + warp * 8 * NT;  // this warp's first row
+    const __nv_bfloat16* Kp = K + pair * L * D;
+    const __nv_bfloat16* Vp = V + pair * L * D;
+    const uint32_t* cols = block_cols + (pair * nbr + br) * keep;
+    const int g = lane >> 2, c4 = lane & 3;
+    constexpr int kChunks16 = D / 8;
+
+    for (int t = lane; t < NT * 8 * kChunks16; t += 32) {
+        const int n = t / (8 * kChunks16), rc = t % (8 * kChunks16);
+        const int r = rc / kChunks16, c = rc % kChunks16;
+        cp_async16(smem_u32(sm.q[warp][n]) + swz<D>(r, c), Q + (pair * L + r0 + n * 8 + r) * D + c * 8, true);
+    }
+    auto load_block = [&](int buf, int ch) {
+        const int64_t j0 = static_cast<int64_t>(__ldg(cols + ch)) * 32;
+        for (int t = tid; t < CHUNK * kChunks16; t += kT) {
+            const int r = t / kChunks16, c = t % kChunks16;
+            cp_async16(smem_u32(sm.k[buf]) + swz<D>(r, c), Kp + (j0 + r) * D + c * 8, true);
+            cp_async16(smem_u32(sm.v[buf]) + swz<D>(r, c), Vp + (j0 + r) * D + c * 8, true);
+        }
+    };
+    const int nchunks = static_cast<int>(keep);
+    load_block(0, 0);
+    cp_async_commit();
+
+    const float sl2 = (scale ? rsqrtf(static_cast<float>(D)) : 1.f) * 1.4426950408889634f;
+    float m_run[NT][2], l_part[NT][2];
+    float zacc[NT][D / 16][4];
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+        m_run[n][0] = m_run[n][1] = -INFINITY;
+        l_part[n][0] = l_part[n][1] = 0.f;
+#pragma unroll
+        for (int t = 0; t < D / 16; ++t)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) zacc[n][t][u] = 0.f;
+    }
+    uint32_t qb[NT][D / 16][2];
+
+    for (int ch = 0; ch < nchunks; ++ch) {
+        const int buf = ch & 1;
+        if (ch + 1 < nchunks) load_block(buf ^ 1, ch + 1);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncthreads();
+        if (ch == 0) {
+#pragma unroll
+            for (int n = 0; n < NT; ++n)
+#pragma unroll
+                for (int ks = 0; ks < D / 16; ++ks) {
+                    const char* qbase = reinterpret_cast<const char*>(sm.q[warp][n]);
+                    qb[n][ks][0] = *reinterpret_cast<const uint32_t*>(qbase + swz<D>(g, 2 * ks) + c4 * 4);
+                    qb[n][ks][1] = *reinterpret_cast<const uint32_t*>(qbase + swz<D>(g, 2 * ks + 1) + c4 * 4);
+                }
+        }
+        float s[NT][CHUNK / 16][4];
+        const uint32_t kb = smem_u32(sm.k[buf]);
+#pragma unroll
+        for (int mt = 0; mt < CHUNK / 16; ++mt) {
+#pragma unroll
+            for (int n = 0; n < NT; ++n)
+#pragma unroll
+                for (int u = 0; u < 4; ++u) s[n][mt][u] = 0.f;
+#pragma unroll
+            for (int ks = 0; ks < D / 16; ++ks) {
+                const int mi = lane >> 3;
+                const int row = mt * 16 + (mi & 1) * 8 + (lane & 7);
+                const int chk = ks * 2 + (mi >> 1);
+                uint32_t a0, a1, a2, a3;
+                ldsm_x4(kb + swz<D>(row, chk), a0, a1, a2, a3);
+#pragma unroll
+                for (int n = 0; n < NT; ++n) mma16816(s[n][mt], a0, a1, a2, a3, qb[n][ks][0], qb[n][ks][1]);
+            }
+        }
+        constexpr int PW = CHUNK + 8;
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+            float cmax[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+            for (int mt = 0; mt < CHUNK / 16; ++mt)
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const float x = s[n][mt][u] * sl2;
+                    s[n][mt][u] = x;
+                    cmax[u & 1] = fmaxf(cmax[u & 1], x);
+                }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                cmax[h] = fmaxf(cmax[h], __shfl_xor_sync(0xffffffffu, cmax[h], 4));
+                cmax[h] = fmaxf(cmax[h], __shfl_xor_sync(0xffffffffu, cmax[h], 8));
+                cmax[h] = fmaxf(cmax[h], __shfl_xor_sync(0xffffffffu, cmax[h], 16));
+            }
+            float corr[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const float mn = fmaxf(m_run[n][h], cmax[h]);
+                corr[h] = m_run[n][h] == -INFINITY ? 0.f : exp2f(m_run[n][h] - mn);
+                m_run[n][h] = mn;
+                l_part[n][h] *= corr[h];
+            }
+#pragma unroll
+            for (int t = 0; t < D / 16; ++t) {
+                zacc[n][t][0] *= corr[0];
+                zacc[n][t][1] *= corr[1];
+                zacc[n][t][2] *= corr[0];
+                zacc[n][t][3] *= corr[1];
+            }
+#pragma unroll
+            for (int mt = 0; mt < CHUNK / 16; ++mt)
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const float pv = exp2f(s[n][mt][u] - m_run[n][u & 1]);
+                    l_part[n][u & 1] += pv;
+                    sm.p[warp][n][(2 * c4 + (u & 1)) * PW + mt * 16 + g + (u >> 1) * 8] = __float2bfloat16_rn(pv);
+                }
+        }
+        __syncwarp();
+        const uint32_t vb = smem_u32(sm.v[buf]);
+#pragma unroll
+        for (int ks = 0; ks < CHUNK / 16; ++ks) {
+            uint32_t b0[NT], b1[NT];
+#pragma unroll
+            for (int n = 0; n < NT; ++n) {
+                b0[n] = *reinterpret_cast<const uint32_t*>(&sm.p[warp][n][g * PW + ks * 16 + 2 * c4]);
+                b1[n] = *reinterpret_cast<const uint32_t*>(&sm.p[warp][n][g * PW + ks * 16 + 8 + 2 * c4]);
+            }
+#pragma unroll
+            for (int mt = 0; mt < D / 16; ++mt) {
+                const int mi = lane >> 3;
+                const int row = ks * 16 + (mi >> 1) * 8 + (lane & 7);
+                const int chk = mt * 2 + (mi & 1);
+                uint32_t a0, a1, a2, a3;
+                ldsm_x4_t(vb + swz<D>(row, chk), a0, a1, a2, a3);
+#pragma unroll
+                for (int n = 0; n < NT; ++n) mma16816(zacc[n][mt], a0, a1, a2, a3, b0[n], b1[n]);
+            }
+        }
+        __syncthreads();  // every warp done with `buf` before it is refilled
+    }
+    cp_async_wait<0>();
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            l_part[n][h] += __shfl_xor_sync(0xffffffffu, l_part[n][h], 4);
+            l_part[n][h] += __shfl_xor_sync(0xffffffffu, l_part[n][h], 8);
+            l_part[n][h] += __shfl_xor_sync(0xffffffffu, l_part[n][h], 16);
+        }
+        const float inv0 = l_part[n][0] > 0.f ? 1.f / l_part[n][0] : 0.f;
+        const float inv1 = l_part[n][1] > 0.f ? 1.f / l_part[n][1] : 0.f;
+        __nv_bfloat16* sq = sm.q[warp][n];
+#pragma unroll
+        for (int mt = 0; mt < D / 16; ++mt) {
+            const int d0 = mt * 16 + g;
+            sq[(2 * c4) * D + d0] = __float2bfloat16_rn(zacc[n][mt][0] * inv0);
+            sq[(2 * c4 + 1) * D + d0] = __float2bfloat16_rn(zacc[n][mt][1] * inv1);
+            sq[(2 * c4) * D + d0 + 8] = __float2bfloat16_rn(zacc[n][mt][2] * inv0);
+            sq[(2 * c4 + 1) * D + d0 + 8] = __float2bfloat16_rn(zacc[n][mt][3] * inv1);
+        }
+    }
+    __syncwarp();
+    for (int t = lane; t < NT * 8 * kChunks16; t += 32) {
+        const int n = t / (8 * kChunks16), rc = t % (8 * kChunks16);
+        const int r = rc / kChunks16, c = rc % kChunks16;
+        *reinterpret_cast<uint4*>(Z + (pair * L + r0 + n * 8 + r) * D + c * 8) =
+            *reinterpret_cast<const uint4*>(&sm.q[warp][n][r * D + c * 8]);
+    }
+}
+
+template <int D, int NT>
+void launch_block_nt(const AttnArgs& a, cudaStream_t st) {
+    const size_t smem = sizeof(BlockSmemN<D, NT>);
+    auto kern = attn_block_nt_kernel<D, NT>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        attr = true;
+    }
+    const dim3 grid(static_cast<unsigned>(a.L / 32), static_cast<unsigned>(a.pairs));
+    kern<<<grid, 128 / NT, smem, st>>>(static_cast<const __nv_bfloat16*>(a.q), static_cast<const __nv_bfloat16*>(a.k),
+                                       static_cast<const __nv_bfloat16*>(a.v), a.cols, a.L, a.keep, a.scale,
+                                       static_cast<__nv_bfloat16*>(a.z));
+}
+
 template <int D>
 void launch_block(const AttnArgs& a, cudaStream_t st) {
     const size_t smem = sizeof(BlockSmem<D>);
@@ -537,8 +747,20 @@ void run_band_attention(const AttnArgs& a, cudaStream_t st) {
             if (a.D == 64) launch_band_v2<64, 16, kBlockList>(a, st);
             else launch_band_v2<128, 8, kBlockList>(a, st);
         } else {
-            if (a.D == 64) launch_block<64>(a, st);
-            else launch_block<128>(a, st);
+            static const int nt = [] {
+                const char* e = std::getenv("DSA_BLOCK_NT");
+                return e ? std::atoi(e) : 2;
+            }();
+            if (nt == 1) {
+                if (a.D == 64) launch_block<64>(a, st);
+                else launch_block<128>(a, st);
+            } else if (nt == 4) {
+                if (a.D == 64) launch_block_nt<64, 4>(a, st);
+                else launch_block_nt<128, 4>(a, st);
+            } else {
+                if (a.D == 64) launch_block_nt<64, 2>(a, st);
+                else launch_block_nt<128, 2>(a, st);
+            }
         }
     } else if (a.mode == kRowTopk || a.mode == kThreshold) {
         static const bool per_row = std::getenv("DSA_ATTN_ROW_PER_WARP") != nullptr;  // A/B switch
