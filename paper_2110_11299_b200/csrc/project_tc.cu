@@ -88,13 +88,13 @@ __device__ __forceinline__ float cert_level(float x, float e, float inv_s, float
     return fminf(fmaxf(copysignf(floorf(at + 0.5f), t), -qmax), qmax);
 }
 
-template <int D, int KD>
+template <int D, int KD, int R = kRows>
 struct ProjSmem {
     static constexpr int N = 3 * KD;                 // B rows: P1 | P2 | P3 columns
-    static constexpr int kX = kRows * D * 2;         // X tile
+    static constexpr int kX = R * D * 2;             // X tile (R rows)
     static constexpr int kB = N * D * 2;             // P-split image
     static constexpr int kImg = kB + KD * 4;         // image + |p_j| (bound factors)
-    static constexpr int kLvl = kRows * KD * 2;      // staged levels [row][KD] bf16
+    static constexpr int kLvl = R * KD * 2;          // staged levels [row][KD] bf16
     static constexpr int kList = kMaxList * 4;
     static constexpr int kMisc = 64;
     static constexpr int bytes() { return kX + kImg + kMisc + kLvl + kList; }
@@ -132,16 +132,18 @@ __global__ void psplit_kernel(const float* __restrict__ p, unsigned char* __rest
 // QUANT = false: exact per-tensor amax (atomic max into amax[pair][2]).
 // QUANT = true : levels (chunk-planar) + scales from the exact amax.
 // grid = (row tiles, 2 tensors, pairs)
-template <int D, int KD, bool QUANT>
-__global__ void __launch_bounds__(kRows)
+// R = 128 or 256 rows per CTA (one or two M = 128 MMAs; two halves amortise
+// the P-image copy and the CTA prologue over twice the rows).
+template <int D, int KD, bool QUANT, int R = kRows>
+__global__ void __launch_bounds__(R)
     project_tc_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k,
                       const float* __restrict__ p, const unsigned char* __restrict__ img, int64_t L,
                       int round_f32, double qmax, unsigned long long* __restrict__ amax,
                       uint16_t* __restrict__ lq, uint16_t* __restrict__ lk, double* __restrict__ sq,
                       double* __restrict__ sk, float* __restrict__ xhat) {
-    using Sm = ProjSmem<D, KD>;
+    using Sm = ProjSmem<D, KD, R>;
     constexpr int N = Sm::N;
-    constexpr int TC = N <= 64 ? 64 : 128;  // TMEM columns
+    constexpr int TC = (R / 128) * N <= 64 ? 64 : ((R / 128) * N <= 128 ? 128 : 256);  // TMEM columns
     extern __shared__ __align__(1024) unsigned char smem[];
     unsigned char* xa = smem;
     unsigned char* pb = smem + Sm::kX;
@@ -157,7 +159,7 @@ __global__ void __launch_bounds__(kRows)
     const int tid = threadIdx.x, warp = tid >> 5;
     const int which = blockIdx.y;
     const int64_t pair = blockIdx.z;
-    const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kRows;
+    const int64_t row0 = static_cast<int64_t>(blockIdx.x) * R;
     const __nv_bfloat16* X = (which ? k : q) + pair * L * D;
 
     if (tid == 0) {
@@ -172,7 +174,7 @@ __global__ void __launch_bounds__(kRows)
         // X tile: 16-byte chunks, 8 consecutive threads = 8 rows of one chunk
         constexpr int kCh = D / 8;
         const uint32_t xs = tc::smem_addr(xa);
-        for (int i = tid; i < kRows * kCh; i += kRows) {
+        for (int i = tid; i < R * kCh; i += R) {
             const int r7 = i & 7, ch = (i >> 3) % kCh, rg = (i >> 3) / kCh;
             const int r = rg * 8 + r7;
             const bool ok = row0 + r < L;
@@ -180,7 +182,7 @@ __global__ void __launch_bounds__(kRows)
         }
         // P-split image (+ |p_j|)
         const uint32_t ps = tc::smem_addr(pb);
-        for (int i = tid; i < Sm::kImg / 16; i += kRows) cp16(ps + i * 16, img + i * 16, true);
+        for (int i = tid; i < Sm::kImg / 16; i += R) cp16(ps + i * 16, img + i * 16, true);
         asm volatile("cp.async.commit_group;\n");
         asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     }
@@ -190,14 +192,16 @@ __global__ void __launch_bounds__(kRows)
     tc::fence_after_sync();
     const uint32_t tmem = *tslot;
     if (tid == 0) {
-        constexpr uint32_t idesc = tc::idesc_bf16_f32(kRows, N);
+        constexpr uint32_t idesc = tc::idesc_bf16_f32(128, N);
         const uint32_t xs = tc::smem_addr(xa), bs = tc::smem_addr(pb);
 #pragma unroll
-        for (int ks = 0; ks < D / 16; ++ks) {
-            const uint64_t ad = tc::desc_kmajor_nosw(xs + ks * 256, 128, D * 16);
-            const uint64_t bd = tc::desc_kmajor_nosw(bs + ks * 256, 128, D * 16);
-            tc::mma_bf16(tmem, ad, bd, idesc, ks > 0);
-        }
+        for (int h = 0; h < R / 128; ++h)  // rows 128h.. -> TMEM columns [hN, hN + N)
+#pragma unroll
+            for (int ks = 0; ks < D / 16; ++ks) {
+                const uint64_t ad = tc::desc_kmajor_nosw(xs + h * 16 * (D * 16) + ks * 256, 128, D * 16);
+                const uint64_t bd = tc::desc_kmajor_nosw(bs + ks * 256, 128, D * 16);
+                tc::mma_bf16(tmem + h * N, ad, bd, idesc, ks > 0);
+            }
         tc::commit(bar);
     }
     // |q| of this thread's row (bound factor), from the staged tile
@@ -225,7 +229,7 @@ __global__ void __launch_bounds__(kRows)
     // x^_j = P1 part + (P2 part + P3 part)
     float xv[KD];
     {
-        const uint32_t base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+        const uint32_t base = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16) + (warp >> 2) * N;
         uint32_t d0[32];
         if constexpr (N == 48) {
             uint32_t d1[16];
@@ -279,7 +283,7 @@ __global__ void __launch_bounds__(kRows)
         __syncthreads();
         const unsigned n = min(*lcount, static_cast<unsigned>(kMaxList));
         double am = 0.0;
-        for (unsigned e = tid; e < n; e += kRows)
+        for (unsigned e = tid; e < n; e += R)
             am = fmax(am, fabs(ref_chain_s<D, KD>(xa, static_cast<int>(list[e] >> 6), p, list[e] & 63, round_f32)));
         if (am > 0.0) atomicMax(red_d, static_cast<unsigned long long>(__double_as_longlong(am)));
         __syncthreads();
@@ -314,7 +318,7 @@ __global__ void __launch_bounds__(kRows)
         }
         __syncthreads();
         const unsigned n = min(*lcount, static_cast<unsigned>(kMaxList));
-        for (unsigned e = tid; e < n; e += kRows) {
+        for (unsigned e = tid; e < n; e += R) {
             const int rr = static_cast<int>(list[e] >> 6), j = static_cast<int>(list[e] & 63);
             const double xe = ref_chain_s<D, KD>(xa, rr, p, j, round_f32);
             const float lv = static_cast<float>(fmin(fmax(round_half_away(xe / s), -qmax), qmax));
@@ -388,14 +392,15 @@ __global__ void __launch_bounds__(256)
     *reinterpret_cast<uint4*>(out + lvl_index(L, r, c * 8)) = make_uint4(w[0], w[1], w[2], w[3]);
 }
 
-template <int D, int KD>
+template <int D, int KD, int R>
 void launch_tc(const PredictArgs& a, cudaStream_t st) {
-    using Sm = ProjSmem<D, KD>;
-    constexpr int TC = 3 * KD <= 64 ? 64 : 128;
+    using Sm = ProjSmem<D, KD, R>;
+    constexpr int N = 3 * KD;
+    constexpr int TC = (R / 128) * N <= 64 ? 64 : ((R / 128) * N <= 128 ? 128 : 256);
     // no more CTAs per SM than TMEM holds (512 columns)
     const int smem = std::max(Sm::bytes(), (228 * 1024) / (512 / TC + 1) + 1024);
-    auto ka = project_tc_kernel<D, KD, false>;
-    auto kq = project_tc_kernel<D, KD, true>;
+    auto ka = project_tc_kernel<D, KD, false, R>;
+    auto kq = project_tc_kernel<D, KD, true, R>;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -404,22 +409,33 @@ void launch_tc(const PredictArgs& a, cudaStream_t st) {
     }
     const auto* q = static_cast<const __nv_bfloat16*>(a.q);
     const auto* k = static_cast<const __nv_bfloat16*>(a.k);
-    const dim3 grid(static_cast<unsigned>(ceil_div_i(a.L, kRows)), 2, static_cast<unsigned>(a.pairs));
+    const dim3 grid(static_cast<unsigned>(ceil_div_i(a.L, R)), 2, static_cast<unsigned>(a.pairs));
     psplit_kernel<D, KD><<<1, 256, 0, st>>>(a.p, a.pimg, a.amax, 2 * a.pairs);
     if (a.xhat != nullptr) {
         // amax pass stores x^ (fp32) + bound factors; the quantise pass streams them
-        ka<<<grid, kRows, smem, st>>>(q, k, a.p, a.pimg, a.L, a.round_f32, a.qmax, a.amax, a.lq, a.lk, a.sq, a.sk,
-                                      a.xhat);
+        ka<<<grid, R, smem, st>>>(q, k, a.p, a.pimg, a.L, a.round_f32, a.qmax, a.amax, a.lq, a.lk, a.sq, a.sk,
+                                  a.xhat);
         const int64_t n = a.pairs * 2 * a.L * (KD / 8);
         quantize_xhat_kernel<D, KD><<<static_cast<unsigned>(ceil_div_i(n, 256)), 256, 0, st>>>(
             a.xhat, q, k, a.p, a.pimg, a.pairs, a.L, a.round_f32, a.qmax, a.amax, a.lq, a.lk, a.sq, a.sk);
     } else {
-        ka<<<grid, kRows, smem, st>>>(q, k, a.p, a.pimg, a.L, a.round_f32, a.qmax, a.amax, a.lq, a.lk, a.sq, a.sk,
-                                      nullptr);
-        kq<<<grid, kRows, smem, st>>>(q, k, a.p, a.pimg, a.L, a.round_f32, a.qmax, a.amax, a.lq, a.lk, a.sq, a.sk,
-                                      nullptr);
+        ka<<<grid, R, smem, st>>>(q, k, a.p, a.pimg, a.L, a.round_f32, a.qmax, a.amax, a.lq, a.lk, a.sq, a.sk,
+                                  nullptr);
+        kq<<<grid, R, smem, st>>>(q, k, a.p, a.pimg, a.L, a.round_f32, a.qmax, a.amax, a.lq, a.lk, a.sq, a.sk,
+                                  nullptr);
     }
     note_launch(3);
+}
+
+template <int D, int KD>
+void launch_tc(const PredictArgs& a, cudaStream_t st) {
+    static const int rows = [] {
+        const char* e = std::getenv("DSA_PREDICT_ROWS");
+        return e ? std::atoi(e) : 0;
+    }();
+    const bool two = rows == 256 || (rows == 0 && D == 128);
+    if (two) launch_tc<D, KD, 256>(a, st);
+    else launch_tc<D, KD, 128>(a, st);
 }
 
 }  // namespace
