@@ -692,6 +692,10 @@ void run_select(const SelectArgs& a, cudaStream_t st) {
         run_topk_tc(a, st);
         return;
     }
+    if (topk_rowwarp_supported(a)) {
+        run_topk_rowwarp(a, st);
+        return;
+    }
     switch (a.KD) {
         case 16: launch_select<16>(a, st); break;
         case 32: launch_select<32>(a, st); break;
