@@ -57,11 +57,11 @@ __device__ __forceinline__ uint32_t tile_off(int r, int chunk16) {
     return static_cast<uint32_t>((r >> 3) * (KD * 16) + chunk16 * 128 + (r & 7) * 16);
 }
 
-template <int KD, int ROWS = kMT>
+template <int KD, int ROWS = kMT, int NT = kThreads>
 __device__ __forceinline__ void load_tile(uint32_t sbase, const uint16_t* __restrict__ src,
                                           int64_t row0, int64_t L, int tid) {
     constexpr int kCh = KD / 8;  // 16-byte chunks per row
-    for (int t = tid; t < ROWS * kCh; t += kThreads) {
+    for (int t = tid; t < ROWS * kCh; t += NT) {
         const int r = t / kCh, c = t % kCh;
         const bool ok = row0 + r < L;
         cp_async16(sbase + tile_off<KD>(r, c), src + lvl_index(L, ok ? (row0 + r) : 0, c * 8), ok);
@@ -103,13 +103,18 @@ struct FusedAttn {
     int scale;
 };
 
+// threads per CTA: four warps per 32-query column group (TMEM lane quarters)
+template <int NQ>
+constexpr int colvec_threads() { return NQ == 32 ? 128 : 256; }
+
 template <int KD, int NQ, bool TMA, bool FUSED = false>
-__global__ void __launch_bounds__(kThreads, NQ == 64 ? 2 : 1)
+__global__ void __launch_bounds__(colvec_threads<NQ>(), NQ == 128 ? 1 : (NQ == 64 ? 2 : 4))
     colvec_tc_kernel(const uint16_t* __restrict__ lq, const uint16_t* __restrict__ lk, int64_t L,
                      int64_t keep, int M, uint32_t* __restrict__ out, int dbg, FusedAttn fa) {
     extern __shared__ __align__(1024) unsigned char smem[];
+    constexpr int kT = colvec_threads<NQ>();
     constexpr int NB = NQ / 8;       // bands per CTA
-    constexpr int CPW = NQ / 2;      // query columns per epilogue warp (lane quarter x half)
+    constexpr int CPW = NQ / (kT / 128);  // query columns per epilogue warp (lane quarter x column group)
     constexpr int NLD = CPW / 32;    // tcgen05.ld x32 per tile
     constexpr int BPW = CPW / 8;     // bands per warp
     constexpr int kTile = ColvecSmem<KD>::kTileBytes;
@@ -119,8 +124,8 @@ __global__ void __launch_bounds__(kThreads, NQ == 64 ? 2 : 1)
     unsigned char* bq = p;                      p += NQ * KD * 2;         // Q~ block (N = NQ)
     unsigned char* ring = p;                    p += kStages * kTile;     // K~ tiles
     int16_t* pooled = reinterpret_cast<int16_t*>(p); p += NB * Lp * 2;   // [band][key]
-    uint32_t* hist = reinterpret_cast<uint32_t*>(p); p += (kThreads / 32) * 64 * 4;
-    uint32_t* obufs = reinterpret_cast<uint32_t*>(p); p += (kThreads / 32) * kList * 4;
+    uint32_t* hist = reinterpret_cast<uint32_t*>(p); p += (kT / 32) * 64 * 4;
+    uint32_t* obufs = reinterpret_cast<uint32_t*>(p); p += (kT / 32) * kList * 4;
     int* bandmax = reinterpret_cast<int*>(p);   p += 16 * 4;
     uint64_t* bars = reinterpret_cast<uint64_t*>(p);  // one per TMEM accumulator
     uint64_t* full = bars + kAcc;                     // TMA: one per ring slot, then the Q~ block
@@ -148,13 +153,13 @@ __global__ void __launch_bounds__(kThreads, NQ == 64 ? 2 : 1)
     // each thread copies the same 16-byte chunk(s) of every K~ tile: the
     // chunk-planar levels put tile n's copy of a chunk n * kMT rows further
     // along the same plane, so the per-tile address math is one add
-    constexpr int kCPT = kMT * (KD / 8) / kThreads;  // chunks per thread per tile
+    constexpr int kCPT = kMT * (KD / 8) / kT;  // chunks per thread per tile
     uint32_t soff[kCPT];
     const uint16_t* gsrc[kCPT];
     int rrow[kCPT];
 #pragma unroll
     for (int i = 0; i < kCPT; ++i) {
-        const int t = tid + i * kThreads, r = t / (KD / 8), c = t % (KD / 8);
+        const int t = tid + i * kT, r = t / (KD / 8), c = t % (KD / 8);
         soff[i] = tile_off<KD>(r, c);
         gsrc[i] = lkp + lvl_index(L, r, c * 8);
         rrow[i] = r;
@@ -170,7 +175,7 @@ __global__ void __launch_bounds__(kThreads, NQ == 64 ? 2 : 1)
     };
     // prologue: Q~ block + first kStages K~ tiles (group t <-> tile t)
     if (!TMA) {
-        load_tile<KD, NQ>(tc::smem_addr(bq), lqp, q0, L, tid);
+        load_tile<KD, NQ, kT>(tc::smem_addr(bq), lqp, q0, L, tid);
         for (int s = 0; s < kStages; ++s) {
             if (s < nt) load_k(s, s);
             cp_commit();
@@ -292,7 +297,7 @@ __global__ void __launch_bounds__(kThreads, NQ == 64 ? 2 : 1)
     // ---- exact per-band selection (one warp per band)
     const int64_t nb = (L + 7) / 8;
     uint32_t* h = hist + warp * 64;
-    for (int b = warp; b < NB && !(dbg & 1); b += kThreads / 32) {
+    for (int b = warp; b < NB && !(dbg & 1); b += kT / 32) {
         const int64_t band = q0 / 8 + b;
         if (band >= nb) break;
         const int16_t* pv = pooled + (b >> 1) * Lp * 2 + (b & 1);
@@ -301,7 +306,7 @@ __global__ void __launch_bounds__(kThreads, NQ == 64 ? 2 : 1)
         __syncwarp();
     }
     if constexpr (FUSED) {
-        static_assert(NQ == 64 && kThreads / 32 == 8, "fused path: one band per warp");
+        static_assert(NQ == 64 && kT / 32 == 8, "fused path: one band per warp");
         // the score-loop buffers (ring, pooled, histograms) are free now
         __syncthreads();
         using BS = bc::BandSmemV2<64>;
@@ -491,7 +496,8 @@ template <int KD, int NQ>
 size_t colvec_smem_bytes(int64_t L) {
     const int64_t nt = (L + kMT - 1) / kMT;
     return ColvecSmem<KD>::kTileBytes * kStages + NQ * KD * 2 + (NQ / 8) * nt * kMT * 2 +
-           (kThreads / 32) * 64 * 4 + (kThreads / 32) * kList * 4 + 16 * 4 + (2 * kAcc + kStages + 1) * 8 + 8;
+           (colvec_threads<NQ>() / 32) * 64 * 4 + (colvec_threads<NQ>() / 32) * kList * 4 + 16 * 4 +
+           (2 * kAcc + kStages + 1) * 8 + 8;
 }
 
 }  // namespace
@@ -512,7 +518,7 @@ void launch_colvec(const SelectArgs& a, int M, int dbg, cudaStream_t st) {
     auto kern = tma ? colvec_tc_kernel<KD, NQ, true> : colvec_tc_kernel<KD, NQ, false>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     const dim3 grid(static_cast<unsigned>(ceil_div_i(a.L, NQ)), static_cast<unsigned>(a.pairs));
-    kern<<<grid, kThreads, smem, st>>>(a.lq, a.lk, a.L, a.keep, M, a.cols, dbg, FusedAttn{});
+    kern<<<grid, colvec_threads<NQ>(), smem, st>>>(a.lq, a.lk, a.L, a.keep, M, a.cols, dbg, FusedAttn{});
 }
 
 void run_colvec_tc(const SelectArgs& a, cudaStream_t st) {
@@ -533,6 +539,16 @@ void run_colvec_tc(const SelectArgs& a, cudaStream_t st) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         const dim3 grid(static_cast<unsigned>(ceil_div_i(a.L, 64)), static_cast<unsigned>(a.pairs));
         kern<<<grid, kThreads + 32, smem, st>>>(a.lq, a.lk, a.L, a.keep, M, a.cols, dbg);
+        note_launch();
+        return;
+    }
+    static const int nq_env = [] {
+        const char* e = std::getenv("DSA_COLVEC_NQ");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (nq_env == 32 && (a.KD == 16 ? colvec_smem_bytes<16, 32>(a.L) : colvec_smem_bytes<32, 32>(a.L)) <= 75 * 1024) {
+        if (a.KD == 16) launch_colvec<16, 32>(a, M, dbg, st);
+        else launch_colvec<32, 32>(a, M, dbg, st);
         note_launch();
         return;
     }
