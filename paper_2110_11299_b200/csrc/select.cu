@@ -22,7 +22,7 @@
 namespace dsa {
 namespace {
 
-constexpr int kNT = 256;
+constexpr int kNT = 128;
 constexpr int kWarps = kNT / 32;
 
 struct SelSmem {
