@@ -75,20 +75,8 @@ struct ColvecSmem {
 
 // NQ = 64: 8 bands per CTA, ~100 KB of shared memory -> two CTAs per SM, so
 // one CTA's selection overlaps the other's tensor-core / TMEM score loop.
-// TMA = true: one lane issues every operand copy as TMA-engine bulk copies
-// (the chunk-planar levels make each 8-column plane of a tile one
-// contiguous run; the planes become the K-adjacent core matrices, LBO =
-// rows * 16, SBO = 128) completing on per-slot mbarriers -- no per-thread
-// cp.async address math and no generic->async proxy fence per tile.
-template <int KD>
-__device__ __forceinline__ void bulk_tile(uint32_t sdst, const uint16_t* __restrict__ src, int64_t row0,
-                                          int rows_cap, int64_t L, uint64_t* bar) {
-    const uint32_t rows = static_cast<uint32_t>(L - row0 < rows_cap ? L - row0 : rows_cap);
-    tc::mbar_expect_tx(bar, (KD / 8) * rows * 16);
-#pragma unroll
-    for (int c = 0; c < KD / 8; ++c)
-        tc::bulk_g2s(sdst + c * (rows_cap * 16), src + (c * L + row0) * 8, rows * 16, bar);
-}
+// (A TMA-engine variant of the K~ tile copies -- one bulk copy per 8-column
+// plane, per-slot mbarriers -- measured slower on C2: 0.85 vs 0.70 ms.)
 
 // Fused select + attention (FUSED, NQ = 64, d = 64): after its bands are
 // selected, each warp runs the band attention (band_core.cuh) over its
@@ -107,7 +95,11 @@ struct FusedAttn {
 template <int NQ>
 constexpr int colvec_threads() { return NQ == 32 ? 128 : 256; }
 
-template <int KD, int NQ, bool TMA, bool FUSED = false>
+constexpr int kTPS = 2;                 // key tiles per pipeline step (one barrier per step)
+constexpr int kSS = kStages / kTPS;     // step slots in the K~ ring
+constexpr int kAS = kAcc / kTPS;        // TMEM accumulator sets
+
+template <int KD, int NQ, bool FUSED = false>
 __global__ void __launch_bounds__(colvec_threads<NQ>(), NQ == 128 ? 1 : (NQ == 64 ? 2 : 4))
     colvec_tc_kernel(const uint16_t* __restrict__ lq, const uint16_t* __restrict__ lk, int64_t L,
                      int64_t keep, int M, uint32_t* __restrict__ out, int dbg, FusedAttn fa) {
@@ -118,7 +110,8 @@ __global__ void __launch_bounds__(colvec_threads<NQ>(), NQ == 128 ? 1 : (NQ == 6
     constexpr int NLD = CPW / 32;    // tcgen05.ld x32 per tile
     constexpr int BPW = CPW / 8;     // bands per warp
     constexpr int kTile = ColvecSmem<KD>::kTileBytes;
-    const int nt = static_cast<int>((L + kMT - 1) / kMT);
+    const int Li = static_cast<int>(L);
+    const int nt = (Li + kMT - 1) / kMT;
     const int Lp = nt * kMT;
     unsigned char* p = smem;
     unsigned char* bq = p;                      p += NQ * KD * 2;         // Q~ block (N = NQ)
@@ -127,8 +120,7 @@ __global__ void __launch_bounds__(colvec_threads<NQ>(), NQ == 128 ? 1 : (NQ == 6
     uint32_t* hist = reinterpret_cast<uint32_t*>(p); p += (kT / 32) * 64 * 4;
     uint32_t* obufs = reinterpret_cast<uint32_t*>(p); p += (kT / 32) * kList * 4;
     int* bandmax = reinterpret_cast<int*>(p);   p += 16 * 4;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(p);  // one per TMEM accumulator
-    uint64_t* full = bars + kAcc;                     // TMA: one per ring slot, then the Q~ block
+    uint64_t* bars = reinterpret_cast<uint64_t*>(p);  // one per TMEM accumulator set
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kAcc + kStages + 1);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -139,13 +131,8 @@ __global__ void __launch_bounds__(colvec_threads<NQ>(), NQ == 128 ? 1 : (NQ == 6
     const uint16_t* lkp = lk + pair * L * KD;
 
     if (tid == 0) {
-        for (int b = 0; b < kAcc + (TMA ? kStages + 1 : 0); ++b) tc::mbar_init(&bars[b], 1);
+        for (int b = 0; b < kAS; ++b) tc::mbar_init(&bars[b], 1);
         tc::fence_barrier_init();
-        if (TMA) {
-            bulk_tile<KD>(tc::smem_addr(bq), lqp, q0, NQ, L, &full[kStages]);
-            for (int s = 0; s < kStages && s < nt; ++s)
-                bulk_tile<KD>(tc::smem_addr(ring + s * kTile), lkp, static_cast<int64_t>(s) * kMT, kMT, L, &full[s]);
-        }
     }
     if (tid < NB) bandmax[tid] = INT32_MIN;
     if (warp == 0) tc::tmem_alloc<kAcc * NQ>(tmem_slot);
@@ -165,21 +152,25 @@ __global__ void __launch_bounds__(colvec_threads<NQ>(), NQ == 128 ? 1 : (NQ == 6
         rrow[i] = r;
     }
     const uint32_t ring_s = tc::smem_addr(ring);
-    auto load_k = [&](int slot, int tile) {
-        const int64_t row0 = static_cast<int64_t>(tile) * kMT;
+    auto load_k = [&](int slot, int tile) {  // tile -> ring slot (tile index)
+        const int row0 = tile * kMT;
 #pragma unroll
         for (int i = 0; i < kCPT; ++i) {
-            const bool ok = row0 + rrow[i] < L;
-            cp_async16(ring_s + slot * kTile + soff[i], ok ? gsrc[i] + row0 * 8 : gsrc[i], ok);
+            const bool ok = row0 + rrow[i] < Li;
+            cp_async16(ring_s + slot * kTile + soff[i], gsrc[i] + (ok ? row0 * 8 : 0), ok);
         }
     };
-    // prologue: Q~ block + first kStages K~ tiles (group t <-> tile t)
-    if (!TMA) {
-        load_tile<KD, NQ, kT>(tc::smem_addr(bq), lqp, q0, L, tid);
-        for (int s = 0; s < kStages; ++s) {
-            if (s < nt) load_k(s, s);
-            cp_commit();
-        }
+    auto load_step = [&](int sslot, int step) {
+#pragma unroll
+        for (int i = 0; i < kTPS; ++i)
+            if (step * kTPS + i < nt) load_k(sslot * kTPS + i, step * kTPS + i);
+    };
+    const int ns = (nt + kTPS - 1) / kTPS;  // pipeline steps
+    // prologue: Q~ block + first kSS steps (group s <-> step s)
+    load_tile<KD, NQ, kT>(tc::smem_addr(bq), lqp, q0, L, tid);
+    for (int s = 0; s < kSS; ++s) {
+        if (s < ns) load_step(s, s);
+        cp_commit();
     }
     tc::fence_before_sync();
     __syncthreads();
@@ -187,100 +178,94 @@ __global__ void __launch_bounds__(colvec_threads<NQ>(), NQ == 128 ? 1 : (NQ == 6
     const uint32_t tmem = *tmem_slot;
     const uint32_t idesc = tc::idesc_bf16_f32(kMT, NQ);
     const uint64_t bdesc = tc::desc_kmajor_nosw(tc::smem_addr(bq), 128, KD * 16);
+    const uint32_t bars_s = tc::smem_addr(bars);
     const bool ragged_q = q0 + NQ > L;
     float bmax[BPW];
 #pragma unroll
     for (int i = 0; i < BPW; ++i) bmax[i] = -INFINITY;
+    const uint32_t tlane = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + half * CPW;
 
-    // Software pipeline, MMA kLag tiles ahead of the epilogue: iteration t
-    // issues the MMA of tile t (accumulator t % kAcc) and drains tile t-kLag,
-    // whose MMA finished long ago; its K~ slot is then refilled with tile
-    // t - kLag + kStages.  One __syncthreads per tile.
-    for (int t = 0; t < nt + kLag; ++t) {
-        if (!TMA && t < nt) {
-            cp_wait<kStages - 1 - kLag>();
+    // Software pipeline over steps of kTPS key tiles: iteration t issues the
+    // MMAs of step t (accumulator set t % kAS) and drains step t - 1, whose
+    // MMAs finished during the previous epilogue; its ring slot is then
+    // refilled with step t - 1 + kSS.  One __syncthreads per step.  Step j's
+    // copies are commit group j (j < kSS) or j + 1, so when step t is needed
+    // at most kSS - 2 younger groups may still be in flight.
+    for (int t = 0; t < ns + 1; ++t) {
+        if (t < ns) {
+            cp_wait<kSS - 2>();
             tc::fence_proxy_async();
         }
         __syncthreads();
-        if (t < nt && tid == 0) {
-            if (TMA) {
-                if (t == 0) tc::mbar_wait(&full[kStages], 0);
-                tc::mbar_wait(&full[t % kStages], (t / kStages) & 1);
-            }
+        if (t < ns && tid == 0) {
             tc::fence_after_sync();
-            const uint32_t abase = tc::smem_addr(ring + (t % kStages) * kTile);
 #pragma unroll
-            for (int ks = 0; ks < KD / 16; ++ks) {
-                if (TMA) {
-                    const uint64_t ad = tc::desc_kmajor_nosw(abase + ks * 2 * (kMT * 16), kMT * 16, 128);
-                    const uint64_t bd = tc::desc_kmajor_nosw(tc::smem_addr(bq) + ks * 2 * (NQ * 16), NQ * 16, 128);
-                    tc::mma_bf16(tmem + (t % kAcc) * NQ, ad, bd, idesc, ks > 0);
-                } else {
+            for (int i = 0; i < kTPS; ++i) {
+                if (t * kTPS + i >= nt) break;
+                const uint32_t abase = ring_s + ((t % kSS) * kTPS + i) * kTile;
+#pragma unroll
+                for (int ks = 0; ks < KD / 16; ++ks) {
                     const uint64_t ad = tc::desc_kmajor_nosw(abase + ks * 256, 128, KD * 16);
                     const uint64_t bd = bdesc + static_cast<uint64_t>((ks * 256) >> 4);
-                    tc::mma_bf16(tmem + (t % kAcc) * NQ, ad, bd, idesc, ks > 0);
+                    tc::mma_bf16(tmem + ((t % kAS) * kTPS + i) * NQ, ad, bd, idesc, ks > 0);
                 }
             }
-            tc::commit(&bars[t % kAcc]);
+            tc::commit_a(bars_s + (t % kAS) * 8);
         }
-        if (t >= kLag) {
-            const int u = t - kLag;
-            tc::mbar_wait(&bars[u % kAcc], (u / kAcc) & 1);
+        if (t >= 1) {
+            const int u = t - 1;
+            tc::mbar_wait_a(bars_s + (u % kAS) * 8, (u / kAS) & 1);
             tc::fence_after_sync();
-            // epilogue of tile u: thread = key u*128 + 32*quarter + lane,
-            // query columns [CPW*half, CPW*half + CPW)
-            const int key = u * kMT + quarter * 32 + lane;
-            const bool kvalid = key < L;
-            const uint32_t base = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + (u % kAcc) * NQ + half * CPW;
-            uint32_t rr[NLD][32];
 #pragma unroll
-            for (int l = 0; l < NLD; ++l) tc::ld_32x32b_x32(base + l * 32, rr[l]);
-            tc::wait_ld();
+            for (int i = 0; i < kTPS; ++i) {
+                const int tile = u * kTPS + i;
+                if (tile >= nt) break;
+                // epilogue of one tile: thread = key tile*128 + 32*quarter + lane,
+                // query columns [CPW*half, CPW*half + CPW)
+                const int key = tile * kMT + quarter * 32 + lane;
+                const bool kvalid = key < Li;
+                const uint32_t base = tlane + ((u % kAS) * kTPS + i) * NQ;
+                uint32_t rr[NLD][32];
 #pragma unroll
-            for (int cb = 0; cb < NLD; ++cb) {
-                uint32_t* r = rr[cb];
-                if (ragged_q) {
+                for (int l = 0; l < NLD; ++l) tc::ld_32x32b_x32(base + l * 32, rr[l]);
+                tc::wait_ld();
 #pragma unroll
-                    for (int x = 0; x < 32; ++x)
-                        if (q0 + half * CPW + cb * 32 + x >= L) r[x] = __float_as_uint(-INFINITY);
-                }
-                float m4[4];
+                for (int cb = 0; cb < NLD; ++cb) {
+                    uint32_t* r = rr[cb];
+                    if (ragged_q) {
 #pragma unroll
-                for (int bb = 0; bb < 4; ++bb) {
-                    float m0, m1, m2;
-                    const float* f = reinterpret_cast<const float*>(&r[bb * 8]);
-                    asm("max.f32 %0, %1, %2, %3;" : "=f"(m0) : "f"(f[0]), "f"(f[1]), "f"(f[2]));
-                    asm("max.f32 %0, %1, %2, %3;" : "=f"(m1) : "f"(f[3]), "f"(f[4]), "f"(f[5]));
-                    asm("max.f32 %0, %1, %2, %3;" : "=f"(m2) : "f"(m0), "f"(m1), "f"(f[6]));
-                    m4[bb] = fmaxf(m2, f[7]);
-                    if (kvalid) bmax[cb * 4 + bb] = fmaxf(bmax[cb * 4 + bb], m4[bb]);
-                }
-                // two bands per 32-bit store: [band / 2][key][2] int16 (the
-                // exact integer maxima convert by the 1.5 * 2^23 addition)
+                        for (int x = 0; x < 32; ++x)
+                            if (q0 + half * CPW + cb * 32 + x >= L) r[x] = __float_as_uint(-INFINITY);
+                    }
+                    float m4[4];
 #pragma unroll
-                for (int pp = 0; pp < 2; ++pp) {
-                    const int v0 = __float_as_int(m4[2 * pp] + 12582912.0f) - 0x4B400000;
-                    const int v1 = __float_as_int(m4[2 * pp + 1] + 12582912.0f) - 0x4B400000;
-                    const uint32_t packed = kvalid ? __byte_perm(static_cast<uint32_t>(v0), static_cast<uint32_t>(v1), 0x5410)
-                                                   : 0x80008000u;
-                    const int band = half * BPW + cb * 4 + 2 * pp;  // even
-                    *reinterpret_cast<uint32_t*>(pooled + ((band >> 1) * Lp + key) * 2) = packed;
+                    for (int bb = 0; bb < 4; ++bb) {
+                        float m0, m1, m2;
+                        const float* f = reinterpret_cast<const float*>(&r[bb * 8]);
+                        asm("max.f32 %0, %1, %2, %3;" : "=f"(m0) : "f"(f[0]), "f"(f[1]), "f"(f[2]));
+                        asm("max.f32 %0, %1, %2, %3;" : "=f"(m1) : "f"(f[3]), "f"(f[4]), "f"(f[5]));
+                        asm("max.f32 %0, %1, %2, %3;" : "=f"(m2) : "f"(m0), "f"(m1), "f"(f[6]));
+                        m4[bb] = fmaxf(m2, f[7]);
+                        if (kvalid) bmax[cb * 4 + bb] = fmaxf(bmax[cb * 4 + bb], m4[bb]);
+                    }
+                    // two bands per 32-bit store: [band / 2][key][2] int16 (the
+                    // exact integer maxima convert by the 1.5 * 2^23 addition)
+#pragma unroll
+                    for (int pp = 0; pp < 2; ++pp) {
+                        const int v0 = __float_as_int(m4[2 * pp] + 12582912.0f) - 0x4B400000;
+                        const int v1 = __float_as_int(m4[2 * pp + 1] + 12582912.0f) - 0x4B400000;
+                        const uint32_t packed = kvalid ? __byte_perm(static_cast<uint32_t>(v0), static_cast<uint32_t>(v1), 0x5410)
+                                                       : 0x80008000u;
+                        const int band = half * BPW + cb * 4 + 2 * pp;  // even
+                        *reinterpret_cast<uint32_t*>(pooled + ((band >> 1) * Lp + key) * 2) = packed;
+                    }
                 }
             }
             tc::fence_before_sync();
-            // tile u's K~ slot is free (its MMA completed): refill it
-            const int nxt = u + kStages;
-            if (nxt < nt) {
-                if (TMA) {
-                    if (tid == 0)
-                        bulk_tile<KD>(tc::smem_addr(ring + (u % kStages) * kTile), lkp, static_cast<int64_t>(nxt) * kMT,
-                                      kMT, L, &full[u % kStages]);
-                } else {
-                    load_k(u % kStages, nxt);
-                }
-            }
+            // step u's ring slot is free (its MMAs completed): refill it
+            if (u + kSS < ns) load_step(u % kSS, u + kSS);
         }
-        if (!TMA) cp_commit();
+        cp_commit();
     }
     __syncthreads();
     // band maxima: warp reduce, then shared atomics across the 4 lane quarters
@@ -512,10 +497,8 @@ bool colvec_tc_supported(const SelectArgs& a) {
 
 template <int KD, int NQ>
 void launch_colvec(const SelectArgs& a, int M, int dbg, cudaStream_t st) {
-    // A/B switch: TMA bulk tile copies measured slower on C2 (0.85 vs 0.73 ms)
-    static const bool tma = std::getenv("DSA_COLVEC_TMA") != nullptr;
     const size_t smem = colvec_smem_bytes<KD, NQ>(a.L);
-    auto kern = tma ? colvec_tc_kernel<KD, NQ, true> : colvec_tc_kernel<KD, NQ, false>;
+    auto kern = colvec_tc_kernel<KD, NQ, false>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     const dim3 grid(static_cast<unsigned>(ceil_div_i(a.L, NQ)), static_cast<unsigned>(a.pairs));
     kern<<<grid, colvec_threads<NQ>(), smem, st>>>(a.lq, a.lk, a.L, a.keep, M, a.cols, dbg, FusedAttn{});
@@ -576,7 +559,7 @@ bool colvec_fused_supported(const SelectArgs& s, const AttnArgs& a) {
 void run_colvec_fused(const SelectArgs& s, const AttnArgs& a, cudaStream_t st) {
     const int M = static_cast<int>(s.KD) * s.qmax * s.qmax;
     const size_t smem = colvec_smem_bytes<16, 64>(s.L);
-    auto kern = colvec_tc_kernel<16, 64, false, true>;
+    auto kern = colvec_tc_kernel<16, 64, true>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     const dim3 grid(static_cast<unsigned>(ceil_div_i(s.L, 64)), static_cast<unsigned>(s.pairs));
     FusedAttn fa{static_cast<const __nv_bfloat16*>(a.q), static_cast<const __nv_bfloat16*>(a.k),

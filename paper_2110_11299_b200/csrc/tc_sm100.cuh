@@ -23,6 +23,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// the same wait on a precomputed shared-memory address
+__device__ __forceinline__ void mbar_wait_a(uint32_t bar_smem, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}\n" ::"r"(bar_smem),
+        "r"(parity)
+        : "memory");
+}
 // Same wait with a nanosleep backoff between probes, for warps whose wait is
 // long (keeps spinning warps from stealing issue slots from working warps).
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
@@ -147,6 +157,11 @@ __device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t adesc, uint64
 __device__ __forceinline__ void commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                      smem_addr(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void commit_a(uint32_t bar_smem) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar_smem)
                  : "memory");
 }
 
