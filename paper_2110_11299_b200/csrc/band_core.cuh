@@ -50,6 +50,14 @@ __device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a1
         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
+// 2^x on the SFU (ex2.approx.ftz: -inf -> +0); softmax weights are rounded
+// to bf16 before use, far coarser than its ~2^-22 relative error
+__device__ __forceinline__ float fast_ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
     return *reinterpret_cast<uint32_t*>(&v);
@@ -114,13 +122,19 @@ __device__ __forceinline__ void band_core(BandSmemV2<D>& sm, const __nv_bfloat16
         }
     }
     const int nchunks = static_cast<int>((nkeys + CH - 1) / CH);
+    // V rows of one chunk: lane owns 16-byte column chunk c of rows rl, rl + RPI, ..
+    // (the swizzle and row offsets fold to constants per unrolled step)
     auto load_v = [&](int buf, uint32_t idx, int ch) {
+        constexpr int RPI = 32 / kChunks16;  // rows per step
+        const int c = lane % kChunks16, rl = lane / kChunks16;
+        const uint32_t vb = smem_u32(sm.v[buf]);
+        const bool full = static_cast<int64_t>(ch + 1) * CH <= nkeys;
+        const int left = static_cast<int>(nkeys - static_cast<int64_t>(ch) * CH);
 #pragma unroll
-        for (int t = lane; t < CH * kChunks16; t += 32) {
-            const int r = t / kChunks16, c = t % kChunks16;
+        for (int i = 0; i < CH / RPI; ++i) {
+            const int r = rl + i * RPI;
             const uint32_t j = __shfl_sync(0xffffffffu, idx, r);
-            const bool ok = static_cast<int64_t>(ch) * CH + r < nkeys;
-            cp_async16(smem_u32(sm.v[buf]) + swz<D>(r, c), Vp + static_cast<int64_t>(j) * D + c * 8, ok);
+            cp_async16(vb + swz<D>(r, c), Vp + static_cast<size_t>(j) * D + c * 8, full || r < left);
         }
     };
     // indices run two chunks ahead, so chunk c+1's K/V loads never wait on
@@ -188,7 +202,7 @@ __device__ __forceinline__ void band_core(BandSmemV2<D>& sm, const __nv_bfloat16
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const float mn = fmaxf(m_run[h], cmax[h]);
-            corr[h] = m_run[h] == -INFINITY ? 0.f : exp2f(m_run[h] - mn);
+            corr[h] = m_run[h] == -INFINITY ? 0.f : fast_ex2(m_run[h] - mn);
             m_run[h] = mn;
             l_part[h] *= corr[h];
         }
@@ -205,7 +219,7 @@ __device__ __forceinline__ void band_core(BandSmemV2<D>& sm, const __nv_bfloat16
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 // a column may have no live key yet (m_run = -inf): weight 0
-                const float pv = (SEG && s[mt][u] == -INFINITY) ? 0.f : exp2f(s[mt][u] - m_run[u & 1]);
+                const float pv = (SEG && s[mt][u] == -INFINITY) ? 0.f : fast_ex2(s[mt][u] - m_run[u & 1]);
                 l_part[u & 1] += pv;
                 sm.p[(2 * c4 + (u & 1)) * PW + mt * 16 + g + (u >> 1) * 8] = __float2bfloat16_rn(pv);
             }
