@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(kBandWarps * 32)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const float mn = fmaxf(m_run[h], cmax[h]);
-            corr[h] = m_run[h] == -INFINITY ? 0.f : exp2f(m_run[h] - mn);
+            corr[h] = m_run[h] == -INFINITY ? 0.f : fast_ex2(m_run[h] - mn);
             m_run[h] = mn;
             l_part[h] *= corr[h];
         }
@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(kBandWarps * 32)
         for (int mt = 0; mt < CHUNK / 16; ++mt)
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const float pv = exp2f(s[mt][u] - m_run[u & 1]);
+                const float pv = fast_ex2(s[mt][u] - m_run[u & 1]);
                 l_part[u & 1] += pv;
                 const int key = mt * 16 + g + (u >> 1) * 8;
                 const int qq = 2 * c4 + (u & 1);
@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(128)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const float mn = fmaxf(m_run[h], cmax[h]);
-            corr[h] = m_run[h] == -INFINITY ? 0.f : exp2f(m_run[h] - mn);
+            corr[h] = m_run[h] == -INFINITY ? 0.f : fast_ex2(m_run[h] - mn);
             m_run[h] = mn;
             l_part[h] *= corr[h];
         }
@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(128)
         for (int mt = 0; mt < CHUNK / 16; ++mt)
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const float pv = exp2f(s[mt][u] - m_run[u & 1]);
+                const float pv = fast_ex2(s[mt][u] - m_run[u & 1]);
                 l_part[u & 1] += pv;
                 sp[(2 * c4 + (u & 1)) * PW + mt * 16 + g + (u >> 1) * 8] = __float2bfloat16_rn(pv);
             }
@@ -420,12 +420,19 @@ __global__ void __launch_bounds__(128 / NT)
         const int r = rc / kChunks16, c = rc % kChunks16;
         cp_async16(smem_u32(sm.q[warp][n]) + swz<D>(r, c), Q + (pair * L + r0 + n * 8 + r) * D + c * 8, true);
     }
+    // thread owns 16-byte column chunk c of rows rl, rl + RPS, .. of the block
+    // (kT is a multiple of the chunks per row, so c is fixed per thread)
     auto load_block = [&](int buf, int ch) {
-        const int64_t j0 = static_cast<int64_t>(__ldg(cols + ch)) * 32;
-        for (int t = tid; t < CHUNK * kChunks16; t += kT) {
-            const int r = t / kChunks16, c = t % kChunks16;
-            cp_async16(smem_u32(sm.k[buf]) + swz<D>(r, c), Kp + (j0 + r) * D + c * 8, true);
-            cp_async16(smem_u32(sm.v[buf]) + swz<D>(r, c), Vp + (j0 + r) * D + c * 8, true);
+        static_assert(kT % kChunks16 == 0, "column chunk fixed per thread");
+        constexpr int RPS = kT / kChunks16;  // rows per step
+        const int c = tid % kChunks16, rl = tid / kChunks16;
+        const size_t j0 = static_cast<size_t>(__ldg(cols + ch)) * 32;
+        const uint32_t kbs = smem_u32(sm.k[buf]), vbs = smem_u32(sm.v[buf]);
+#pragma unroll
+        for (int i = 0; i < CHUNK / RPS; ++i) {
+            const int r = rl + i * RPS;
+            cp_async16(kbs + swz<D>(r, c), Kp + (j0 + r) * D + c * 8, true);
+            cp_async16(vbs + swz<D>(r, c), Vp + (j0 + r) * D + c * 8, true);
         }
     };
     const int nchunks = static_cast<int>(keep);
@@ -503,7 +510,7 @@ __global__ void __launch_bounds__(128 / NT)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const float mn = fmaxf(m_run[n][h], cmax[h]);
-                corr[h] = m_run[n][h] == -INFINITY ? 0.f : exp2f(m_run[n][h] - mn);
+                corr[h] = m_run[n][h] == -INFINITY ? 0.f : fast_ex2(m_run[n][h] - mn);
                 m_run[n][h] = mn;
                 l_part[n][h] *= corr[h];
             }
@@ -518,7 +525,7 @@ __global__ void __launch_bounds__(128 / NT)
             for (int mt = 0; mt < CHUNK / 16; ++mt)
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    const float pv = exp2f(s[n][mt][u] - m_run[n][u & 1]);
+                    const float pv = fast_ex2(s[n][mt][u] - m_run[n][u & 1]);
                     l_part[n][u & 1] += pv;
                     sm.p[warp][n][(2 * c4 + (u & 1)) * PW + mt * 16 + g + (u >> 1) * 8] = __float2bfloat16_rn(pv);
                 }
