@@ -78,12 +78,14 @@ __device__ __forceinline__ float xbound(float x, float qp, int round_f32, float 
 
 // Certified level, or NaN when t = x/s may round differently from the
 // reference's (fp32 arithmetic; the margin covers the bound and the fp32
-// rounding of x * (1/s)).
-__device__ __forceinline__ float cert_level(float x, float e, float inv_s, float qmax) {
+// rounding of x * (1/s)).  With e = dq p_j + |x| rel, the scaled margin
+// e inv_s 1.001 + |t| 1e-6 is folded to  |t| K1 + B_j  where
+// K1 = 1e-6 + 1.001 rel and B_j = 1.001 dq inv_s p_j (per row and column).
+__device__ __forceinline__ float cert_level(float x, float bj, float k1, float inv_s, float qmax) {
     const float t = x * inv_s;
     const float at = fabsf(t);
     const float frac = at - floorf(at);
-    const float margin = fmaf(at, 1e-6f, e * inv_s * 1.001f) + 1e-30f;
+    const float margin = fmaf(at, k1, bj) + 1e-30f;
     if (fabsf(frac - 0.5f) <= margin) return __int_as_float(0x7fc00000);
     return fminf(fmaxf(copysignf(floorf(at + 0.5f), t), -qmax), qmax);
 }
@@ -296,11 +298,12 @@ __global__ void __launch_bounds__(R)
         if (row0 == 0 && tid == 0) (which ? sk : sq)[pair] = am == 0.0 ? 0.0 : s;
         // certified levels -> staging; the rest -> shared list, recomputed
         // exactly by the whole CTA, then each thread writes its row
+        const float k1 = 1e-6f + 1.001f * rel, arow = dq * inv_s * 1.001f;
 #pragma unroll
         for (int j = 0; j < KD; ++j) {
             float lv = 0.f;
             if (am != 0.0) {
-                lv = cert_level(xv[j], fmaf(dq, pn[j], fabsf(xv[j]) * rel) + 1e-30f, inv_s, qm);
+                lv = cert_level(xv[j], arow * pn[j], k1, inv_s, qm);
                 if (lv != lv) {
                     lv = 0.f;
                     if (valid) {
@@ -365,6 +368,7 @@ __global__ void __launch_bounds__(256)
     const float4 a1 = __ldg(reinterpret_cast<const float4*>(xhat + rr * KD + c * 8 + 4));
     const float dq = __ldg(xhat + pairs * 2 * L * KD + rr);
     const float xv[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+    const float k1 = 1e-6f + 1.001f * rel, arow = dq * inv_s * 1.001f;
     uint32_t w[4];
 #pragma unroll
     for (int h = 0; h < 4; ++h) {
@@ -374,7 +378,7 @@ __global__ void __launch_bounds__(256)
             const int j = c * 8 + 2 * h + u;
             float lv = 0.f;
             if (am != 0.0) {
-                lv = cert_level(xv[2 * h + u], fmaf(dq, __ldg(pn + j), fabsf(xv[2 * h + u]) * rel) + 1e-30f, inv_s, qm);
+                lv = cert_level(xv[2 * h + u], arow * __ldg(pn + j), k1, inv_s, qm);
                 if (lv != lv) {  // uncertified: the reference chain
                     const __nv_bfloat16* row = (which ? k : q) + (pair * L + r) * D;
                     double acc = 0.0;
