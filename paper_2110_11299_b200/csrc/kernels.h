@@ -81,6 +81,8 @@ bool threshold_tc_supported(const SelectArgs& a);
 bool topk_tc_supported(const SelectArgs& a);
 bool topk_rowwarp_supported(const SelectArgs& a);
 void run_topk_rowwarp(const SelectArgs& a, cudaStream_t st);
+bool topk_rowsel_supported(const SelectArgs& a);
+void run_topk_rowsel(const SelectArgs& a, cudaStream_t st);
 void run_topk_tc(const SelectArgs& a, cudaStream_t st);
 void launch_topk_scaled_list(const SelectArgs& a, const int64_t* list, const unsigned* nlist, cudaStream_t st);
 void run_threshold_tc(const SelectArgs& a, cudaStream_t st);

@@ -688,6 +688,10 @@ void run_select(const SelectArgs& a, cudaStream_t st) {
         run_threshold_tc(a, st);
         return;
     }
+    if (topk_rowsel_supported(a)) {
+        run_topk_rowsel(a, st);
+        return;
+    }
     if (topk_tc_supported(a)) {
         run_topk_tc(a, st);
         return;

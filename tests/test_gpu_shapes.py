@@ -36,6 +36,14 @@ CASES = [
     ("row_topk", 512, 64, 16, 8, "bf16", "row", {"keep": 40}),
     ("row_topk", 640, 128, 32, 4, "bf16", "row", {"keep": 3}),
     ("row_topk", 1024, 64, 16, 4, "bf16", "tensor", {"keep": 64}),
+    # per-row scales on the warp-per-row window select (L = 32 * NPL): every
+    # group count G, k = 32, 2-bit levels (tied keys -> candidate sets /
+    # overflow rows), keep 1 and keep = 32 G exactly
+    ("row_topk", 2048, 64, 16, 2, "bf16", "row", {"keep": 102}),
+    ("row_topk", 1024, 128, 32, 4, "bf16", "row", {"keep": 256}),
+    ("row_topk", 2048, 64, 32, 8, "bf16", "row", {"keep": 1}),
+    ("row_topk", 512, 64, 16, 4, "f32", "row", {"keep": 33}),
+    ("row_topk", 1024, 64, 16, 4, "bf16", "row", {"keep": 64}),
     ("threshold", 700, 64, 16, 4, "bf16", "tensor", {"cap": 5, "causal": True}),
     # theta = 400 / L: most rows keep one key or none (empty-row flags)
     ("threshold", 700, 64, 16, 4, "bf16", "tensor", {"cap": 50, "causal": True, "frac_num": 1, "frac_den": 400}),
