@@ -17,8 +17,9 @@
 //
 //   count kernel:  pass 1  row max m                          (FMNMX3)
 //                  pass 2  per-thread histogram of t = m - s over the first
-//                          kW bins (exact Z from it + direct E lookups for
-//                          the rare t >= kW with E[t] > 0)
+//                          kW bins (Z from it; keys beyond the bins with
+//                          E[t] > 0 only bound Z, and a rare extra pass sums
+//                          them exactly when the bound leaves t* ambiguous)
 //                  -> t* (largest kept t, binary search on E), kept count,
 //                     cap cut and tie quota from the histogram prefix sums;
 //                     rows whose cut lies beyond kW bins run extra counting
@@ -33,7 +34,6 @@
 #include <cuda_bf16.h>
 
 #include <cstdlib>
-#include <type_traits>
 
 #include "device_common.cuh"
 #include "kernels.h"
@@ -166,28 +166,25 @@ __global__ void __launch_bounds__(kTQ, 3) threshold_tc_kernel(ThrParams a) {
                     if (k0 + x < klim) m = fmaxf(m, f[x]);
             }
         });
-        // ---- pass 2: histogram of t = m - s (bins [0, kW)); the tail
-        // t in [kW, tz) (E[t] > 0 beyond the bins; uniform per pair, rare)
-        // adds E[t] to Z directly
+        // ---- pass 2: histogram of t = m - s over bins [0, wh), wh = min(tz, kW);
+        // every other key (t >= wh, and masked keys) lands in the trash bin wh
         const int tz = *tz_s;
         const int wh = tz < kW ? tz : kW;
         const float mb = m + kMagic;
-        uint64_t zx = 0;
         uint32_t* hcol = hist + tid;
-        auto hist_pass = [&](auto tail_tag) {
-            constexpr bool kTail = decltype(tail_tag)::value;
+        {
+            // bin bits = kMagicBits + t (float magic), clamped to the trash
+            // bin; one IMAD gives the thread's bin address bits * 4 kTQ + base
+            const uint32_t lim = static_cast<uint32_t>(kMagicBits + wh);
+            const uint32_t abase = tc::smem_addr(hcol) - static_cast<uint32_t>(kMagicBits) * (kTQ * 4u);
             score_pass<KD>(c, g, [&](int u, const uint32_t* r, int col0) {
                 const float* f = reinterpret_cast<const float*>(r);
                 const int64_t k0 = static_cast<int64_t>(u) * kTN + col0;
-                // branch-free: out-of-window t lands in the trash bin kW
                 auto one = [&](float v) {
-                    const int t = __float_as_int(fmaf(v, -1.0f, mb)) - kMagicBits;
-                    const bool in = static_cast<unsigned>(t) < static_cast<unsigned>(wh);
-                    if (kTail && !in && static_cast<unsigned>(t) < static_cast<unsigned>(tz))
-                        zx += static_cast<uint64_t>(__ldg(E + t));
+                    const uint32_t bits = min(__float_as_uint(fmaf(v, -1.0f, mb)), lim);
                     // shared-memory reduction without return value: no
                     // load -> add -> store chain between consecutive keys
-                    atomicAdd(hcol + (in ? t : kW) * kTQ, 1u);
+                    asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(bits * (kTQ * 4u) + abase) : "memory");
                 };
                 if (k0 + 32 <= kfree) {
 #pragma unroll
@@ -197,12 +194,10 @@ __global__ void __launch_bounds__(kTQ, 3) threshold_tc_kernel(ThrParams a) {
                     for (int x = 0; x < 32; ++x) one(k0 + x < klim ? f[x] : -INFINITY);
                 }
             });
-        };
-        if (tz > kW) hist_pass(std::true_type{});
-        else hist_pass(std::false_type{});
+        }
         // ---- per-row rule from the histogram
         auto bin = [&](int t) -> uint32_t { return hcol[t * kTQ]; };
-        uint64_t Z = zx;
+        uint64_t Z = 0;
         uint32_t htot = 0;
         for (int t = 0; t < wh; ++t) {
             const uint32_t h = bin(t);
@@ -210,16 +205,44 @@ __global__ void __launch_bounds__(kTQ, 3) threshold_tc_kernel(ThrParams a) {
             htot += h;
         }
         // t* = largest t with E[t] kept (E non-increasing); -1: nothing kept
-        int tstar = -1;
-        if (rvalid && keep_rule(es[0], Z, a.ln, a.den)) {
+        auto tstar_of = [&](uint64_t Zv) -> int {
+            if (!rvalid || !keep_rule(es[0], Zv, a.ln, a.den)) return -1;
             int lo = 0, hi = tz - 1;  // keep_rule(E[lo]) holds; E[tz] == 0 never kept
             while (lo < hi) {
                 const int mid = (lo + hi + 1) >> 1;
                 const uint64_t e = mid < kW ? es[mid] : static_cast<uint64_t>(__ldg(E + mid));
-                if (keep_rule(e, Z, a.ln, a.den)) lo = mid;
+                if (keep_rule(e, Zv, a.ln, a.den)) lo = mid;
                 else hi = mid - 1;
             }
-            tstar = lo;
+            return lo;
+        };
+        // keys beyond the bins with E[t] > 0 (t in [kW, tz), tz > kW) add at
+        // most E[kW] each: Z lies in [Z, Z + trash * E[kW]].  When both ends
+        // give the same t*, it is exact; otherwise (rare) one more pass sums
+        // those E[t] exactly.
+        int tstar = tstar_of(Z);
+        bool amb = false;
+        if (tz > wh && rvalid) {
+            const uint64_t zhi = Z + static_cast<uint64_t>(bin(wh)) * static_cast<uint64_t>(__ldg(E + wh));
+            amb = tstar_of(zhi) != tstar;
+        }
+        if (__syncthreads_or(amb)) {
+            uint64_t zt = 0;
+            const uint32_t span = static_cast<uint32_t>(tz - wh);
+            score_pass<KD>(c, g, [&](int u, const uint32_t* r, int col0) {
+                if (!amb) return;
+                const float* f = reinterpret_cast<const float*>(r);
+                const int64_t k0 = static_cast<int64_t>(u) * kTN + col0;
+                for (int y = 0; y < 32; ++y) {
+                    const int t = __float_as_int(fmaf(f[y], -1.0f, mb)) - kMagicBits;
+                    if (k0 + y < klim && static_cast<uint32_t>(t - wh) < span)
+                        zt += static_cast<uint64_t>(__ldg(E + t));
+                }
+            });
+            if (amb) {
+                Z += zt;
+                tstar = tstar_of(Z);
+            }
         }
         const uint32_t cap = static_cast<uint32_t>(a.cap);
         uint32_t take = 0, quota = kAll;
