@@ -81,15 +81,17 @@ struct BandSmemV2 {
 template <int D>
 __device__ __forceinline__ void load_k_frag(const __nv_bfloat16* __restrict__ Kp, uint32_t idx,
                                             int g, int c4, uint4 (&kw)[2][2][D / 64 * 2]) {
-    // two m-tiles x rows (g, g+8): this lane's D/4-wide segment [c4*D/4, ...)
+    // two m-tiles x rows (g, g+8): this lane's D/4 elements are the 16-byte
+    // pieces [32 v + 8 c4, +8): one load instruction covers 64 contiguous
+    // bytes of each row (full 32-byte sectors)
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const uint32_t j = __shfl_sync(0xffffffffu, idx, mt * 16 + g + h * 8);
-            const uint4* src = reinterpret_cast<const uint4*>(Kp + static_cast<int64_t>(j) * D + c4 * (D / 4));
+            const uint4* src = reinterpret_cast<const uint4*>(Kp + static_cast<int64_t>(j) * D + c4 * 8);
 #pragma unroll
-            for (int v = 0; v < D / 32; ++v) kw[mt][h][v] = __ldg(src + v);
+            for (int v = 0; v < D / 32; ++v) kw[mt][h][v] = __ldg(src + v * 4);
         }
 }
 
@@ -107,14 +109,14 @@ __device__ __forceinline__ void band_core(BandSmemV2<D>& sm, const __nv_bfloat16
     const int g = lane >> 2, c4 = lane & 3;
     constexpr int kChunks16 = D / 8;
 
-    // Q^T B-fragments (same d permutation as K): row g, segment [c4*D/4, +D/4)
+    // Q^T B-fragments (same d permutation as K): row g, pieces [32 v + 8 c4, +8)
     uint32_t qw[D / 8];
     {
         const bool ok = g < kRows && r0 + g < L;
-        const uint4* src = reinterpret_cast<const uint4*>(Q + (pair * L + (ok ? r0 + g : 0)) * D + c4 * (D / 4));
+        const uint4* src = reinterpret_cast<const uint4*>(Q + (pair * L + (ok ? r0 + g : 0)) * D + c4 * 8);
 #pragma unroll
         for (int v = 0; v < NW; ++v) {
-            const uint4 x = ok ? __ldg(src + v) : make_uint4(0, 0, 0, 0);
+            const uint4 x = ok ? __ldg(src + v * 4) : make_uint4(0, 0, 0, 0);
             qw[4 * v + 0] = x.x;
             qw[4 * v + 1] = x.y;
             qw[4 * v + 2] = x.z;
