@@ -24,6 +24,9 @@
  *   dsa_pipeline         <- the per-head composition above (predict -> select -> attend)
  *   dsa_counters         <- OpCounters P/include/dsattn/sparse.hpp:14-21
  *   dsa_last_error       <- exception what() strings
+ *   dsa_project_qkv      <- project_qkv (per-head X W_Q / X W_K / X W_V)
+ *                           P/src/attention.cpp:36-46 and the predictor input
+ *                           R = X P, P/src/trainer.cpp:162
  */
 #ifndef DSA_B200_H
 #define DSA_B200_H
@@ -143,6 +146,22 @@ dsa_status dsa_sparse_attention(const dsa_config* cfg, const void* q, const void
 dsa_status dsa_pipeline(const dsa_config* cfg, const void* q, const void* k, const void* v,
                         const float* p, void* z, const dsa_mask* mask_out, void* workspace,
                         size_t workspace_bytes, void* stream);
+
+/* (0) the step before the path: every head's Q, K, V and the predictor
+ * input R = X P of one attention layer in ONE bf16 tensor-core GEMM over X
+ * (fp32 accumulation, outputs rounded once).
+ *   x: [batch][L][d_model] bf16, d_model % 64 == 0
+ *   w: packed weights [heads*(2*dk + dv) + npred][d_model] bf16 (K-major):
+ *      row h*dk + c        = column c of W_Q[h]   (h < heads, c < dk)
+ *      row heads*dk + ...  = W_K rows, then heads*dv W_V rows, then the
+ *      npred rows of P^T (npred <= 32, 0 = no predictor input)
+ *   q, k: [batch*heads][L][dk] bf16; v: [batch*heads][L][dv] bf16 -- the
+ *      (b,h)-pair layout dsa_predict / dsa_pipeline consume
+ *   r: [batch][L][npred] f32 (NULL when npred == 0)
+ * dk, dv in {32, 64, 96, 128, ...} (multiples of 32). */
+dsa_status dsa_project_qkv(int64_t batch, int64_t L, int64_t d_model, int64_t heads, int64_t dk,
+                           int64_t dv, int64_t npred, const void* x, const void* w, void* q,
+                           void* k, void* v, float* r, void* stream);
 
 /* Kernels launched by this library since load (process-wide, monotonic);
  * bench.py reads it around timed regions. */

@@ -51,6 +51,8 @@ _SIGS = {
     "dsa_pipeline": (C.c_int, [C.POINTER(DsaConfig), _P, _P, _P, _P, _P, C.POINTER(DsaMask), _P,
                                C.c_size_t, _P]),
     "dsa_launch_counter": (C.c_uint64, []),
+    "dsa_project_qkv": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
+                                  C.c_int64, _P, _P, _P, _P, _P, _P, _P]),
     "dsa_counters": (C.c_int, [C.POINTER(DsaConfig), C.POINTER(DsaMask), C.POINTER(DsaCounts), _P]),
     "dsa_generate": (C.c_int, [C.POINTER(DsaConfig), C.c_uint64, C.c_int32, C.c_int32, C.c_int64,
                                C.c_int64, _P, _P, _P, _P, C.c_int32]),

@@ -464,6 +464,27 @@ dsa_status dsa_select(const dsa_config* cfg, const uint16_t* levels_q, const uin
     });
 }
 
+dsa_status dsa_project_qkv(int64_t batch, int64_t L, int64_t d_model, int64_t heads, int64_t dk,
+                           int64_t dv, int64_t npred, const void* x, const void* w, void* q,
+                           void* k, void* v, float* r, void* stream) {
+    return guard([&] {
+        if (batch < 1 || L < 1 || heads < 1 || d_model < 1 || dk < 1 || dv < 1)
+            throw Error(DSA_ERR_SHAPE, "dsa_project_qkv: sizes must be >= 1");
+        if (d_model % 64 != 0) throw Error(DSA_ERR_UNSUPPORTED, "dsa_project_qkv: d_model must be a multiple of 64");
+        if (dk % 32 != 0 || dv % 32 != 0)
+            throw Error(DSA_ERR_UNSUPPORTED, "dsa_project_qkv: d_k and d_v must be multiples of 32");
+        if (npred < 0 || npred > 32) throw Error(DSA_ERR_PARAM, "dsa_project_qkv: npred must be in [0, 32]");
+        if (!x || !w || !q || !k || !v || (npred > 0 && !r))
+            throw Error(DSA_ERR_PARAM, "dsa_project_qkv: null pointer");
+        if (batch * L >= (int64_t{1} << 31) || heads * (2 * dk + dv) + npred >= (int64_t{1} << 31))
+            throw Error(DSA_ERR_SHAPE, "dsa_project_qkv: operand too large for 32-bit TMA coordinates");
+        require_device();
+        QkvGemmArgs g{batch, L, d_model, heads, dk, dv, npred, x, w, q, k, v, r};
+        run_qkv_gemm(g, static_cast<cudaStream_t>(stream));
+        check_cuda(cudaGetLastError(), "dsa_project_qkv launch");
+    });
+}
+
 dsa_status dsa_sparse_attention(const dsa_config* cfg, const void* q, const void* k,
                                 const void* v, const dsa_mask* mask, void* z, void* stream) {
     return guard([&] {

@@ -89,6 +89,18 @@ void run_threshold_tc(const SelectArgs& a, cudaStream_t st);
 void launch_exp_table(const SelectArgs& a, cudaStream_t st);
 void scan_counts(const SelectArgs& a, cudaStream_t st);
 
+// fused per-head Q/K/V (+ predictor input) projection GEMM
+struct QkvGemmArgs {
+    int64_t batch, L, d_model, heads, dk, dv, npred;
+    const void* x;   // [batch][L][d_model] bf16
+    const void* w;   // [heads*(2 dk + dv) + npred][d_model] bf16
+    void* q;         // [batch*heads][L][dk] bf16
+    void* k;
+    void* v;         // [batch*heads][L][dv] bf16
+    float* r;        // [batch][L][npred] f32 (may be null when npred == 0)
+};
+void run_qkv_gemm(const QkvGemmArgs& g, cudaStream_t st);
+
 struct AttnArgs {
     int mode;
     int64_t pairs, L, D;

@@ -245,6 +245,43 @@ class Phases:
                                                    C.byref(self._cm), _ptr(z), _stream(stream)))
 
 
+# ------------------------------------------------- step before the path
+def pack_qkv_weights(wq, wk, wv, p_model=None) -> torch.Tensor:
+    """Reference per-head weights (lists of [d_model, d] matrices, as in
+    AttentionParams wq/wk/wv, P/include/dsattn/attention.hpp) and the
+    optional predictor projection P [d_model, npred] -> the K-major packed
+    operand [H*(2dk+dv) + npred, d_model] bf16 of dsa_project_qkv."""
+    rows = [w.t() for w in wq] + [w.t() for w in wk] + [w.t() for w in wv]
+    if p_model is not None:
+        rows.append(p_model.t())
+    return torch.cat([r.to(torch.bfloat16) for r in rows], 0).contiguous()
+
+
+def project_qkv(x: torch.Tensor, w: torch.Tensor, heads: int, dk: int, dv: int, npred: int = 0,
+                stream=None, out=None):
+    """project_qkv (P/src/attention.cpp:36-46) for every head plus the
+    predictor input R = X P (P/src/trainer.cpp:162) in one tensor-core GEMM.
+    x: [batch, L, d_model] bf16 CUDA; w: pack_qkv_weights(...).  Returns
+    (q, k, v, r): q/k [batch*heads, L, dk], v [batch*heads, L, dv] bf16 (the
+    (b,h)-pair layout the hot path consumes), r [batch, L, npred] f32 or None."""
+    if x.dim() != 3 or x.dtype != torch.bfloat16 or not x.is_cuda or not x.is_contiguous():
+        raise ParamError("project_qkv: x must be a contiguous [batch, L, d_model] bf16 CUDA tensor")
+    batch, L, dm = x.shape
+    n_out = heads * (2 * dk + dv) + npred
+    if w.shape != (n_out, dm) or w.dtype != torch.bfloat16 or not w.is_contiguous():
+        raise ShapeError(f"project_qkv: packed weights must be [{n_out}, {dm}] bf16")
+    if out is None:
+        q = torch.empty((batch * heads, L, dk), dtype=torch.bfloat16, device=x.device)
+        k = torch.empty_like(q)
+        v = torch.empty((batch * heads, L, dv), dtype=torch.bfloat16, device=x.device)
+        r = torch.empty((batch, L, npred), dtype=torch.float32, device=x.device) if npred else None
+    else:
+        q, k, v, r = out
+    _abi.check(_abi.lib().dsa_project_qkv(batch, L, dm, heads, dk, dv, npred, _ptr(x), _ptr(w), _ptr(q),
+                                          _ptr(k), _ptr(v), _ptr(r), _stream(stream)))
+    return q, k, v, r
+
+
 def launch_counter() -> int:
     return int(_abi.lib().dsa_launch_counter())
 

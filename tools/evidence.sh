@@ -16,7 +16,7 @@ for c in c2_vector c3_block c4_threshold c1_bert_base c0_smoke; do
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $out/${tag}_launches_$c.csv \
     python bench.py --config $c --steps 2 --warmup 3 --no-cpu-baseline > $out/${tag}_ncu_launch_$c.log 2>&1
 done
-declare -A dom=([c2_vector]=colvec [c3_block]=attn_block [c4_threshold]=threshold_tc [c1_bert_base]=topk_rows_scaled [c0_smoke]=project)
+declare -A dom=([c2_vector]=colvec [c3_block]=attn_block [c4_threshold]=threshold_tc [c1_bert_base]=topk_rowsel [c0_smoke]=project)
 for c in c2_vector c3_block c4_threshold c1_bert_base c0_smoke; do
   timeout 900 ncu --set full --import-source on --clock-control none -k regex:${dom[$c]} -c 1 -o $out/${tag}_full_$c \
     python tools/run_once.py --config $c --reps 1 > $out/${tag}_ncu_full_$c.log 2>&1
