@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "dsa_b200.h"
+#include "dsattn/attention.hpp"
 #include "dsattn/errors.hpp"
 #include "dsattn/mask.hpp"
 #include "dsattn/matrix.hpp"
@@ -370,6 +371,59 @@ inline Matrix sparse_attention(const Matrix& q, const Matrix& k, const Matrix& v
         check_cuda(cudaMemcpy(empty_rows->data(), de.get(), mask.l, cudaMemcpyDeviceToHost));
     }
     return z;
+}
+
+// project_qkv (P/src/attention.cpp:36-46) on the tensor cores: every head's
+// Q, K, V in one bf16 GEMM over X (dsa_project_qkv).  X and the weights are
+// rounded to bf16 (exact when they already are), products accumulate in
+// fp32 and the outputs are rounded to bf16 -- the BASELINE bf16 tolerance,
+// not the reference's f64.  Same signature, value semantics and exceptions.
+inline Qkv project_qkv(const Matrix& x, const AttentionParams& p) {
+    p.validate();
+    if (x.cols() != p.d()) throw ShapeError("project_qkv: X feature dim != d");
+    const int64_t L = static_cast<int64_t>(x.rows()), dm = static_cast<int64_t>(p.d());
+    const int64_t H = static_cast<int64_t>(p.heads), dk = static_cast<int64_t>(p.d_k()),
+                  dv = static_cast<int64_t>(p.d_v());
+    const int64_t n_out = H * (2 * dk + dv);
+    std::vector<uint16_t> hx(x.size()), hw(static_cast<size_t>(n_out * dm));
+    for (size_t i = 0; i < x.size(); ++i) hx[i] = detail::bf16_bits(x.data()[i]);
+    int64_t row = 0;
+    auto pack = [&](const std::vector<Matrix>& ws) {
+        for (const Matrix& w : ws)
+            for (size_t c = 0; c < w.cols(); ++c, ++row)
+                for (size_t r = 0; r < w.rows(); ++r) hw[static_cast<size_t>(row * dm) + r] = detail::bf16_bits(w(r, c));
+    };
+    pack(p.wq);
+    pack(p.wk);
+    pack(p.wv);
+    DeviceBuffer dx(hx.size() * 2), dw(hw.size() * 2), dq(static_cast<size_t>(H * L * dk) * 2),
+        dkb(static_cast<size_t>(H * L * dk) * 2), dvb(static_cast<size_t>(H * L * dv) * 2);
+    check_cuda(cudaMemcpy(dx.get(), hx.data(), dx.size(), cudaMemcpyHostToDevice));
+    check_cuda(cudaMemcpy(dw.get(), hw.data(), dw.size(), cudaMemcpyHostToDevice));
+    check(dsa_project_qkv(1, L, dm, H, dk, dv, 0, dx.get(), dw.get(), dq.get(), dkb.get(), dvb.get(), nullptr,
+                          nullptr));
+    auto fetch = [&](const DeviceBuffer& d, int64_t cols) {
+        std::vector<uint16_t> h(static_cast<size_t>(H * L * cols));
+        check_cuda(cudaMemcpy(h.data(), d.get(), h.size() * 2, cudaMemcpyDeviceToHost));
+        std::vector<Matrix> out;
+        for (int64_t hd = 0; hd < H; ++hd) {
+            Matrix m(static_cast<size_t>(L), static_cast<size_t>(cols), x.precision());
+            for (int64_t i = 0; i < L * cols; ++i) {
+                uint32_t u = static_cast<uint32_t>(h[static_cast<size_t>(hd * L * cols + i)]) << 16;
+                float f;
+                std::memcpy(&f, &u, 4);
+                m.raw()[static_cast<size_t>(i)] = f;
+            }
+            m.round_to_precision();
+            out.push_back(std::move(m));
+        }
+        return out;
+    };
+    Qkv out;
+    out.q = fetch(dq, dk);
+    out.k = fetch(dkb, dk);
+    out.v = fetch(dvb, dv);
+    return out;
 }
 
 }  // namespace dsattn::gpu

@@ -45,7 +45,8 @@ constexpr int kStages = 4;
 constexpr int kABytes = kBM * kBK * 2;   // 16 KB
 constexpr int kBBytes = kBN * kBK * 2;   // 32 KB
 constexpr int kThreads = 192;            // 6 warps
-constexpr int kSmem = kStages * (kABytes + kBBytes) + 1024 + 256;
+constexpr int kStg = 32 * 128;           // one warp's 32 rows x 64 bf16 staging tile (TMA store)
+constexpr int kSmem = kStages * (kABytes + kBBytes) + 4 * 2 * kStg + 1024 + 256;
 
 struct QkvArgs {
     int64_t M, L, H, dk, dv, npred, n_out, kdim;
@@ -53,6 +54,7 @@ struct QkvArgs {
     __nv_bfloat16* k;
     __nv_bfloat16* v;
     float* r;
+    int tma_store;  // Q/K/V tiles leave through TMA (d_k, d_v % 64 == 0, L % 32 == 0)
 };
 
 // K-major operand tile written by TMA with 128-byte swizzle: rows of 128 B,
@@ -83,18 +85,28 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
 __device__ __forceinline__ void expect_tx(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int x, int y, uint32_t src) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(x), "r"(y), "r"(src)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+}
 __device__ __forceinline__ void arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
-    qkv_gemm_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w, QkvArgs a) {
+    qkv_gemm_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w,
+                    const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
+                    const __grid_constant__ CUtensorMap map_v, QkvArgs a) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-byte alignment for the swizzled tiles
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t{1023});
     unsigned char* sa = smem;                                  // [kStages][kABytes]
     unsigned char* sb = smem + kStages * kABytes;              // [kStages][kBBytes]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sb + kStages * kBBytes);
+    unsigned char* stg = sb + kStages * kBBytes;               // [4 warps][2][kStg], 1024-aligned
+    uint64_t* bars = reinterpret_cast<uint64_t*>(stg + 4 * 2 * kStg);
     uint64_t* full = bars;               // [kStages] TMA -> MMA
     uint64_t* empty = bars + kStages;    // [kStages] MMA -> TMA
     uint64_t* tfull = bars + 2 * kStages;      // [2] MMA -> epilogue
@@ -188,7 +200,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ------------------------------------------------ epilogue (warps 2-5)
         const int quarter = warp & 3;  // TMEM lane quarter this warp may access
         const int64_t HK = a.H * a.dk, HV = a.H * a.dv;
-        int acc = 0;
+        int acc = 0, sbuf = 0;
         uint32_t aphase = 0;
         for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
             const int64_t m0 = (t / ntl) * kBM;
@@ -200,7 +212,55 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool mvalid = m < a.M;
             const int64_t b = mvalid ? m / a.L : 0, l = mvalid ? m - b * a.L : 0;
             const uint32_t tbase = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * kBN);
-            for (int c0 = 0; c0 < ncols; c0 += 32) {
+            int c0 = 0;
+            // TMA-store path: this warp's 32 rows lie in one batch row block,
+            // so each 64-column head chunk is a [32][64] box of the head's slab
+            const int64_t mw = m0 + quarter * 32;
+            if (a.tma_store && mw + 32 <= a.M && (mw % a.L) + 32 <= a.L) {
+                const int64_t bw = mw / a.L, lw = mw - bw * a.L;
+                for (; c0 < ncols && n0 + c0 < 2 * HK + HV; c0 += 64) {
+                    uint32_t r0[32], r1[32];
+                    tc::ld_32x32b_x32(tbase + c0, r0);
+                    tc::ld_32x32b_x32(tbase + c0 + 32, r1);
+                    tc::wait_ld();
+                    const int64_t n = n0 + c0;
+                    const CUtensorMap* map;
+                    int64_t y;
+                    int x;
+                    if (n < HK) {
+                        map = &map_q;
+                        y = (bw * a.H + n / a.dk) * a.L + lw;
+                        x = static_cast<int>(n % a.dk);
+                    } else if (n < 2 * HK) {
+                        map = &map_k;
+                        y = (bw * a.H + (n - HK) / a.dk) * a.L + lw;
+                        x = static_cast<int>((n - HK) % a.dk);
+                    } else {
+                        map = &map_v;
+                        y = (bw * a.H + (n - 2 * HK) / a.dv) * a.L + lw;
+                        x = static_cast<int>((n - 2 * HK) % a.dv);
+                    }
+                    // the staging buffer's previous TMA store has read its bytes
+                    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+                    __syncwarp();
+                    unsigned char* st = stg + ((warp - 2) * 2 + sbuf) * kStg;
+                    const uint32_t sro = tc::smem_addr(st) + lane * 128;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {  // 128-byte swizzle: chunk j of row r at j ^ (r & 7)
+                        const uint32_t* rr = j < 4 ? &r0[8 * j] : &r1[8 * (j - 4)];
+                        const uint32_t w0 = bc_pack(rr[0], rr[1]), w1 = bc_pack(rr[2], rr[3]);
+                        const uint32_t w2 = bc_pack(rr[4], rr[5]), w3 = bc_pack(rr[6], rr[7]);
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(sro + ((j ^ (lane & 7)) << 4)),
+                                     "r"(w0), "r"(w1), "r"(w2), "r"(w3)
+                                     : "memory");
+                    }
+                    tc::fence_proxy_async();
+                    __syncwarp();
+                    if (lane == 0) tma_store_2d(map, x, static_cast<int>(y), tc::smem_addr(st));
+                    sbuf ^= 1;
+                }
+            }
+            for (; c0 < ncols; c0 += 32) {
                 uint32_t r[32];
                 tc::ld_32x32b_x32(tbase + c0, r);
                 tc::wait_ld();
@@ -242,6 +302,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     }
+    if (warp >= 2 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
     __syncthreads();
     if (warp == 2) tc::tmem_dealloc<512>(tmem);
 }
@@ -264,11 +325,11 @@ EncodeFn encode_fn() {
 }
 
 // 2-D bf16 row-major [rows][cols] -> box [box_rows][64] with 128-byte swizzle
-CUtensorMap make_map(const void* ptr, int64_t rows, int64_t cols, int box_rows) {
+CUtensorMap make_map(const void* ptr, int64_t rows, int64_t cols, int box_rows, int box_cols = kBK) {
     CUtensorMap m;
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
     const cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols * 2)};
-    const cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(box_rows)};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
     const cuuint32_t es[2] = {1, 1};
     EncodeFn fn = encode_fn();
     if (!fn) throw_unsupported("cuTensorMapEncodeTiled unavailable");
@@ -297,6 +358,11 @@ void run_qkv_gemm(const QkvGemmArgs& g, cudaStream_t st) {
     a.r = g.r;
     const CUtensorMap mx = make_map(g.x, a.M, a.kdim, kBM);
     const CUtensorMap mw = make_map(g.w, a.n_out, a.kdim, kBN);
+    a.tma_store = (g.dk % 64 == 0 && g.dv % 64 == 0 && g.L % 32 == 0) ? 1 : 0;
+    // store maps: each head slab as rows of d columns, [32 rows][64 cols] boxes
+    const CUtensorMap mq = a.tma_store ? make_map(g.q, g.batch * g.heads * g.L, g.dk, 32, 64) : mx;
+    const CUtensorMap mk = a.tma_store ? make_map(g.k, g.batch * g.heads * g.L, g.dk, 32, 64) : mx;
+    const CUtensorMap mv = a.tma_store ? make_map(g.v, g.batch * g.heads * g.L, g.dv, 32, 64) : mx;
     static int sms = 0;
     if (sms == 0) {
         int dev = 0;
@@ -306,7 +372,7 @@ void run_qkv_gemm(const QkvGemmArgs& g, cudaStream_t st) {
     const int64_t ntiles = ceil_div_i(a.M, kBM) * ceil_div_i(a.n_out, kBN);
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>(ntiles, sms));
     cudaFuncSetAttribute(qkv_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-    qkv_gemm_kernel<<<grid, kThreads, kSmem, st>>>(mx, mw, a);
+    qkv_gemm_kernel<<<grid, kThreads, kSmem, st>>>(mx, mw, mq, mk, mv, a);
     note_launch();
 }
 

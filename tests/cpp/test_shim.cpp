@@ -5,9 +5,11 @@
 // run on a GPU by tests/test_gpu_cpp_shim.py.  Cases mirror the reference's
 // own tests (P/tests/test_linalg.cpp:97-101, test_maskgen.cpp, test_sparse.cpp).
 #include <cmath>
+#include <cstring>
 #include <cstdio>
 #include <vector>
 
+#include "dsattn/attention.hpp"
 #include "dsattn/linalg.hpp"
 #include "dsattn/maskgen.hpp"
 #include "dsattn/predictor.hpp"
@@ -123,6 +125,35 @@ int main() {
         bool zero = true;
         for (size_t j = 0; j < d; ++j) zero &= ze(3, j) == 0.0;
         CHECK(zero && flags[3] == 1 && flags[2] == 0);
+    }
+
+    // project_qkv vs the reference (P/src/attention.cpp:36-46) on bf16-exact
+    // operands: within the bf16 bar per head
+    {
+        Rng prng(99);
+        const size_t dm = 128, Lx = 200, H = 3;
+        AttentionParams ap = random_attention_params(dm, 64, 64, H, prng);
+        auto to_bf16 = [](Matrix& m) {
+            for (size_t i = 0; i < m.size(); ++i) {
+                float f = static_cast<float>(m.data()[i]);
+                uint32_t u;
+                std::memcpy(&u, &f, 4);
+                u &= 0xffff0000u;
+                std::memcpy(&f, &u, 4);
+                m.raw()[i] = f;
+            }
+        };
+        for (auto* ws : {&ap.wq, &ap.wk, &ap.wv})
+            for (Matrix& w : *ws) to_bf16(w);
+        Matrix x = random_normal(Lx, dm, 0.0, 1.0, prng);
+        to_bf16(x);
+        Qkv g = gpu::project_qkv(x, ap), ref = project_qkv(x, ap);
+        for (size_t h = 0; h < H; ++h) {
+            CHECK(max_abs_diff(g.q[h], ref.q[h]) <= 1e-2 * max_abs(ref.q[h]));
+            CHECK(max_abs_diff(g.k[h], ref.k[h]) <= 1e-2 * max_abs(ref.k[h]));
+            CHECK(max_abs_diff(g.v[h], ref.v[h]) <= 1e-2 * max_abs(ref.v[h]));
+        }
+        CHECK(throws<ShapeError>([&] { gpu::project_qkv(Matrix(Lx, dm + 1), ap); }));
     }
 
     // reference exception types (P/include/dsattn/errors.hpp)
