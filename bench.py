@@ -385,6 +385,7 @@ def run_gpu_arm(args, p, rank, local, world):
     phases["attention"]["gather_reuse"] = reuse
     tokens = p.tokens * world
     value = tokens / (ms * 1e-3)
+    adjacent = None if args.no_adjacent else {"project_qkv": time_project_qkv(p, peaks["bf16_tflops"])}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         # bounded sample: repeat pair batches until >= 10 s of CPU wall time (<= ~30 s)
@@ -423,7 +424,44 @@ def run_gpu_arm(args, p, rank, local, world):
                      "softmax_exps": cnt["softmax_exps"]},
         "checksum": [float(csum[0].item()), float(csum[1].item())],
     }
+    if adjacent:
+        line["adjacent"] = adjacent
     print(json.dumps(line), flush=True)
+
+
+def time_project_qkv(p, peak_tflops, reps=10):
+    """The step before the path, outside the timed region and
+    not part of `value`: dsa_project_qkv on this config's layer shape
+    (d_model, heads, d_k, d_v from the preset `shape`, npred = k), CUDA
+    events on the launching stream."""
+    import torch
+    from paper_2110_11299_b200 import ops
+    sh = p.shape
+    dm, heads, dk, dv = sh["d"], p.heads, sh["d_k"], sh["d_v"]
+    batch = max(1, min(p.batch, 131072 // p.L))
+    M, N = batch * p.L, heads * (2 * dk + dv) + p.k
+    x = torch.randn(batch, p.L, dm, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(N, dm, device="cuda") / dm ** 0.5).to(torch.bfloat16)
+    out = (torch.empty(batch * heads, p.L, dk, dtype=torch.bfloat16, device="cuda"),
+           torch.empty(batch * heads, p.L, dk, dtype=torch.bfloat16, device="cuda"),
+           torch.empty(batch * heads, p.L, dv, dtype=torch.bfloat16, device="cuda"),
+           torch.empty(batch, p.L, p.k, dtype=torch.float32, device="cuda"))
+    st = torch.cuda.current_stream()
+    for _ in range(3):
+        ops.project_qkv(x, w, heads, dk, dv, p.k, stream=st, out=out)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(reps):
+        ops.project_qkv(x, w, heads, dk, dv, p.k, stream=st, out=out)
+    e1.record(st)
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    tf = 2.0 * M * N * dm / (ms * 1e-3) / 1e12
+    return {"kernel": "qkv_gemm_kernel (tcgen05, TMA)", "M": M, "N": N, "K": dm, "ms": ms, "bound": "tensor",
+            "achieved": tf, "unit": "TFLOP/s", "peak": peak_tflops, "frac": tf / peak_tflops,
+            "note": "X W^T for every head's Q/K/V + predictor input R = X P (project_qkv, "
+                    "P/src/attention.cpp:36-46); random weights; not part of value"}
 
 
 def main():
@@ -435,6 +473,7 @@ def main():
     ap.add_argument("--config", default="c2_vector")
     ap.add_argument("--ref-pairs", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-adjacent", action="store_true", help="skip the project_qkv GEMM measurement")
     ap.add_argument("--no-graph", action="store_true", help="eager launches in the timed region")
     args = ap.parse_args()
     from paper_2110_11299_b200 import load_preset
