@@ -20,6 +20,7 @@
 
 #include <cmath>
 #include <cstring>
+#include <span>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -423,6 +424,77 @@ inline Qkv project_qkv(const Matrix& x, const AttentionParams& p) {
     out.q = fetch(dq, dk);
     out.k = fetch(dkb, dk);
     out.v = fetch(dvb, dv);
+    return out;
+}
+
+// sparse_attention(x, params, per-head masks) (P/src/sparse.cpp:93-120): the
+// layer-level composition -- project_qkv for every head in one tensor-core
+// GEMM (device-resident Q/K/V, bf16), then SDDMM -> sparse softmax -> SpMM
+// for all heads in one batched call over the heads' masks, heads
+// concatenated by columns.  Needs d_v == d_k.
+inline Matrix sparse_attention(const Matrix& x, const AttentionParams& p, std::span<const SparseMask> per_head) {
+    if (per_head.size() != p.heads) throw ShapeError("sparse_attention: need one mask per head");
+    p.validate();
+    if (x.cols() != p.d()) throw ShapeError("project_qkv: X feature dim != d");
+    const int64_t L = static_cast<int64_t>(x.rows()), dm = static_cast<int64_t>(p.d());
+    const int64_t H = static_cast<int64_t>(p.heads), dk = static_cast<int64_t>(p.d_k()),
+                  dv = static_cast<int64_t>(p.d_v());
+    if (dk != dv) throw ShapeError("dsattn::gpu: needs d_v == d_k");
+    std::vector<uint64_t> rp(static_cast<size_t>(H * L) + 1, 0);
+    std::vector<uint32_t> cols;
+    for (int64_t h = 0; h < H; ++h) {
+        const SparseMask& m = per_head[static_cast<size_t>(h)];
+        if (m.l != static_cast<size_t>(L)) throw ShapeError("sddmm: mask size != sequence length");
+        m.validate();
+        for (int64_t i = 0; i < L; ++i) {
+            const auto& row = m.kept[static_cast<size_t>(i)];
+            rp[static_cast<size_t>(h * L + i) + 1] = rp[static_cast<size_t>(h * L + i)] + row.size();
+            cols.insert(cols.end(), row.begin(), row.end());
+        }
+    }
+    std::vector<uint16_t> hx(x.size()), hw(static_cast<size_t>(H * (2 * dk + dv) * dm));
+    for (size_t i = 0; i < x.size(); ++i) hx[i] = detail::bf16_bits(x.data()[i]);
+    int64_t row = 0;
+    for (const auto* ws : {&p.wq, &p.wk, &p.wv})
+        for (const Matrix& w : *ws)
+            for (size_t c = 0; c < w.cols(); ++c, ++row)
+                for (size_t r = 0; r < w.rows(); ++r) hw[static_cast<size_t>(row * dm) + r] = detail::bf16_bits(w(r, c));
+    const size_t nqkv = static_cast<size_t>(H * L * dk) * 2;
+    DeviceBuffer dx(hx.size() * 2), dw(hw.size() * 2), dq(nqkv), dkb(nqkv), dvb(nqkv), dz(nqkv), drp(rp.size() * 8),
+        dc(std::max<size_t>(cols.size(), 1) * 4);
+    check_cuda(cudaMemcpy(dx.get(), hx.data(), dx.size(), cudaMemcpyHostToDevice));
+    check_cuda(cudaMemcpy(dw.get(), hw.data(), dw.size(), cudaMemcpyHostToDevice));
+    check_cuda(cudaMemcpy(drp.get(), rp.data(), drp.size(), cudaMemcpyHostToDevice));
+    if (!cols.empty()) check_cuda(cudaMemcpy(dc.get(), cols.data(), cols.size() * 4, cudaMemcpyHostToDevice));
+    check(dsa_project_qkv(1, L, dm, H, dk, dv, 0, dx.get(), dw.get(), dq.get(), dkb.get(), dvb.get(), nullptr, nullptr));
+    dsa_config c{};
+    c.batch = 1;
+    c.heads = H;
+    c.L = L;
+    c.d = dk;
+    c.k = 16;
+    c.dtype = DSA_BF16;
+    c.bits = 4;
+    c.mask_mode = DSA_MASK_THRESHOLD;  // general CSR over every (head, row)
+    c.scale = p.scale ? 1 : 0;
+    c.frac_num = 1;
+    c.frac_den = 1;
+    c.cap = c.L;
+    check(dsa_config_validate(&c));
+    dsa_mask m{dc.as<uint32_t>(), drp.as<uint64_t>(), static_cast<int64_t>(cols.size()), nullptr};
+    check(dsa_sparse_attention(&c, dq.get(), dkb.get(), dvb.get(), &m, dz.get(), nullptr));
+    std::vector<uint16_t> hz(static_cast<size_t>(H * L * dv));
+    check_cuda(cudaMemcpy(hz.data(), dz.get(), hz.size() * 2, cudaMemcpyDeviceToHost));
+    Matrix out(static_cast<size_t>(L), static_cast<size_t>(H * dv), x.precision());
+    for (int64_t h = 0; h < H; ++h)
+        for (int64_t i = 0; i < L; ++i)
+            for (int64_t j = 0; j < dv; ++j) {
+                uint32_t u = static_cast<uint32_t>(hz[static_cast<size_t>((h * L + i) * dv + j)]) << 16;
+                float f;
+                std::memcpy(&f, &u, 4);
+                out.raw()[static_cast<size_t>(i * H * dv + h * dv + j)] = f;
+            }
+    out.round_to_precision();
     return out;
 }
 

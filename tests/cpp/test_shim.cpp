@@ -154,6 +154,19 @@ int main() {
             CHECK(max_abs_diff(g.v[h], ref.v[h]) <= 1e-2 * max_abs(ref.v[h]));
         }
         CHECK(throws<ShapeError>([&] { gpu::project_qkv(Matrix(Lx, dm + 1), ap); }));
+        // the layer-level sparse_attention (P/src/sparse.cpp:93-120) with one
+        // predicted mask per head: Q/K/V and Z pass through bf16 (two
+        // roundings), bar 2e-2 of max |Z|
+        std::vector<SparseMask> masks;
+        for (size_t h = 0; h < H; ++h)
+            masks.push_back(predicted_topk_mask(matmul_nt(ref.q[h], ref.k[h]), 20 + 5 * h));
+        masks[1].kept[7].clear();  // an empty row: zero output
+        Matrix zg = gpu::sparse_attention(x, ap, std::span<const SparseMask>(masks));
+        Matrix zr = sparse_attention(x, ap, std::span<const SparseMask>(masks));
+        CHECK(zg.rows() == zr.rows() && zg.cols() == zr.cols());
+        CHECK(max_abs_diff(zg, zr) <= 2e-2 * max_abs(zr));
+        CHECK(zg(7, 64) == 0.0 && zg(7, 127) == 0.0);
+        CHECK(throws<ShapeError>([&] { gpu::sparse_attention(x, ap, std::span<const SparseMask>(masks.data(), 2)); }));
     }
 
     // reference exception types (P/include/dsattn/errors.hpp)
