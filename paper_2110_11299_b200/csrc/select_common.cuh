@@ -25,18 +25,24 @@ __device__ __forceinline__ uint32_t window_hist(const int16_t* __restrict__ pv, 
                                                 uint32_t* h, int lane) {
     for (int i = lane; i < W; i += 32) h[i] = 0;
     __syncwarp();
+    // branch-free: the bin address is v * 4 + (h - 4 lo), the reduction is
+    // predicated on v >= lo (no divergent branch around each atomic)
+    const uint32_t hb = static_cast<uint32_t>(__cvta_generic_to_shared(h)) - static_cast<uint32_t>(lo) * 4u;
+    auto add = [&](int v) {
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ge.s32 p, %1, %2;\n\t@p red.shared.add.u32 [%0], 1;\n\t}\n" ::"r"(
+                         hb + static_cast<uint32_t>(v) * 4u),
+                     "r"(v), "r"(lo)
+                     : "memory");
+    };
     int j = lane;
     for (; j + 96 < L; j += 128) {
         const int v0 = pv[j * S], v1 = pv[(j + 32) * S], v2 = pv[(j + 64) * S], v3 = pv[(j + 96) * S];
-        if (v0 >= lo) atomicAdd(&h[v0 - lo], 1u);
-        if (v1 >= lo) atomicAdd(&h[v1 - lo], 1u);
-        if (v2 >= lo) atomicAdd(&h[v2 - lo], 1u);
-        if (v3 >= lo) atomicAdd(&h[v3 - lo], 1u);
+        add(v0);
+        add(v1);
+        add(v2);
+        add(v3);
     }
-    for (; j < L; j += 32) {
-        const int v = pv[j * S];
-        if (v >= lo) atomicAdd(&h[v - lo], 1u);
-    }
+    for (; j < L; j += 32) add(pv[j * S]);
     __syncwarp();
     uint32_t c = 0;
     for (int i = lane; i < W; i += 32) c += h[i];
@@ -183,6 +189,7 @@ __device__ __forceinline__ void band_select(const int16_t* __restrict__ pv, int 
     const unsigned lt = lanemask_lt();
     if (nge <= static_cast<uint32_t>(kList)) {
         uint32_t taken = 0;
+        const uint32_t ob = static_cast<uint32_t>(__cvta_generic_to_shared(obuf));
         for (int j0 = 0; j0 < Lp; j0 += 128) {
             int v[4];
 #pragma unroll
@@ -191,7 +198,11 @@ __device__ __forceinline__ void band_select(const int16_t* __restrict__ pv, int 
             for (int u = 0; u < 4; ++u) {
                 const bool ge = v[u] >= T;
                 const unsigned b = vote_ballot(ge);
-                if (ge) obuf[taken + __popc(b & lt)] = static_cast<uint32_t>(j0 + u * 32 + lane);
+                // predicated store: no divergent branch per value
+                asm volatile("{\n\t.reg .pred p;\n\tsetp.ge.s32 p, %2, %3;\n\t@p st.shared.u32 [%0], %1;\n\t}\n" ::"r"(
+                                 ob + (taken + __popc(b & lt)) * 4u),
+                             "r"(static_cast<uint32_t>(j0 + u * 32 + lane)), "r"(v[u]), "r"(T)
+                             : "memory");
                 taken += __popc(b);
             }
         }

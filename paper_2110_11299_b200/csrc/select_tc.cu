@@ -286,6 +286,13 @@ __global__ void __launch_bounds__(colvec_threads<NQ>(), NQ == 128 ? 1 : (NQ == 6
         const int64_t band = q0 / 8 + b;
         if (band >= nb) break;
         const int16_t* pv = pooled + (b >> 1) * Lp * 2 + (b & 1);
+        if (dbg & 2) {  // profiling ablation: threshold only (no emission)
+            int T;
+            uint32_t rem, nge;
+            band_threshold<2>(pv, static_cast<int>(L), static_cast<int>(keep), bandmax[b], M, h, lane, T, rem, nge);
+            if (out && lane == 0) out[(pair * nb + band) * keep] = static_cast<uint32_t>(T) + rem + nge;
+            continue;
+        }
         band_select<2>(pv, static_cast<int>(L), Lp, static_cast<int>(keep), bandmax[b], M, h,
                        obufs + warp * kList, out ? out + (pair * nb + band) * keep : nullptr, lane);
         __syncwarp();
