@@ -350,17 +350,28 @@ __global__ void __launch_bounds__(256)
                          uint16_t* __restrict__ lk, double* __restrict__ sq, double* __restrict__ sk) {
     using Sm = ProjSmem<D, KD>;
     constexpr int NC = KD / 8;
+    // grid = (ceil(L * NC / 256), pairs * 2): one tensor per blockIdx.y, so
+    // its scale is computed once per block (no 64-bit division per thread)
+    const int64_t pw = blockIdx.y;  // pair * 2 + which
     const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (idx >= pairs * 2 * L * NC) return;
+    __shared__ double s_s;
+    __shared__ float s_inv;
+    if (threadIdx.x == 0) {
+        const double am0 = __longlong_as_double(static_cast<long long>(amax[pw]));
+        s_s = am0 / qmax;
+        s_inv = static_cast<float>(qmax / am0);
+    }
+    __syncthreads();
+    if (idx >= L * NC) return;
     const int c = static_cast<int>(idx % NC);
-    const int64_t rr = idx / NC;  // (pair * 2 + which) * L + r
-    const int64_t r = rr % L, pw = rr / L;
+    const int64_t r = idx / NC;
+    const int64_t rr = pw * L + r;  // (pair * 2 + which) * L + r
     const int which = static_cast<int>(pw & 1);
     const int64_t pair = pw >> 1;
     const double am = __longlong_as_double(static_cast<long long>(amax[pw]));
-    const double s = am / qmax;
+    const double s = s_s;
     if (r == 0 && c == 0) (which ? sk : sq)[pair] = am == 0.0 ? 0.0 : s;
-    const float inv_s = static_cast<float>(qmax / am);
+    const float inv_s = s_inv;
     const float qm = static_cast<float>(qmax);
     const float rel = round_f32 ? 2.4e-7f : 1.2e-7f;
     const float* pn = reinterpret_cast<const float*>(img + Sm::kB);
@@ -419,8 +430,8 @@ void launch_tc(const PredictArgs& a, cudaStream_t st) {
         // amax pass stores x^ (fp32) + bound factors; the quantise pass streams them
         ka<<<grid, R, smem, st>>>(q, k, a.p, a.pimg, a.L, a.round_f32, a.qmax, a.amax, a.lq, a.lk, a.sq, a.sk,
                                   a.xhat);
-        const int64_t n = a.pairs * 2 * a.L * (KD / 8);
-        quantize_xhat_kernel<D, KD><<<static_cast<unsigned>(ceil_div_i(n, 256)), 256, 0, st>>>(
+        const dim3 gq(static_cast<unsigned>(ceil_div_i(a.L * (KD / 8), 256)), static_cast<unsigned>(a.pairs * 2));
+        quantize_xhat_kernel<D, KD><<<gq, 256, 0, st>>>(
             a.xhat, q, k, a.p, a.pimg, a.pairs, a.L, a.round_f32, a.qmax, a.amax, a.lq, a.lk, a.sq, a.sk);
     } else {
         ka<<<grid, R, smem, st>>>(q, k, a.p, a.pimg, a.L, a.round_f32, a.qmax, a.amax, a.lq, a.lk, a.sq, a.sk,
