@@ -415,7 +415,7 @@ def run_gpu_arm(args, p, rank, local, world):
                 "d2h_bytes_per_step": d2h},
         "roofline": {"kernel": dom, "bound": w["bound"], "achieved": achieved, "peak": peak,
                      "unit": w["unit"], "frac": achieved / peak, "traffic": traffic,
-                     "peak_source": peak_src},
+                     "peak_source": peak_src, "note": ROOFLINE_NOTES.get(dom, "")},
         "phases": phases,
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
@@ -427,6 +427,18 @@ def run_gpu_arm(args, p, rank, local, world):
     if adjacent:
         line["adjacent"] = adjacent
     print(json.dumps(line), flush=True)
+
+
+# what bounds each phase beyond its nominal roofline
+ROOFLINE_NOTES = {
+    "select": "achieved = the 2*L^2*k score-GEMM flops (K = k = 16/32 per MMA) over the select time; the "
+              "kernel is bound by the per-score integer selection work that follows each MMA (issue-bound, "
+              "ncu IPC ~2.3-2.6), not by the tensor pipe, so this fraction is small by construction -- "
+              "phases.select.candidates_per_s is the throughput that matters",
+    "attention": "bytes = compulsory Q/K/V/Z traffic; the kernels are bound by the row gathers "
+                 "(phases.attention.gathered_GBps, served from L2/L1)",
+    "predict": "bytes = Q/K read once + levels written",
+}
 
 
 def time_project_qkv(p, peak_tflops, reps=10):
