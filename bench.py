@@ -415,7 +415,9 @@ def run_gpu_arm(args, p, rank, local, world):
                 "d2h_bytes_per_step": d2h},
         "roofline": {"kernel": dom, "bound": w["bound"], "achieved": achieved, "peak": peak,
                      "unit": w["unit"], "frac": achieved / peak, "traffic": traffic,
-                     "peak_source": peak_src, "note": ROOFLINE_NOTES.get(dom, "")},
+                     "peak_source": peak_src,
+                     "note": ROOFLINE_NOTES.get(dom if not (dom == "attention" and w["bound"] == "tensor")
+                                                else "attention_block", "")},
         "phases": phases,
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
@@ -437,6 +439,8 @@ ROOFLINE_NOTES = {
               "phases.select.candidates_per_s is the throughput that matters",
     "attention": "bytes = compulsory Q/K/V/Z traffic; the kernels are bound by the row gathers "
                  "(phases.attention.gathered_GBps, served from L2/L1)",
+    "attention_block": "flops = 4*nnz*d (32x32 blocks: each kept block's K/V rows staged once in shared "
+                       "memory for the 32 queries of its block row, mma.sync m16n8k16)",
     "predict": "bytes = Q/K read once + levels written",
 }
 
