@@ -385,7 +385,11 @@ def run_gpu_arm(args, p, rank, local, world):
     phases["attention"]["gather_reuse"] = reuse
     tokens = p.tokens * world
     value = tokens / (ms * 1e-3)
-    adjacent = None if args.no_adjacent else {"project_qkv": time_project_qkv(p, peaks["bf16_tflops"])}
+    adjacent = None
+    if not args.no_adjacent:
+        adjacent = {"project_qkv": time_project_qkv(p, peaks["bf16_tflops"])}
+        if world == 1:
+            adjacent["layer_e2e"] = time_layer_e2e(p, steps=max(3, min(args.steps, 10)))
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         # bounded sample: repeat pair batches until >= 10 s of CPU wall time (<= ~30 s)
@@ -443,6 +447,66 @@ ROOFLINE_NOTES = {
                        "memory for the 32 queries of its block row, mma.sync m16n8k16)",
     "predict": "bytes = Q/K read once + levels written",
 }
+
+
+def time_layer_e2e(p, steps=5):
+    """Layer-level end to end (adjacent, not `value`/`e2e`): the caller hands
+    over the layer input X (pinned host, bf16) instead of Q/K/V; per step X
+    goes H2D, dsa_project_qkv makes every head's Q/K/V on the device, the
+    DSA pipeline runs and Z comes back D2H.  Pipelined over two buffer sets
+    like `e2e`; weights (packed W, P) are device-resident parameters."""
+    import torch
+    from paper_2110_11299_b200 import ops
+    sh = p.shape
+    dm, heads, dk, dv = sh["d"], p.heads, sh["d_k"], sh["d_v"]
+    if dk != p.d or dv != p.d or p.dtype != "bf16":
+        return None
+    dev = torch.device("cuda")
+    x = torch.randn(p.batch, p.L, dm).to(torch.bfloat16).pin_memory()
+    w = (torch.randn(heads * (2 * dk + dv), dm, device=dev) / dm ** 0.5).to(torch.bfloat16)
+    _, _, _, Pm = ops.generate(p.replace(batch=1, heads=1), npairs=1)
+    Pd = Pm.to(dev)
+    pipe = ops.Pipeline(p, device=dev)
+    zh = torch.empty(p.pairs, p.L, p.d, dtype=torch.bfloat16).pin_memory()
+    bufs = [(torch.empty_like(x, device=dev),
+             ops.project_qkv(torch.empty_like(x, device=dev), w, heads, dk, dv)[:3],
+             torch.empty(p.pairs, p.L, p.d, dtype=torch.bfloat16, device=dev)) for _ in range(2)]
+    stream, s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    ev_in = [torch.cuda.Event() for _ in range(2)]
+    ev_comp = [torch.cuda.Event() for _ in range(2)]
+    ev_out = [torch.cuda.Event() for _ in range(2)]
+
+    def run(n):
+        for i in range(n):
+            b = i & 1
+            xd, (qd, kd, vd), zd = bufs[b]
+            with torch.cuda.stream(s_in):
+                if i >= 2:
+                    s_in.wait_event(ev_comp[b])
+                xd.copy_(x, non_blocking=True)
+                ev_in[b].record(s_in)
+            stream.wait_event(ev_in[b])
+            if i >= 2:
+                stream.wait_event(ev_out[b])
+            ops.project_qkv(xd, w, heads, dk, dv, stream=stream, out=(qd, kd, vd, None))
+            pipe(qd, kd, vd, Pd, out=zd, stream=stream)
+            ev_comp[b].record(stream)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(ev_comp[b])
+                zh.copy_(zd, non_blocking=True)
+                ev_out[b].record(s_out)
+
+    run(2)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    run(steps)
+    torch.cuda.synchronize()
+    ms = (time.perf_counter() - t0) * 1e3 / steps
+    return {"value": p.tokens / (ms * 1e-3), "unit": "tokens/s", "ms_per_step": ms, "steps": steps,
+            "h2d_bytes_per_step": x.numel() * 2, "d2h_bytes_per_step": zh.numel() * 2,
+            "note": "adjacent, NOT the metric: from the layer input X (d_model = %d) instead of Q/K/V -- "
+                    "H2D X, dsa_project_qkv, dsa_pipeline, D2H Z per step (wall clock over the pipelined "
+                    "steps); only X crosses PCIe" % dm}
 
 
 def time_project_qkv(p, peak_tflops, reps=10):
