@@ -6,6 +6,7 @@
 // column groups.  Levels are chunk-planar ([k/8][L][8] per pair).
 #pragma once
 
+#include <cuda_fp16.h>
 #include <stdint.h>
 
 #include "device_common.cuh"
@@ -32,14 +33,42 @@ template <int KD>
 __device__ __forceinline__ uint32_t toff(int r, int c) {
     return static_cast<uint32_t>((r >> 3) * (KD * 16) + c * 128 + (r & 7) * 16);
 }
-template <int KD, int ROWS>
+// PERM: key r of each 32-key group goes to tile row 2(r%16) + r/16, so a
+// .pack::16b TMEM load of an f16 accumulator gives register i = (key i,
+// key 16+i) of the group (bit i / bit 16+i of a packed compare mask = key
+// order)
+template <int KD, int ROWS, bool PERM = false>
 __device__ __forceinline__ void load_rows(uint32_t sbase, const uint16_t* __restrict__ src, int64_t row0,
                                           int64_t L, int tid) {
     constexpr int kCh = KD / 8;
     for (int t = tid; t < ROWS * kCh; t += kTQ) {
         const int c = t / ROWS, r = t % ROWS;
         const bool ok = row0 + r < L;
-        cp16(sbase + toff<KD>(r, c), src + lvl_index(L, ok ? (row0 + r) : 0, c * 8), ok);
+        const int rd = PERM ? ((r & ~31) | ((r & 15) << 1) | ((r >> 4) & 1)) : r;
+        cp16(sbase + toff<KD>(rd, c), src + lvl_index(L, ok ? (row0 + r) : 0, c * 8), ok);
+    }
+}
+
+// In-place bf16 -> f16 conversion of the 16-byte pieces THIS thread copied
+// with load_rows<KD, ROWS, PERM> (after its cp.async group completed): the
+// levels are small integers, exact in both formats.  The f16-accumulator
+// MMA (P16) needs f16 operands.
+template <int KD, int ROWS, bool PERM = false>
+__device__ __forceinline__ void cvt_rows_f16(unsigned char* sbase, int tid) {
+    constexpr int kCh = KD / 8;
+    for (int t = tid; t < ROWS * kCh; t += kTQ) {
+        const int c = t / ROWS, r = t % ROWS;
+        const int rd = PERM ? ((r & ~31) | ((r & 15) << 1) | ((r >> 4) & 1)) : r;
+        uint4* q = reinterpret_cast<uint4*>(sbase + toff<KD>(rd, c));
+        uint4 v = *q;
+        uint32_t* w = reinterpret_cast<uint32_t*>(&v);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float lo = __uint_as_float(w[i] << 16), hi = __uint_as_float(w[i] & 0xffff0000u);
+            __half2 h = __floats2half2_rn(lo, hi);
+            w[i] = *reinterpret_cast<uint32_t*>(&h);
+        }
+        *q = v;
     }
 }
 
@@ -57,12 +86,20 @@ struct PassCtx {
 // Streams key tiles 0..nkt-1 through the tensor core and calls
 // f(tile, regs, col0) with 32 score columns of this thread's row.  `g`
 // counts tiles over all passes (TMEM buffer + mbarrier phase).
-template <int KD, class F>
+//
+// P16 (exact only when every score and partial sum is an integer of
+// magnitude <= 2048, i.e. KD * qmax^2 <= 2048): f16 operands (converted in
+// shared memory, cvt_rows_f16; the caller converts the Q~ tile) and f16
+// accumulator (bf16 operands need an f32 accumulator), key rows
+// permuted (load_rows PERM) and ONE .pack::16b load per tile, so
+// f(tile, regs, 0) gets 32 registers of f16 pairs: register i (i < 16) =
+// (key i, key 16+i), register 16+i = (key 32+i, key 48+i).
+template <int KD, bool P16 = false, class F>
 __device__ __forceinline__ void score_pass(const PassCtx& c, uint32_t& g, F&& f) {
     constexpr int kTile = kTN * KD * 2;
-    constexpr uint32_t idesc = tc::idesc_bf16_f32(kTQ, kTN);
+    constexpr uint32_t idesc = P16 ? tc::idesc_f16_f16(kTQ, kTN) : tc::idesc_bf16_f32(kTQ, kTN);
     for (int s = 0; s < kSt; ++s) {
-        if (s < c.nkt) load_rows<KD, kTN>(tc::smem_addr(c.ring + s * kTile), c.lkp, static_cast<int64_t>(s) * kTN, c.L, c.tid);
+        if (s < c.nkt) load_rows<KD, kTN, P16>(tc::smem_addr(c.ring + s * kTile), c.lkp, static_cast<int64_t>(s) * kTN, c.L, c.tid);
         cp_commit();
     }
     for (int t = 0; t <= c.nkt; ++t) {
@@ -72,12 +109,13 @@ __device__ __forceinline__ void score_pass(const PassCtx& c, uint32_t& g, F&& f)
             tc::fence_after_sync();
             const int nxt = t - 1 + kSt;
             if (nxt < c.nkt)
-                load_rows<KD, kTN>(tc::smem_addr(c.ring + ((t - 1) % kSt) * kTile), c.lkp,
+                load_rows<KD, kTN, P16>(tc::smem_addr(c.ring + ((t - 1) % kSt) * kTile), c.lkp,
                                    static_cast<int64_t>(nxt) * kTN, c.L, c.tid);
             cp_commit();
         }
         if (t < c.nkt) {
             cp_wait<kSt - 1>();
+            if (P16) cvt_rows_f16<KD, kTN, true>(c.ring + (t % kSt) * kTile, c.tid);
             tc::fence_proxy_async();
             __syncthreads();
             if (c.tid == 0) {
@@ -95,15 +133,26 @@ __device__ __forceinline__ void score_pass(const PassCtx& c, uint32_t& g, F&& f)
         if (t >= 1) {
             const int u = t - 1;
             const uint32_t base = c.tmem + (static_cast<uint32_t>(c.warp * 32) << 16) + ((g + u) & 1) * kTN;
-            uint32_t r0[32], r1[32];
-            tc::ld_32x32b_x32(base, r0);
-            tc::ld_32x32b_x32(base + 32, r1);
-            tc::wait_ld();
-            f(u, r0, 0);
-            f(u, r1, 32);
+            if (P16) {
+                uint32_t r0[32];
+                tc::ld_32x32b_x32_pack16(base, r0);
+                tc::wait_ld();
+                f(u, r0, 0);
+            } else {
+                uint32_t r0[32], r1[32];
+                tc::ld_32x32b_x32(base, r0);
+                tc::ld_32x32b_x32(base + 32, r1);
+                tc::wait_ld();
+                f(u, r0, 0);
+                f(u, r1, 32);
+            }
             tc::fence_before_sync();
         }
-        __syncthreads();
+        // TMEM buffer (t-1)&1 is next written by MMA(t+1), issued only after
+        // the __syncthreads of iteration t+1, which every thread reaches
+        // after draining tile t-1 here -- so the only barrier needed per
+        // tile is that one; keep one at the end of the pass for the caller
+        if (t == c.nkt) __syncthreads();
     }
     cp_wait<0>();
     g += static_cast<uint32_t>(c.nkt);

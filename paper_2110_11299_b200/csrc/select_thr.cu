@@ -32,6 +32,7 @@
 // The L x L score matrix never exists in HBM; K~ tiles are the only
 // streamed operand (bulk cp.async into a 3-stage ring).
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include <cstdlib>
 
@@ -79,7 +80,9 @@ struct ThrLayout {
     static constexpr int bytes(bool emit) { return kQ + kSt * kTile + (emit ? 0 : kHist + kE) + 64; }
 };
 
-template <int KD, bool EMIT>
+// P16 (emit only, KD * qmax^2 <= 2048): scores in an f16 accumulator, two
+// keys per packed compare (see rs::score_pass)
+template <int KD, bool EMIT, bool P16 = false>
 __global__ void __launch_bounds__(kTQ, 3) threshold_tc_kernel(ThrParams a) {
     extern __shared__ __align__(1024) unsigned char smem[];
     using Ly = ThrLayout<KD>;
@@ -126,6 +129,7 @@ __global__ void __launch_bounds__(kTQ, 3) threshold_tc_kernel(ThrParams a) {
     load_rows<KD, kTQ>(tc::smem_addr(bq), a.lq + pair * L * KD, q0, L, tid);
     cp_commit();
     cp_wait<0>();
+    if (P16) cvt_rows_f16<KD, kTQ>(bq, tid);
     tc::fence_proxy_async();
     tc::fence_before_sync();
     __syncthreads();
@@ -336,6 +340,57 @@ __global__ void __launch_bounds__(kTQ, 3) threshold_tc_kernel(ThrParams a) {
         const float vc = ci.x == INT32_MAX ? INFINITY : static_cast<float>(ci.x);
         uint32_t quota = static_cast<uint32_t>(ci.y);
         uint32_t n = 0;
+        // keep the first `quota` set bits of eq (ties, lowest key first)
+        auto ties = [&](uint32_t ge, uint32_t eq) -> uint32_t {
+            eq &= ge;
+            uint32_t keq = eq;
+            const uint32_t ne = static_cast<uint32_t>(__popc(eq));
+            if (ne > quota) {
+                keq = 0;
+                uint32_t e = eq;
+                for (uint32_t i = 0; i < quota; ++i) {
+                    keq |= e & (~e + 1u);
+                    e &= e - 1u;
+                }
+            }
+            quota -= static_cast<uint32_t>(__popc(keq));
+            return (ge & ~eq) | keq;
+        };
+        if (P16) {
+            // every score is an integer in [-2048, 2048]: clamping v_cut to
+            // that range keeps the comparisons exact in f16
+            const float vcl = fminf(fmaxf(vc, -2048.f), 4096.f);
+            const __half2 v2 = __half2half2(__float2half_rn(vc > 2048.f ? INFINITY : vcl));
+            score_pass<KD, true>(c, g, [&](int u, const uint32_t* r, int) {
+                const int64_t kt = static_cast<int64_t>(u) * kTN;
+#pragma unroll
+                for (int grp = 0; grp < 2; ++grp) {
+                    const int64_t k0 = kt + grp * 32;
+                    const int lim = k0 + 32 <= kfree ? 32 : static_cast<int>(klim - k0);
+                    uint32_t ge = 0;
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const __half2 x = *reinterpret_cast<const __half2*>(&r[grp * 16 + i]);
+                        ge |= __hge2_mask(x, v2) & (0x00010001u << i);
+                    }
+                    if (lim < 32) ge &= lim > 0 ? (0xffffffffu >> (32 - lim)) : 0u;
+                    if (quota != kAll && ge) {
+                        uint32_t eq = 0;
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) {
+                            const __half2 x = *reinterpret_cast<const __half2*>(&r[grp * 16 + i]);
+                            eq |= __heq2_mask(x, v2) & (0x00010001u << i);
+                        }
+                        ge = ties(ge, eq);
+                    }
+                    while (ge) {
+                        const int y = __ffs(ge) - 1;
+                        ge &= ge - 1u;
+                        out[n++] = static_cast<uint32_t>(k0 + y);
+                    }
+                }
+            });
+        } else
         score_pass<KD>(c, g, [&](int u, const uint32_t* r, int col0) {
             const float* f = reinterpret_cast<const float*>(r);
             const int64_t k0 = static_cast<int64_t>(u) * kTN + col0;
@@ -348,19 +403,7 @@ __global__ void __launch_bounds__(kTQ, 3) threshold_tc_kernel(ThrParams a) {
                 uint32_t eq = 0;
 #pragma unroll
                 for (int y = 0; y < 32; ++y) eq |= f[y] == vc ? (1u << y) : 0u;
-                eq &= ge;
-                uint32_t keq = eq;
-                const uint32_t ne = static_cast<uint32_t>(__popc(eq));
-                if (ne > quota) {  // keep the lowest `quota` set bits
-                    keq = 0;
-                    uint32_t e = eq;
-                    for (uint32_t i = 0; i < quota; ++i) {
-                        keq |= e & (~e + 1u);
-                        e &= e - 1u;
-                    }
-                }
-                quota -= static_cast<uint32_t>(__popc(keq));
-                ge = (ge & ~eq) | keq;
+                ge = ties(ge, eq);
             }
             while (ge) {
                 const int y = __ffs(ge) - 1;
@@ -373,12 +416,12 @@ __global__ void __launch_bounds__(kTQ, 3) threshold_tc_kernel(ThrParams a) {
     if (warp == 0) tc::tmem_dealloc<2 * kTN>(c.tmem);
 }
 
-template <int KD, bool EMIT>
+template <int KD, bool EMIT, bool P16 = false>
 void launch_thr(const ThrParams& p, int64_t pairs, cudaStream_t st) {
     // at least 46 KB so no fifth CTA lands on an SM whose TMEM is taken
     // (the count kernel's 64 KB histogram allows three per SM)
     const int smem = std::max(ThrLayout<KD>::bytes(EMIT), 46 * 1024);
-    auto kern = threshold_tc_kernel<KD, EMIT>;
+    auto kern = threshold_tc_kernel<KD, EMIT, P16>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const dim3 grid(static_cast<unsigned>(ceil_div_i(p.L, kTQ)), static_cast<unsigned>(pairs));
     kern<<<grid, kTQ, smem, st>>>(p);
@@ -413,8 +456,16 @@ void run_threshold_tc(const SelectArgs& a, cudaStream_t st) {
     if (a.KD == 16) launch_thr<16, false>(p, a.pairs, st);
     else launch_thr<32, false>(p, a.pairs, st);
     scan_counts(a, st);
-    if (a.KD == 16) launch_thr<16, true>(p, a.pairs, st);
-    else launch_thr<32, true>(p, a.pairs, st);
+    // f16 scores are exact when |S| and every partial sum stay <= 2048
+    static const bool f32_emit = std::getenv("DSA_THR_EMIT_F32") != nullptr;  // A/B switch
+    const bool p16 = !f32_emit && a.KD * static_cast<int64_t>(a.qmax) * a.qmax <= 2048;
+    if (a.KD == 16) {
+        if (p16) launch_thr<16, true, true>(p, a.pairs, st);
+        else launch_thr<16, true>(p, a.pairs, st);
+    } else {
+        if (p16) launch_thr<32, true, true>(p, a.pairs, st);
+        else launch_thr<32, true>(p, a.pairs, st);
+    }
 }
 
 }  // namespace dsa
