@@ -147,7 +147,7 @@ Plan plan(const dsa_config& c, bool pipeline, bool own_mask) {
     p.has_xhat = per_tensor && tc_path && c.bits <= 4 && std::getenv("DSA_PREDICT_TWO_READS") == nullptr;
     p.xhat = take(p.has_xhat ? sizeof(float) * P * 2 * c.L * (c.k + 1) : 0);
     p.amax = take(per_tensor ? sizeof(unsigned long long) * P * 2 : 0);
-    p.pimg = take(per_tensor ? align_up(predict_tc_image_bytes(c.d, c.k)) * kMaxChunks : 0);
+    p.pimg = take(tc_path ? align_up(predict_tc_image_bytes(c.d, c.k)) * kMaxChunks : 0);
     const bool row_scaled = c.mask_mode == DSA_MASK_ROW_TOPK && !per_tensor;
     p.ovf = take(row_scaled ? 16 + sizeof(int64_t) * P * c.L : 0);  // overflow count + row list
     p.pooled = take(c.mask_mode == DSA_MASK_BLOCK ? sizeof(int32_t) * P * 2 * ceil_div(c.L, c.block) * c.k : 0);
@@ -203,9 +203,9 @@ Scratch scratch_of(const dsa_config& c, const Plan& pl, void* ws, int64_t pair0 
     r.x64 = at<double>(ws, pl.x64) + pair0 * 2 * c.L * c.k;
     r.xhat = pl.has_xhat ? at<float>(ws, pl.xhat) + pair0 * 2 * c.L * (c.k + 1) : nullptr;
     r.amax = at<unsigned long long>(ws, pl.amax) + pair0 * 2;
-    r.pimg = c.quant_scope == DSA_QUANT_PER_TENSOR
-                 ? at<unsigned char>(ws, pl.pimg) + static_cast<size_t>(ci) * align_up(predict_tc_image_bytes(c.d, c.k))
-                 : nullptr;
+    const bool tc_path = c.dtype == DSA_BF16 && (c.d == 64 || c.d == 128) && (c.k == 16 || c.k == 32);
+    r.pimg = tc_path ? at<unsigned char>(ws, pl.pimg) + static_cast<size_t>(ci) * align_up(predict_tc_image_bytes(c.d, c.k))
+                     : nullptr;
     r.pooled = at<int32_t>(ws, pl.pooled) + pair0 * 2 * ceil_div(c.L, c.block > 0 ? c.block : 1) * c.k;
     r.etab = at<int64_t>(ws, pl.etab);
     r.counts = at<uint64_t>(ws, pl.counts);

@@ -99,7 +99,8 @@ struct ProjSmem {
     static constexpr int kLvl = R * KD * 2;          // staged levels [row][KD] bf16
     static constexpr int kList = kMaxList * 4;
     static constexpr int kMisc = 64;
-    static constexpr int bytes() { return kX + kImg + kMisc + kLvl + kList; }
+    static constexpr int kRowMax = R * 8;            // per-row exact max (ROW scope)
+    static constexpr int bytes() { return kX + kImg + kMisc + kLvl + kList + kRowMax; }
 };
 
 // P -> exact three-way bf16 split in the B-operand layout + |p_j| * 1.001
@@ -108,7 +109,8 @@ template <int D, int KD>
 __global__ void psplit_kernel(const float* __restrict__ p, unsigned char* __restrict__ img,
                               unsigned long long* __restrict__ amax, int64_t namax) {
     using Sm = ProjSmem<D, KD>;
-    for (int64_t i = threadIdx.x; i < namax; i += blockDim.x) amax[i] = 0ull;  // amax pass accumulators
+    if (amax != nullptr)
+        for (int64_t i = threadIdx.x; i < namax; i += blockDim.x) amax[i] = 0ull;  // amax pass accumulators
     for (int i = threadIdx.x; i < D * KD; i += blockDim.x) {
         const int c = i / KD, j = i % KD;
         const float v = p[i];
@@ -136,7 +138,9 @@ __global__ void psplit_kernel(const float* __restrict__ p, unsigned char* __rest
 // grid = (row tiles, 2 tensors, pairs)
 // R = 128 or 256 rows per CTA (one or two M = 128 MMAs; two halves amortise
 // the P-image copy and the CTA prologue over twice the rows).
-template <int D, int KD, bool QUANT, int R = kRows>
+// ROW = true: per-row scale (quant_scope = row) in ONE pass:
+// the row's exact max from its candidates, then its levels and scale.
+template <int D, int KD, bool QUANT, int R = kRows, bool ROW = false>
 __global__ void __launch_bounds__(R)
     project_tc_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k,
                       const float* __restrict__ p, const unsigned char* __restrict__ img, int64_t L,
@@ -157,6 +161,7 @@ __global__ void __launch_bounds__(R)
     unsigned int* lcount = reinterpret_cast<unsigned int*>(bar + 4);
     uint16_t* lvl_s = reinterpret_cast<uint16_t*>(pb + Sm::kImg + Sm::kMisc);
     uint32_t* list = reinterpret_cast<uint32_t*>(pb + Sm::kImg + Sm::kMisc + Sm::kLvl);
+    unsigned long long* rowmax = reinterpret_cast<unsigned long long*>(pb + Sm::kImg + Sm::kMisc + Sm::kLvl + Sm::kList);
 
     const int tid = threadIdx.x, warp = tid >> 5;
     const int which = blockIdx.y;
@@ -253,6 +258,81 @@ __global__ void __launch_bounds__(R)
         }
     }
     tc::fence_before_sync();
+    if constexpr (ROW) {
+        // row max candidates: |x^_j| + e_j >= max_j(|x^_j| - e_j), one bound
+        // per row (e_j <= E_row); recomputed exactly by the whole CTA
+        float xm = 0.f, pm = 0.f;
+#pragma unroll
+        for (int j = 0; j < KD; ++j) {
+            xm = fmaxf(xm, fabsf(xv[j]));
+            pm = fmaxf(pm, pn[j]);
+        }
+        const float er = fmaf(dq, pm, xm * rel) + 1e-30f;
+        const float thr = fmaxf(0.f, (xm - er) * 0.999999f) - er;
+        rowmax[tid] = 0ull;
+#pragma unroll
+        for (int j = 0; j < KD; ++j)
+            if (valid && fabsf(xv[j]) >= thr) {
+                const unsigned slot = atomicAdd(lcount, 1u);
+                if (slot < kMaxList) list[slot] = (static_cast<uint32_t>(tid) << 6) | j;
+                else atomicMax(&rowmax[tid], static_cast<unsigned long long>(__double_as_longlong(
+                                                 fabs(ref_chain_s<D, KD>(xa, tid, p, j, round_f32)))));
+            }
+        __syncthreads();
+        {
+            const unsigned n = min(*lcount, static_cast<unsigned>(kMaxList));
+            for (unsigned e = tid; e < n; e += R) {
+                const int rr = static_cast<int>(list[e] >> 6);
+                const double v = fabs(ref_chain_s<D, KD>(xa, rr, p, list[e] & 63, round_f32));
+                atomicMax(&rowmax[rr], static_cast<unsigned long long>(__double_as_longlong(v)));
+            }
+        }
+        __syncthreads();
+        if (tid == 0) *lcount = 0u;
+        const double am = __longlong_as_double(static_cast<long long>(rowmax[tid]));
+        const double s = am / qmax;
+        const float inv_s = static_cast<float>(qmax / am);
+        const float qm = static_cast<float>(qmax);
+        if (valid) (which ? sk : sq)[pair * L + r] = am == 0.0 ? 0.0 : s;
+        __syncthreads();
+        const float k1 = 1e-6f + 1.001f * rel, arow = dq * inv_s * 1.001f;
+#pragma unroll
+        for (int j = 0; j < KD; ++j) {
+            float lv = 0.f;
+            if (am != 0.0) {
+                lv = cert_level(xv[j], arow * pn[j], k1, inv_s, qm);
+                if (lv != lv) {
+                    lv = 0.f;
+                    if (valid) {
+                        const unsigned slot = atomicAdd(lcount, 1u);
+                        if (slot < kMaxList) {
+                            list[slot] = (static_cast<uint32_t>(tid) << 6) | j;
+                        } else {
+                            const double xe = ref_chain_s<D, KD>(xa, tid, p, j, round_f32);
+                            lv = static_cast<float>(fmin(fmax(round_half_away(xe / s), -qmax), qmax));
+                        }
+                    }
+                }
+            }
+            lvl_s[tid * KD + j] = static_cast<uint16_t>(__float_as_uint(lv) >> 16);
+        }
+        __syncthreads();
+        const unsigned n = min(*lcount, static_cast<unsigned>(kMaxList));
+        for (unsigned e = tid; e < n; e += R) {
+            const int rr = static_cast<int>(list[e] >> 6), j = static_cast<int>(list[e] & 63);
+            const double sr = __longlong_as_double(static_cast<long long>(rowmax[rr])) / qmax;
+            const double xe = ref_chain_s<D, KD>(xa, rr, p, j, round_f32);
+            const float lv = static_cast<float>(fmin(fmax(round_half_away(xe / sr), -qmax), qmax));
+            lvl_s[rr * KD + j] = static_cast<uint16_t>(__float_as_uint(lv) >> 16);
+        }
+        __syncthreads();
+        if (valid) {
+            uint16_t* out = (which ? lk : lq) + pair * L * KD;
+            const uint4* src = reinterpret_cast<const uint4*>(lvl_s + tid * KD);
+#pragma unroll
+            for (int c = 0; c < KD / 8; ++c) *reinterpret_cast<uint4*>(out + lvl_index(L, r, c * 8)) = src[c];
+        }
+    } else {
     if (!QUANT && xhat != nullptr && valid) {
         // x^ and the row's bound factor for the streaming quantise pass:
         // [pair][tensor][L][KD] floats, then [pair][tensor][L] factors
@@ -335,6 +415,7 @@ __global__ void __launch_bounds__(R)
             for (int c = 0; c < KD / 8; ++c) *reinterpret_cast<uint4*>(out + lvl_index(L, r, c * 8)) = src[c];
         }
     }
+    }  // !ROW
     __syncthreads();
     if (warp == 0) tc::tmem_dealloc<TC>(tmem);
 }
@@ -425,7 +506,19 @@ void launch_tc(const PredictArgs& a, cudaStream_t st) {
     const auto* q = static_cast<const __nv_bfloat16*>(a.q);
     const auto* k = static_cast<const __nv_bfloat16*>(a.k);
     const dim3 grid(static_cast<unsigned>(ceil_div_i(a.L, R)), 2, static_cast<unsigned>(a.pairs));
-    psplit_kernel<D, KD><<<1, 256, 0, st>>>(a.p, a.pimg, a.amax, 2 * a.pairs);
+    psplit_kernel<D, KD><<<1, 256, 0, st>>>(a.p, a.pimg, a.per_row ? nullptr : a.amax, 2 * a.pairs);
+    if (a.per_row) {
+        auto kr = project_tc_kernel<D, KD, true, R, true>;
+        static bool rattr = false;
+        if (!rattr) {
+            cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            rattr = true;
+        }
+        kr<<<grid, R, smem, st>>>(q, k, a.p, a.pimg, a.L, a.round_f32, a.qmax, nullptr, a.lq, a.lk, a.sq, a.sk,
+                                  nullptr);
+        note_launch(2);
+        return;
+    }
     if (a.xhat != nullptr) {
         // amax pass stores x^ (fp32) + bound factors; the quantise pass streams them
         ka<<<grid, R, smem, st>>>(q, k, a.p, a.pimg, a.L, a.round_f32, a.qmax, a.amax, a.lq, a.lk, a.sq, a.sk,
@@ -458,7 +551,8 @@ void launch_tc(const PredictArgs& a, cudaStream_t st) {
 size_t predict_tc_image_bytes(int64_t D, int64_t KD) { return static_cast<size_t>(3 * KD * D * 2 + KD * 4); }
 
 bool predict_tc_supported(const PredictArgs& a) {
-    if (!a.bf16 || a.per_row || a.pimg == nullptr) return false;
+    if (!a.bf16 || a.pimg == nullptr) return false;
+    if (a.per_row && std::getenv("DSA_PREDICT_ROWS_DMMA") != nullptr) return false;  // A/B switch
     if (std::getenv("DSA_PREDICT_CLUSTER") != nullptr) return false;  // A/B switch
     return (a.D == 64 || a.D == 128) && (a.KD == 16 || a.KD == 32);
 }
