@@ -90,7 +90,7 @@ __device__ __forceinline__ float cert_level(float x, float bj, float k1, float i
     return fminf(fmaxf(copysignf(floorf(at + 0.5f), t), -qmax), qmax);
 }
 
-template <int D, int KD, int R = kRows>
+template <int D, int KD, int R = kRows, bool ROW = false>
 struct ProjSmem {
     static constexpr int N = 3 * KD;                 // B rows: P1 | P2 | P3 columns
     static constexpr int kX = R * D * 2;             // X tile (R rows)
@@ -99,7 +99,7 @@ struct ProjSmem {
     static constexpr int kLvl = R * KD * 2;          // staged levels [row][KD] bf16
     static constexpr int kList = kMaxList * 4;
     static constexpr int kMisc = 64;
-    static constexpr int kRowMax = R * 8;            // per-row exact max (ROW scope)
+    static constexpr int kRowMax = ROW ? R * 8 : 0;  // per-row exact max (ROW scope)
     static constexpr int bytes() { return kX + kImg + kMisc + kLvl + kList + kRowMax; }
 };
 
@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(R)
                       int round_f32, double qmax, unsigned long long* __restrict__ amax,
                       uint16_t* __restrict__ lq, uint16_t* __restrict__ lk, double* __restrict__ sq,
                       double* __restrict__ sk, float* __restrict__ xhat) {
-    using Sm = ProjSmem<D, KD, R>;
+    using Sm = ProjSmem<D, KD, R, ROW>;
     constexpr int N = Sm::N;
     constexpr int TC = (R / 128) * N <= 64 ? 64 : ((R / 128) * N <= 128 ? 128 : 256);  // TMEM columns
     extern __shared__ __align__(1024) unsigned char smem[];
@@ -509,12 +509,13 @@ void launch_tc(const PredictArgs& a, cudaStream_t st) {
     psplit_kernel<D, KD><<<1, 256, 0, st>>>(a.p, a.pimg, a.per_row ? nullptr : a.amax, 2 * a.pairs);
     if (a.per_row) {
         auto kr = project_tc_kernel<D, KD, true, R, true>;
+        const int rsmem = std::max(ProjSmem<D, KD, R, true>::bytes(), (228 * 1024) / (512 / TC + 1) + 1024);
         static bool rattr = false;
         if (!rattr) {
-            cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, rsmem);
             rattr = true;
         }
-        kr<<<grid, R, smem, st>>>(q, k, a.p, a.pimg, a.L, a.round_f32, a.qmax, nullptr, a.lq, a.lk, a.sq, a.sk,
+        kr<<<grid, R, rsmem, st>>>(q, k, a.p, a.pimg, a.L, a.round_f32, a.qmax, nullptr, a.lq, a.lk, a.sq, a.sk,
                                   nullptr);
         note_launch(2);
         return;

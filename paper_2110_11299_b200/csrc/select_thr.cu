@@ -46,7 +46,8 @@ namespace {
 
 using namespace rs;
 
-constexpr int kW = 119;   // histogram bins per row (t = m - s in [0, kW)); 60 KB -> 3 CTAs/SM
+constexpr int kW = 119;   // histogram bins per row (t = m - s in [0, kW)); 30 KB -> 4 CTAs/SM
+constexpr int kHC = kTQ / 2;  // histogram columns: rows r and r + 64 share a word (16-bit halves)
 constexpr uint32_t kAll = 0xffffffffu;
 constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: float -> int by addition
 constexpr int kMagicBits = 0x4B400000;
@@ -75,7 +76,7 @@ template <int KD>
 struct ThrLayout {
     static constexpr int kQ = kTQ * KD * 2;
     static constexpr int kTile = kTN * KD * 2;
-    static constexpr int kHist = (kW + 1) * kTQ * 4;  // [bin][row] + trash bin: each thread its own bank
+    static constexpr int kHist = (kW + 1) * kHC * 4;  // [bin][row % 64] + trash bin: each warp conflict-free
     static constexpr int kE = kW * 8;
     static constexpr int bytes(bool emit) { return kQ + kSt * kTile + (emit ? 0 : kHist + kE) + 64; }
 };
@@ -83,7 +84,7 @@ struct ThrLayout {
 // P16 (emit only, KD * qmax^2 <= 2048): scores in an f16 accumulator, two
 // keys per packed compare (see rs::score_pass)
 template <int KD, bool EMIT, bool P16 = false>
-__global__ void __launch_bounds__(kTQ, 3) threshold_tc_kernel(ThrParams a) {
+__global__ void __launch_bounds__(kTQ, 4) threshold_tc_kernel(ThrParams a) {
     extern __shared__ __align__(1024) unsigned char smem[];
     using Ly = ThrLayout<KD>;
     unsigned char* bq = smem;
@@ -115,7 +116,7 @@ __global__ void __launch_bounds__(kTQ, 3) threshold_tc_kernel(ThrParams a) {
     const int64_t* E = a.etab + pair * a.span;
     if (!EMIT) {
         for (int t = tid; t < kW; t += kTQ) es[t] = t < a.span ? static_cast<uint64_t>(__ldg(E + t)) : 0ull;
-        for (int t = tid; t < (kW + 1) * kTQ; t += kTQ) hist[t] = 0u;
+        for (int t = tid; t < (kW + 1) * kHC; t += kTQ) hist[t] = 0u;
         if (tid == 0) {  // tz = first t with E[t] == 0 (E is non-increasing), or span
             int64_t lo = 0, hi = a.span;
             while (lo < hi) {
@@ -175,12 +176,16 @@ __global__ void __launch_bounds__(kTQ, 3) threshold_tc_kernel(ThrParams a) {
         const int tz = *tz_s;
         const int wh = tz < kW ? tz : kW;
         const float mb = m + kMagic;
-        uint32_t* hcol = hist + tid;
+        // row tid counts in the low (tid < 64) or high 16-bit half of word
+        // [bin][tid % 64] (a row has < 65536 candidate keys)
+        uint32_t* hcol = hist + (tid & (kHC - 1));
+        const uint32_t hinc = tid < kHC ? 1u : 0x10000u;
+        const int hsh = tid < kHC ? 0 : 16;
         {
             // bin bits = kMagicBits + t (float magic), clamped to the trash
             // bin; one IMAD gives the thread's bin address bits * 4 kTQ + base
             const uint32_t lim = static_cast<uint32_t>(kMagicBits + wh);
-            const uint32_t abase = tc::smem_addr(hcol) - static_cast<uint32_t>(kMagicBits) * (kTQ * 4u);
+            const uint32_t abase = tc::smem_addr(hcol) - static_cast<uint32_t>(kMagicBits) * (kHC * 4u);
             score_pass<KD>(c, g, [&](int u, const uint32_t* r, int col0) {
                 const float* f = reinterpret_cast<const float*>(r);
                 const int64_t k0 = static_cast<int64_t>(u) * kTN + col0;
@@ -188,7 +193,7 @@ __global__ void __launch_bounds__(kTQ, 3) threshold_tc_kernel(ThrParams a) {
                     const uint32_t bits = min(__float_as_uint(fmaf(v, -1.0f, mb)), lim);
                     // shared-memory reduction without return value: no
                     // load -> add -> store chain between consecutive keys
-                    asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(bits * (kTQ * 4u) + abase) : "memory");
+                    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(bits * (kHC * 4u) + abase), "r"(hinc) : "memory");
                 };
                 if (k0 + 32 <= kfree) {
 #pragma unroll
@@ -200,7 +205,7 @@ __global__ void __launch_bounds__(kTQ, 3) threshold_tc_kernel(ThrParams a) {
             });
         }
         // ---- per-row rule from the histogram
-        auto bin = [&](int t) -> uint32_t { return hcol[t * kTQ]; };
+        auto bin = [&](int t) -> uint32_t { return (hcol[t * kHC] >> hsh) & 0xffffu; };
         uint64_t Z = 0;
         uint32_t htot = 0;
         for (int t = 0; t < wh; ++t) {
@@ -419,7 +424,7 @@ __global__ void __launch_bounds__(kTQ, 3) threshold_tc_kernel(ThrParams a) {
 template <int KD, bool EMIT, bool P16 = false>
 void launch_thr(const ThrParams& p, int64_t pairs, cudaStream_t st) {
     // at least 46 KB so no fifth CTA lands on an SM whose TMEM is taken
-    // (the count kernel's 64 KB histogram allows three per SM)
+    // (TMEM: 4 x 128 columns)
     const int smem = std::max(ThrLayout<KD>::bytes(EMIT), 46 * 1024);
     auto kern = threshold_tc_kernel<KD, EMIT, P16>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -431,7 +436,8 @@ void launch_thr(const ThrParams& p, int64_t pairs, cudaStream_t st) {
 }  // namespace
 
 bool threshold_tc_supported(const SelectArgs& a) {
-    return a.mode == kThreshold && !a.per_row && (a.KD == 16 || a.KD == 32) && a.L < 65536 &&
+    return a.mode == kThreshold && !a.per_row && (a.KD == 16 || a.KD == 32) && a.L < 65536 - kTN &&  // 16-bit histogram halves
+          
            a.cut != nullptr && std::getenv("DSA_THRESHOLD_GENERIC") == nullptr;
 }
 
