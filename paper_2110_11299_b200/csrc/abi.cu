@@ -141,11 +141,13 @@ Plan plan(const dsa_config& c, bool pipeline, bool own_mask) {
                                          std::getenv("DSA_PREDICT_CLUSTER") != nullptr);
     p.x64 = take(need_x64 ? sizeof(double) * P * 2 * c.L * c.k : 0);
     // stored x^ for the streaming quantise pass (DSA_PREDICT_TWO_READS=1: the
-    // quantise pass re-reads Q/K and recomputes x^ instead).  8-bit levels
-    // leave ~1 % of the levels uncertified, which the cooperative recompute
-    // of the two-read pass handles far better than a per-thread chain.
+    // quantise pass re-reads Q/K and recomputes x^ instead).  Uncertified
+    // levels go to a deferred list (quantize_fix_kernel).  8-bit configs keep
+    // the two-read pass: with x^ they measured slower (C3 0.533 vs 0.471 ms:
+    // the amax pass of the d = 128 shape is latency-bound and the x^ writes
+    // lengthen it).
     p.has_xhat = per_tensor && tc_path && c.bits <= 4 && std::getenv("DSA_PREDICT_TWO_READS") == nullptr;
-    p.xhat = take(p.has_xhat ? sizeof(float) * P * 2 * c.L * (c.k + 1) : 0);
+    p.xhat = take(p.has_xhat ? sizeof(float) * P * xhat_floats_per_pair(c.L, c.k) : 0);
     p.amax = take(per_tensor ? sizeof(unsigned long long) * P * 2 : 0);
     p.pimg = take(tc_path ? align_up(predict_tc_image_bytes(c.d, c.k)) * kMaxChunks : 0);
     const bool row_scaled = c.mask_mode == DSA_MASK_ROW_TOPK && !per_tensor;
@@ -201,7 +203,7 @@ struct Scratch {
 Scratch scratch_of(const dsa_config& c, const Plan& pl, void* ws, int64_t pair0 = 0, int ci = 0) {
     Scratch r{};
     r.x64 = at<double>(ws, pl.x64) + pair0 * 2 * c.L * c.k;
-    r.xhat = pl.has_xhat ? at<float>(ws, pl.xhat) + pair0 * 2 * c.L * (c.k + 1) : nullptr;
+    r.xhat = pl.has_xhat ? at<float>(ws, pl.xhat) + pair0 * xhat_floats_per_pair(c.L, c.k) : nullptr;
     r.amax = at<unsigned long long>(ws, pl.amax) + pair0 * 2;
     const bool tc_path = c.dtype == DSA_BF16 && (c.d == 64 || c.d == 128) && (c.k == 16 || c.k == 32);
     r.pimg = tc_path ? at<unsigned char>(ws, pl.pimg) + static_cast<size_t>(ci) * align_up(predict_tc_image_bytes(c.d, c.k))

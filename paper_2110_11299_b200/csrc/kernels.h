@@ -32,6 +32,11 @@ struct PredictArgs {
     unsigned char* pimg;       // tensor-core path: P-split operand image
     float* xhat;               // tensor-core path: x^ [pairs][2][L][KD] + bound factors [pairs][2][L]
 };
+// x^ scratch per pair (floats): x^ [2][L][KD] + bound factors [2][L] + a
+// share of the deferred-recompute list (u64 entries, 1/8 of the levels)
+// and of its counter.  Layout of a call's view over n pairs: x^ of all n,
+// factors of all n, the counter (u64), then the list (capacity n L KD / 4).
+inline int64_t xhat_floats_per_pair(int64_t L, int64_t KD) { return 2 * L * (KD + 1) + L * KD / 2 + 2; }
 void run_predict(const PredictArgs& a, cudaStream_t st);
 bool predict_fast_supported(const PredictArgs& a);
 void run_predict_fast(const PredictArgs& a, cudaStream_t st);

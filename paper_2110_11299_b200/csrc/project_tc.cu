@@ -107,8 +107,10 @@ struct ProjSmem {
 // (one CTA; the image is the same for every pair).
 template <int D, int KD>
 __global__ void psplit_kernel(const float* __restrict__ p, unsigned char* __restrict__ img,
-                              unsigned long long* __restrict__ amax, int64_t namax) {
+                              unsigned long long* __restrict__ amax, int64_t namax,
+                              unsigned long long* __restrict__ lcnt) {
     using Sm = ProjSmem<D, KD>;
+    if (lcnt != nullptr && threadIdx.x == 0) *lcnt = 0ull;  // deferred-recompute list
     if (amax != nullptr)
         for (int64_t i = threadIdx.x; i < namax; i += blockDim.x) amax[i] = 0ull;  // amax pass accumulators
     for (int i = threadIdx.x; i < D * KD; i += blockDim.x) {
@@ -421,10 +423,12 @@ __global__ void __launch_bounds__(R)
 }
 
 // Streaming quantise pass over the stored x^ (thread = row x 8 columns):
-// certified level, or the reference chain from the row in global memory.
+// certified levels; the uncertified ones get list slots (one global atomic
+// per block) and are recomputed by quantize_fix_kernel, one thread each
+// (in place, by the reference chain, only if the list is full).
 template <int D, int KD>
 __global__ void __launch_bounds__(256)
-    quantize_xhat_kernel(const float* __restrict__ xhat, const __nv_bfloat16* __restrict__ q,
+    quantize_xhat_kernel(const float* xhat, const __nv_bfloat16* __restrict__ q,
                          const __nv_bfloat16* __restrict__ k, const float* __restrict__ p,
                          const unsigned char* __restrict__ img, int64_t pairs, int64_t L, int round_f32,
                          double qmax, const unsigned long long* __restrict__ amax, uint16_t* __restrict__ lq,
@@ -443,49 +447,124 @@ __global__ void __launch_bounds__(256)
         s_inv = static_cast<float>(qmax / am0);
     }
     __syncthreads();
-    if (idx >= L * NC) return;
+    // no early exit: the deferred-list slots are allocated block-wide
+    const bool active = idx < L * NC;
     const int c = static_cast<int>(idx % NC);
-    const int64_t r = idx / NC;
+    const int64_t r = active ? idx / NC : 0;
     const int64_t rr = pw * L + r;  // (pair * 2 + which) * L + r
     const int which = static_cast<int>(pw & 1);
     const int64_t pair = pw >> 1;
     const double am = __longlong_as_double(static_cast<long long>(amax[pw]));
     const double s = s_s;
-    if (r == 0 && c == 0) (which ? sk : sq)[pair] = am == 0.0 ? 0.0 : s;
+    if (active && r == 0 && c == 0) (which ? sk : sq)[pair] = am == 0.0 ? 0.0 : s;
     const float inv_s = s_inv;
     const float qm = static_cast<float>(qmax);
     const float rel = round_f32 ? 2.4e-7f : 1.2e-7f;
     const float* pn = reinterpret_cast<const float*>(img + Sm::kB);
-    const float4 a0 = __ldg(reinterpret_cast<const float4*>(xhat + rr * KD + c * 8));
-    const float4 a1 = __ldg(reinterpret_cast<const float4*>(xhat + rr * KD + c * 8 + 4));
-    const float dq = __ldg(xhat + pairs * 2 * L * KD + rr);
-    const float xv[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+    // deferred list: counter then entries after the bound factors
+    unsigned long long* lcnt = reinterpret_cast<unsigned long long*>(const_cast<float*>(xhat) + pairs * 2 * L * (KD + 1));
+    unsigned long long* list = lcnt + 1;
+    const int64_t lcap = pairs * L * KD / 4;
+    float xv[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    float dq = 0.f;
+    if (active) {
+        const float4 a0 = __ldg(reinterpret_cast<const float4*>(xhat + rr * KD + c * 8));
+        const float4 a1 = __ldg(reinterpret_cast<const float4*>(xhat + rr * KD + c * 8 + 4));
+        dq = __ldg(xhat + pairs * 2 * L * KD + rr);
+        xv[0] = a0.x; xv[1] = a0.y; xv[2] = a0.z; xv[3] = a0.w;
+        xv[4] = a1.x; xv[5] = a1.y; xv[6] = a1.z; xv[7] = a1.w;
+    }
     const float k1 = 1e-6f + 1.001f * rel, arow = dq * inv_s * 1.001f;
+    float lv[8];
+    unsigned um = 0;  // uncertified columns of this thread
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        lv[u] = 0.f;
+        if (active && am != 0.0) {
+            lv[u] = cert_level(xv[u], arow * __ldg(pn + c * 8 + u), k1, inv_s, qm);
+            if (lv[u] != lv[u]) {
+                lv[u] = 0.f;
+                um |= 1u << u;
+            }
+        }
+    }
+    // block-wide slot allocation: one global atomic per block
+    __shared__ unsigned wsum[8];
+    __shared__ unsigned long long lbase;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const unsigned cnt = static_cast<unsigned>(__popc(um));
+    unsigned incl = cnt;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += y;
+    }
+    if (lane == 31) wsum[wid] = incl;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned tot = 0;
+        for (int x = 0; x < static_cast<int>(blockDim.x >> 5); ++x) {
+            const unsigned t = wsum[x];
+            wsum[x] = tot;
+            tot += t;
+        }
+        lbase = tot ? atomicAdd(lcnt, static_cast<unsigned long long>(tot)) : 0ull;
+    }
+    __syncthreads();
+    unsigned long long slot = lbase + wsum[wid] + (incl - cnt);
+    while (um) {
+        const int u = __ffs(um) - 1;
+        um &= um - 1u;
+        const int j = c * 8 + u;
+        if (slot < static_cast<unsigned long long>(lcap)) {
+            list[slot] = (static_cast<unsigned long long>(pw) << 40) | (static_cast<unsigned long long>(r) << 6) |
+                         static_cast<unsigned long long>(j);
+        } else {  // list full: the reference chain in place
+            const __nv_bfloat16* row = (which ? k : q) + (pair * L + r) * D;
+            double acc = 0.0;
+            for (int t = 0; t < D; ++t) acc = fma(to_double(row[t]), static_cast<double>(__ldg(p + t * KD + j)), acc);
+            if (round_f32) acc = static_cast<double>(static_cast<float>(acc));
+            lv[u] = static_cast<float>(fmin(fmax(round_half_away(acc / s), -qmax), qmax));
+        }
+        ++slot;
+    }
+    if (!active) return;
     uint32_t w[4];
 #pragma unroll
-    for (int h = 0; h < 4; ++h) {
-        float lv2[2];
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            const int j = c * 8 + 2 * h + u;
-            float lv = 0.f;
-            if (am != 0.0) {
-                lv = cert_level(xv[2 * h + u], arow * __ldg(pn + j), k1, inv_s, qm);
-                if (lv != lv) {  // uncertified: the reference chain
-                    const __nv_bfloat16* row = (which ? k : q) + (pair * L + r) * D;
-                    double acc = 0.0;
-                    for (int t = 0; t < D; ++t)
-                        acc = fma(to_double(row[t]), static_cast<double>(__ldg(p + t * KD + j)), acc);
-                    if (round_f32) acc = static_cast<double>(static_cast<float>(acc));
-                    lv = static_cast<float>(fmin(fmax(round_half_away(acc / s), -qmax), qmax));
-                }
-            }
-            lv2[u] = lv;
-        }
-        w[h] = (__float_as_uint(lv2[0]) >> 16) | ((__float_as_uint(lv2[1]) >> 16) << 16);
-    }
+    for (int h = 0; h < 4; ++h)
+        w[h] = (__float_as_uint(lv[2 * h]) >> 16) | ((__float_as_uint(lv[2 * h + 1]) >> 16) << 16);
     uint16_t* out = (which ? lk : lq) + pair * L * KD;
     *reinterpret_cast<uint4*>(out + lvl_index(L, r, c * 8)) = make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// The levels quantize_xhat_kernel could not certify: one thread per list
+// entry runs the reference's fp64 chain (P/src/kernels/scalar.cpp:19-32) and
+// overwrites the placeholder level.
+template <int D, int KD>
+__global__ void __launch_bounds__(256)
+    quantize_fix_kernel(const float* __restrict__ xhat, const __nv_bfloat16* __restrict__ q,
+                        const __nv_bfloat16* __restrict__ k, const float* __restrict__ p, int64_t pairs, int64_t L,
+                        int round_f32, double qmax, const unsigned long long* __restrict__ amax,
+                        uint16_t* __restrict__ lq, uint16_t* __restrict__ lk) {
+    const unsigned long long* lcnt =
+        reinterpret_cast<const unsigned long long*>(xhat + pairs * 2 * L * (KD + 1));
+    const unsigned long long* list = lcnt + 1;
+    const int64_t n = min(static_cast<int64_t>(*lcnt), pairs * L * KD / 4);
+    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const unsigned long long v = list[e];
+        const int64_t pw = static_cast<int64_t>(v >> 40), r = static_cast<int64_t>((v >> 6) & 0x3ffffffffull);
+        const int j = static_cast<int>(v & 63);
+        const int which = static_cast<int>(pw & 1);
+        const int64_t pair = pw >> 1;
+        const double s = __longlong_as_double(static_cast<long long>(amax[pw])) / qmax;
+        const __nv_bfloat16* row = (which ? k : q) + (pair * L + r) * D;
+        double acc = 0.0;
+        for (int t = 0; t < D; ++t) acc = fma(to_double(row[t]), static_cast<double>(__ldg(p + t * KD + j)), acc);
+        if (round_f32) acc = static_cast<double>(static_cast<float>(acc));
+        const float lv = static_cast<float>(fmin(fmax(round_half_away(acc / s), -qmax), qmax));
+        (which ? lk : lq)[pair * L * KD + lvl_index(L, r, j)] = static_cast<uint16_t>(__float_as_uint(lv) >> 16);
+    }
 }
 
 template <int D, int KD, int R>
@@ -506,7 +585,9 @@ void launch_tc(const PredictArgs& a, cudaStream_t st) {
     const auto* q = static_cast<const __nv_bfloat16*>(a.q);
     const auto* k = static_cast<const __nv_bfloat16*>(a.k);
     const dim3 grid(static_cast<unsigned>(ceil_div_i(a.L, R)), 2, static_cast<unsigned>(a.pairs));
-    psplit_kernel<D, KD><<<1, 256, 0, st>>>(a.p, a.pimg, a.per_row ? nullptr : a.amax, 2 * a.pairs);
+    unsigned long long* lcnt =
+        a.xhat != nullptr && !a.per_row ? reinterpret_cast<unsigned long long*>(a.xhat + a.pairs * 2 * a.L * (KD + 1)) : nullptr;
+    psplit_kernel<D, KD><<<1, 256, 0, st>>>(a.p, a.pimg, a.per_row ? nullptr : a.amax, 2 * a.pairs, lcnt);
     if (a.per_row) {
         auto kr = project_tc_kernel<D, KD, true, R, true>;
         const int rsmem = std::max(ProjSmem<D, KD, R, true>::bytes(), (228 * 1024) / (512 / TC + 1) + 1024);
@@ -527,6 +608,9 @@ void launch_tc(const PredictArgs& a, cudaStream_t st) {
         const dim3 gq(static_cast<unsigned>(ceil_div_i(a.L * (KD / 8), 256)), static_cast<unsigned>(a.pairs * 2));
         quantize_xhat_kernel<D, KD><<<gq, 256, 0, st>>>(
             a.xhat, q, k, a.p, a.pimg, a.pairs, a.L, a.round_f32, a.qmax, a.amax, a.lq, a.lk, a.sq, a.sk);
+        quantize_fix_kernel<D, KD><<<2 * 148, 256, 0, st>>>(a.xhat, q, k, a.p, a.pairs, a.L, a.round_f32, a.qmax,
+                                                           a.amax, a.lq, a.lk);
+        note_launch();
     } else {
         ka<<<grid, R, smem, st>>>(q, k, a.p, a.pimg, a.L, a.round_f32, a.qmax, a.amax, a.lq, a.lk, a.sq, a.sk,
                                   nullptr);
