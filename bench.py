@@ -7,9 +7,12 @@
 One JSON line on rank 0.  A "step" is one pass of the hot path over the
 config's full batch: all B*H (b,h) pairs, phases 1 -> 2 -> 3, inputs resident
 in HBM (`value`), or through the C-ABI with host buffers and H2D/D2H copies
-inside the timed region (`e2e`).  Under torchrun every rank runs the config's
-pairs (its own seeded pair range: weak scaling, no collective on the hot
-path); checksums are all-reduced over NCCL after timing stops.
+inside the timed region (`e2e`).  With N GPUs the config's B*H pairs are
+partitioned over the ranks (strong scaling): rank r runs
+shard.pair_range(r, N, B*H) with no collective on the hot path; the time is
+the max over ranks; per-pair checksums are all-gathered over NCCL after
+timing stops.  `--gpus N` without torchrun re-launches itself under
+torch.distributed.run with N ranks.
 """
 from __future__ import annotations
 
@@ -121,90 +124,185 @@ def max_over_ranks(x: float, world: int, device) -> float:
 
 
 # ---------------------------------------------------------------- CPU arms
-def reference_sample(p, npairs: int, threads: int, rng_pair0: int = 0):
-    """Time the reference implementation (oracle/_ref, the unmodified
-    reference sources) on `npairs` pairs over `threads` host threads."""
-    from oracle.oracle import REF_SO, Oracle, Reference
-    from paper_2110_11299_b200 import ops
+REF_MODES = {"row_topk": 0, "colvec": 1, "block": 2, "threshold": 3}
 
-    sub = p.replace(batch=npairs, heads=1)
-    q, k, v, P = ops.generate(sub, pair0=rng_pair0, npairs=npairs)
-    qn, kn, vn, Pn = (t.double().numpy() for t in (q, k, v, P))
-    mode = {"row_topk": 0, "colvec": 1, "block": 2}.get(p.mask_mode)
-    if REF_SO.exists() and mode is not None and p.quant_scope == "tensor":
-        ref = Reference()
-        t0 = time.perf_counter()
-        ref.pipeline(qn, kn, vn, Pn, p.bits, p.dtype == "f32", mode, p.keep, p.vec_v, p.block,
-                     p.force_diag, threads=threads)
-        dt = time.perf_counter() - t0
-        return dt, "reference", f"oracle/_ref (reference sources, isa={ref.isa()})"
-    # modes without a reference composition: the oracle restatement ("port")
-    o = Oracle()
+
+def cpu_model() -> str:
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def reference_inputs(p, pair0: int, npairs: int):
+    """The config's seeded inputs drawn with the REFERENCE Rng (oracle/_ref,
+    ref_generate; bit-identical to dsa_generate, tests/test_oracle.py) -- the
+    reference arm never loads libdsa_b200.so."""
+    from oracle.oracle import Reference
+    return Reference().generate(p.L, p.d, p.k, p.dtype == "bf16", p.seed, p.planted_per_mille,
+                                p.band_width, pair0, npairs)
+
+
+def reference_run(p, inputs, threads: int) -> float:
+    """One pass of the reference implementation (oracle/_ref: the unmodified
+    reference sources + extern "C" compositions of reference functions) over
+    the pairs in `inputs`, on `threads` host threads; returns wall seconds."""
+    from oracle.oracle import Reference
+    ref = Reference()
+    q, k, v, P = inputs
     t0 = time.perf_counter()
-    from concurrent.futures import ThreadPoolExecutor
+    ref.pipeline(q, k, v, P, p.bits, p.dtype == "f32", REF_MODES[p.mask_mode], p.keep, p.vec_v, p.block,
+                 p.force_diag, threads=threads, per_row=p.quant_scope == "row", frac_num=p.frac_num,
+                 frac_den=p.frac_den, cap=p.cap, causal=p.causal)
+    return time.perf_counter() - t0
 
-    def one(i):
-        lq, sq = o.levels(qn[i], Pn, p.bits, per_row=p.quant_scope == "row", round_f32=p.round_proj_f32)
-        lk, sk = o.levels(kn[i], Pn, p.bits, per_row=p.quant_scope == "row", round_f32=p.round_proj_f32)
-        import numpy as np
-        if p.mask_mode == "threshold":
-            c = sq * sk / np.sqrt(float(p.d))
-            rp, cols, _ = o.mask_threshold(lq, lk, c, p.frac_num, p.frac_den, p.cap, p.causal)
-        else:
-            m = o.mask_topk(lq, lk, p.keep, sk=sk)
-            rp = np.arange(0, p.L * p.keep + 1, p.keep, dtype=np.uint64)
-            cols = m.ravel()
-        o.sparse_attention(qn[i], kn[i], vn[i], rp, cols, p.scale, p.dtype == "f32")
 
-    with ThreadPoolExecutor(threads) as ex:
-        list(ex.map(one, range(npairs)))
-    return time.perf_counter() - t0, "port", "oracle/dsa_oracle.c restatement"
+def reference_pairs(p, threads: int) -> int:
+    """Pairs per reference step: every pair for C0-C2 (L <= 4096, BASELINE.md
+    2); a bounded sample of C3/C4 (seconds of CPU work per pair), so the whole
+    --impl reference run ends within minutes."""
+    if p.L <= 4096:
+        return p.pairs
+    return min(p.pairs, max(1, threads))
 
 
 def run_reference_arm(args, p, rank, world):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    npairs = min(p.pairs, max(1, args.ref_pairs or 4 * threads))
+    npairs = min(p.pairs, args.ref_pairs) if args.ref_pairs else reference_pairs(p, threads)
+    inputs = reference_inputs(p, 0, npairs)
     tokens = npairs * p.L / p.heads
     for _ in range(args.warmup):
-        reference_sample(p, npairs, threads)
-    times = []
-    kind = sample = None
-    for _ in range(args.steps):
-        dt, kind, sample = reference_sample(p, npairs, threads)
-        times.append(dt)
+        reference_run(p, inputs, threads)
+    times = [reference_run(p, inputs, threads) for _ in range(args.steps)]
     mean = statistics.mean(times)
     value = tokens / mean
+    from oracle.oracle import Reference
+    isa = Reference().isa()
+    sample = (f"{npairs} of {p.pairs} (b,h) pairs per step through oracle/_ref (the reference sources, "
+              f"isa={isa}; inputs from the reference Rng); tokens = pairs*L/heads; cpu: {cpu_model()}")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded BASELINE generator)",
-        "config": {**p.summary(), "sample_pairs": npairs},
-        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": kind,
-                         "sample": f"{npairs} of {p.pairs} (b,h) pairs per step via {sample}; "
-                                   f"tokens = pairs*L/heads"},
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded BASELINE generator, reference Rng)",
+        "config": {**p.summary(), "sample_pairs": npairs, "same_config": npairs == p.pairs},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "reference",
+                         "sample": sample, "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+def cpu_baseline_sample(p):
+    """Bounded sample of the reference CPU path on this host (rank 0, N = 1):
+    repeated pair batches until >= 10 s of wall time (<= ~30 s)."""
+    threads = os.cpu_count() or 1
+    npairs = min(p.pairs, max(1, threads if p.L > 4096 else 4 * threads))
+    total_t, total_pairs, reps = 0.0, 0, 0
+    while total_t < 10.0 and reps < 64:
+        pair0 = (reps * npairs) % p.pairs
+        n = min(npairs, p.pairs - pair0)
+        dt = reference_run(p, reference_inputs(p, pair0, n), threads)
+        total_t += dt
+        total_pairs += n
+        reps += 1
+        if dt > 20.0:
+            break
+    return {"value": total_pairs * p.L / p.heads / total_t, "unit": "tokens/s", "cores": threads,
+            "kind": "reference",
+            "sample": f"{reps} batches, {total_pairs} of {p.pairs} (b,h) pairs through oracle/_ref (the "
+                      f"reference sources), {total_t:.1f} s wall; tokens = pairs*L/heads",
+            "cpu_model": cpu_model()}
+
+
+# ------------------------------------------------------- rank partitioning
+def rank_slice(p, rank: int, world: int) -> tuple[int, int]:
+    """This rank's contiguous (b,h)-pair range of the ONE config (strong
+    scaling): the config's B*H pairs split over the ranks."""
+    from paper_2110_11299_b200.shard import pair_range
+    return pair_range(rank, world, p.pairs)
+
+
+def rank_inputs(p, rank: int, world: int, pinned: bool = False):
+    """Seeded inputs of this rank's pairs only (each pair from its own
+    substream, so the union over ranks is exactly the N = 1 input)."""
+    from paper_2110_11299_b200 import ops
+    lo, hi = rank_slice(p, rank, world)
+    q, k, v, P = ops.generate(p, pair0=lo, npairs=hi - lo, pinned=pinned)
+    return lo, hi, q, k, v, P
+
+
+def global_checksum(z_local, p, world: int):
+    """Per-pair checksums (fp64 sum of Z, max |Z|) of every rank, gathered
+    over the process group after timing; returns [sum, max] over the config
+    -- identical for every world size."""
+    import torch
+    from paper_2110_11299_b200.shard import gather_checksums, pair_checksums
+    cs = pair_checksums(z_local)
+    if world > 1:
+        cs = gather_checksums(cs, p.pairs)
+    return [float(cs[:, 0].sum().item()), float(cs[:, 1].max().item())] if cs.shape[0] else [0.0, 0.0]
+
+
 # ---------------------------------------------------------------- GPU arm
+def graph_of(fn, stream):
+    """One call of `fn(stream)` captured as a CUDA graph (None if capture fails)."""
+    import torch
+    try:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            fn(stream)
+        with torch.cuda.stream(stream):
+            g.replay()
+        stream.synchronize()
+        return g
+    except Exception as e:  # pragma: no cover - capture unsupported
+        print(f"[bench] graph capture failed ({e}); eager launches", file=sys.stderr)
+        torch.cuda.synchronize()
+        return None
+
+
+def time_graph(fn, g, stream, reps: int, flush=None) -> float:
+    """Mean ms of `reps` replays of graph `g` (or eager `fn`), CUDA events on `stream`."""
+    import torch
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    total = 0.0
+    for _ in range(reps):
+        with torch.cuda.stream(stream):
+            if flush is not None:
+                flush.fill_(1.0)
+            evs[0].record(stream)
+            if g is not None:
+                g.replay()
+            else:
+                fn(stream)
+            evs[1].record(stream)
+        evs[1].synchronize()
+        total += evs[0].elapsed_time(evs[1])
+    return total / reps
+
+
 def run_gpu_arm(args, p, rank, local, world):
     import torch
     from paper_2110_11299_b200 import ops
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    P_ = p.pairs
-    pair0 = rank * P_  # weak scaling: each rank its own seeded pair range
-    q, k, v, Pm = ops.generate(p, pair0=pair0, npairs=P_, pinned=True)
+    ndev = torch.cuda.device_count()
+    torch.cuda.set_device(local % ndev)
+    dev = torch.device("cuda", local % ndev)
+    lo, hi, q, k, v, Pm = rank_inputs(p, rank, world, pinned=True)
+    P_ = hi - lo
+    if P_ == 0:
+        raise SystemExit(f"[bench] {p.name} has {p.pairs} (b,h) pairs: fewer than {world} ranks")
     qd, kd, vd, Pd = (t.to(dev) for t in (q, k, v, Pm))
     zd = torch.empty_like(qd)
     zh = torch.empty_like(q).pin_memory()
     stream = torch.cuda.Stream(device=dev)
-    pipe = ops.Pipeline(p, device=dev)
+    pipe = ops.Pipeline(p, pairs=P_, device=dev)
     ph = ops.Phases(p, P_, device=dev)
     in_bytes = q.numel() * q.element_size() * 3
     l2_note = (f"inputs {in_bytes / 1e6:.0f} MB > 126 MB L2 (no flush needed)" if in_bytes > 126e6
@@ -225,27 +323,16 @@ def run_gpu_arm(args, p, rank, local, world):
     # kernels, without host launch gaps); eager launches if capture fails
     graph, per_step = None, None
     if not args.no_graph:
-        try:
-            g = torch.cuda.CUDAGraph()
-            c0 = ops.launch_counter()
-            with torch.cuda.graph(g, stream=stream):
-                step(stream)
-            per_step = ops.launch_counter() - c0
-            graph = g
-            with torch.cuda.stream(stream):
-                graph.replay()
-            stream.synchronize()
-        except Exception as e:  # pragma: no cover - capture unsupported
-            print(f"[bench] graph capture failed ({e}); eager launches", file=sys.stderr)
-            graph = None
-            torch.cuda.synchronize(dev)
+        c0 = ops.launch_counter()
+        graph = graph_of(step, stream)
+        per_step = ops.launch_counter() - c0
 
-    # ---- device-resident timed region
+    # ---- device-resident timed region (barrier + sync on both sides, max over ranks)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     n0 = ops.launch_counter()
     barrier(world)
     torch.cuda.synchronize(dev)
-    with ClockSampler(local) as clk:
+    with ClockSampler(local % ndev) as clk:
         with torch.cuda.stream(stream):
             ev0.record(stream)
             for _ in range(args.steps):
@@ -257,8 +344,8 @@ def run_gpu_arm(args, p, rank, local, world):
         ev1.synchronize()
         torch.cuda.synchronize(dev)
     launches = per_step * args.steps if graph is not None else ops.launch_counter() - n0
-    ms = ev0.elapsed_time(ev1) / args.steps
-    ms = max_over_ranks(ms, world, dev)
+    ms_local = ev0.elapsed_time(ev1) / args.steps
+    ms = max_over_ranks(ms_local, world, dev)
     barrier(world)
 
     # ---- end to end through the C-ABI with host buffers.  Every step copies
@@ -309,39 +396,26 @@ def run_gpu_arm(args, p, rank, local, world):
     e2e_ms = max_over_ranks(t_start.elapsed_time(t_end) / args.steps, world, dev)
     torch.cuda.synchronize(dev)
 
-    # ---- per-phase timing (same stream, events; for the roofline)
-    phase_ms = {}
-    evs = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-    with torch.cuda.stream(stream):
-        ph.predict(qd, kd, Pd, stream)
-        ph.select(stream)
-        ph.attend(qd, kd, vd, zd, stream)
-    stream.synchronize()
-    acc = {"predict": 0.0, "select": 0.0, "attention": 0.0}
+    # ---- per-kernel timing for the roofline (CUDA events on the launching
+    # stream, graphs replayed like the timed step).  The timed step is
+    # predict + the rest of dsa_pipeline (for COLVEC one fused select +
+    # attention kernel); the three unfused phases explain it.
     reps = max(3, args.steps)
-    for _ in range(reps):
-        with torch.cuda.stream(stream):
-            if flush is not None:
-                flush.fill_(1.0)
-            evs[0].record(stream)
-            ph.predict(qd, kd, Pd, stream)
-            evs[1].record(stream)
-            ph.select(stream)
-            evs[2].record(stream)
-            ph.attend(qd, kd, vd, zd, stream)
-            evs[3].record(stream)
-        evs[3].synchronize()
-        acc["predict"] += evs[0].elapsed_time(evs[1])
-        acc["select"] += evs[1].elapsed_time(evs[2])
-        acc["attention"] += evs[2].elapsed_time(evs[3])
-    for kx in acc:
-        phase_ms[kx] = acc[kx] / reps
+    g_pred = graph_of(lambda s: ph.predict(qd, kd, Pd, s), stream)
+    predict_ms = time_graph(lambda s: ph.predict(qd, kd, Pd, s), g_pred, stream, reps, flush)
+    step_ms = time_graph(step, graph, stream, reps) if flush is None else time_graph(
+        lambda s: pipe(qd, kd, vd, Pd, out=zd, stream=s), None, stream, reps, flush)
+    ph.select(stream)
+    stream.synchronize()
+    g_sel = graph_of(lambda s: ph.select(s), stream)
+    select_ms = time_graph(lambda s: ph.select(s), g_sel, stream, reps, flush)
+    g_att = graph_of(lambda s: ph.attend(qd, kd, vd, zd, s), stream)
+    attend_ms = time_graph(lambda s: ph.attend(qd, kd, vd, zd, s), g_att, stream, reps, flush)
+    pipe(qd, kd, vd, Pd, out=zd, stream=stream)  # Z of the timed path, for the checksum
+    stream.synchronize()
 
-    # ---- checksums over NCCL after timing (not on the hot path)
-    from paper_2110_11299_b200.shard import gather_checksums, pair_checksums
-    local_cs = pair_checksums(zd)
-    cs_all = gather_checksums(local_cs, P_ * world) if world > 1 else local_cs
-    csum = torch.stack([cs_all[:, 0].sum(), cs_all[:, 1].max()])
+    # ---- checksums over the process group after timing (not on the hot path)
+    csum = global_checksum(zd, p, world)
 
     if rank != 0:
         return
@@ -350,40 +424,60 @@ def run_gpu_arm(args, p, rank, local, world):
     pairs = P_
     cnt = ops.counters(p, ph.mask, pairs, stream=stream)
     nnz = cnt["nnz"]
-    # algorithmic work per launch of each phase, over all pairs
+    causal = p.mask_mode == "threshold" and p.causal
+    score_flops = (L * (L + 1) if causal else 2 * L * L) * k_ * pairs
+    # algorithmic work per launch of each phase over this rank's pairs
     work = {
         "predict": {"bound": "hbm", "amount": (2 * L * d * e + 2 * L * k_ * 2) * pairs + d * k_ * 4,
                     "unit": "GB/s", "scale": 1e9},
-        "select": {"bound": "tensor", "amount": (L * (L + 1) if (p.mask_mode == "threshold" and p.causal)
-                                                  else 2 * L * L) * k_ * pairs,
-                   "unit": "TFLOP/s", "scale": 1e12},
+        "select": {"bound": "tensor", "amount": score_flops, "unit": "TFLOP/s", "scale": 1e12},
         "attention": {"bound": "hbm", "amount": 4 * L * d * e * pairs, "unit": "GB/s", "scale": 1e9},
     }
-    if p.mask_mode == "block":  # C3: 32x32 blocks put attention near the ridge
+    if p.mask_mode == "block":
+        # C3: the selection ranks pooled block scores (no L^2 score GEMM): it
+        # streams the levels and writes the block lists -> HBM; 32x32 blocks
+        # put the attention near the ridge -> tensor
+        nbk = -(-L // p.block)
+        work["select"] = {"bound": "hbm", "amount": (2 * L * k_ * 2 + nbk * p.keep * 4) * pairs,
+                          "unit": "GB/s", "scale": 1e9}
         work["attention"] = {"bound": "tensor", "amount": 4 * nnz * d, "unit": "TFLOP/s", "scale": 1e12}
-    dom = max(phase_ms, key=phase_ms.get)
-    w = work[dom]
-    achieved = w["amount"] / (phase_ms[dom] * 1e-3) / w["scale"]
+    phase_ms = {"predict": predict_ms, "select": select_ms, "attention": attend_ms}
+    fused = p.mask_mode == "colvec" and ops.fused_pipeline(p, pairs)
+    rest_ms = max(step_ms - predict_ms, 1e-6)
+    if fused:
+        # the timed step's dominant kernel: colvec_tc_kernel<.., FUSED> =
+        # score GEMM + pooling + selection + SDDMM/softmax/SpMM
+        dom = "select+attention (fused colvec_tc_kernel)"
+        w = {"bound": "tensor", "amount": score_flops + 4 * nnz * d, "unit": "TFLOP/s", "scale": 1e12}
+        dom_ms = rest_ms
+    else:
+        dom = max(phase_ms, key=phase_ms.get)
+        w = work[dom]
+        dom_ms = phase_ms[dom]
+    achieved = w["amount"] / (dom_ms * 1e-3) / w["scale"]
     peak = peaks["hbm_gbs"] if w["bound"] == "hbm" else peaks["bf16_tflops"]
     traffic = None
     tf = ROOT / "profiles" / "traffic.json"
     if tf.exists():
-        traffic = json.loads(tf.read_text()).get(f"{p.name}:{dom}")
+        traffic = json.loads(tf.read_text()).get(f"{p.name}:{'fused' if fused else dom}")
     phases = {}
     for kx, ms_k in phase_ms.items():
         wk = work[kx]
         a_k = wk["amount"] / (ms_k * 1e-3) / wk["scale"]
         pk = peaks["hbm_gbs"] if wk["bound"] == "hbm" else peaks["bf16_tflops"]
-        phases[kx] = {"ms": ms_k, "bound": wk["bound"], "achieved": a_k, "unit": wk["unit"],
-                      "frac": a_k / pk}
+        phases[kx] = {"ms": ms_k, "bound": wk["bound"], "achieved": a_k, "unit": wk["unit"], "frac": a_k / pk}
+    if fused:
+        phases["fused_select_attention"] = {"ms": rest_ms, "bound": "tensor", "achieved": achieved,
+                                            "unit": "TFLOP/s", "frac": achieved / peak,
+                                            "note": "timed step minus predict (both CUDA-event timed)"}
     # explanatory counters: candidates scored per second, and the
     # K/V row bytes the attention gathers (reuse = query rows sharing a gather)
-    cand = (L * (L + 1) // 2 if (p.mask_mode == "threshold" and p.causal) else L * L) * pairs
-    phases["select"]["candidates_per_s"] = cand / (phase_ms["select"] * 1e-3)
+    cand = (L * (L + 1) // 2 if causal else L * L) * pairs
+    phases["select"]["candidates_per_s"] = cand / (select_ms * 1e-3)
     reuse = {"colvec": p.vec_v, "block": p.block}.get(p.mask_mode, 1)
-    phases["attention"]["gathered_GBps"] = 2 * nnz * d * e / reuse / (phase_ms["attention"] * 1e-3) / 1e9
+    phases["attention"]["gathered_GBps"] = 2 * nnz * d * e / reuse / (attend_ms * 1e-3) / 1e9
     phases["attention"]["gather_reuse"] = reuse
-    tokens = p.tokens * world
+    tokens = p.tokens  # the whole config: every rank's pairs
     value = tokens / (ms * 1e-3)
     adjacent = None
     if not args.no_adjacent:
@@ -392,43 +486,30 @@ def run_gpu_arm(args, p, rank, local, world):
             adjacent["layer_e2e"] = time_layer_e2e(p, steps=max(3, min(args.steps, 10)))
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        # bounded sample: repeat pair batches until >= 10 s of CPU wall time (<= ~30 s)
-        threads = os.cpu_count() or 1
-        npairs = min(pairs, max(1, args.ref_pairs or 4 * threads))
-        total_t, total_pairs, reps = 0.0, 0, 0
-        kind = sample = None
-        while total_t < 10.0 and reps < 64:
-            dt, kind, sample = reference_sample(p, npairs, threads, rng_pair0=(reps * npairs) % pairs)
-            total_t += dt
-            total_pairs += npairs
-            reps += 1
-            if dt > 20.0:
-                break
-        cpu = {"value": total_pairs * L / p.heads / total_t, "unit": "tokens/s", "cores": threads, "kind": kind,
-               "sample": f"{reps} x {npairs} of {pairs} (b,h) pairs via {sample}, {total_t:.1f} s wall; "
-                         f"tokens = pairs*L/heads"}
+        cpu = cpu_baseline_sample(p)
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16" if p.dtype == "bf16" else "f32",
         "data": "synthetic (seeded BASELINE generator, SURVEY 8.0)",
-        "config": {**p.summary(), "pairs_per_gpu": pairs, "parallelism": f"(b,h)-pairs x{world}",
+        "config": {**p.summary(), "pairs_per_gpu": pairs, "parallelism": f"(b,h)-pairs /{world}",
                    "launch": "cuda graph per step" if graph is not None else "eager",
-                   "l2": l2_note},
+                   "l2": l2_note, **({"oversubscribed_gpus": True} if world > ndev else {})},
         "e2e": {"value": tokens / (e2e_ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
         "roofline": {"kernel": dom, "bound": w["bound"], "achieved": achieved, "peak": peak,
                      "unit": w["unit"], "frac": achieved / peak, "traffic": traffic,
                      "peak_source": peak_src,
-                     "note": ROOFLINE_NOTES.get(dom if not (dom == "attention" and w["bound"] == "tensor")
-                                                else "attention_block", "")},
+                     "note": ROOFLINE_NOTES.get("fused" if fused else
+                                                (dom if not (dom == "attention" and w["bound"] == "tensor")
+                                                 else "attention_block"), "")},
         "phases": phases,
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
         "gpu_launches": int(launches),
         "counters": {"nnz": nnz, "sddmm_mults": cnt["sddmm_mults"], "spmm_mults": cnt["spmm_mults"],
                      "softmax_exps": cnt["softmax_exps"]},
-        "checksum": [float(csum[0].item()), float(csum[1].item())],
+        "checksum": csum,
     }
     if adjacent:
         line["adjacent"] = adjacent
@@ -437,6 +518,9 @@ def run_gpu_arm(args, p, rank, local, world):
 
 # what bounds each phase beyond its nominal roofline
 ROOFLINE_NOTES = {
+    "fused": "achieved = (2*L^2*k score-GEMM + 4*nnz*d attention) flops over the fused kernel's time "
+             "(timed step minus predict); the kernel is bound by the per-score integer work of pooling and "
+             "exact selection (issue-bound), not by the tensor pipe -- DESIGN.md 4",
     "select": "achieved = the 2*L^2*k score-GEMM flops (K = k = 16/32 per MMA) over the select time; the "
               "kernel is bound by the per-score integer selection work that follows each MMA (issue-bound, "
               "ncu IPC ~2.3-2.6), not by the tensor pipe, so this fraction is small by construction -- "
@@ -544,6 +628,19 @@ def time_project_qkv(p, peak_tflops, reps=10):
                     "P/src/attention.cpp:36-46); random weights; not part of value"}
 
 
+def spawn_ranks(n: int) -> None:
+    """`--gpus N` outside torchrun: re-launch this command as N ranks (one
+    process per GPU) under torch.distributed.run on 127.0.0.1."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -559,6 +656,8 @@ def main():
     from paper_2110_11299_b200 import load_preset
 
     p = load_preset(args.config)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn_ranks(args.gpus)
     rank, local, world = dist_setup()
     try:
         if args.impl == "reference":

@@ -163,6 +163,12 @@ dsa_status dsa_project_qkv(int64_t batch, int64_t L, int64_t d_model, int64_t he
                            int64_t dv, int64_t npred, const void* x, const void* w, void* q,
                            void* k, void* v, float* r, void* stream);
 
+/* 1 when dsa_pipeline runs selection and attention as ONE fused kernel for
+ * this config (COLVEC on the tensor-core path), 0 when it runs them as
+ * separate phases, -1 for an invalid config.  Introspection for bench.py's
+ * roofline attribution; no reference counterpart. */
+int dsa_pipeline_fused(const dsa_config* cfg);
+
 /* Kernels launched by this library since load (process-wide, monotonic);
  * bench.py reads it around timed regions. */
 uint64_t dsa_launch_counter(void);

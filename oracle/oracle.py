@@ -203,8 +203,12 @@ class Reference:
             "ref_colvec_maxpool_mask": (I32, [_d, I64, I64, I64, _u32]),
             "ref_sparse_attention": (I32, [_d, _d, _d, I64, I64, I64, I32, _u64, _u32, I32, _d, _u8, _u64]),
             "ref_masked_attention": (I32, [_d, _d, _d, I64, I64, I64, _u64, _u32, I32, _d]),
-            "ref_pipeline": (I32, [I64, I32, _d, _d, _d, _d, I64, I64, I64, I32, I32, I32, I64, I64,
-                                   I64, I32, _d]),
+            "ref_pipeline": (I32, [I64, I32, _d, _d, _d, _d, I64, I64, I64, I32, I32, I32, I32, I64, I64,
+                                   I64, I32, I64, I64, I64, I32, _d]),
+            "ref_block_mask": (I32, [_i32, _i32, I64, I64, I64, I64, I32, _u32]),
+            "ref_causal_threshold_mask": (I32, [_i32, _i32, I64, I64, D, D, I64, I32, _u64, C.c_void_p]),
+            "ref_threshold_row_probs": (I32, [_i32, _i32, I64, I64, D, I64, I32, _d]),
+            "ref_generate": (I32, [I64, I64, I64, I32, C.c_uint64, I32, I32, I64, I64, _d, _d, _d, _d]),
             "ref_write_mask": (I32, [C.c_char_p, I64, _u64, _u32]),
             "ref_read_mask": (I32, [C.c_char_p, C.POINTER(I64), C.POINTER(I64), C.c_void_p, C.c_void_p]),
             "ref_write_sparse_scores": (I32, [C.c_char_p, I64, _u64, _u32, _d]),
@@ -357,11 +361,47 @@ class Reference:
         return z
 
     def pipeline(self, q, k, v, p, bits, f32, mode, keep, vec_v=8, block=32, force_diag=False,
-                 threads=1):
-        """[pairs, L, d] doubles -> Z [pairs, L, d] through reference functions."""
+                 threads=1, per_row=False, frac_num=1, frac_den=1, cap=1, causal=False):
+        """[pairs, L, d] doubles -> Z [pairs, L, d] through reference functions.
+        mode 0 row top-k (per_row scales optional), 1 colvec, 2 block, 3 threshold."""
         q, k, v, p = _f64(q), _f64(k), _f64(v), _f64(p)
         pairs, L, d = q.shape
         z = np.empty_like(q)
         self._chk(self.L.ref_pipeline(pairs, threads, q, k, v, p, L, d, p.shape[1], bits, int(f32),
-                                      mode, keep, vec_v, block, int(force_diag), z))
+                                      mode, int(per_row), keep, vec_v, block, int(force_diag), frac_num,
+                                      frac_den, cap, int(causal), z))
         return z
+
+    # ---- O5 / O6 compositions of reference primitives (block, causal threshold)
+    def block_mask(self, lq, lk, bs, keep, force_diag):
+        lq, lk = np.ascontiguousarray(lq, np.int32), np.ascontiguousarray(lk, np.int32)
+        L = lq.shape[0]
+        out = np.empty((-(-L // bs), keep), np.uint32)
+        self._chk(self.L.ref_block_mask(lq, lk, L, lq.shape[1], bs, keep, int(force_diag), out))
+        return out
+
+    def causal_threshold_mask(self, lq, lk, c, theta, cap, causal):
+        lq, lk = np.ascontiguousarray(lq, np.int32), np.ascontiguousarray(lk, np.int32)
+        L = lq.shape[0]
+        rp = np.zeros(L + 1, np.uint64)
+        self._chk(self.L.ref_causal_threshold_mask(lq, lk, L, lq.shape[1], c, theta, cap, int(causal), rp, None))
+        cols = np.empty(max(int(rp[-1]), 1), np.uint32)
+        self._chk(self.L.ref_causal_threshold_mask(lq, lk, L, lq.shape[1], c, theta, cap, int(causal), rp,
+                                                   cols.ctypes.data_as(C.c_void_p)))
+        return rp, cols[: int(rp[-1])]
+
+    def threshold_row_probs(self, lq, lk, c, i, causal):
+        lq, lk = np.ascontiguousarray(lq, np.int32), np.ascontiguousarray(lk, np.int32)
+        L = lq.shape[0]
+        out = np.empty(i + 1 if causal else L)
+        self._chk(self.L.ref_threshold_row_probs(lq, lk, L, lq.shape[1], c, i, int(causal), out))
+        return out
+
+    def generate(self, L, d, kdim, bf16, seed, planted_pm, band_w, pair0, npairs):
+        """Seeded BASELINE inputs drawn with the reference Rng (doubles rounded
+        to the dtype): q, k, v [npairs, L, d], P [d, kdim]."""
+        q, k, v = (np.empty((npairs, L, d)) for _ in range(3))
+        p = np.empty((d, kdim))
+        self._chk(self.L.ref_generate(L, d, kdim, int(bf16), seed, planted_pm, band_w, pair0, npairs,
+                                      q, k, v, p))
+        return q, k, v, p

@@ -219,73 +219,290 @@ int ref_masked_attention(const double* q, const double* k, const double* v, int6
     });
 }
 
+}  // extern "C"
+
+// ------------------------------------------- block and causal threshold (O5, O6)
+// Exact-integer S~ rows [r0, r1) through the reference matmul_nt
+// (P/src/linalg.cpp:19-27) on integer-valued f64 level Matrices.
+static Matrix score_rows(const int32_t* lq, const int32_t* lk, int64_t L, int64_t k, int64_t r0, int64_t r1) {
+    Matrix a(static_cast<size_t>(r1 - r0), static_cast<size_t>(k), Precision::f64);
+    for (int64_t i = 0; i < (r1 - r0) * k; ++i) a.raw()[i] = static_cast<double>(lq[r0 * k + i]);
+    Matrix b(static_cast<size_t>(L), static_cast<size_t>(k), Precision::f64);
+    for (int64_t i = 0; i < L * k; ++i) b.raw()[i] = static_cast<double>(lk[i]);
+    return matmul_nt(a, b);
+}
+
+// O5 from reference primitives: per block row, the mean of S~ over each
+// bs x bs block (sum / count, both exact integers in f64), the diagonal
+// block forced first (+1e300), then row_topk_indices (P/src/linalg.cpp:69-85,
+// ties to the lowest block) on the 1 x nb row of means.
+static std::vector<std::vector<uint32_t>> block_lists(const int32_t* lq, const int32_t* lk, int64_t L,
+                                                      int64_t k, int64_t bs, int64_t keep, int force_diag) {
+    const int64_t nb = (L + bs - 1) / bs;
+    std::vector<std::vector<uint32_t>> out(static_cast<size_t>(nb));
+    for (int64_t ib = 0; ib < nb; ++ib) {
+        const int64_t r0 = ib * bs, r1 = std::min(r0 + bs, L);
+        const Matrix s = score_rows(lq, lk, L, k, r0, r1);
+        Matrix mean(1, static_cast<size_t>(nb), Precision::f64);
+        for (int64_t jb = 0; jb < nb; ++jb) {
+            const int64_t c0 = jb * bs, c1 = std::min(c0 + bs, L);
+            double sum = 0.0;
+            for (int64_t i = 0; i < r1 - r0; ++i)
+                for (int64_t j = c0; j < c1; ++j) sum += s(static_cast<size_t>(i), static_cast<size_t>(j));
+            mean.raw()[jb] = sum / static_cast<double>((r1 - r0) * (c1 - c0));
+        }
+        if (force_diag) mean.raw()[ib] = 1e300;
+        out[static_cast<size_t>(ib)] = row_topk_indices(mean, static_cast<size_t>(keep))[0];
+    }
+    return out;
+}
+
+// O6 from reference primitives, one query row: p = row_softmax(c * S~)
+// (P/src/linalg.cpp:51-67) over the candidates j <= i (causal) or all j,
+// kept where p >= theta (the threshold_mask rule, P/src/maskgen.cpp:29);
+// more than `cap` survivors -> the cap largest by S~ via row_topk_indices
+// (ties to the lowest index).
+static std::vector<uint32_t> threshold_row(const Matrix& s, size_t ri, int64_t i, int64_t L, double c,
+                                           double theta, int64_t cap, int causal, double* probs) {
+    const int64_t n = causal ? i + 1 : L;
+    Matrix x(1, static_cast<size_t>(n), Precision::f64);
+    for (int64_t j = 0; j < n; ++j) x.raw()[j] = s(ri, static_cast<size_t>(j));
+    const Matrix p = row_softmax(scale(x, c));
+    if (probs) std::memcpy(probs, p.data(), static_cast<size_t>(n) * sizeof(double));
+    std::vector<uint32_t> kept;
+    for (int64_t j = 0; j < n; ++j)
+        if (p(0, static_cast<size_t>(j)) >= theta) kept.push_back(static_cast<uint32_t>(j));
+    if (static_cast<int64_t>(kept.size()) > cap) {
+        Matrix key(1, static_cast<size_t>(n), Precision::f64);
+        for (int64_t j = 0; j < n; ++j) key.raw()[j] = -1e300;
+        for (uint32_t j : kept) key.raw()[j] = x(0, j);
+        kept = row_topk_indices(key, static_cast<size_t>(cap))[0];
+    }
+    return kept;
+}
+
+static void threshold_lists(const int32_t* lq, const int32_t* lk, int64_t L, int64_t k, double c, double theta,
+                            int64_t cap, int causal, std::vector<std::vector<uint32_t>>& rows) {
+    rows.assign(static_cast<size_t>(L), {});
+    constexpr int64_t kChunk = 256;  // S~ rows materialised at a time
+    for (int64_t r0 = 0; r0 < L; r0 += kChunk) {
+        const int64_t r1 = std::min(r0 + kChunk, L);
+        const Matrix s = score_rows(lq, lk, L, k, r0, r1);
+        for (int64_t i = r0; i < r1; ++i)
+            rows[static_cast<size_t>(i)] = threshold_row(s, static_cast<size_t>(i - r0), i, L, c, theta, cap, causal, nullptr);
+    }
+}
+
+extern "C" {
+
+// Block-column lists [ceil(L/bs)][keep] of the BLOCK mode.
+int ref_block_mask(const int32_t* lq, const int32_t* lk, int64_t L, int64_t k, int64_t bs, int64_t keep,
+                   int force_diag, uint32_t* block_cols) {
+    return guarded([&] {
+        const auto lists = block_lists(lq, lk, L, k, bs, keep, force_diag);
+        for (size_t b = 0; b < lists.size(); ++b)
+            std::memcpy(block_cols + b * keep, lists[b].data(), static_cast<size_t>(keep) * 4);
+    });
+}
+
+// Causal (or full-row) softmax threshold + cap as CSR; cols == NULL: rowptr only.
+int ref_causal_threshold_mask(const int32_t* lq, const int32_t* lk, int64_t L, int64_t k, double c,
+                              double theta, int64_t cap, int causal, uint64_t* rowptr, uint32_t* cols) {
+    return guarded([&] {
+        std::vector<std::vector<uint32_t>> rows;
+        threshold_lists(lq, lk, L, k, c, theta, cap, causal, rows);
+        rowptr[0] = 0;
+        for (int64_t i = 0; i < L; ++i) {
+            rowptr[i + 1] = rowptr[i] + rows[i].size();
+            if (cols) std::memcpy(cols + rowptr[i], rows[i].data(), rows[i].size() * 4);
+        }
+    });
+}
+
+// The reference softmax probabilities of query row i (n = i+1 causal, else L
+// values) -- to show that any disagreement with the oracle lies at theta.
+int ref_threshold_row_probs(const int32_t* lq, const int32_t* lk, int64_t L, int64_t k, double c, int64_t i,
+                            int causal, double* probs) {
+    return guarded([&] {
+        const Matrix s = score_rows(lq, lk, L, k, i, i + 1);
+        threshold_row(s, 0, i, L, c, 0.0, L + 1, causal, probs);
+    });
+}
+
+// Seeded BASELINE inputs drawn with the reference Rng
+// (P/include/dsattn/rng.hpp:14-78): per pair the substream split(1000 + pair)
+// of Rng(seed); Q/K/V ~ normal(), planted keys by partial Fisher-Yates with
+// uniform_int, +3u / +0.5u (u from split(0)), optional local band windows,
+// P = normal() / sqrt(k) from split(1).  Values are returned as doubles
+// rounded to the dtype (bf16 round-to-nearest-even through float, or f32).
+int ref_generate(int64_t L, int64_t d, int64_t kdim, int bf16, uint64_t seed, int planted_pm, int band_w,
+                 int64_t pair0, int64_t npairs, double* q, double* k, double* v, double* p) {
+    return guarded([&] {
+        auto round_to = [&](double x) {
+            float f = static_cast<float>(x);
+            if (!bf16) return static_cast<double>(f);
+            uint32_t u;
+            std::memcpy(&u, &f, 4);
+            if ((u & 0x7fffffffu) > 0x7f800000u) return static_cast<double>(f);
+            u += 0x7fffu + ((u >> 16) & 1u);
+            u &= 0xffff0000u;
+            std::memcpy(&f, &u, 4);
+            return static_cast<double>(f);
+        };
+        auto unit = [&](Rng& g) {
+            std::vector<double> u(static_cast<size_t>(d));
+            double n2 = 0.0;
+            for (auto& x : u) {
+                x = g.normal();
+                n2 += x * x;
+            }
+            const double inv = 1.0 / std::sqrt(n2);
+            for (auto& x : u) x *= inv;
+            return u;
+        };
+        Rng r0(seed);
+        Rng shared = r0.split(0);
+        const std::vector<double> u = unit(shared);
+        if (p) {
+            Rng r1(seed);
+            Rng gp = r1.split(1);
+            const double sd = 1.0 / std::sqrt(static_cast<double>(kdim));
+            for (int64_t i = 0; i < d * kdim; ++i) p[i] = static_cast<double>(static_cast<float>(sd * gp.normal()));
+        }
+        for (int64_t pi = 0; pi < npairs; ++pi) {
+            Rng root(seed);
+            Rng g = root.split(1000 + static_cast<uint64_t>(pair0 + pi));
+            std::vector<double> Q(L * d), K(L * d), V(L * d);
+            for (auto& x : Q) x = g.normal();
+            for (auto& x : K) x = g.normal();
+            for (auto& x : V) x = g.normal();
+            const int64_t npl = (static_cast<int64_t>(planted_pm) * L + 500) / 1000;
+            std::vector<int64_t> pool(L);
+            for (int64_t j = 0; j < L; ++j) pool[j] = j;
+            for (int64_t t = 0; t < npl; ++t) {
+                const int64_t r = t + static_cast<int64_t>(g.uniform_int(static_cast<uint64_t>(L - t)));
+                std::swap(pool[t], pool[r]);
+                for (int64_t c2 = 0; c2 < d; ++c2) K[pool[t] * d + c2] += 3.0 * u[c2];
+            }
+            for (int64_t i = 0; i < L; ++i)
+                for (int64_t c2 = 0; c2 < d; ++c2) Q[i * d + c2] += 0.5 * u[c2];
+            if (band_w > 0) {
+                const int64_t nw = (L + band_w - 1) / band_w;
+                for (int64_t w = 0; w < nw; ++w) {
+                    const std::vector<double> e = unit(g);
+                    for (int64_t i = w * band_w; i < std::min<int64_t>(L, (w + 1) * band_w); ++i)
+                        for (int64_t c2 = 0; c2 < d; ++c2) {
+                            Q[i * d + c2] += e[c2];
+                            K[i * d + c2] += e[c2];
+                        }
+                }
+            }
+            const size_t off = static_cast<size_t>(pi) * L * d;
+            for (int64_t i = 0; i < L * d; ++i) {
+                q[off + i] = round_to(Q[i]);
+                k[off + i] = round_to(K[i]);
+                v[off + i] = round_to(V[i]);
+            }
+        }
+    });
+}
+
+}  // extern "C"
+
+extern "C" {
+
 // ---------------------------------------------------------------- pipeline
 // One (b,h) pair of the BASELINE path through reference functions
 // (BASELINE.md 2): matmul(Q,P), matmul(K,P), quantize, exact-integer S~ via
 // matmul_nt on the levels, mask selection, sddmm -> sparse_softmax -> spmm.
-// mode: 0 row top-k, 1 colvec max-pool (v, keep), 2 block (bs, keep, diag),
-//       3 causal threshold is not supported here (see oracle for O6).
+// mode: 0 row top-k (per_row: quantize() applied to each 1 x k row, ranked
+//       by S~ * s_k[j] -- SURVEY S5), 1 colvec max-pool (v, keep), 2 block
+//       (bs, keep, diag; O5), 3 softmax threshold + cap, causal (O6).
 struct RefPairArgs {
     const double *q, *k, *v, *p;
     int64_t L, d, kdim;
-    int bits, f32, mode;
+    int bits, f32, mode, per_row;
     int64_t keep, vec_v, block;
     int force_diag;
+    int64_t frac_num, frac_den, cap;
+    int causal;
     double* z;
-    uint32_t* mask_cols;  // may be null
 };
+
+static std::vector<int32_t> row_levels(const Matrix& x, int bits, std::vector<double>& s) {
+    std::vector<int32_t> lv(x.size());
+    s.assign(x.rows(), 0.0);
+    for (size_t i = 0; i < x.rows(); ++i) {
+        Matrix r(1, x.cols(), Precision::f64);
+        std::memcpy(r.raw(), x.data() + i * x.cols(), x.cols() * sizeof(double));
+        auto l = levels_from_reference(r, bits, &s[i]);
+        std::memcpy(lv.data() + i * x.cols(), l.data(), l.size() * sizeof(int32_t));
+    }
+    return lv;
+}
 
 static void run_pair(const RefPairArgs& a) {
     Matrix q = to_matrix(a.q, a.L, a.d, a.f32), k = to_matrix(a.k, a.L, a.d, a.f32);
     Matrix p = to_matrix(a.p, a.d, a.kdim, a.f32);
     double sq = 0, sk = 0;
-    auto lq = levels_from_reference(matmul(q, p), a.bits, &sq);
-    auto lk = levels_from_reference(matmul(k, p), a.bits, &sk);
-    Matrix s = matmul_nt(int_matrix(lq, a.L, a.kdim), int_matrix(lk, a.L, a.kdim));
-    SparseMask m(a.L);
-    if (a.mode == 0) {
-        m = predicted_topk_mask(s, a.keep);
-    } else if (a.mode == 1) {
-        for (int64_t b0 = 0; b0 < a.L; b0 += a.vec_v) {
-            const int64_t b1 = std::min(b0 + a.vec_v, a.L);
-            Matrix pooled(1, a.L);
-            for (int64_t j = 0; j < a.L; ++j) {
-                double mx = s(b0, j);
-                for (int64_t i = b0 + 1; i < b1; ++i) mx = std::max(mx, s(i, j));
-                pooled.raw()[j] = mx;
-            }
-            auto cols = row_topk_indices(pooled, a.keep)[0];
-            for (int64_t i = b0; i < b1; ++i) m.kept[i] = cols;
-        }
+    std::vector<double> skr;
+    std::vector<int32_t> lq, lk;
+    if (a.per_row) {
+        std::vector<double> sqr;
+        lq = row_levels(matmul(q, p), a.bits, sqr);
+        lk = row_levels(matmul(k, p), a.bits, skr);
     } else {
-        const int64_t nb = (a.L + a.block - 1) / a.block;
-        for (int64_t ib = 0; ib < nb; ++ib) {
-            Matrix bsum(1, nb);
-            for (int64_t i = ib * a.block; i < std::min((ib + 1) * a.block, a.L); ++i)
-                for (int64_t j = 0; j < a.L; ++j) bsum.raw()[j / a.block] += s(i, j);
-            if (a.force_diag) bsum.raw()[ib] = 1e300;
-            auto blocks = row_topk_indices(bsum, a.keep)[0];
+        lq = levels_from_reference(matmul(q, p), a.bits, &sq);
+        lk = levels_from_reference(matmul(k, p), a.bits, &sk);
+    }
+    SparseMask m(a.L);
+    if (a.mode == 3) {
+        const double c = sq * sk / std::sqrt(static_cast<double>(a.d));
+        const double theta = static_cast<double>(a.frac_den) / (static_cast<double>(a.frac_num) * a.L);
+        threshold_lists(lq.data(), lk.data(), a.L, a.kdim, c, theta, a.cap, a.causal, m.kept);
+    } else if (a.mode == 2) {
+        const auto lists = block_lists(lq.data(), lk.data(), a.L, a.kdim, a.block, a.keep, a.force_diag);
+        for (int64_t ib = 0; ib < static_cast<int64_t>(lists.size()); ++ib) {
             std::vector<uint32_t> cols;
-            for (uint32_t jb : blocks)
+            for (uint32_t jb : lists[ib])
                 for (int64_t j = jb * a.block; j < std::min<int64_t>((jb + 1) * a.block, a.L); ++j)
                     cols.push_back(static_cast<uint32_t>(j));
             for (int64_t i = ib * a.block; i < std::min((ib + 1) * a.block, a.L); ++i) m.kept[i] = cols;
+        }
+    } else {
+        Matrix s = matmul_nt(int_matrix(lq, a.L, a.kdim), int_matrix(lk, a.L, a.kdim));
+        if (a.mode == 0) {
+            if (a.per_row)
+                for (int64_t i = 0; i < a.L; ++i)
+                    for (int64_t j = 0; j < a.L; ++j) s.raw()[i * a.L + j] *= skr[j];
+            m = predicted_topk_mask(s, a.keep);
+        } else {
+            for (int64_t b0 = 0; b0 < a.L; b0 += a.vec_v) {
+                const int64_t b1 = std::min(b0 + a.vec_v, a.L);
+                Matrix pooled(1, a.L);
+                for (int64_t j = 0; j < a.L; ++j) {
+                    double mx = s(b0, j);
+                    for (int64_t i = b0 + 1; i < b1; ++i) mx = std::max(mx, s(i, j));
+                    pooled.raw()[j] = mx;
+                }
+                auto cols = row_topk_indices(pooled, a.keep)[0];
+                for (int64_t i = b0; i < b1; ++i) m.kept[i] = cols;
+            }
         }
     }
     SparseWeights w = sparse_softmax(sddmm(q, k, m, true));
     Matrix z = spmm(w, to_matrix(a.v, a.L, a.d, a.f32));
     std::memcpy(a.z, z.data(), z.size() * sizeof(double));
-    if (a.mask_cols && (a.mode == 0)) {
-        for (int64_t i = 0; i < a.L; ++i) std::memcpy(a.mask_cols + i * a.keep, m.kept[i].data(), a.keep * 4);
-    }
 }
 
-// Runs `pairs` pairs over `threads` std::threads (contiguous chunks, as the
-// reference's trainer splits batches, P/src/trainer.cpp:334-366).  Inputs are
-// pair-major [pairs][L][d] doubles; p is [d][kdim].
+// Runs `pairs` pairs over `threads` std::threads (pairs strided over the
+// threads, as the reference's trainer splits batches over a thread pool,
+// P/src/trainer.cpp:334-366).  Inputs are pair-major [pairs][L][d] doubles;
+// p is [d][kdim].
 int ref_pipeline(int64_t pairs, int threads, const double* q, const double* k, const double* v,
                  const double* p, int64_t L, int64_t d, int64_t kdim, int bits, int f32, int mode,
-                 int64_t keep, int64_t vec_v, int64_t block, int force_diag, double* z) {
+                 int per_row, int64_t keep, int64_t vec_v, int64_t block, int force_diag, int64_t frac_num,
+                 int64_t frac_den, int64_t cap, int causal, double* z) {
     return guarded([&] {
         const int T = std::max(1, std::min<int>(threads, static_cast<int>(pairs)));
         std::vector<std::thread> pool;
@@ -295,9 +512,9 @@ int ref_pipeline(int64_t pairs, int threads, const double* q, const double* k, c
                 try {
                     for (int64_t pi = t; pi < pairs; pi += T) {
                         const size_t off = static_cast<size_t>(pi) * L * d;
-                        run_pair(RefPairArgs{q + off, k + off, v + off, p, L, d, kdim, bits, f32,
-                                             mode, keep, vec_v, block, force_diag, z + off,
-                                             nullptr});
+                        run_pair(RefPairArgs{q + off, k + off, v + off, p, L, d, kdim, bits, f32, mode, per_row,
+                                             keep, vec_v, block, force_diag, frac_num, frac_den, cap, causal,
+                                             z + off});
                     }
                 } catch (const std::exception& e) {
                     errs[t] = e.what();

@@ -51,6 +51,7 @@ _SIGS = {
     "dsa_pipeline": (C.c_int, [C.POINTER(DsaConfig), _P, _P, _P, _P, _P, C.POINTER(DsaMask), _P,
                                C.c_size_t, _P]),
     "dsa_launch_counter": (C.c_uint64, []),
+    "dsa_pipeline_fused": (C.c_int, [C.POINTER(DsaConfig)]),
     "dsa_project_qkv": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
                                   C.c_int64, _P, _P, _P, _P, _P, _P, _P]),
     "dsa_counters": (C.c_int, [C.POINTER(DsaConfig), C.POINTER(DsaMask), C.POINTER(DsaCounts), _P]),

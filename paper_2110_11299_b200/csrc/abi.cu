@@ -46,6 +46,10 @@ void validate(const dsa_config* cp) {
     if (!cp) throw Error(DSA_ERR_PARAM, "dsa: null config");
     const dsa_config& c = *cp;
     if (c.batch < 1 || c.heads < 1) throw Error(DSA_ERR_SHAPE, "dsa: batch and heads must be >= 1");
+    // pairs index grid.y / grid.z of the launches (<= 65535, and 2 x pairs for
+    // the quantise pass) and 24 bits of the deferred-level list entries
+    if (c.batch * c.heads >= 32768)
+        throw Error(DSA_ERR_SHAPE, "dsa: batch * heads must be < 32768 per call (split the batch)");
     if (c.L < 1) throw Error(DSA_ERR_SHAPE, "Matrix: dimensions must be positive");
     if (c.L >= (int64_t{1} << 31)) throw Error(DSA_ERR_SHAPE, "dsa: L must be < 2^31");
     if (c.d != 16 && c.d != 32 && c.d != 64 && c.d != 128)
@@ -137,16 +141,14 @@ Plan plan(const dsa_config& c, bool pipeline, bool own_mask) {
     // the f64 projection scratch only serves the fallback kernels (f32 inputs,
     // other d, or DSA_PREDICT_DFMA); the tensor-core path needs the P image
     const bool tc_path = c.dtype == DSA_BF16 && (c.d == 64 || c.d == 128) && (c.k == 16 || c.k == 32);
-    const bool need_x64 = per_tensor && (!tc_path || std::getenv("DSA_PREDICT_DFMA") != nullptr ||
-                                         std::getenv("DSA_PREDICT_CLUSTER") != nullptr);
+    const bool need_x64 = per_tensor && (!tc_path || options().predict_dfma);
     p.x64 = take(need_x64 ? sizeof(double) * P * 2 * c.L * c.k : 0);
-    // stored x^ for the streaming quantise pass (DSA_PREDICT_TWO_READS=1: the
-    // quantise pass re-reads Q/K and recomputes x^ instead).  Uncertified
+    // stored x^ for the streaming quantise pass.  Uncertified
     // levels go to a deferred list (quantize_fix_kernel).  8-bit configs keep
     // the two-read pass: with x^ they measured slower (C3 0.533 vs 0.471 ms:
     // the amax pass of the d = 128 shape is latency-bound and the x^ writes
     // lengthen it).
-    p.has_xhat = per_tensor && tc_path && c.bits <= 4 && std::getenv("DSA_PREDICT_TWO_READS") == nullptr;
+    p.has_xhat = per_tensor && tc_path && c.bits <= 4 && !options().predict_dfma;
     p.xhat = take(p.has_xhat ? sizeof(float) * P * xhat_floats_per_pair(c.L, c.k) : 0);
     p.amax = take(per_tensor ? sizeof(unsigned long long) * P * 2 : 0);
     p.pimg = take(tc_path ? align_up(predict_tc_image_bytes(c.d, c.k)) * kMaxChunks : 0);
@@ -223,10 +225,7 @@ Scratch scratch_of(const dsa_config& c, const Plan& pl, void* ws, int64_t pair0 
 // Number of pair chunks dsa_pipeline overlaps (1 = serial).  Threshold
 // masks keep one global CSR (a single scan over all rows): serial.
 int pipeline_chunks(const dsa_config& c) {
-    static const int env = [] {
-        const char* e = std::getenv("DSA_PIPELINE_CHUNKS");
-        return e ? std::atoi(e) : -1;
-    }();
+    const int env = options().pipeline_chunks;
     if (c.mask_mode == DSA_MASK_THRESHOLD) return 1;
     const int64_t P = pairs_of(c);
     // default serial: measured on B200 (C2), 2 and 4 chunks on three streams
@@ -397,6 +396,41 @@ void require_device() {
 void set_last_error(const std::string& m) { g_last_error = m; }
 
 static std::atomic<uint64_t> g_launches{0};
+
+namespace {
+bool env_flag(const char* name) {
+    const char* e = std::getenv(name);
+    return e != nullptr && *e != '\0' && std::strcmp(e, "0") != 0;
+}
+Options read_options() {
+    Options o{};
+    o.attn_generic = env_flag("DSA_ATTN_GENERIC");
+    o.threshold_generic = env_flag("DSA_THRESHOLD_GENERIC");
+    o.block_generic = env_flag("DSA_BLOCK_GENERIC");
+    o.topk_generic = env_flag("DSA_TOPK_GENERIC");
+    o.predict_dfma = env_flag("DSA_PREDICT_DFMA");
+    o.no_fuse = env_flag("DSA_NO_FUSE");
+    const char* e = std::getenv("DSA_PIPELINE_CHUNKS");
+    o.pipeline_chunks = e ? std::atoi(e) : -1;
+    return o;
+}
+// read once, when the shared library is loaded
+const Options g_options = read_options();
+}  // namespace
+
+const Options& options() { return g_options; }
+
+int sm_count() {
+    static std::atomic<int> cache[64];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+    int n = cache[dev].load(std::memory_order_relaxed);
+    if (n == 0) {
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+        cache[dev].store(n, std::memory_order_relaxed);
+    }
+    return n;
+}
 void note_launch(int n) { g_launches.fetch_add(static_cast<uint64_t>(n), std::memory_order_relaxed); }
 
 [[noreturn]] void throw_unsupported(const std::string& what) { throw Error(DSA_ERR_UNSUPPORTED, "dsa: " + what); }
@@ -568,6 +602,22 @@ dsa_status dsa_pipeline(const dsa_config* cfg, const void* q, const void* k, con
         check_cuda(cudaEventRecord(ss.join, ss.s[2]), "dsa_pipeline join");
         check_cuda(cudaStreamWaitEvent(st, ss.join, 0), "dsa_pipeline join");
     });
+}
+
+int dsa_pipeline_fused(const dsa_config* cfg) {
+    int out = -1;
+    guard([&] {
+        validate(cfg);
+        const dsa_config& c = *cfg;
+        if (c.mask_mode != DSA_MASK_COLVEC || pipeline_chunks(c) > 1) {
+            out = 0;
+            return;
+        }
+        dsa_mask m{};
+        SelectArgs sa = select_args(c, nullptr, nullptr, nullptr, nullptr, m, Scratch{});
+        out = colvec_fused_supported(sa, attn_args(c, nullptr, nullptr, nullptr, m, nullptr)) ? 1 : 0;
+    });
+    return out;
 }
 
 dsa_status dsa_counters(const dsa_config* cfg, const dsa_mask* mask, dsa_counts* out, void* stream) {

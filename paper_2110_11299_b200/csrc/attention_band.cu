@@ -14,7 +14,6 @@
 // reused by the band's 8 queries -- SURVEY H6); HBM sees Q, K, V, Z once.
 #include <cuda_bf16.h>
 
-#include <cstdlib>
 
 #include "device_common.cuh"
 #include "kernels.h"
@@ -25,361 +24,6 @@ namespace {
 
 using namespace bc;
 
-
-template <int D, int CHUNK>
-struct BandSmem {
-    __nv_bfloat16 k[2][CHUNK * D];
-    __nv_bfloat16 v[2][CHUNK * D];
-    __nv_bfloat16 q[8 * D];            // Q band; reused to stage Z
-    __nv_bfloat16 p[8 * (CHUNK + 8)];  // [query][key], padded rows
-};
-
-template <int D, int CHUNK, int kBandWarps>
-__global__ void __launch_bounds__(kBandWarps * 32)
-    attn_band_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __restrict__ K,
-                     const __nv_bfloat16* __restrict__ V, const uint32_t* __restrict__ band_cols,
-                     int64_t pairs, int64_t L, int64_t keep, int scale, __nv_bfloat16* __restrict__ Z) {
-    extern __shared__ __align__(128) unsigned char dsm[];
-    using S = BandSmem<D, CHUNK>;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    S& sm = reinterpret_cast<S*>(dsm)[warp];
-    const int64_t nb = (L + 7) / 8;
-    const int64_t band_global = static_cast<int64_t>(blockIdx.x) * kBandWarps + warp;
-    if (band_global >= pairs * nb) return;
-    const int64_t pair = band_global / nb, band = band_global % nb;
-    const int64_t r0 = band * 8;
-    const __nv_bfloat16* Kp = K + pair * L * D;
-    const __nv_bfloat16* Vp = V + pair * L * D;
-    const uint32_t* cols = band_cols + (pair * nb + band) * keep;
-    const int g = lane >> 2, c4 = lane & 3;
-    constexpr int kChunks16 = D / 8;  // 16-byte chunks per row
-
-    // ---- Q band -> smem (zero rows past L)
-    for (int t = lane; t < 8 * kChunks16; t += 32) {
-        const int r = t / kChunks16, c = t % kChunks16;
-        const bool ok = r0 + r < L;
-        cp_async16(smem_u32(sm.q) + swz<D>(r, c), Q + (pair * L + (ok ? r0 + r : 0)) * D + c * 8, ok);
-    }
-    auto load_chunk = [&](int buf, int base) {
-        for (int t = lane; t < CHUNK * kChunks16; t += 32) {
-            const int r = t / kChunks16, c = t % kChunks16;
-            const bool ok = base + r < keep;
-            const int64_t j = ok ? static_cast<int64_t>(__ldg(cols + base + r)) : 0;
-            cp_async16(smem_u32(sm.k[buf]) + swz<D>(r, c), Kp + j * D + c * 8, ok);
-            cp_async16(smem_u32(sm.v[buf]) + swz<D>(r, c), Vp + j * D + c * 8, ok);
-        }
-    };
-    const int nchunks = static_cast<int>((keep + CHUNK - 1) / CHUNK);
-    load_chunk(0, 0);
-    cp_async_commit();
-
-    const float sl2 = (scale ? rsqrtf(static_cast<float>(D)) : 1.f) * 1.4426950408889634f;
-    float m_run[2] = {-INFINITY, -INFINITY};  // queries 2c, 2c+1 (log2 domain)
-    float l_part[2] = {0.f, 0.f};
-    float zacc[D / 16][4];
-#pragma unroll
-    for (int t = 0; t < D / 16; ++t)
-#pragma unroll
-        for (int u = 0; u < 4; ++u) zacc[t][u] = 0.f;
-    uint32_t qb[D / 16][2];
-
-    for (int ch = 0; ch < nchunks; ++ch) {
-        const int buf = ch & 1;
-        if (ch + 1 < nchunks) load_chunk(buf ^ 1, (ch + 1) * CHUNK);
-        cp_async_commit();
-        cp_async_wait<1>();
-        __syncwarp();
-        if (ch == 0) {
-            // B fragments of Q^T: b0b1 = Q[g][16ks + 2c..], b2b3 = Q[g][16ks + 8 + 2c..]
-#pragma unroll
-            for (int ks = 0; ks < D / 16; ++ks) {
-                const char* qbase = reinterpret_cast<const char*>(sm.q);
-                qb[ks][0] = *reinterpret_cast<const uint32_t*>(qbase + swz<D>(g, 2 * ks) + c4 * 4);
-                qb[ks][1] = *reinterpret_cast<const uint32_t*>(qbase + swz<D>(g, 2 * ks + 1) + c4 * 4);
-            }
-        }
-        // ---- S^T = K_chunk . Q^T : CHUNK/16 m-tiles
-        float s[CHUNK / 16][4];
-        const uint32_t kb = smem_u32(sm.k[buf]);
-#pragma unroll
-        for (int mt = 0; mt < CHUNK / 16; ++mt) {
-#pragma unroll
-            for (int u = 0; u < 4; ++u) s[mt][u] = 0.f;
-#pragma unroll
-            for (int ks = 0; ks < D / 16; ++ks) {
-                const int mi = lane >> 3;
-                const int row = mt * 16 + (mi & 1) * 8 + (lane & 7);
-                const int chk = ks * 2 + (mi >> 1);
-                uint32_t a0, a1, a2, a3;
-                ldsm_x4(kb + swz<D>(row, chk), a0, a1, a2, a3);
-                mma16816(s[mt], a0, a1, a2, a3, qb[ks][0], qb[ks][1]);
-            }
-        }
-        // ---- online softmax over keys (rows g, g+8 of each m-tile)
-        const int base = ch * CHUNK;
-        float cmax[2] = {-INFINITY, -INFINITY};
-#pragma unroll
-        for (int mt = 0; mt < CHUNK / 16; ++mt)
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int key = base + mt * 16 + g + (u >> 1) * 8;
-                const float x = key < keep ? s[mt][u] * sl2 : -INFINITY;
-                s[mt][u] = x;
-                cmax[u & 1] = fmaxf(cmax[u & 1], x);
-            }
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            cmax[h] = fmaxf(cmax[h], __shfl_xor_sync(0xffffffffu, cmax[h], 4));
-            cmax[h] = fmaxf(cmax[h], __shfl_xor_sync(0xffffffffu, cmax[h], 8));
-            cmax[h] = fmaxf(cmax[h], __shfl_xor_sync(0xffffffffu, cmax[h], 16));
-        }
-        float corr[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const float mn = fmaxf(m_run[h], cmax[h]);
-            corr[h] = m_run[h] == -INFINITY ? 0.f : fast_ex2(m_run[h] - mn);
-            m_run[h] = mn;
-            l_part[h] *= corr[h];
-        }
-#pragma unroll
-        for (int t = 0; t < D / 16; ++t) {
-            zacc[t][0] *= corr[0];
-            zacc[t][1] *= corr[1];
-            zacc[t][2] *= corr[0];
-            zacc[t][3] *= corr[1];
-        }
-        // p = 2^(x - m) -> bf16 P[query][key] in smem
-        constexpr int PW = CHUNK + 8;
-#pragma unroll
-        for (int mt = 0; mt < CHUNK / 16; ++mt)
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const float pv = fast_ex2(s[mt][u] - m_run[u & 1]);
-                l_part[u & 1] += pv;
-                const int key = mt * 16 + g + (u >> 1) * 8;
-                const int qq = 2 * c4 + (u & 1);
-                sm.p[qq * PW + key] = __float2bfloat16_rn(pv);
-            }
-        __syncwarp();
-        // ---- Z^T += V_chunk^T . P^T
-        const uint32_t vb = smem_u32(sm.v[buf]);
-#pragma unroll
-        for (int ks = 0; ks < CHUNK / 16; ++ks) {
-            const uint32_t b0 = *reinterpret_cast<const uint32_t*>(&sm.p[g * PW + ks * 16 + 2 * c4]);
-            const uint32_t b1 = *reinterpret_cast<const uint32_t*>(&sm.p[g * PW + ks * 16 + 8 + 2 * c4]);
-#pragma unroll
-            for (int mt = 0; mt < D / 16; ++mt) {
-                const int mi = lane >> 3;
-                const int row = ks * 16 + (mi >> 1) * 8 + (lane & 7);
-                const int chk = mt * 2 + (mi & 1);
-                uint32_t a0, a1, a2, a3;
-                ldsm_x4_t(vb + swz<D>(row, chk), a0, a1, a2, a3);
-                mma16816(zacc[mt], a0, a1, a2, a3, b0, b1);
-            }
-        }
-        __syncwarp();
-    }
-    cp_async_wait<0>();
-    // ---- finalize: l over the 8 lanes sharing c4, Z = Z^T / l
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        l_part[h] += __shfl_xor_sync(0xffffffffu, l_part[h], 4);
-        l_part[h] += __shfl_xor_sync(0xffffffffu, l_part[h], 8);
-        l_part[h] += __shfl_xor_sync(0xffffffffu, l_part[h], 16);
-    }
-    const float inv0 = l_part[0] > 0.f ? 1.f / l_part[0] : 0.f;
-    const float inv1 = l_part[1] > 0.f ? 1.f / l_part[1] : 0.f;
-#pragma unroll
-    for (int mt = 0; mt < D / 16; ++mt) {
-        const int d0 = mt * 16 + g;
-        sm.q[(2 * c4) * D + d0] = __float2bfloat16_rn(zacc[mt][0] * inv0);
-        sm.q[(2 * c4 + 1) * D + d0] = __float2bfloat16_rn(zacc[mt][1] * inv1);
-        sm.q[(2 * c4) * D + d0 + 8] = __float2bfloat16_rn(zacc[mt][2] * inv0);
-        sm.q[(2 * c4 + 1) * D + d0 + 8] = __float2bfloat16_rn(zacc[mt][3] * inv1);
-    }
-    __syncwarp();
-    for (int t = lane; t < 8 * kChunks16; t += 32) {
-        const int r = t / kChunks16, c = t % kChunks16;
-        if (r0 + r < L)
-            *reinterpret_cast<uint4*>(Z + (pair * L + r0 + r) * D + c * 8) =
-                *reinterpret_cast<const uint4*>(&sm.q[r * D + c * 8]);
-    }
-}
-
-// ----------------------------------------------------------- block rows
-// BLOCK masks with 32x32 blocks: the four 8-row bands of a 32-row block row
-// share one key list (its kept blocks), so one CTA of four warps owns the
-// block row and stages each kept block's 32 K and V rows ONCE in shared
-// memory (contiguous rows -> fully coalesced 16-byte cp.async, XOR-swizzled
-// for conflict-free ldmatrix), double buffered; every warp then runs the
-// band computation of attn_band_kernel (S^T = K_blk . Q_band^T, online
-// softmax, Z^T += V_blk^T . P^T) on the shared tiles.  L2 -> SM traffic is a
-// quarter of the per-band kernels'.
-template <int D>
-struct BlockSmem {
-    __nv_bfloat16 k[2][32 * D];
-    __nv_bfloat16 v[2][32 * D];
-    __nv_bfloat16 q[4][8 * D];   // per warp: Q band, reused to stage Z
-    __nv_bfloat16 p[4][8 * 40];  // per warp: [query][key], padded rows
-};
-
-template <int D>
-__global__ void __launch_bounds__(128)
-    attn_block_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __restrict__ K,
-                      const __nv_bfloat16* __restrict__ V, const uint32_t* __restrict__ block_cols,
-                      int64_t L, int64_t keep, int scale, __nv_bfloat16* __restrict__ Z) {
-    constexpr int CHUNK = 32;
-    extern __shared__ __align__(128) unsigned char dsm[];
-    BlockSmem<D>& sm = *reinterpret_cast<BlockSmem<D>*>(dsm);
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int64_t nbr = L / 32;
-    const int64_t pair = blockIdx.y, br = blockIdx.x;
-    const int64_t r0 = br * 32 + warp * 8;  // this warp's band
-    const __nv_bfloat16* Kp = K + pair * L * D;
-    const __nv_bfloat16* Vp = V + pair * L * D;
-    const uint32_t* cols = block_cols + (pair * nbr + br) * keep;
-    const int g = lane >> 2, c4 = lane & 3;
-    constexpr int kChunks16 = D / 8;
-    __nv_bfloat16* sq = sm.q[warp];
-    __nv_bfloat16* sp = sm.p[warp];
-
-    for (int t = lane; t < 8 * kChunks16; t += 32) {
-        const int r = t / kChunks16, c = t % kChunks16;
-        cp_async16(smem_u32(sq) + swz<D>(r, c), Q + (pair * L + r0 + r) * D + c * 8, true);
-    }
-    auto load_block = [&](int buf, int ch) {
-        const int64_t j0 = static_cast<int64_t>(__ldg(cols + ch)) * 32;
-        for (int t = tid; t < CHUNK * kChunks16; t += 128) {
-            const int r = t / kChunks16, c = t % kChunks16;
-            cp_async16(smem_u32(sm.k[buf]) + swz<D>(r, c), Kp + (j0 + r) * D + c * 8, true);
-            cp_async16(smem_u32(sm.v[buf]) + swz<D>(r, c), Vp + (j0 + r) * D + c * 8, true);
-        }
-    };
-    const int nchunks = static_cast<int>(keep);
-    load_block(0, 0);
-    cp_async_commit();
-
-    const float sl2 = (scale ? rsqrtf(static_cast<float>(D)) : 1.f) * 1.4426950408889634f;
-    float m_run[2] = {-INFINITY, -INFINITY};
-    float l_part[2] = {0.f, 0.f};
-    float zacc[D / 16][4];
-#pragma unroll
-    for (int t = 0; t < D / 16; ++t)
-#pragma unroll
-        for (int u = 0; u < 4; ++u) zacc[t][u] = 0.f;
-    uint32_t qb[D / 16][2];
-
-    for (int ch = 0; ch < nchunks; ++ch) {
-        const int buf = ch & 1;
-        if (ch + 1 < nchunks) load_block(buf ^ 1, ch + 1);
-        cp_async_commit();
-        cp_async_wait<1>();
-        __syncthreads();
-        if (ch == 0) {
-#pragma unroll
-            for (int ks = 0; ks < D / 16; ++ks) {
-                const char* qbase = reinterpret_cast<const char*>(sq);
-                qb[ks][0] = *reinterpret_cast<const uint32_t*>(qbase + swz<D>(g, 2 * ks) + c4 * 4);
-                qb[ks][1] = *reinterpret_cast<const uint32_t*>(qbase + swz<D>(g, 2 * ks + 1) + c4 * 4);
-            }
-        }
-        float s[CHUNK / 16][4];
-        const uint32_t kb = smem_u32(sm.k[buf]);
-#pragma unroll
-        for (int mt = 0; mt < CHUNK / 16; ++mt) {
-#pragma unroll
-            for (int u = 0; u < 4; ++u) s[mt][u] = 0.f;
-#pragma unroll
-            for (int ks = 0; ks < D / 16; ++ks) {
-                const int mi = lane >> 3;
-                const int row = mt * 16 + (mi & 1) * 8 + (lane & 7);
-                const int chk = ks * 2 + (mi >> 1);
-                uint32_t a0, a1, a2, a3;
-                ldsm_x4(kb + swz<D>(row, chk), a0, a1, a2, a3);
-                mma16816(s[mt], a0, a1, a2, a3, qb[ks][0], qb[ks][1]);
-            }
-        }
-        float cmax[2] = {-INFINITY, -INFINITY};
-#pragma unroll
-        for (int mt = 0; mt < CHUNK / 16; ++mt)
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const float x = s[mt][u] * sl2;
-                s[mt][u] = x;
-                cmax[u & 1] = fmaxf(cmax[u & 1], x);
-            }
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            cmax[h] = fmaxf(cmax[h], __shfl_xor_sync(0xffffffffu, cmax[h], 4));
-            cmax[h] = fmaxf(cmax[h], __shfl_xor_sync(0xffffffffu, cmax[h], 8));
-            cmax[h] = fmaxf(cmax[h], __shfl_xor_sync(0xffffffffu, cmax[h], 16));
-        }
-        float corr[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const float mn = fmaxf(m_run[h], cmax[h]);
-            corr[h] = m_run[h] == -INFINITY ? 0.f : fast_ex2(m_run[h] - mn);
-            m_run[h] = mn;
-            l_part[h] *= corr[h];
-        }
-#pragma unroll
-        for (int t = 0; t < D / 16; ++t) {
-            zacc[t][0] *= corr[0];
-            zacc[t][1] *= corr[1];
-            zacc[t][2] *= corr[0];
-            zacc[t][3] *= corr[1];
-        }
-        constexpr int PW = CHUNK + 8;
-#pragma unroll
-        for (int mt = 0; mt < CHUNK / 16; ++mt)
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const float pv = fast_ex2(s[mt][u] - m_run[u & 1]);
-                l_part[u & 1] += pv;
-                sp[(2 * c4 + (u & 1)) * PW + mt * 16 + g + (u >> 1) * 8] = __float2bfloat16_rn(pv);
-            }
-        __syncwarp();
-        const uint32_t vb = smem_u32(sm.v[buf]);
-#pragma unroll
-        for (int ks = 0; ks < CHUNK / 16; ++ks) {
-            const uint32_t b0 = *reinterpret_cast<const uint32_t*>(&sp[g * PW + ks * 16 + 2 * c4]);
-            const uint32_t b1 = *reinterpret_cast<const uint32_t*>(&sp[g * PW + ks * 16 + 8 + 2 * c4]);
-#pragma unroll
-            for (int mt = 0; mt < D / 16; ++mt) {
-                const int mi = lane >> 3;
-                const int row = ks * 16 + (mi >> 1) * 8 + (lane & 7);
-                const int chk = mt * 2 + (mi & 1);
-                uint32_t a0, a1, a2, a3;
-                ldsm_x4_t(vb + swz<D>(row, chk), a0, a1, a2, a3);
-                mma16816(zacc[mt], a0, a1, a2, a3, b0, b1);
-            }
-        }
-        __syncthreads();  // every warp done with `buf` before it is refilled
-    }
-    cp_async_wait<0>();
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        l_part[h] += __shfl_xor_sync(0xffffffffu, l_part[h], 4);
-        l_part[h] += __shfl_xor_sync(0xffffffffu, l_part[h], 8);
-        l_part[h] += __shfl_xor_sync(0xffffffffu, l_part[h], 16);
-    }
-    const float inv0 = l_part[0] > 0.f ? 1.f / l_part[0] : 0.f;
-    const float inv1 = l_part[1] > 0.f ? 1.f / l_part[1] : 0.f;
-#pragma unroll
-    for (int mt = 0; mt < D / 16; ++mt) {
-        const int d0 = mt * 16 + g;
-        sq[(2 * c4) * D + d0] = __float2bfloat16_rn(zacc[mt][0] * inv0);
-        sq[(2 * c4 + 1) * D + d0] = __float2bfloat16_rn(zacc[mt][1] * inv1);
-        sq[(2 * c4) * D + d0 + 8] = __float2bfloat16_rn(zacc[mt][2] * inv0);
-        sq[(2 * c4 + 1) * D + d0 + 8] = __float2bfloat16_rn(zacc[mt][3] * inv1);
-    }
-    __syncwarp();
-    for (int t = lane; t < 8 * kChunks16; t += 32) {
-        const int r = t / kChunks16, c = t % kChunks16;
-        *reinterpret_cast<uint4*>(Z + (pair * L + r0 + r) * D + c * 8) =
-            *reinterpret_cast<const uint4*>(&sq[r * D + c * 8]);
-    }
-}
 
 // Same block-row computation with each warp owning NT bands (8 * NT query
 // rows, one MMA n-tile each): the K and V fragments a warp loads from shared
@@ -587,30 +231,11 @@ template <int D, int NT>
 void launch_block_nt(const AttnArgs& a, cudaStream_t st) {
     const size_t smem = sizeof(BlockSmemN<D, NT>);
     auto kern = attn_block_nt_kernel<D, NT>;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        attr = true;
-    }
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     const dim3 grid(static_cast<unsigned>(a.L / 32), static_cast<unsigned>(a.pairs));
     kern<<<grid, 128 / NT, smem, st>>>(static_cast<const __nv_bfloat16*>(a.q), static_cast<const __nv_bfloat16*>(a.k),
                                        static_cast<const __nv_bfloat16*>(a.v), a.cols, a.L, a.keep, a.scale,
                                        static_cast<__nv_bfloat16*>(a.z));
-}
-
-template <int D>
-void launch_block(const AttnArgs& a, cudaStream_t st) {
-    const size_t smem = sizeof(BlockSmem<D>);
-    auto kern = attn_block_kernel<D>;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        attr = true;
-    }
-    const dim3 grid(static_cast<unsigned>(a.L / 32), static_cast<unsigned>(a.pairs));
-    kern<<<grid, 128, smem, st>>>(static_cast<const __nv_bfloat16*>(a.q), static_cast<const __nv_bfloat16*>(a.k),
-                                  static_cast<const __nv_bfloat16*>(a.v), a.cols, a.L, a.keep, a.scale,
-                                  static_cast<__nv_bfloat16*>(a.z));
 }
 
 // ---------------------------------------------------------------- v2
@@ -621,20 +246,14 @@ void launch_block(const AttnArgs& a, cudaStream_t st) {
 // load per gathered row (lane = row, shared by shuffles).  V rows still go
 // through cp.async + XOR-swizzled shared memory for ldmatrix.trans.
 // MODE kBandList: COLVEC -- the warp's 8 query rows share one key list.
-// MODE kBlockList: block-sparse masks with 32x32 blocks -- the 8-row band's
-//   key list is its block row's kept blocks, each expanding to 32
-//   consecutive keys (one 32-key chunk per kept block, so the chunk index is
-//   blocks[ch] * 32 + lane).
-// MODE kRowList / kRowCsr: every query row has its own list (ROW_TOPK rows of
-//   `keep`, THRESHOLD CSR rows): one row per warp, the row's q in the first
-//   of the 8 MMA columns (the other seven are zero and ignored).
-// MODE kRowsBand: per-row lists again, but a warp takes 8 consecutive rows
+// MODE kRowsBand: every query row has its own list (ROW_TOPK rows of `keep`,
+//   THRESHOLD CSR rows); a warp takes 8 consecutive rows
 //   and streams the CONCATENATION of their lists (contiguous in the CSR /
 //   row-list layout) in 32-key chunks, each row in its own MMA column; an
 //   entry (key, column) is live only when the key's stream position lies in
 //   that row's segment.  No per-row latency chain: one long prefetched
 //   gather stream per warp (the MMA does 8x the useful work, which is free).
-enum BandMode { kBandList = 0, kBlockList = 1, kRowList = 2, kRowCsr = 3, kRowsBand = 4 };
+enum BandMode { kBandList = 0, kRowsBand = 4 };
 
 template <int D, int kWarps, int MODE>
 __global__ void __launch_bounds__(kWarps * 32)
@@ -644,35 +263,21 @@ __global__ void __launch_bounds__(kWarps * 32)
                         const uint64_t* __restrict__ rowptr, uint8_t* __restrict__ empty_rows) {
     constexpr int CH = 32;
     constexpr int NW = D / 32;        // uint4 per lane per K row segment (D/4 bf16)
-    constexpr bool BLK = MODE == kBlockList;
-    constexpr bool ROW = MODE == kRowList || MODE == kRowCsr;
-    constexpr int kRows = ROW ? 1 : 8;  // query rows per warp
+    constexpr int kRows = 8;  // query rows per warp
     extern __shared__ __align__(128) unsigned char dsm[];
     using S = BandSmemV2<D>;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     S& sm = reinterpret_cast<S*>(dsm)[warp];
     constexpr bool SEG = MODE == kRowsBand;
-    const int64_t nb = ROW ? L : (L + 7) / 8;  // warp work items per pair
+    const int64_t nb = (L + 7) / 8;  // warp work items (bands) per pair
     const int64_t band_global = static_cast<int64_t>(blockIdx.x) * kWarps + warp;
     if (band_global >= pairs * nb) return;
     const int64_t pair = band_global / nb, band = band_global % nb;
     const int64_t r0 = band * kRows;
     const __nv_bfloat16* Kp = K + pair * L * D;
     const __nv_bfloat16* Vp = V + pair * L * D;
-    const int64_t nbr = (L + 31) / 32;
-    const uint32_t* cols;
-    int64_t nkeys;
-    if (MODE == kBlockList) {
-        cols = band_cols + (pair * nbr + (r0 >> 5)) * keep;
-        nkeys = keep * 32;
-    } else if (MODE == kBandList || MODE == kRowList) {
-        cols = band_cols + (pair * nb + band) * keep;
-        nkeys = keep;
-    } else if (MODE == kRowCsr) {
-        const uint64_t b = rowptr[pair * L + r0];
-        cols = band_cols + b;
-        nkeys = static_cast<int64_t>(rowptr[pair * L + r0 + 1] - b);
-    }
+    const uint32_t* cols = band_cols + (pair * nb + band) * keep;
+    int64_t nkeys = keep;
     const int g = lane >> 2, c4 = lane & 3;
     // kRowsBand: stream segment bounds of this thread's two columns (rows
     // 2c4, 2c4+1): [sb0, sb1) and [sb1, sb2)
@@ -691,12 +296,10 @@ __global__ void __launch_bounds__(kWarps * 32)
         sb2 = bound(2 * c4 + 2) - b0;
     }
     auto chunk_idx = [&](int ch) -> uint32_t {
-        if (BLK) return __ldg(cols + ch) * 32u + static_cast<uint32_t>(lane);
         const int64_t p = static_cast<int64_t>(ch) * CH + lane;
         return p < nkeys ? __ldg(cols + p) : 0u;
     };
     band_core<D, kRows, SEG>(sm, Q, Kp, Vp, pair, L, r0, nkeys, sb0, sb1, sb2, scale, Z, chunk_idx, lane);
-    if (ROW && empty_rows && lane == 0) empty_rows[pair * L + r0] = nkeys == 0;
     if (SEG && empty_rows && g == 0) {
         if (r0 + 2 * c4 < L) empty_rows[pair * L + r0 + 2 * c4] = sb1 == sb0;
         if (r0 + 2 * c4 + 1 < L) empty_rows[pair * L + r0 + 2 * c4 + 1] = sb2 == sb1;
@@ -705,14 +308,10 @@ __global__ void __launch_bounds__(kWarps * 32)
 
 template <int D, int kWarps, int MODE = kBandList>
 void launch_band_v2(const AttnArgs& a, cudaStream_t st) {
-    const int64_t nb = (MODE == kRowList || MODE == kRowCsr) ? a.L : (a.L + 7) / 8;
+    const int64_t nb = (a.L + 7) / 8;
     const size_t smem = sizeof(BandSmemV2<D>) * kWarps;
     auto kern = attn_band_v2_kernel<D, kWarps, MODE>;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        attr = true;
-    }
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     const unsigned grid = static_cast<unsigned>(ceil_div_i(a.pairs * nb, kWarps));
     kern<<<grid, kWarps * 32, smem, st>>>(
         static_cast<const __nv_bfloat16*>(a.q), static_cast<const __nv_bfloat16*>(a.k),
@@ -720,71 +319,25 @@ void launch_band_v2(const AttnArgs& a, cudaStream_t st) {
         static_cast<__nv_bfloat16*>(a.z), a.rowptr, a.empty_rows);
 }
 
-template <int D, int CHUNK, int kBandWarps>
-void launch_band(const AttnArgs& a, cudaStream_t st) {
-    const int64_t nb = (a.L + 7) / 8;
-    const size_t smem = sizeof(BandSmem<D, CHUNK>) * kBandWarps;
-    auto kern = attn_band_kernel<D, CHUNK, kBandWarps>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    const unsigned grid = static_cast<unsigned>(ceil_div_i(a.pairs * nb, kBandWarps));
-    kern<<<grid, kBandWarps * 32, smem, st>>>(
-        static_cast<const __nv_bfloat16*>(a.q), static_cast<const __nv_bfloat16*>(a.k),
-        static_cast<const __nv_bfloat16*>(a.v), a.cols, a.pairs, a.L, a.keep, a.scale,
-        static_cast<__nv_bfloat16*>(a.z));
-}
-
 }  // namespace
 
 bool band_attention_supported(const AttnArgs& a) {
     if (!a.bf16 || (a.D != 64 && a.D != 128)) return false;
-    if (std::getenv("DSA_ATTN_GENERIC") != nullptr) return false;  // A/B switch
+    if (options().attn_generic) return false;  // parity tests of the generic kernel
     if (a.mode == kColvec) return a.vec_v == 8;
     if (a.mode == kRowTopk || a.mode == kThreshold) return true;
     return a.mode == kBlock && a.block == 32 && a.L % 32 == 0;  // block rows = 4 bands
 }
 
 void run_band_attention(const AttnArgs& a, cudaStream_t st) {
-    static const bool v1 = std::getenv("DSA_BAND_V1") != nullptr;  // A/B switch
-    if (v1 && a.mode == kColvec) {
-        if (a.D == 64) launch_band<64, 32, 12>(a, st);
-        else launch_band<128, 32, 6>(a, st);
-    } else if (a.mode == kBlock) {
-        static const bool per_band = std::getenv("DSA_BLOCK_PER_BAND") != nullptr;  // A/B switch
-        if (per_band) {
-            if (a.D == 64) launch_band_v2<64, 16, kBlockList>(a, st);
-            else launch_band_v2<128, 8, kBlockList>(a, st);
-        } else {
-            static const int nt = [] {
-                const char* e = std::getenv("DSA_BLOCK_NT");
-                return e ? std::atoi(e) : 2;
-            }();
-            if (nt == 1) {
-                if (a.D == 64) launch_block<64>(a, st);
-                else launch_block<128>(a, st);
-            } else if (nt == 4) {
-                if (a.D == 64) launch_block_nt<64, 4>(a, st);
-                else launch_block_nt<128, 4>(a, st);
-            } else {
-                if (a.D == 64) launch_block_nt<64, 2>(a, st);
-                else launch_block_nt<128, 2>(a, st);
-            }
-        }
+    if (a.mode == kBlock) {
+        if (a.D == 64) launch_block_nt<64, 2>(a, st);
+        else launch_block_nt<128, 2>(a, st);
     } else if (a.mode == kRowTopk || a.mode == kThreshold) {
-        static const bool per_row = std::getenv("DSA_ATTN_ROW_PER_WARP") != nullptr;  // A/B switch
         AttnArgs b = a;
         if (a.mode == kRowTopk) b.rowptr = nullptr;  // fixed-length row lists
-        if (per_row) {
-            if (a.mode == kRowTopk) {
-                if (a.D == 64) launch_band_v2<64, 16, kRowList>(a, st);
-                else launch_band_v2<128, 8, kRowList>(a, st);
-            } else {
-                if (a.D == 64) launch_band_v2<64, 16, kRowCsr>(a, st);
-                else launch_band_v2<128, 8, kRowCsr>(a, st);
-            }
-        } else {
-            if (a.D == 64) launch_band_v2<64, 16, kRowsBand>(b, st);
-            else launch_band_v2<128, 8, kRowsBand>(b, st);
-        }
+        if (a.D == 64) launch_band_v2<64, 16, kRowsBand>(b, st);
+        else launch_band_v2<128, 8, kRowsBand>(b, st);
     } else {
         if (a.D == 64) launch_band_v2<64, 16>(a, st);
         else launch_band_v2<128, 8>(a, st);

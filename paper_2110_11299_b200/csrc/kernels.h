@@ -13,6 +13,22 @@ namespace dsa {
 [[noreturn]] void throw_cuda(cudaError_t e, const char* where);
 // Counts kernel launches of this library (dsa_launch_counter()).
 void note_launch(int n = 1);
+// Multiprocessor count of the current device (cached per device).
+int sm_count();
+
+// Kernel-selection switches, read from the environment ONCE when the
+// library loads (never per call).  Each forces a slower, simpler kernel so
+// the parity tests can cover it; the defaults are the measured-fastest path.
+struct Options {
+    bool attn_generic;       // DSA_ATTN_GENERIC: attn_rows_generic for every mask
+    bool threshold_generic;  // DSA_THRESHOLD_GENERIC: CTA-per-row threshold kernels
+    bool block_generic;      // DSA_BLOCK_GENERIC: CTA-per-row block selection
+    bool topk_generic;       // DSA_TOPK_GENERIC: CTA-per-row radix top-k
+    bool predict_dfma;       // DSA_PREDICT_DFMA: exact fp64 projection chain
+    bool no_fuse;            // DSA_NO_FUSE: unfused COLVEC select + attention
+    int pipeline_chunks;     // DSA_PIPELINE_CHUNKS: pair chunks overlapped on 3 streams
+};
+const Options& options();
 
 inline int64_t ceil_div_i(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
@@ -36,7 +52,11 @@ struct PredictArgs {
 // share of the deferred-recompute list (u64 entries, 1/8 of the levels)
 // and of its counter.  Layout of a call's view over n pairs: x^ of all n,
 // factors of all n, the counter (u64), then the list (capacity n L KD / 4).
-inline int64_t xhat_floats_per_pair(int64_t L, int64_t KD) { return 2 * L * (KD + 1) + L * KD / 2 + 2; }
+// Rounded up to 64 floats (256 B) so a chunk's view at any pair0 keeps the
+// float4 / u64 alignment of its parts.
+inline int64_t xhat_floats_per_pair(int64_t L, int64_t KD) {
+    return (2 * L * (KD + 1) + L * KD / 2 + 2 + 63) / 64 * 64;
+}
 void run_predict(const PredictArgs& a, cudaStream_t st);
 bool predict_fast_supported(const PredictArgs& a);
 void run_predict_fast(const PredictArgs& a, cudaStream_t st);
@@ -79,16 +99,10 @@ struct SelectArgs {
 void run_select(const SelectArgs& a, cudaStream_t st);
 size_t select_scan_tmp_bytes(int64_t n);
 bool colvec_tc_supported(const SelectArgs& a);
-bool colvec_ws_supported(const SelectArgs& a);
-void run_colvec_ws(const SelectArgs& a, cudaStream_t st);
 void run_colvec_tc(const SelectArgs& a, cudaStream_t st);
 bool threshold_tc_supported(const SelectArgs& a);
-bool topk_tc_supported(const SelectArgs& a);
-bool topk_rowwarp_supported(const SelectArgs& a);
-void run_topk_rowwarp(const SelectArgs& a, cudaStream_t st);
 bool topk_rowsel_supported(const SelectArgs& a);
 void run_topk_rowsel(const SelectArgs& a, cudaStream_t st);
-void run_topk_tc(const SelectArgs& a, cudaStream_t st);
 void launch_topk_scaled_list(const SelectArgs& a, const int64_t* list, const unsigned* nlist, cudaStream_t st);
 void run_threshold_tc(const SelectArgs& a, cudaStream_t st);
 void launch_exp_table(const SelectArgs& a, cudaStream_t st);

@@ -189,7 +189,7 @@ void dispatch_d(const PredictArgs& a, cudaStream_t st) {
 }  // namespace
 
 void run_predict(const PredictArgs& a, cudaStream_t st) {
-    static const bool force_dfma = std::getenv("DSA_PREDICT_DFMA") != nullptr;  // A/B switch
+    const bool force_dfma = options().predict_dfma;
     if (!force_dfma && predict_tc_supported(a)) {
         run_predict_tc(a, st);
         return;

@@ -26,13 +26,17 @@
 // X tiles arrive by 16-byte cp.async into the K-major no-swizzle layout, the
 // P-split operand image (built once per call by psplit_kernel) by cp.async
 // from L2, one MMA batch per CTA; many CTAs per SM overlap each other's
-// loads.  Uncertified elements go to a shared list and are recomputed by the
-// whole CTA (the reference chain is sequential, so one element per thread).
-// HBM traffic: Q and K read twice (amax pass, quantise pass), levels
-// written once.
+// loads.  Uncertified elements: in the two-read quantise pass (8-bit levels)
+// and the per-row pass they go to a shared list recomputed by the whole CTA
+// (the reference chain is sequential, so one element per thread); in the
+// streaming x^ pass (<= 4-bit levels) they go to a global deferred list
+// (one atomic per block) that quantize_fix_kernel recomputes, one thread per
+// entry, grid = 2 x SM count.  When the list is full the streaming pass
+// recomputes the level in place.
+// HBM traffic: Q and K read twice (amax pass, quantise pass) or once plus
+// the x^ round trip, levels written once.
 #include <cuda_bf16.h>
 
-#include <cstdlib>
 
 #include "device_common.cuh"
 #include "kernels.h"
@@ -576,12 +580,8 @@ void launch_tc(const PredictArgs& a, cudaStream_t st) {
     const int smem = std::max(Sm::bytes(), (228 * 1024) / (512 / TC + 1) + 1024);
     auto ka = project_tc_kernel<D, KD, false, R>;
     auto kq = project_tc_kernel<D, KD, true, R>;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr = true;
-    }
+    cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const auto* q = static_cast<const __nv_bfloat16*>(a.q);
     const auto* k = static_cast<const __nv_bfloat16*>(a.k);
     const dim3 grid(static_cast<unsigned>(ceil_div_i(a.L, R)), 2, static_cast<unsigned>(a.pairs));
@@ -591,11 +591,7 @@ void launch_tc(const PredictArgs& a, cudaStream_t st) {
     if (a.per_row) {
         auto kr = project_tc_kernel<D, KD, true, R, true>;
         const int rsmem = std::max(ProjSmem<D, KD, R, true>::bytes(), (228 * 1024) / (512 / TC + 1) + 1024);
-        static bool rattr = false;
-        if (!rattr) {
-            cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, rsmem);
-            rattr = true;
-        }
+        cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, rsmem);
         kr<<<grid, R, rsmem, st>>>(q, k, a.p, a.pimg, a.L, a.round_f32, a.qmax, nullptr, a.lq, a.lk, a.sq, a.sk,
                                   nullptr);
         note_launch(2);
@@ -608,7 +604,7 @@ void launch_tc(const PredictArgs& a, cudaStream_t st) {
         const dim3 gq(static_cast<unsigned>(ceil_div_i(a.L * (KD / 8), 256)), static_cast<unsigned>(a.pairs * 2));
         quantize_xhat_kernel<D, KD><<<gq, 256, 0, st>>>(
             a.xhat, q, k, a.p, a.pimg, a.pairs, a.L, a.round_f32, a.qmax, a.amax, a.lq, a.lk, a.sq, a.sk);
-        quantize_fix_kernel<D, KD><<<2 * 148, 256, 0, st>>>(a.xhat, q, k, a.p, a.pairs, a.L, a.round_f32, a.qmax,
+        quantize_fix_kernel<D, KD><<<2 * sm_count(), 256, 0, st>>>(a.xhat, q, k, a.p, a.pairs, a.L, a.round_f32, a.qmax,
                                                            a.amax, a.lq, a.lk);
         note_launch();
     } else {
@@ -622,12 +618,8 @@ void launch_tc(const PredictArgs& a, cudaStream_t st) {
 
 template <int D, int KD>
 void launch_tc(const PredictArgs& a, cudaStream_t st) {
-    static const int rows = [] {
-        const char* e = std::getenv("DSA_PREDICT_ROWS");
-        return e ? std::atoi(e) : 0;
-    }();
-    const bool two = rows == 256 || (rows == 0 && D == 128);
-    if (two) launch_tc<D, KD, 256>(a, st);
+    // d = 128: 256 rows per CTA (two M = 128 MMAs share the P image and prologue)
+    if (D == 128) launch_tc<D, KD, 256>(a, st);
     else launch_tc<D, KD, 128>(a, st);
 }
 
@@ -637,8 +629,6 @@ size_t predict_tc_image_bytes(int64_t D, int64_t KD) { return static_cast<size_t
 
 bool predict_tc_supported(const PredictArgs& a) {
     if (!a.bf16 || a.pimg == nullptr) return false;
-    if (a.per_row && std::getenv("DSA_PREDICT_ROWS_DMMA") != nullptr) return false;  // A/B switch
-    if (std::getenv("DSA_PREDICT_CLUSTER") != nullptr) return false;  // A/B switch
     return (a.D == 64 || a.D == 128) && (a.KD == 16 || a.KD == 32);
 }
 

@@ -296,7 +296,7 @@ __device__ __forceinline__ void topk_row_scaled(const SelectArgs& a, int64_t pai
 }
 
 // rows = blockIdx (grid L x pairs), or the rows listed in `list` (pair * L +
-// row, count *nlist; grid-stride) -- the overflow fallback of topk_tc.
+// row, count *nlist; grid-stride) -- the overflow fallback of topk_rowsel.
 template <int KD>
 __global__ void __launch_bounds__(kNT) topk_rows_scaled(SelectArgs a, const int64_t* list, const unsigned* nlist) {
     extern __shared__ __align__(16) unsigned char dsm[];
@@ -569,8 +569,7 @@ void launch_select(const SelectArgs& a, cudaStream_t st) {
     const unsigned P = static_cast<unsigned>(a.pairs);
     switch (a.mode) {
         case kRowTopk: {
-            if (a.per_row && a.L <= 8192 && a.qmax * a.qmax * KD < 32768 &&
-                std::getenv("DSA_TOPK64") == nullptr) {  // int16 exact scores
+            if (a.per_row && a.L <= 8192 && a.qmax * a.qmax * KD < 32768) {  // int16 exact scores
                 const size_t sm = static_cast<size_t>(a.L) * 11;
                 auto kern = topk_rows_scaled<KD>;
                 cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
@@ -607,7 +606,7 @@ void launch_select(const SelectArgs& a, cudaStream_t st) {
             const double bq = static_cast<double>(a.block) * a.qmax;  // |pooled level| bound
             const bool warp_ok = a.keep <= 32 && a.L % a.block == 0 && nb <= 512 &&
                                  static_cast<double>(a.KD) * bq * bq < 2147483647.0 &&  // int32 dot exact
-                                 std::getenv("DSA_BLOCK_GENERIC") == nullptr;
+                                 !options().block_generic;
             const dim3 gw(static_cast<unsigned>(ceil_div_i(nb, 8)), P);
             if (warp_ok && nb <= 128) {
                 block_select_warp<KD, 4><<<gw, 256, 0, st>>>(a, nb);
@@ -675,11 +674,6 @@ size_t select_scan_tmp_bytes(int64_t n) {
 }
 
 void run_select(const SelectArgs& a, cudaStream_t st) {
-    static const bool ws = std::getenv("DSA_SELECT_WS") != nullptr;  // experimental warp-specialised variant
-    if (ws && colvec_ws_supported(a)) {
-        run_colvec_ws(a, st);
-        return;
-    }
     if (colvec_tc_supported(a)) {
         run_colvec_tc(a, st);
         return;
@@ -690,14 +684,6 @@ void run_select(const SelectArgs& a, cudaStream_t st) {
     }
     if (topk_rowsel_supported(a)) {
         run_topk_rowsel(a, st);
-        return;
-    }
-    if (topk_tc_supported(a)) {
-        run_topk_tc(a, st);
-        return;
-    }
-    if (topk_rowwarp_supported(a)) {
-        run_topk_rowwarp(a, st);
         return;
     }
     switch (a.KD) {

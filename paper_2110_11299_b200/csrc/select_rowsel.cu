@@ -387,7 +387,7 @@ bool topk_rowsel_supported(const SelectArgs& a) {
     // 32 * G groups >= keep with G <= 8 and G | NPL
     if (a.keep < 1 || a.keep > 256 || a.keep > 32 * std::min<int64_t>(8, npl)) return false;
     if (a.qmax > 127) return false;  // int8 levels
-    return std::getenv("DSA_TOPK_ROWSEL_OFF") == nullptr;
+    return !options().topk_generic;
 }
 
 void run_topk_rowsel(const SelectArgs& a, cudaStream_t st) {

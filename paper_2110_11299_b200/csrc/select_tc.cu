@@ -21,7 +21,6 @@
 // exists in HBM.
 #include <cuda_bf16.h>
 
-#include <cstdlib>
 
 #include "device_common.cuh"
 #include "kernels.h"
@@ -102,7 +101,7 @@ constexpr int kAS = kAcc / kTPS;        // TMEM accumulator sets
 template <int KD, int NQ, bool FUSED = false>
 __global__ void __launch_bounds__(colvec_threads<NQ>(), NQ == 128 ? 1 : (NQ == 64 ? 2 : 4))
     colvec_tc_kernel(const uint16_t* __restrict__ lq, const uint16_t* __restrict__ lk, int64_t L,
-                     int64_t keep, int M, uint32_t* __restrict__ out, int dbg, FusedAttn fa) {
+                     int64_t keep, int M, uint32_t* __restrict__ out, FusedAttn fa) {
     extern __shared__ __align__(1024) unsigned char smem[];
     constexpr int kT = colvec_threads<NQ>();
     constexpr int NB = NQ / 8;       // bands per CTA
@@ -282,17 +281,10 @@ __global__ void __launch_bounds__(colvec_threads<NQ>(), NQ == 128 ? 1 : (NQ == 6
     // ---- exact per-band selection (one warp per band)
     const int64_t nb = (L + 7) / 8;
     uint32_t* h = hist + warp * 64;
-    for (int b = warp; b < NB && !(dbg & 1); b += kT / 32) {
+    for (int b = warp; b < NB; b += kT / 32) {
         const int64_t band = q0 / 8 + b;
         if (band >= nb) break;
         const int16_t* pv = pooled + (b >> 1) * Lp * 2 + (b & 1);
-        if (dbg & 2) {  // profiling ablation: threshold only (no emission)
-            int T;
-            uint32_t rem, nge;
-            band_threshold<2>(pv, static_cast<int>(L), static_cast<int>(keep), bandmax[b], M, h, lane, T, rem, nge);
-            if (out && lane == 0) out[(pair * nb + band) * keep] = static_cast<uint32_t>(T) + rem + nge;
-            continue;
-        }
         band_select<2>(pv, static_cast<int>(L), Lp, static_cast<int>(keep), bandmax[b], M, h,
                        obufs + warp * kList, out ? out + (pair * nb + band) * keep : nullptr, lane);
         __syncwarp();
@@ -316,174 +308,6 @@ __global__ void __launch_bounds__(colvec_threads<NQ>(), NQ == 128 ? 1 : (NQ == 6
     }
 }
 
-// Warp-specialised variant (NQ = 64, 9 warps): warp 8 is the producer --
-// its lanes cp.async the K~ tiles into the ring and lane 0 issues each MMA
-// once the tile has landed and the accumulator is released -- while warps
-// 0-7 run the epilogue free of CTA-wide barriers: per tile they wait on the
-// MMA's mbarrier, drain TMEM, and release the accumulator through an
-// "empty" mbarrier (8 warp arrivals).  Selection afterwards is unchanged.
-template <int KD>
-__global__ void __launch_bounds__(kThreads + 32, 2)
-    colvec_ws2_kernel(const uint16_t* __restrict__ lq, const uint16_t* __restrict__ lk, int64_t L,
-                      int64_t keep, int M, uint32_t* __restrict__ out, int dbg) {
-    constexpr int NQ = 64;
-    extern __shared__ __align__(1024) unsigned char smem[];
-    constexpr int NB = NQ / 8;
-    constexpr int CPW = NQ / 2;
-    constexpr int NLD = CPW / 32;
-    constexpr int BPW = CPW / 8;
-    constexpr int kTile = ColvecSmem<KD>::kTileBytes;
-    const int nt = static_cast<int>((L + kMT - 1) / kMT);
-    const int Lp = nt * kMT;
-    unsigned char* p = smem;
-    unsigned char* bq = p;                      p += NQ * KD * 2;
-    unsigned char* ring = p;                    p += kStages * kTile;
-    int16_t* pooled = reinterpret_cast<int16_t*>(p); p += NB * Lp * 2;
-    uint32_t* hist = reinterpret_cast<uint32_t*>(p); p += (kThreads / 32) * 64 * 4;
-    uint32_t* obufs = reinterpret_cast<uint32_t*>(p); p += (kThreads / 32) * kList * 4;
-    int* bandmax = reinterpret_cast<int*>(p);   p += 16 * 4;
-    uint64_t* done = reinterpret_cast<uint64_t*>(p);   // [kAcc] MMA -> epilogue
-    uint64_t* empty = done + kAcc;                     // [kAcc] epilogue -> MMA (8 arrivals)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(empty + kAcc);
-
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int64_t pair = blockIdx.y;
-    const int64_t q0 = static_cast<int64_t>(blockIdx.x) * NQ;
-    const uint16_t* lqp = lq + pair * L * KD;
-    const uint16_t* lkp = lk + pair * L * KD;
-
-    if (tid == 0) {
-        for (int b = 0; b < kAcc; ++b) {
-            tc::mbar_init(&done[b], 1);
-            tc::mbar_init(&empty[b], 8);
-        }
-        tc::fence_barrier_init();
-    }
-    if (tid < NB) bandmax[tid] = INT32_MIN;
-    if (warp == 0) tc::tmem_alloc<kAcc * NQ>(tmem_slot);
-    tc::fence_before_sync();
-    __syncthreads();
-    tc::fence_after_sync();
-    const uint32_t tmem = *tmem_slot;
-
-    if (warp == 8) {
-        // ---------------------------------------------------------- producer
-        auto load = [&](int slot, int tile) {
-            const int64_t row0 = static_cast<int64_t>(tile) * kMT;
-            constexpr int kCh = KD / 8;
-            for (int t = lane; t < kMT * kCh; t += 32) {
-                const int r = t / kCh, c = t % kCh;
-                const bool ok = row0 + r < L;
-                cp_async16(tc::smem_addr(ring + slot * kTile) + tile_off<KD>(r, c),
-                           lkp + lvl_index(L, ok ? (row0 + r) : 0, c * 8), ok);
-            }
-        };
-        {
-            constexpr int kCh = KD / 8;
-            for (int t = lane; t < NQ * kCh; t += 32) {
-                const int r = t / kCh, c = t % kCh;
-                const bool ok = q0 + r < L;
-                cp_async16(tc::smem_addr(bq) + tile_off<KD>(r, c), lqp + lvl_index(L, ok ? (q0 + r) : 0, c * 8), ok);
-            }
-        }
-        for (int s = 0; s < kStages; ++s) {
-            if (s < nt) load(s, s);
-            cp_commit();
-        }
-        const uint32_t idesc = tc::idesc_bf16_f32(kMT, NQ);
-        const uint64_t bdesc = tc::desc_kmajor_nosw(tc::smem_addr(bq), 128, KD * 16);
-        for (int t = 0; t < nt; ++t) {
-            cp_wait<kStages - 2>();  // tile t (and the Q~ block) landed: tile j >= kStages is group j + 1
-            tc::fence_proxy_async();
-            __syncwarp();
-            if (t >= kAcc) tc::mbar_wait(&empty[t % kAcc], ((t / kAcc) - 1) & 1);
-            if (lane == 0) {
-                tc::fence_after_sync();
-                const uint32_t abase = tc::smem_addr(ring + (t % kStages) * kTile);
-#pragma unroll
-                for (int ks = 0; ks < KD / 16; ++ks) {
-                    const uint64_t ad = tc::desc_kmajor_nosw(abase + ks * 256, 128, KD * 16);
-                    const uint64_t bd = bdesc + static_cast<uint64_t>((ks * 256) >> 4);
-                    tc::mma_bf16(tmem + (t % kAcc) * NQ, ad, bd, idesc, ks > 0);
-                }
-                tc::commit(&done[t % kAcc]);
-            }
-            __syncwarp();
-            // refill the slot of tile t-1 once its MMA completed
-            if (t >= 1) {
-                const int u = t - 1;
-                tc::mbar_wait(&done[u % kAcc], (u / kAcc) & 1);
-                if (u + kStages < nt) load(u % kStages, u + kStages);
-            }
-            cp_commit();
-        }
-        cp_wait<0>();
-    } else {
-        // ---------------------------------------------------------- epilogue
-        const int quarter = warp & 3, half = warp >> 2;
-        const bool ragged_q = q0 + NQ > L;
-        float bmax[BPW];
-#pragma unroll
-        for (int i = 0; i < BPW; ++i) bmax[i] = -INFINITY;
-        for (int u = 0; u < nt; ++u) {
-            tc::mbar_wait(&done[u % kAcc], (u / kAcc) & 1);
-            tc::fence_after_sync();
-            const int key = u * kMT + quarter * 32 + lane;
-            const bool kvalid = key < L;
-            const uint32_t base = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + (u % kAcc) * NQ + half * CPW;
-            uint32_t rr[NLD][32];
-#pragma unroll
-            for (int l = 0; l < NLD; ++l) tc::ld_32x32b_x32(base + l * 32, rr[l]);
-            tc::wait_ld();
-            tc::fence_before_sync();
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&empty[u % kAcc]);  // accumulator drained
-#pragma unroll
-            for (int cb = 0; cb < NLD; ++cb) {
-                uint32_t* r = rr[cb];
-                if (ragged_q) {
-#pragma unroll
-                    for (int x = 0; x < 32; ++x)
-                        if (q0 + half * CPW + cb * 32 + x >= L) r[x] = __float_as_uint(-INFINITY);
-                }
-#pragma unroll
-                for (int bb = 0; bb < 4; ++bb) {
-                    float m0, m1, m2;
-                    const float* f = reinterpret_cast<const float*>(&r[bb * 8]);
-                    asm("max.f32 %0, %1, %2, %3;" : "=f"(m0) : "f"(f[0]), "f"(f[1]), "f"(f[2]));
-                    asm("max.f32 %0, %1, %2, %3;" : "=f"(m1) : "f"(f[3]), "f"(f[4]), "f"(f[5]));
-                    asm("max.f32 %0, %1, %2, %3;" : "=f"(m2) : "f"(m0), "f"(m1), "f"(f[6]));
-                    const float mx = fmaxf(m2, f[7]);
-                    const int band = half * BPW + cb * 4 + bb;
-                    pooled[band * Lp + key] = kvalid ? static_cast<int16_t>(__float2int_rn(mx)) : INT16_MIN;
-                    if (kvalid) bmax[cb * 4 + bb] = fmaxf(bmax[cb * 4 + bb], mx);
-                }
-            }
-        }
-#pragma unroll
-        for (int i = 0; i < BPW; ++i) {
-            float v = bmax[i];
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, off));
-            if (lane == 0) atomicMax(&bandmax[half * BPW + i], __float2int_rn(v));
-        }
-    }
-    __syncthreads();
-    if (warp == 0) tc::tmem_dealloc<kAcc * NQ>(tmem);
-    if (warp == 8) return;
-
-    const int64_t nb = (L + 7) / 8;
-    uint32_t* h = hist + warp * 64;
-    for (int b = warp; b < NB && !(dbg & 1); b += kThreads / 32) {
-        const int64_t band = q0 / 8 + b;
-        if (band >= nb) break;
-        const int16_t* pv = pooled + b * Lp;
-        band_select(pv, static_cast<int>(L), Lp, static_cast<int>(keep), bandmax[b], M, h,
-                    obufs + warp * kList, out + (pair * nb + band) * keep, lane);
-        __syncwarp();
-    }
-}
-
 template <int KD, int NQ>
 size_t colvec_smem_bytes(int64_t L) {
     const int64_t nt = (L + kMT - 1) / kMT;
@@ -503,57 +327,30 @@ bool colvec_tc_supported(const SelectArgs& a) {
 }
 
 template <int KD, int NQ>
-void launch_colvec(const SelectArgs& a, int M, int dbg, cudaStream_t st) {
+void launch_colvec(const SelectArgs& a, int M, cudaStream_t st) {
     const size_t smem = colvec_smem_bytes<KD, NQ>(a.L);
     auto kern = colvec_tc_kernel<KD, NQ, false>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     const dim3 grid(static_cast<unsigned>(ceil_div_i(a.L, NQ)), static_cast<unsigned>(a.pairs));
-    kern<<<grid, colvec_threads<NQ>(), smem, st>>>(a.lq, a.lk, a.L, a.keep, M, a.cols, dbg, FusedAttn{});
+    kern<<<grid, colvec_threads<NQ>(), smem, st>>>(a.lq, a.lk, a.L, a.keep, M, a.cols, FusedAttn{});
 }
 
 void run_colvec_tc(const SelectArgs& a, cudaStream_t st) {
-    // DSA_PROFILE_SWITCH: profiling-only ablations (1: skip selection)
-    static const int dbg = [] {
-        const char* e = std::getenv("DSA_PROFILE_SWITCH");
-        return e ? std::atoi(e) : 0;
-    }();
-    static const bool force128 = std::getenv("DSA_COLVEC_NQ128") != nullptr;  // A/B switch
     const int M = static_cast<int>(a.KD) * a.qmax * a.qmax;
     // two 64-query CTAs per SM when their shared memory fits, else one 128-query CTA
-    const bool two = !force128 && (a.KD == 16 ? colvec_smem_bytes<16, 64>(a.L) : colvec_smem_bytes<32, 64>(a.L)) <=
-                                       113 * 1024;
-    static const bool ws2 = std::getenv("DSA_COLVEC_WS2") != nullptr;  // A/B switch
-    if (ws2 && two) {
-        auto kern = a.KD == 16 ? colvec_ws2_kernel<16> : colvec_ws2_kernel<32>;
-        const size_t smem = a.KD == 16 ? colvec_smem_bytes<16, 64>(a.L) : colvec_smem_bytes<32, 64>(a.L);
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        const dim3 grid(static_cast<unsigned>(ceil_div_i(a.L, 64)), static_cast<unsigned>(a.pairs));
-        kern<<<grid, kThreads + 32, smem, st>>>(a.lq, a.lk, a.L, a.keep, M, a.cols, dbg);
-        note_launch();
-        return;
-    }
-    static const int nq_env = [] {
-        const char* e = std::getenv("DSA_COLVEC_NQ");
-        return e ? std::atoi(e) : 0;
-    }();
-    if (nq_env == 32 && (a.KD == 16 ? colvec_smem_bytes<16, 32>(a.L) : colvec_smem_bytes<32, 32>(a.L)) <= 75 * 1024) {
-        if (a.KD == 16) launch_colvec<16, 32>(a, M, dbg, st);
-        else launch_colvec<32, 32>(a, M, dbg, st);
-        note_launch();
-        return;
-    }
+    const bool two = (a.KD == 16 ? colvec_smem_bytes<16, 64>(a.L) : colvec_smem_bytes<32, 64>(a.L)) <= 113 * 1024;
     if (a.KD == 16) {
-        if (two) launch_colvec<16, 64>(a, M, dbg, st);
-        else launch_colvec<16, 128>(a, M, dbg, st);
+        if (two) launch_colvec<16, 64>(a, M, st);
+        else launch_colvec<16, 128>(a, M, st);
     } else {
-        if (two) launch_colvec<32, 64>(a, M, dbg, st);
-        else launch_colvec<32, 128>(a, M, dbg, st);
+        if (two) launch_colvec<32, 64>(a, M, st);
+        else launch_colvec<32, 128>(a, M, st);
     }
     note_launch();
 }
 
 bool colvec_fused_supported(const SelectArgs& s, const AttnArgs& a) {
-    if (std::getenv("DSA_NO_FUSE") != nullptr) return false;
+    if (options().no_fuse) return false;
     if (!colvec_tc_supported(s) || s.KD != 16 || !a.bf16 || a.D != 64 || a.vec_v != 8) return false;
     if (s.keep > kList - 32) return false;  // band list must stay in the staging buffer
     const size_t smem = colvec_smem_bytes<16, 64>(s.L);
@@ -571,7 +368,7 @@ void run_colvec_fused(const SelectArgs& s, const AttnArgs& a, cudaStream_t st) {
     const dim3 grid(static_cast<unsigned>(ceil_div_i(s.L, 64)), static_cast<unsigned>(s.pairs));
     FusedAttn fa{static_cast<const __nv_bfloat16*>(a.q), static_cast<const __nv_bfloat16*>(a.k),
                  static_cast<const __nv_bfloat16*>(a.v), static_cast<__nv_bfloat16*>(a.z), a.scale};
-    kern<<<grid, kThreads, smem, st>>>(s.lq, s.lk, s.L, s.keep, M, s.cols, 0, fa);
+    kern<<<grid, kThreads, smem, st>>>(s.lq, s.lk, s.L, s.keep, M, s.cols, fa);
     note_launch();
 }
 

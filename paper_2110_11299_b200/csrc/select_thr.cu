@@ -438,7 +438,7 @@ void launch_thr(const ThrParams& p, int64_t pairs, cudaStream_t st) {
 bool threshold_tc_supported(const SelectArgs& a) {
     return a.mode == kThreshold && !a.per_row && (a.KD == 16 || a.KD == 32) && a.L < 65536 - kTN &&  // 16-bit histogram halves
           
-           a.cut != nullptr && std::getenv("DSA_THRESHOLD_GENERIC") == nullptr;
+           a.cut != nullptr && !options().threshold_generic;
 }
 
 // exp table -> count kernel -> scan -> emit kernel
@@ -463,8 +463,7 @@ void run_threshold_tc(const SelectArgs& a, cudaStream_t st) {
     else launch_thr<32, false>(p, a.pairs, st);
     scan_counts(a, st);
     // f16 scores are exact when |S| and every partial sum stay <= 2048
-    static const bool f32_emit = std::getenv("DSA_THR_EMIT_F32") != nullptr;  // A/B switch
-    const bool p16 = !f32_emit && a.KD * static_cast<int64_t>(a.qmax) * a.qmax <= 2048;
+    const bool p16 = a.KD * static_cast<int64_t>(a.qmax) * a.qmax <= 2048;
     if (a.KD == 16) {
         if (p16) launch_thr<16, true, true>(p, a.pairs, st);
         else launch_thr<16, true>(p, a.pairs, st);

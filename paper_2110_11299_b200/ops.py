@@ -139,13 +139,25 @@ def _check_inputs(p: Preset, pairs: int, *ts: torch.Tensor) -> None:
             raise ParamError("dsa: inputs must be contiguous CUDA tensors")
 
 
-def _ws(nbytes: int, device) -> torch.Tensor:
-    return torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
+def _ws(nbytes: int, device, stream=None) -> torch.Tensor:
+    """Scratch for one call.  The caching allocator hands out memory per
+    stream, so a buffer used by a launch on another stream is tied to it
+    (record_stream) and is not reused before that stream's work is done."""
+    t = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
+    if stream is not None and t.is_cuda:
+        t.record_stream(stream)
+    return t
+
+
+def _check_projection(p: Preset, P: torch.Tensor) -> None:
+    if P.shape != (p.d, p.k) or P.dtype != torch.float32 or not P.is_cuda or not P.is_contiguous():
+        raise ParamError(f"dsa: P must be a contiguous CUDA float32 tensor of shape [{p.d}, {p.k}]")
 
 
 def predict(p: Preset, q: torch.Tensor, k: torch.Tensor, P: torch.Tensor, stream=None) -> Levels:
     pairs = q.shape[0]
     _check_inputs(p, pairs, q, k)
+    _check_projection(p, P)
     c = config_of(p, pairs)
     dev = q.device
     lq = torch.empty((pairs, p.k // 8, p.L, 8), dtype=torch.bfloat16, device=dev)
@@ -153,8 +165,8 @@ def predict(p: Preset, q: torch.Tensor, k: torch.Tensor, P: torch.Tensor, stream
     ns = (pairs,) if p.quant_scope == "tensor" else (pairs, p.L)
     sq = torch.empty(ns, dtype=torch.float64, device=dev)
     sk = torch.empty_like(sq)
-    ws = _ws(workspace_bytes(p, pairs), dev)
-    _abi.check(_abi.lib().dsa_predict(C.byref(c), _ptr(q), _ptr(k), _ptr(P.contiguous()), _ptr(lq),
+    ws = _ws(workspace_bytes(p, pairs), dev, stream)
+    _abi.check(_abi.lib().dsa_predict(C.byref(c), _ptr(q), _ptr(k), _ptr(P), _ptr(lq),
                                       _ptr(lk), _ptr(sq), _ptr(sk), _ptr(ws), ws.numel(),
                                       _stream(stream)))
     return Levels(lq, lk, sq, sk)
@@ -174,7 +186,7 @@ def select(p: Preset, lv: Levels, stream=None, mask: Mask | None = None) -> Mask
     c = config_of(p, pairs)
     dev = lv.lq.device
     m = mask or alloc_mask(p, pairs, dev)
-    ws = _ws(workspace_bytes(p, pairs), dev)
+    ws = _ws(workspace_bytes(p, pairs), dev, stream)
     cm = m.as_c()
     _abi.check(_abi.lib().dsa_select(C.byref(c), _ptr(lv.lq), _ptr(lv.lk), _ptr(lv.sq),
                                      _ptr(lv.sk), C.byref(cm), _ptr(ws), ws.numel(),
@@ -280,6 +292,15 @@ def project_qkv(x: torch.Tensor, w: torch.Tensor, heads: int, dk: int, dv: int, 
     _abi.check(_abi.lib().dsa_project_qkv(batch, L, dm, heads, dk, dv, npred, _ptr(x), _ptr(w), _ptr(q),
                                           _ptr(k), _ptr(v), _ptr(r), _stream(stream)))
     return q, k, v, r
+
+
+def fused_pipeline(p: Preset, pairs: int | None = None) -> bool:
+    """True when dsa_pipeline fuses selection + attention into one kernel."""
+    c = config_of(p, pairs)
+    r = _abi.lib().dsa_pipeline_fused(C.byref(c))
+    if r < 0:
+        _abi.check(_abi.lib().dsa_config_validate(C.byref(c)))
+    return r == 1
 
 
 def launch_counter() -> int:
