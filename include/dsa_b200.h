@@ -13,6 +13,8 @@
  * errors.hpp:9-31) so reference callers and CLI exit codes are unchanged.
  *
  * Reference interfaces replaced (P/ = /root/reference/proj/):
+ *   dsa_predict_wtilde   <- approx_scores / approx_scores_from_r (R = X P, per-head W~)
+ *                           P/include/dsattn/predictor.hpp:44-49, P/src/predictor.cpp:67-80
  *   dsa_predict          <- Matrix quantize(const Matrix&, QuantSpec) applied to
  *                           matmul(Q,P) / matmul(K,P)   P/include/dsattn/predictor.hpp:31-49,
  *                           P/src/predictor.cpp:34-45,67-80; kernels::matmul/quantize
@@ -130,6 +132,26 @@ int64_t dsa_mask_capacity(const dsa_config* cfg);
 dsa_status dsa_predict(const dsa_config* cfg, const void* q, const void* k, const float* p,
                        uint16_t* levels_q, uint16_t* levels_k, double* scale_q, double* scale_k,
                        void* workspace, size_t workspace_bytes, void* stream);
+
+/* (1') The reference's own predictor entry point, approx_scores /
+ * approx_scores_from_r (P/include/dsattn/predictor.hpp:44-49,
+ * P/src/predictor.cpp:67-80) with its trainable per-head k x k W~:
+ *     R = X P  (per sample, shared by the heads, P/src/trainer.cpp:162),
+ *     Q~[b,h] = quantize(R[b] W~_Q[h]),  K~[b,h] = quantize(R[b] W~_K[h]).
+ * Every product is the reference matmul's sequential fp64 FMA chain
+ * (P/src/kernels/scalar.cpp:19-32), rounded through float when
+ * cfg->round_proj_f32 (f32 Matrices), so levels and scales are bit-exact.
+ *   x : [batch][L][d_model] f64, or NULL: then r is the INPUT
+ *   p : [d_model][k] f64 (ignored when x == NULL)
+ *   r : [batch][L][k] f64, written when x != NULL
+ *   wq, wk: [heads][k][k] f64 (row-major: Q~ = R . wq[h])
+ * Outputs as dsa_predict for pair = b * heads + h (quant_scope honoured;
+ * cfg->d is not used).  Workspace: dsa_predict_wtilde_workspace_bytes(). */
+size_t dsa_predict_wtilde_workspace_bytes(const dsa_config* cfg);
+dsa_status dsa_predict_wtilde(const dsa_config* cfg, int64_t d_model, const double* x, const double* p,
+                              double* r, const double* wq, const double* wk, uint16_t* levels_q,
+                              uint16_t* levels_k, double* scale_q, double* scale_k, void* workspace,
+                              size_t workspace_bytes, void* stream);
 
 /* (2) exact-integer approximate scores -> mask selection. */
 dsa_status dsa_select(const dsa_config* cfg, const uint16_t* levels_q, const uint16_t* levels_k,

@@ -205,6 +205,9 @@ class Reference:
             "ref_masked_attention": (I32, [_d, _d, _d, I64, I64, I64, _u64, _u32, I32, _d]),
             "ref_pipeline": (I32, [I64, I32, _d, _d, _d, _d, I64, I64, I64, I32, I32, I32, I32, I64, I64,
                                    I64, I32, I64, I64, I64, I32, _d]),
+            "ref_levels_wtilde": (I32, [C.c_void_p, C.c_void_p, C.c_void_p, _d, I64, I64, I64, I32, I32,
+                                        C.c_void_p, _i32, C.POINTER(C.c_double)]),
+            "ref_init_projection": (I32, [I64, I64, C.c_uint64, _d]),
             "ref_block_mask": (I32, [_i32, _i32, I64, I64, I64, I64, I32, _u32]),
             "ref_causal_threshold_mask": (I32, [_i32, _i32, I64, I64, D, D, I64, I32, _u64, C.c_void_p]),
             "ref_threshold_row_probs": (I32, [_i32, _i32, I64, I64, D, I64, I32, _d]),
@@ -371,6 +374,30 @@ class Reference:
                                       mode, int(per_row), keep, vec_v, block, int(force_diag), frac_num,
                                       frac_den, cap, int(causal), z))
         return z
+
+    # ---- the reference predictor (approx_scores / approx_scores_from_r)
+    def levels_wtilde(self, w, bits, f32=False, x=None, p=None, r=None):
+        """Levels / scale of quantize(matmul(R, W~)), R = matmul(x, p) when x is
+        given (returned too), else r."""
+        w = _f64(w)
+        k = w.shape[0]
+        xp = _f64(x) if x is not None else None
+        L = xp.shape[0] if xp is not None else r.shape[0]
+        dm = xp.shape[1] if xp is not None else 0
+        pp = _f64(p) if p is not None else None
+        rin = _f64(r) if r is not None else None
+        rout = np.empty((L, k))
+        lv = np.empty((L, k), np.int32)
+        s = C.c_double()
+        ptr = lambda a: a.ctypes.data_as(C.c_void_p) if a is not None else None  # noqa: E731
+        self._chk(self.L.ref_levels_wtilde(ptr(xp), ptr(pp), ptr(rin), w, L, dm, k, bits, int(f32),
+                                           rout.ctypes.data_as(C.c_void_p), lv, C.byref(s)))
+        return lv, s.value, rout
+
+    def init_projection(self, d, k, seed):
+        out = np.empty((d, k))
+        self._chk(self.L.ref_init_projection(d, k, seed, out))
+        return out
 
     # ---- O5 / O6 compositions of reference primitives (block, causal threshold)
     def block_mask(self, lq, lk, bs, keep, force_diag):

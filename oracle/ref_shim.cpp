@@ -121,6 +121,24 @@ int ref_quantize_levels(const double* x, int64_t rows, int64_t cols, int bits, i
     });
 }
 
+// The reference predictor path (P/src/predictor.cpp:67-80) for one head and
+// one side: r = matmul(x, p) when x != NULL (written to r_out), then
+// levels / scale of quantize(matmul(r, w)).  f32: every Matrix is f32.
+int ref_levels_wtilde(const double* x, const double* p, const double* r_in, const double* w, int64_t L,
+                      int64_t dm, int64_t k, int bits, int f32, double* r_out, int32_t* levels, double* scale) {
+    return guarded([&] {
+        Matrix r = x ? matmul(to_matrix(x, L, dm, f32), to_matrix(p, dm, k, f32)) : to_matrix(r_in, L, k, f32);
+        if (r_out) from_matrix(r, r_out);
+        auto lv = levels_from_reference(matmul(r, to_matrix(w, k, k, f32)), bits, scale);
+        std::memcpy(levels, lv.data(), lv.size() * sizeof(int32_t));
+    });
+}
+
+// init_projection (P/src/predictor.cpp:10-20): the reference's ternary P.
+int ref_init_projection(int64_t d, int64_t k, uint64_t seed, double* p) {
+    return guarded([&] { from_matrix(init_projection(static_cast<size_t>(d), static_cast<size_t>(k), seed).p, p); });
+}
+
 // row_topk_indices on a 1 x n row (P/src/linalg.cpp:69-85).
 int ref_row_topk(const double* row, int64_t n, int64_t keep, uint32_t* out) {
     return guarded([&] {

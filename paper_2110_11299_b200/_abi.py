@@ -51,6 +51,9 @@ _SIGS = {
     "dsa_pipeline": (C.c_int, [C.POINTER(DsaConfig), _P, _P, _P, _P, _P, C.POINTER(DsaMask), _P,
                                C.c_size_t, _P]),
     "dsa_launch_counter": (C.c_uint64, []),
+    "dsa_predict_wtilde_workspace_bytes": (C.c_size_t, [C.POINTER(DsaConfig)]),
+    "dsa_predict_wtilde": (C.c_int, [C.POINTER(DsaConfig), C.c_int64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
+                                     C.c_size_t, _P]),
     "dsa_pipeline_fused": (C.c_int, [C.POINTER(DsaConfig)]),
     "dsa_project_qkv": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
                                   C.c_int64, _P, _P, _P, _P, _P, _P, _P]),

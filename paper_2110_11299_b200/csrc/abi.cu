@@ -486,6 +486,60 @@ dsa_status dsa_predict(const dsa_config* cfg, const void* q, const void* k, cons
     });
 }
 
+size_t dsa_predict_wtilde_workspace_bytes(const dsa_config* cfg) {
+    size_t out = 0;
+    dsa_status s = guard([&] {
+        validate(cfg);
+        const int64_t P = pairs_of(*cfg);
+        out = cfg->quant_scope == DSA_QUANT_PER_TENSOR
+                  ? align_up(sizeof(double) * P * 2 * cfg->L * cfg->k) + align_up(sizeof(unsigned long long) * P * 2)
+                  : 0;
+    });
+    return s == DSA_OK ? out : 0;
+}
+
+dsa_status dsa_predict_wtilde(const dsa_config* cfg, int64_t d_model, const double* x, const double* p,
+                              double* r, const double* wq, const double* wk, uint16_t* levels_q,
+                              uint16_t* levels_k, double* scale_q, double* scale_k, void* workspace,
+                              size_t workspace_bytes, void* stream) {
+    return guard([&] {
+        validate(cfg);
+        require_device();
+        const dsa_config& c = *cfg;
+        if (x && (d_model < 1 || !p)) throw Error(DSA_ERR_SHAPE, "approx_scores: X feature dim != d");
+        if (!r || !wq || !wk || !levels_q || !levels_k || !scale_q || !scale_k)
+            throw Error(DSA_ERR_PARAM, "dsa_predict_wtilde: null pointer");
+        const size_t need = dsa_predict_wtilde_workspace_bytes(cfg);
+        if (need > 0 && (!workspace || workspace_bytes < need))
+            throw Error(DSA_ERR_PARAM, "dsa: workspace too small (need " + std::to_string(need) + " bytes)");
+        WtildeArgs a{};
+        a.batch = c.batch;
+        a.heads = c.heads;
+        a.L = c.L;
+        a.dm = d_model;
+        a.KD = c.k;
+        a.x = x;
+        a.p = p;
+        a.r = r;
+        a.wq = wq;
+        a.wk = wk;
+        a.round_f32 = c.round_proj_f32;
+        a.per_row = c.quant_scope == DSA_QUANT_PER_ROW;
+        a.qmax = static_cast<double>(qmax_of(c.bits));
+        a.lq = levels_q;
+        a.lk = levels_k;
+        a.sq = scale_q;
+        a.sk = scale_k;
+        if (!a.per_row) {
+            a.x64 = static_cast<double*>(workspace);
+            a.amax = reinterpret_cast<unsigned long long*>(static_cast<char*>(workspace) +
+                                                           align_up(sizeof(double) * pairs_of(c) * 2 * c.L * c.k));
+        }
+        run_predict_wtilde(a, static_cast<cudaStream_t>(stream));
+        check_cuda(cudaGetLastError(), "dsa_predict_wtilde launch");
+    });
+}
+
 dsa_status dsa_select(const dsa_config* cfg, const uint16_t* levels_q, const uint16_t* levels_k,
                       const double* scale_q, const double* scale_k, const dsa_mask* mask,
                       void* workspace, size_t workspace_bytes, void* stream) {

@@ -64,6 +64,28 @@ bool predict_tc_supported(const PredictArgs& a);
 size_t predict_tc_image_bytes(int64_t D, int64_t KD);
 void run_predict_tc(const PredictArgs& a, cudaStream_t st);
 
+// approx_scores_from_r with the per-head k x k W~ (P/src/predictor.cpp:67-80)
+struct WtildeArgs {
+    int64_t batch, heads, L, dm, KD;
+    const double* x;   // [batch][L][dm] or null (r is then the input)
+    const double* p;   // [dm][KD]
+    double* r;         // [batch][L][KD]
+    const double* wq;  // [heads][KD][KD]
+    const double* wk;
+    int round_f32, per_row;
+    double qmax;
+    uint16_t* lq;
+    uint16_t* lk;
+    double* sq;
+    double* sk;
+    double* x64;                // per-tensor scratch [pairs][2][L][KD]
+    unsigned long long* amax;   // [pairs][2]
+};
+void run_predict_wtilde(const WtildeArgs& a, cudaStream_t st);
+// per-tensor pass B over an f64 projection scratch [pairs][2][L][KD]
+void launch_quantize_x64(const double* x64, const unsigned long long* amax, int64_t pairs, int64_t L, int64_t KD,
+                         double qmax, uint16_t* lq, uint16_t* lk, double* sq, double* sk, cudaStream_t st);
+
 enum SelectMode { kRowTopk = 0, kColvec = 1, kBlock = 2, kThreshold = 3 };
 
 struct SelectArgs {

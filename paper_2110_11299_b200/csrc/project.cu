@@ -188,6 +188,13 @@ void dispatch_d(const PredictArgs& a, cudaStream_t st) {
 
 }  // namespace
 
+void launch_quantize_x64(const double* x64, const unsigned long long* amax, int64_t pairs, int64_t L, int64_t KD,
+                         double qmax, uint16_t* lq, uint16_t* lk, double* sq, double* sk, cudaStream_t st) {
+    const dim3 g2(static_cast<unsigned>(std::min<int64_t>(ceil_div_i(L * KD, 256), 64)), static_cast<unsigned>(pairs), 2);
+    quantize_tensor_kernel<<<g2, 256, 0, st>>>(x64, amax, L, KD, qmax, lq, lk, sq, sk);
+    note_launch();
+}
+
 void run_predict(const PredictArgs& a, cudaStream_t st) {
     const bool force_dfma = options().predict_dfma;
     if (!force_dfma && predict_tc_supported(a)) {

@@ -172,6 +172,42 @@ def predict(p: Preset, q: torch.Tensor, k: torch.Tensor, P: torch.Tensor, stream
     return Levels(lq, lk, sq, sk)
 
 
+def predict_wtilde(p: Preset, wq: torch.Tensor, wk: torch.Tensor, x: torch.Tensor | None = None,
+                   P: torch.Tensor | None = None, r: torch.Tensor | None = None, stream=None):
+    """The reference predictor, approx_scores / approx_scores_from_r
+    (P/src/predictor.cpp:67-80): R = X P once per sample (returned), then per
+    head Q~ = quantize(R W~_Q[h]), K~ = quantize(R W~_K[h]), bit-exact fp64
+    chains.  x [batch, L, d_model] f64, P [d_model, k] f64 (or r [batch, L, k]
+    f64 instead), wq/wk [heads, k, k] f64, all CUDA.  Returns (Levels, r)."""
+    batch = (x if x is not None else r).shape[0]
+    if p.batch != batch:
+        raise ShapeError(f"predict_wtilde: preset batch {p.batch} != input batch {batch}")
+    for t in (wq, wk):
+        if t.shape != (p.heads, p.k, p.k) or t.dtype != torch.float64 or not t.is_cuda:
+            raise ShapeError(f"predict_wtilde: W~ must be [{p.heads}, {p.k}, {p.k}] float64 CUDA")
+    c = config_of(p)
+    dev = wq.device
+    dm = 0
+    if x is not None:
+        dm = x.shape[2]
+        if x.shape != (batch, p.L, dm) or P is None or P.shape != (dm, p.k):
+            raise ShapeError("approx_scores: X feature dim != d")
+        r = torch.empty((batch, p.L, p.k), dtype=torch.float64, device=dev)
+    elif r is None or r.shape != (batch, p.L, p.k):
+        raise ShapeError("approx_scores: R width != projection k")
+    pairs = p.pairs
+    lq = torch.empty((pairs, p.k // 8, p.L, 8), dtype=torch.bfloat16, device=dev)
+    lk = torch.empty_like(lq)
+    ns = (pairs,) if p.quant_scope == "tensor" else (pairs, p.L)
+    sq = torch.empty(ns, dtype=torch.float64, device=dev)
+    sk = torch.empty_like(sq)
+    ws = _ws(int(_abi.lib().dsa_predict_wtilde_workspace_bytes(C.byref(c))), dev, stream)
+    _abi.check(_abi.lib().dsa_predict_wtilde(C.byref(c), dm, _ptr(x), _ptr(P), _ptr(r), _ptr(wq.contiguous()),
+                                             _ptr(wk.contiguous()), _ptr(lq), _ptr(lk), _ptr(sq), _ptr(sk),
+                                             _ptr(ws), ws.numel(), _stream(stream)))
+    return Levels(lq, lk, sq, sk), r
+
+
 def alloc_mask(p: Preset, pairs: int, device, empty_rows: bool = True) -> Mask:
     cap = mask_capacity(p, pairs)
     cols = torch.empty(cap, dtype=torch.int32, device=device)
