@@ -9,9 +9,15 @@
 //   dsattn::gpu::block_mask           <- (block extension)
 //   dsattn::gpu::threshold_mask       <- threshold_mask (causal, fixed-point softmax, O6)
 //   dsattn::gpu::sparse_attention     <- sddmm -> sparse_softmax -> spmm    P/include/dsattn/sparse.hpp:47-55
-// The GPU entry points take the per-head Q and K (the reference's mask
-// generators take the dense S~ they would otherwise materialise; here S~ is
-// computed exactly on the tensor cores and never leaves the GPU).  Status
+//   dsattn::gpu::approx_levels / predicted_topk_mask(x, PredictorParams, keep)
+//                                     <- approx_scores / approx_scores_from_r (per-head W~)
+//                                        P/include/dsattn/predictor.hpp:44-49, the caller's
+//                                        predicted_topk_mask(approx_scores(x, pp), keep)
+//                                        (P/src/trainer.cpp:162,173-175,190-195)
+// The mask generators take the per-head Q and K (or X and PredictorParams)
+// instead of the dense S~ the reference would materialise: S~ is computed
+// exactly on the tensor cores (the integer product of the levels)
+// and never leaves the GPU.  Status
 // codes are rethrown as ShapeError / ParamError / ConfigError / IoError
 // (P/include/dsattn/errors.hpp:9-31), so CLI exit codes are unchanged.
 #pragma once
@@ -227,6 +233,85 @@ inline SparseMask run_select(const dsa_config& c, const DeviceLevels& lv) {
     return out;
 }
 
+inline DeviceBuffer upload_f64(const Matrix& m) {
+    DeviceBuffer d(m.size() * 8);
+    check_cuda(cudaMemcpy(d.get(), m.data(), d.size(), cudaMemcpyHostToDevice));
+    return d;
+}
+
+// approx_scores / approx_scores_from_r levels on the device (x or r given).
+inline DeviceLevels run_predict_wtilde(const dsa_config& c, const Matrix* x, const Matrix* r,
+                                       const PredictorParams& pp) {
+    pp.validate();
+    const Matrix& P = pp.proj->p;
+    DeviceBuffer dx, dp, dr(static_cast<size_t>(c.L * c.k) * 8);
+    if (x) {
+        if (x->cols() != P.rows()) throw ShapeError("approx_scores: X feature dim != d");
+        dx = upload_f64(*x);
+        dp = upload_f64(P);
+    } else {
+        if (r->cols() != P.cols()) throw ShapeError("approx_scores: R width != projection k");
+        dr = upload_f64(*r);
+    }
+    DeviceBuffer dwq = upload_f64(pp.wq), dwk = upload_f64(pp.wk);
+    DeviceLevels lv;
+    lv.lq = DeviceBuffer(static_cast<size_t>(c.L * c.k) * 2);
+    lv.lk = DeviceBuffer(static_cast<size_t>(c.L * c.k) * 2);
+    const size_t ns = c.quant_scope == DSA_QUANT_PER_ROW ? static_cast<size_t>(c.L) : 1;
+    lv.sq = DeviceBuffer(ns * 8);
+    lv.sk = DeviceBuffer(ns * 8);
+    DeviceBuffer ws(dsa_predict_wtilde_workspace_bytes(&c));
+    check(dsa_predict_wtilde(&c, x ? static_cast<int64_t>(x->cols()) : 0, x ? dx.as<double>() : nullptr,
+                             x ? dp.as<double>() : nullptr, dr.as<double>(), dwq.as<double>(), dwk.as<double>(),
+                             lv.lq.as<uint16_t>(), lv.lk.as<uint16_t>(), lv.sq.as<double>(), lv.sk.as<double>(),
+                             ws.get(), ws.size(), nullptr));
+    return lv;
+}
+
+// Every operand f32 (true) or every operand f64 (false): the device chain
+// rounds all of the predictor's matmuls alike (round_proj_f32).
+inline bool uniform_f32(std::initializer_list<const Matrix*> ms) {
+    size_t n32 = 0;
+    for (const Matrix* m : ms) n32 += m->precision() == Precision::f32;
+    if (n32 != 0 && n32 != ms.size())
+        throw ParamError("dsattn::gpu: mixed f32/f64 predictor operands are not supported");
+    return n32 != 0;
+}
+
+inline dsa_config wtilde_config(size_t L, const PredictorParams& pp, bool f32) {
+    dsa_config c{};
+    c.batch = c.heads = 1;
+    c.L = static_cast<int64_t>(L);
+    c.d = 64;  // unused by the predictor; a valid head width for dsa_config_validate
+    c.k = static_cast<int64_t>(pp.proj->p.cols());
+    c.dtype = DSA_BF16;
+    c.bits = pp.quant.bits;
+    c.quant_scope = DSA_QUANT_PER_TENSOR;
+    c.round_proj_f32 = f32 ? 1 : 0;
+    c.scale = 1;
+    c.keep = 1;
+    c.vec_v = 8;
+    c.block = 32;
+    c.frac_num = 1;
+    c.frac_den = 20;
+    c.cap = c.L;
+    return c;
+}
+
+inline Matrix levels_to_matrix(const DeviceBuffer& d, size_t L, size_t K) {
+    std::vector<uint16_t> h(L * K);
+    check_cuda(cudaMemcpy(h.data(), d.get(), h.size() * 2, cudaMemcpyDeviceToHost));
+    Matrix m(L, K);
+    for (size_t r = 0; r < L; ++r)
+        for (size_t c = 0; c < K; ++c) {  // chunk-planar [K/8][L][8] -> row-major
+            uint32_t u = static_cast<uint32_t>(h[((c / 8) * L + r) * 8 + c % 8]) << 16;
+            float f;
+            std::memcpy(&f, &u, 4);
+            m.raw()[r * K + c] = f;
+        }
+    return m;
+}
+
 }  // namespace detail
 
 // Integer levels (held exactly in f64 Matrices) and scales of quant(Q.P),
@@ -262,6 +347,45 @@ inline Levels predict(const Matrix& q, const Matrix& k, const Matrix& p, QuantSp
         check_cuda(cudaMemcpy(s.data(), (w ? lv.sk : lv.sq).get(), s.size() * 8, cudaMemcpyDeviceToHost));
     }
     return out;
+}
+
+// approx_scores(x, pp) / approx_scores_from_r(r, pp) (P/src/predictor.cpp:
+// 67-80) as exact integer levels + per-tensor scales: R = X P, Q~ =
+// quantize(R W~_Q), K~ = quantize(R W~_K) -- bit-identical to the
+// reference's (fp64 chains on the device; f32 when every operand is f32).
+// S~ = s_q s_k (levels_q levels_k^T).
+inline Levels approx_levels(const Matrix& x, const PredictorParams& pp) {
+    const bool f32 = detail::uniform_f32({&x, &pp.proj->p, &pp.wq, &pp.wk});
+    dsa_config c = detail::wtilde_config(x.rows(), pp, f32);
+    check(dsa_config_validate(&c));
+    detail::DeviceLevels lv = detail::run_predict_wtilde(c, &x, nullptr, pp);
+    Levels out{detail::levels_to_matrix(lv.lq, x.rows(), c.k), detail::levels_to_matrix(lv.lk, x.rows(), c.k),
+               std::vector<double>(1), std::vector<double>(1)};
+    check_cuda(cudaMemcpy(out.scale_q.data(), lv.sq.get(), 8, cudaMemcpyDeviceToHost));
+    check_cuda(cudaMemcpy(out.scale_k.data(), lv.sk.get(), 8, cudaMemcpyDeviceToHost));
+    return out;
+}
+
+// The reference caller's predicted mask, predicted_topk_mask(approx_scores(x,
+// pp), keep) (P/src/trainer.cpp:190-195), ranked on the exact integer S~
+// (ties to the lowest column).
+inline SparseMask predicted_topk_mask(const Matrix& x, const PredictorParams& pp, size_t keep_per_row) {
+    const bool f32 = detail::uniform_f32({&x, &pp.proj->p, &pp.wq, &pp.wk});
+    dsa_config c = detail::wtilde_config(x.rows(), pp, f32);
+    c.mask_mode = DSA_MASK_ROW_TOPK;
+    c.keep = static_cast<int64_t>(keep_per_row);
+    check(dsa_config_validate(&c));
+    return detail::run_select(c, detail::run_predict_wtilde(c, &x, nullptr, pp));
+}
+
+// Same from a precomputed R = X P (approx_scores_from_r).
+inline SparseMask predicted_topk_mask_from_r(const Matrix& r, const PredictorParams& pp, size_t keep_per_row) {
+    const bool f32 = detail::uniform_f32({&r, &pp.wq, &pp.wk});
+    dsa_config c = detail::wtilde_config(r.rows(), pp, f32);
+    c.mask_mode = DSA_MASK_ROW_TOPK;
+    c.keep = static_cast<int64_t>(keep_per_row);
+    check(dsa_config_validate(&c));
+    return detail::run_select(c, detail::run_predict_wtilde(c, nullptr, &r, pp));
 }
 
 inline SparseMask predicted_topk_mask(const Matrix& q, const Matrix& k, const Matrix& p,
@@ -315,8 +439,66 @@ inline SparseMask threshold_mask(const Matrix& q, const Matrix& k, const Matrix&
     return detail::run_select(c, detail::run_predict(c, q, k, p));
 }
 
+namespace detail {
+
+// The densest device layout a reference SparseMask fits (dsa_mask, dsa_b200.h):
+//   COLVEC   every 8-row band shares one list (band-shared tensor-core tiles)
+//   BLOCK    32 x 32 blocks: every 32-row block row shares a list that is a
+//            union of whole, aligned 32-column blocks (L % 32 == 0)
+//   ROW_TOPK every row keeps the same number of keys
+//   THRESHOLD (CSR) anything else (ragged rows, empty rows)
+struct MaskLayout {
+    dsa_mask_mode mode;
+    int64_t keep;
+    std::vector<uint32_t> cols;
+    std::vector<uint64_t> rowptr;
+};
+
+inline MaskLayout layout_of(const SparseMask& m) {
+    const size_t L = m.l;
+    MaskLayout out{DSA_MASK_THRESHOLD, 0, {}, {}};
+    bool uniform = L > 0 && !m.kept[0].empty();
+    for (size_t i = 1; i < L && uniform; ++i) uniform = m.kept[i].size() == m.kept[0].size();
+    if (uniform) {
+        const size_t n = m.kept[0].size();
+        bool bands = true;
+        for (size_t i = 0; i < L && bands; ++i) bands = m.kept[i] == m.kept[i - i % 8];
+        bool blocks = L % 32 == 0 && n % 32 == 0;
+        for (size_t i = 0; i < L && blocks; ++i) blocks = m.kept[i] == m.kept[i - i % 32];
+        for (size_t i = 0; i < L && blocks; i += 32)
+            for (size_t t = 0; t < n && blocks; ++t)
+                blocks = m.kept[i][t] == m.kept[i][t - t % 32] + t % 32 && m.kept[i][t - t % 32] % 32 == 0;
+        if (blocks) {
+            out.mode = DSA_MASK_BLOCK;
+            out.keep = static_cast<int64_t>(n / 32);
+            for (size_t i = 0; i < L; i += 32)
+                for (size_t t = 0; t < n; t += 32) out.cols.push_back(m.kept[i][t] / 32);
+        } else if (bands) {
+            out.mode = DSA_MASK_COLVEC;
+            out.keep = static_cast<int64_t>(n);
+            for (size_t i = 0; i < L; i += 8) out.cols.insert(out.cols.end(), m.kept[i].begin(), m.kept[i].end());
+        } else {
+            out.mode = DSA_MASK_ROW_TOPK;
+            out.keep = static_cast<int64_t>(n);
+            for (size_t i = 0; i < L; ++i) out.cols.insert(out.cols.end(), m.kept[i].begin(), m.kept[i].end());
+        }
+        return out;
+    }
+    out.rowptr.assign(L + 1, 0);
+    for (size_t i = 0; i < L; ++i) {
+        out.rowptr[i + 1] = out.rowptr[i] + m.kept[i].size();
+        out.cols.insert(out.cols.end(), m.kept[i].begin(), m.kept[i].end());
+    }
+    return out;
+}
+
+}  // namespace detail
+
 // sddmm -> sparse_softmax -> spmm for one head; empty rows give zero rows
-// (flagged in *empty_rows when given).  Output precision follows V.
+// (flagged in *empty_rows when given).  Output precision follows V.  The
+// mask is routed by its structure (detail::layout_of): band-shared and
+// block masks reach the tensor-core band / block kernels, uniform rows the
+// row-list layout, everything else the CSR layout.
 inline Matrix sparse_attention(const Matrix& q, const Matrix& k, const Matrix& v,
                                const SparseMask& mask, bool scale,
                                std::vector<uint8_t>* empty_rows = nullptr) {
@@ -326,6 +508,7 @@ inline Matrix sparse_attention(const Matrix& q, const Matrix& k, const Matrix& v
     if (v.cols() != q.cols()) throw ShapeError("dsattn::gpu: needs d_v == d_k");
     mask.validate();
     const dsa_dtype dt = detail::pick_dtype({&q, &k, &v});
+    const detail::MaskLayout ml = detail::layout_of(mask);
     dsa_config c{};
     c.batch = c.heads = 1;
     c.L = static_cast<int64_t>(q.rows());
@@ -333,23 +516,25 @@ inline Matrix sparse_attention(const Matrix& q, const Matrix& k, const Matrix& v
     c.k = 16;
     c.dtype = dt;
     c.bits = 4;
-    c.mask_mode = DSA_MASK_THRESHOLD;  // general CSR layout
+    c.mask_mode = ml.mode;
+    c.keep = std::max<int64_t>(ml.keep, 1);
+    c.vec_v = 8;
+    c.block = 32;
     c.scale = scale ? 1 : 0;
     c.frac_num = 1;
     c.frac_den = 1;
     c.cap = c.L;
     check(dsa_config_validate(&c));
-    std::vector<uint64_t> rp(mask.l + 1, 0);
-    std::vector<uint32_t> cols;
-    for (size_t i = 0; i < mask.l; ++i) {
-        rp[i + 1] = rp[i] + mask.kept[i].size();
-        cols.insert(cols.end(), mask.kept[i].begin(), mask.kept[i].end());
-    }
     DeviceBuffer dq = detail::upload(q, dt), dk = detail::upload(k, dt), dv = detail::upload(v, dt);
-    DeviceBuffer dz(dq.size()), drp(rp.size() * 8), dc(std::max<size_t>(cols.size(), 1) * 4), de(mask.l);
-    check_cuda(cudaMemcpy(drp.get(), rp.data(), rp.size() * 8, cudaMemcpyHostToDevice));
-    if (!cols.empty()) check_cuda(cudaMemcpy(dc.get(), cols.data(), cols.size() * 4, cudaMemcpyHostToDevice));
-    dsa_mask m{dc.as<uint32_t>(), drp.as<uint64_t>(), static_cast<int64_t>(cols.size()), de.as<uint8_t>()};
+    DeviceBuffer dz(dq.size()), drp(std::max<size_t>(ml.rowptr.size(), 1) * 8),
+        dc(std::max<size_t>(ml.cols.size(), 1) * 4), de(mask.l);
+    if (!ml.rowptr.empty())
+        check_cuda(cudaMemcpy(drp.get(), ml.rowptr.data(), ml.rowptr.size() * 8, cudaMemcpyHostToDevice));
+    if (!ml.cols.empty())
+        check_cuda(cudaMemcpy(dc.get(), ml.cols.data(), ml.cols.size() * 4, cudaMemcpyHostToDevice));
+    if (ml.mode != DSA_MASK_THRESHOLD) check_cuda(cudaMemset(de.get(), 0, mask.l));
+    dsa_mask m{dc.as<uint32_t>(), ml.rowptr.empty() ? nullptr : drp.as<uint64_t>(),
+               static_cast<int64_t>(ml.cols.size()), de.as<uint8_t>()};
     check(dsa_sparse_attention(&c, dq.get(), dk.get(), dv.get(), &m, dz.get(), nullptr));
     Matrix z(mask.l, v.cols(), v.precision());
     if (dt == DSA_BF16) {

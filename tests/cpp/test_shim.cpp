@@ -4,7 +4,9 @@
 // Built by oracle/Makefile (target shim_test) into oracle/_ref/test_shim;
 // run on a GPU by tests/test_gpu_cpp_shim.py.  Cases mirror the reference's
 // own tests (P/tests/test_linalg.cpp:97-101, test_maskgen.cpp, test_sparse.cpp).
+#include <algorithm>
 #include <cmath>
+#include <memory>
 #include <cstring>
 #include <cstdio>
 #include <vector>
@@ -167,6 +169,115 @@ int main() {
         CHECK(max_abs_diff(zg, zr) <= 2e-2 * max_abs(zr));
         CHECK(zg(7, 64) == 0.0 && zg(7, 127) == 0.0);
         CHECK(throws<ShapeError>([&] { gpu::sparse_attention(x, ap, std::span<const SparseMask>(masks.data(), 2)); }));
+    }
+
+    // threshold_mask mirror.  Full rows, no cap: the reference threshold_mask
+    // itself on c * S~ post-softmax (P/src/maskgen.cpp:22-31).  Causal + cap:
+    // row_softmax over j <= i, ">= theta", the cap largest S~ by
+    // row_topk_indices.
+    {
+        const double sq = max_abs(matmul(q, p)) / 7.0, sk = max_abs(matmul(kk, p)) / 7.0;
+        const double c = sq * sk / std::sqrt(static_cast<double>(d));
+        const Matrix s = matmul_nt(rq, rk);
+        SparseMask gt = gpu::threshold_mask(q, kk, p, QuantSpec{4}, 1, 20, L, false);
+        CHECK(gt == threshold_mask(scale(s, c), 20.0 / L, true));
+        const double theta = 4.0 / L;
+        SparseMask gcz = gpu::threshold_mask(q, kk, p, QuantSpec{4}, 1, 4, 6, true);
+        bool ok = true;
+        size_t capped = 0;
+        for (size_t i = 0; i < L; ++i) {
+            Matrix x(1, i + 1);
+            for (size_t j = 0; j <= i; ++j) x.raw()[j] = s(i, j);
+            const Matrix pr = row_softmax(scale(x, c));
+            std::vector<uint32_t> kept;
+            for (uint32_t j = 0; j <= i; ++j)
+                if (pr(0, j) >= theta) kept.push_back(j);
+            if (kept.size() > 6) {
+                ++capped;
+                Matrix key(1, i + 1);
+                for (size_t j = 0; j <= i; ++j) key.raw()[j] = -1e300;
+                for (uint32_t j : kept) key.raw()[j] = x(0, j);
+                kept = row_topk_indices(key, 6)[0];
+            }
+            ok &= gcz.kept[i] == kept;
+        }
+        CHECK(ok);
+        CHECK(capped > 0);
+    }
+
+    // block_mask mirror: 32 x 32 block means, the diagonal block
+    // forced, row_topk_indices over the block row; L = 300 leaves a ragged
+    // 12-row / 12-column last block
+    {
+        const Matrix s = matmul_nt(rq, rk);
+        const size_t bs = 32, nb = (L + bs - 1) / bs, keep = 3;
+        SparseMask gb = gpu::block_mask(q, kk, p, QuantSpec{4}, bs, keep, true);
+        bool ok = true;
+        for (size_t ib = 0; ib < nb; ++ib) {
+            Matrix mean(1, nb);
+            const size_t r0 = ib * bs, r1 = std::min(L, r0 + bs);
+            for (size_t jb = 0; jb < nb; ++jb) {
+                const size_t c0 = jb * bs, c1 = std::min(L, c0 + bs);
+                double sum = 0;
+                for (size_t i = r0; i < r1; ++i)
+                    for (size_t j = c0; j < c1; ++j) sum += s(i, j);
+                mean.raw()[jb] = sum / static_cast<double>((r1 - r0) * (c1 - c0));
+            }
+            mean.raw()[ib] = 1e300;
+            std::vector<uint32_t> cols;
+            for (uint32_t jb : row_topk_indices(mean, keep)[0])
+                for (size_t j = jb * bs; j < std::min(L, (jb + 1) * bs); ++j) cols.push_back(static_cast<uint32_t>(j));
+            for (size_t i = r0; i < r1; ++i) ok &= gb.kept[i] == cols;
+        }
+        CHECK(ok);
+    }
+
+    // the reference predictor with its per-head W~: approx_scores(x, pp)
+    // levels bit-exact (R = X P, quantize(R W~)), and the caller's
+    // predicted_topk_mask on the exact integer S~ (P/src/trainer.cpp:162-195)
+    {
+        Rng wrng(7);
+        const size_t dm = 96, Lx = 257;
+        auto proj = std::make_shared<const ProjectionMatrix>(init_projection(dm, k, 11));
+        PredictorParams pp = random_predictor_params(proj, 0.3, wrng, QuantSpec{4});
+        Matrix x = random_normal(Lx, dm, 0.0, 1.0, wrng);
+        const Matrix r = matmul(x, proj->p);
+        auto lev = [&](const Matrix& w) {
+            const Matrix xw = matmul(r, w);
+            const Matrix qt = quantize(xw, QuantSpec{4});
+            const double sc = max_abs(xw) / 7.0;
+            Matrix lv(qt.rows(), qt.cols());
+            for (size_t i = 0; i < qt.size(); ++i) lv.raw()[i] = std::lround(qt.data()[i] / sc);
+            return lv;
+        };
+        const Matrix lq = lev(pp.wq), lk = lev(pp.wk);
+        gpu::Levels gl = gpu::approx_levels(x, pp);
+        CHECK(max_abs_diff(gl.q, lq) == 0.0 && max_abs_diff(gl.k, lk) == 0.0);
+        CHECK(gl.scale_q[0] == max_abs(matmul(r, pp.wq)) / 7.0);
+        CHECK(gpu::predicted_topk_mask(x, pp, 17) == predicted_topk_mask(matmul_nt(lq, lk), 17));
+        CHECK(gpu::predicted_topk_mask_from_r(r, pp, 9) == predicted_topk_mask(matmul_nt(lq, lk), 9));
+        CHECK(throws<ShapeError>([&] { gpu::predicted_topk_mask(Matrix(Lx, dm + 1), pp, 3); }));
+    }
+
+    // per-head sparse_attention routed by mask structure: band-shared
+    // (COLVEC) and 32 x 32 block masks reach the tensor-core kernels; same
+    // result as the reference within the bf16 bar
+    {
+        const size_t Lb = 256;
+        Matrix qb = bf16_normal(Lb, d, rng), kb = bf16_normal(Lb, d, rng), vb = bf16_normal(Lb, d, rng);
+        SparseMask band(Lb), blk(Lb);
+        for (size_t i = 0; i < Lb; ++i) {
+            for (uint32_t j = (i / 8) % 5; j < Lb; j += 7) band.kept[i].push_back(j);
+            // block row ib keeps blocks ib and (ib + 3) % 8
+            for (uint32_t b : {static_cast<uint32_t>(i / 32), static_cast<uint32_t>((i / 32 + 3) % 8)})
+                for (uint32_t j = b * 32; j < b * 32 + 32; ++j) blk.kept[i].push_back(j);
+            std::sort(blk.kept[i].begin(), blk.kept[i].end());
+        }
+        for (const SparseMask* m : {&band, &blk}) {
+            Matrix zg = gpu::sparse_attention(qb, kb, vb, *m, true);
+            Matrix zr = spmm(sparse_softmax(sddmm(qb, kb, *m, true)), vb);
+            CHECK(max_abs_diff(zg, zr) <= 1e-2 * max_abs(zr));
+        }
     }
 
     // reference exception types (P/include/dsattn/errors.hpp)
