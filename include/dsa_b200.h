@@ -195,6 +195,13 @@ int dsa_pipeline_fused(const dsa_config* cfg);
  * bench.py reads it around timed regions. */
 uint64_t dsa_launch_counter(void);
 
+/* prediction_accuracy (P/src/maskgen.cpp:94-107) between two device masks
+ * of cfg's layout over all pairs: |pred n oracle| / |pred|.  Per-row
+ * counts must be equal (ParamError otherwise, as the reference); empty
+ * masks are a ParamError.  Synchronises `stream`. */
+dsa_status dsa_prediction_accuracy(const dsa_config* cfg, const dsa_mask* pred, const dsa_mask* oracle,
+                                   double* accuracy, void* stream);
+
 /* Exact operation counts for a computed mask (synchronises `stream`). */
 dsa_status dsa_counters(const dsa_config* cfg, const dsa_mask* mask, dsa_counts* out,
                         void* stream);

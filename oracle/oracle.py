@@ -208,6 +208,7 @@ class Reference:
             "ref_levels_wtilde": (I32, [C.c_void_p, C.c_void_p, C.c_void_p, _d, I64, I64, I64, I32, I32,
                                         C.c_void_p, _i32, C.POINTER(C.c_double)]),
             "ref_init_projection": (I32, [I64, I64, C.c_uint64, _d]),
+            "ref_prediction_accuracy": (I32, [I64, _u64, _u32, _u64, _u32, C.POINTER(C.c_double)]),
             "ref_block_mask": (I32, [_i32, _i32, I64, I64, I64, I64, I32, _u32]),
             "ref_causal_threshold_mask": (I32, [_i32, _i32, I64, I64, D, D, I64, I32, _u64, C.c_void_p]),
             "ref_threshold_row_probs": (I32, [_i32, _i32, I64, I64, D, I64, I32, _d]),
@@ -393,6 +394,13 @@ class Reference:
         self._chk(self.L.ref_levels_wtilde(ptr(xp), ptr(pp), ptr(rin), w, L, dm, k, bits, int(f32),
                                            rout.ctypes.data_as(C.c_void_p), lv, C.byref(s)))
         return lv, s.value, rout
+
+    def prediction_accuracy(self, rp_pred, c_pred, rp_orc, c_orc):
+        out = C.c_double()
+        f = lambda a, t: np.ascontiguousarray(a if len(a) else np.zeros(1), t)  # noqa: E731
+        self._chk(self.L.ref_prediction_accuracy(len(rp_pred) - 1, f(rp_pred, np.uint64), f(c_pred, np.uint32),
+                                                 f(rp_orc, np.uint64), f(c_orc, np.uint32), C.byref(out)))
+        return out.value
 
     def init_projection(self, d, k, seed):
         out = np.empty((d, k))

@@ -134,6 +134,15 @@ int ref_levels_wtilde(const double* x, const double* p, const double* r_in, cons
     });
 }
 
+// prediction_accuracy (P/src/maskgen.cpp:94-107) of two CSR masks.
+int ref_prediction_accuracy(int64_t L, const uint64_t* rp_pred, const uint32_t* c_pred, const uint64_t* rp_orc,
+                            const uint32_t* c_orc, double* out) {
+    return guarded([&] {
+        *out = prediction_accuracy(mask_from_csr(static_cast<size_t>(L), rp_pred, c_pred),
+                                   mask_from_csr(static_cast<size_t>(L), rp_orc, c_orc));
+    });
+}
+
 // init_projection (P/src/predictor.cpp:10-20): the reference's ternary P.
 int ref_init_projection(int64_t d, int64_t k, uint64_t seed, double* p) {
     return guarded([&] { from_matrix(init_projection(static_cast<size_t>(d), static_cast<size_t>(k), seed).p, p); });

@@ -55,6 +55,8 @@ _SIGS = {
     "dsa_predict_wtilde": (C.c_int, [C.POINTER(DsaConfig), C.c_int64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
                                      C.c_size_t, _P]),
     "dsa_pipeline_fused": (C.c_int, [C.POINTER(DsaConfig)]),
+    "dsa_prediction_accuracy": (C.c_int, [C.POINTER(DsaConfig), C.POINTER(DsaMask), C.POINTER(DsaMask),
+                                          C.POINTER(C.c_double), _P]),
     "dsa_project_qkv": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
                                   C.c_int64, _P, _P, _P, _P, _P, _P, _P]),
     "dsa_counters": (C.c_int, [C.POINTER(DsaConfig), C.POINTER(DsaMask), C.POINTER(DsaCounts), _P]),

@@ -658,6 +658,31 @@ dsa_status dsa_pipeline(const dsa_config* cfg, const void* q, const void* k, con
     });
 }
 
+dsa_status dsa_prediction_accuracy(const dsa_config* cfg, const dsa_mask* pred, const dsa_mask* oracle,
+                                   double* accuracy, void* stream) {
+    return guard([&] {
+        validate(cfg);
+        require_device();
+        if (!pred || !oracle || !accuracy || !pred->cols || !oracle->cols)
+            throw Error(DSA_ERR_PARAM, "dsa_prediction_accuracy: null pointer");
+        if (cfg->mask_mode == DSA_MASK_THRESHOLD && (!pred->rowptr || !oracle->rowptr))
+            throw Error(DSA_ERR_PARAM, "dsa_prediction_accuracy: threshold masks need rowptr");
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        unsigned long long* d = nullptr;
+        check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&d), 3 * sizeof(unsigned long long), st), "alloc");
+        check_cuda(cudaMemsetAsync(d, 0, 3 * sizeof(unsigned long long), st), "memset");
+        run_prediction_accuracy(attn_args(*cfg, nullptr, nullptr, nullptr, *pred, nullptr),
+                                attn_args(*cfg, nullptr, nullptr, nullptr, *oracle, nullptr), d, st);
+        unsigned long long h[3] = {0, 0, 0};
+        check_cuda(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, st), "copy");
+        check_cuda(cudaFreeAsync(d, st), "free");
+        check_cuda(cudaStreamSynchronize(st), "sync");
+        if (h[2] != 0) throw Error(DSA_ERR_PARAM, "prediction_accuracy: per-row counts differ");
+        if (h[1] == 0) throw Error(DSA_ERR_PARAM, "prediction_accuracy: empty masks");
+        *accuracy = static_cast<double>(h[0]) / static_cast<double>(h[1]);
+    });
+}
+
 int dsa_pipeline_fused(const dsa_config* cfg) {
     int out = -1;
     guard([&] {

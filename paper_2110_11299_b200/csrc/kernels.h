@@ -156,6 +156,8 @@ struct AttnArgs {
     uint8_t* empty_rows;
 };
 void run_attention(const AttnArgs& a, cudaStream_t st);
+// prediction_accuracy counts {intersection, total, rows with unequal counts}
+void run_prediction_accuracy(const AttnArgs& pred, const AttnArgs& orc, unsigned long long* out, cudaStream_t st);
 bool band_attention_supported(const AttnArgs& a);
 void run_band_attention(const AttnArgs& a, cudaStream_t st);
 // fused COLVEC select + band attention (mask optional): dsa_pipeline

@@ -339,6 +339,17 @@ def fused_pipeline(p: Preset, pairs: int | None = None) -> bool:
     return r == 1
 
 
+def prediction_accuracy(p: Preset, pred: Mask, oracle: Mask, pairs: int, stream=None) -> float:
+    """prediction_accuracy (P/src/maskgen.cpp:94-107) of two device masks of
+    the preset's layout: |pred n oracle| / |pred| over every pair."""
+    c = config_of(p, pairs)
+    out = C.c_double()
+    a, b = pred.as_c(), oracle.as_c()
+    _abi.check(_abi.lib().dsa_prediction_accuracy(C.byref(c), C.byref(a), C.byref(b), C.byref(out),
+                                                  _stream(stream)))
+    return out.value
+
+
 def launch_counter() -> int:
     return int(_abi.lib().dsa_launch_counter())
 
