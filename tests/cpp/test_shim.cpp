@@ -66,7 +66,10 @@ static Matrix ref_levels(const Matrix& x, const Matrix& p, int bits) {
     return lv;
 }
 
+#define STEP(name) std::printf("-- %s\n", name)
+
 int main() {
+    std::setvbuf(stdout, nullptr, _IONBF, 0);
     Rng rng(2110);
     const size_t L = 300, d = 64, k = 16;
     Matrix q = bf16_normal(L, d, rng), kk = bf16_normal(L, d, rng), v = bf16_normal(L, d, rng);
@@ -129,6 +132,7 @@ int main() {
         CHECK(zero && flags[3] == 1 && flags[2] == 0);
     }
 
+    STEP("project_qkv");
     // project_qkv vs the reference (P/src/attention.cpp:36-46) on bf16-exact
     // operands: within the bf16 bar per head
     {
@@ -171,6 +175,7 @@ int main() {
         CHECK(throws<ShapeError>([&] { gpu::sparse_attention(x, ap, std::span<const SparseMask>(masks.data(), 2)); }));
     }
 
+    STEP("threshold");
     // threshold_mask mirror.  Full rows, no cap: the reference threshold_mask
     // itself on c * S~ post-softmax (P/src/maskgen.cpp:22-31).  Causal + cap:
     // row_softmax over j <= i, ">= theta", the cap largest S~ by
@@ -205,6 +210,7 @@ int main() {
         CHECK(capped > 0);
     }
 
+    STEP("block");
     // block_mask mirror: 32 x 32 block means, the diagonal block
     // forced, row_topk_indices over the block row; L = 300 leaves a ragged
     // 12-row / 12-column last block
@@ -225,13 +231,15 @@ int main() {
             }
             mean.raw()[ib] = 1e300;
             std::vector<uint32_t> cols;
-            for (uint32_t jb : row_topk_indices(mean, keep)[0])
+            const std::vector<uint32_t> top = row_topk_indices(mean, keep)[0];
+            for (uint32_t jb : top)
                 for (size_t j = jb * bs; j < std::min(L, (jb + 1) * bs); ++j) cols.push_back(static_cast<uint32_t>(j));
             for (size_t i = r0; i < r1; ++i) ok &= gb.kept[i] == cols;
         }
         CHECK(ok);
     }
 
+    STEP("wtilde");
     // the reference predictor with its per-head W~: approx_scores(x, pp)
     // levels bit-exact (R = X P, quantize(R W~)), and the caller's
     // predicted_topk_mask on the exact integer S~ (P/src/trainer.cpp:162-195)
@@ -259,6 +267,7 @@ int main() {
         CHECK(throws<ShapeError>([&] { gpu::predicted_topk_mask(Matrix(Lx, dm + 1), pp, 3); }));
     }
 
+    STEP("routing");
     // per-head sparse_attention routed by mask structure: band-shared
     // (COLVEC) and 32 x 32 block masks reach the tensor-core kernels; same
     // result as the reference within the bf16 bar
