@@ -1,0 +1,484 @@
+// Phase 2 for vector-wise masks (COLVEC, v = 8, <= 4-bit levels): the exact
+// integer score GEMM on the 5th-gen tensor cores fused with band
+// max-pooling, an in-flight histogram per band and exact top-k selection,
+// optionally fused with the band attention (dsa_pipeline).
+//
+// Reference rule (P/src/maskgen.cpp:33-61): bands of 8 query
+// rows, band score of key j = max over the band rows of the exact integer
+// S~[i][j], keep `keep` keys per band by row_topk_indices (value desc, the
+// LOWER key first among equals, P/src/linalg.cpp:77-80), ascending list.
+//
+// One CTA = 64 queries (8 bands) of one (b,h) pair, 9 warps:
+//   * warp 8 (producer, one lane): K~ tiles (128 keys) by bulk TMA copies
+//     straight from the chunk-planar levels (one copy per 8-column plane)
+//     into a 4-stage ring, one tcgen05.mma (M = 128 keys, N = 64 queries,
+//     K = 16 per instruction) per tile into one of 4 TMEM accumulators,
+//     commits to the accumulator's "full" and the stage's "empty" barrier;
+//   * warps 0-7 (epilogue): warp w drains TMEM lanes 32 (w & 3).. (= keys)
+//     x columns 32 (w >> 2).. (= 4 bands) with ONE tcgen05.ld per tile and
+//     frees the accumulator, then per band: max over 8 columns (FMNMX3), one
+//     FADD with 1.5 2^23 + 2^14 (bits = 0x4B404000 + v), whose low 16 bits
+//     are stored as the band's pooled code (0x4000 + v: a positive normal
+//     f16, monotone in v) and whose bits address the band's histogram word
+//     (M - v) of one RED -- 8 instructions per (band, key);
+// then per band (one warp each): the keep-th largest value T from the
+// histogram (top-down cumulative counts, 256 bins per warp step), one pass
+// over the band's pooled codes with packed f16 compares (HSET2, 8 keys per
+// 16-byte load) building a key bitmap of v >= T, a warp prefix sum placing
+// every such key in ascending order, and a pass over that short list
+// dropping the surplus ties (lowest keys kept).  The L x L scores never
+// leave the SM.
+//
+// FUSED (d = 64, k = 16): the 8 warps then run the band attention
+// (band_core.cuh) on their lists straight from shared memory, so the mask
+// never touches HBM unless the caller asks for it.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "band_core.cuh"
+#include "device_common.cuh"
+#include "kernels.h"
+#include "tc_sm100.cuh"
+
+namespace dsa {
+namespace {
+
+constexpr int kMT = 128;       // keys per tile (UMMA M)
+constexpr int kNQ = 64;        // queries per CTA (UMMA N) = 8 bands
+constexpr int kBands = kNQ / 8;
+constexpr int kStages = 4;     // K~ ring
+constexpr int kAcc = 4;        // TMEM accumulators (kNQ columns each)
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = (kEpiWarps + 1) * 32;
+constexpr int kList = 512;     // per-band staging list (keys)
+constexpr uint32_t kCodeBias = 0x4B404000u;  // bits of 1.5 * 2^23 + 2^14
+constexpr float kCodeMagic = 12599296.0f;    // 1.5 * 2^23 + 2^14
+
+template <int KD>
+struct Layout {
+    static constexpr int kPlanesA = KD / 8;
+    static constexpr int kTile = kMT * KD * 2;          // one K~ tile (bytes)
+    static constexpr int kQ = kNQ * KD * 2;             // the Q~ block
+    static constexpr int kMaxM = KD * 49;               // |score| bound, qmax <= 7
+    static constexpr int kBins = (2 * kMaxM + 1 + 255) / 256 * 256;  // per band pair (u32 = 2 x u16)
+    static constexpr int kHist = (kBands / 2) * kBins * 4;
+    static constexpr int kObuf = kBands * kList * 4;
+    static constexpr int kHistRegion = kHist > kObuf ? kHist : kObuf;
+    static constexpr int kBars = (2 * kStages + 2 * kAcc + 1) * 8 + 16;
+    // ring + pooled codes (reused by the fused attention's per-warp buffers)
+    __host__ __device__ static size_t work_bytes(int64_t L, bool fused) {
+        const size_t nt = static_cast<size_t>((L + kMT - 1) / kMT);
+        const size_t w = static_cast<size_t>(kStages) * kTile + static_cast<size_t>(kBands) * nt * kMT * 2;
+        const size_t f = fused ? sizeof(bc::BandSmemV2<64>) * kEpiWarps : 0;
+        return w > f ? w : f;
+    }
+    __host__ __device__ static size_t smem_bytes(int64_t L, bool fused) { return kQ + work_bytes(L, fused) + kHistRegion + kBars; }
+};
+
+__device__ __forceinline__ void named_sync_epi() { asm volatile("bar.sync 1, %0;\n" ::"n"(kEpiWarps * 32) : "memory"); }
+
+__device__ __forceinline__ void sts_u16(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared.u16 [%0], %1;\n" ::"r"(addr), "h"(static_cast<unsigned short>(v)) : "memory");
+}
+__device__ __forceinline__ void red_add(uint32_t addr, uint32_t v) {
+    asm volatile("red.shared.add.u32 [%0], %1;\n" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+    uint4 r;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];\n" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(addr));
+    return r;
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
+    unsigned short v;
+    asm volatile("ld.shared.u16 %0, [%1];\n" : "=h"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+__device__ __forceinline__ uint32_t hge2(uint32_t a, uint32_t b) {
+    return __hge2_mask(*reinterpret_cast<const __half2*>(&a), *reinterpret_cast<const __half2*>(&b));
+}
+
+// Byte offset of key j's pooled code inside its band row (a row = Lp codes):
+// 128-key segments of 16 16-byte chunks, chunk c stored at c ^ (seg & 7), so
+// 32 lanes reading chunk c of 32 consecutive segments hit every bank group
+// 4 times (the minimum), and the epilogue's 32 consecutive keys stay in one
+// 128-byte row.
+__device__ __forceinline__ uint32_t code_off(int j) {
+    const int seg = j >> 7, c = (j >> 3) & 15;
+    return static_cast<uint32_t>(((seg << 4) + (c ^ (seg & 7))) << 4) + ((j & 7) << 1);
+}
+
+struct FusedAttn {
+    const __nv_bfloat16* q;
+    const __nv_bfloat16* k;
+    const __nv_bfloat16* v;
+    __nv_bfloat16* z;
+    int scale;
+};
+
+template <int KD, bool FUSED>
+__global__ void __launch_bounds__(kThreads, 2)
+    colvec_kernel(const uint16_t* __restrict__ lq, const uint16_t* __restrict__ lk, int L, int keep, int M,
+                  uint32_t* __restrict__ out, FusedAttn fa) {
+    using Lay = Layout<KD>;
+    extern __shared__ __align__(1024) unsigned char smem[];
+    const int nt = (L + kMT - 1) / kMT;
+    const int Lp = nt * kMT;
+    const size_t work = Lay::work_bytes(L, FUSED);
+    unsigned char* q_sm = smem;
+    unsigned char* ring = smem + Lay::kQ;
+    unsigned char* pooled = ring + kStages * Lay::kTile;
+    unsigned char* histp = smem + Lay::kQ + work;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(histp + Lay::kHistRegion);
+    uint64_t* full = bars;                   // [kStages] TMA -> MMA
+    uint64_t* empty = bars + kStages;        // [kStages] MMA done -> refill
+    uint64_t* accf = bars + 2 * kStages;     // [kAcc] MMA done -> epilogue
+    uint64_t* acce = accf + kAcc;            // [kAcc] epilogue drained -> MMA (8 arrivals)
+    uint64_t* qbar = acce + kAcc;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(qbar + 1);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t pair = blockIdx.y;
+    const int q0 = blockIdx.x * kNQ;
+    const uint16_t* lqp = lq + pair * static_cast<int64_t>(L) * KD;
+    const uint16_t* lkp = lk + pair * static_cast<int64_t>(L) * KD;
+
+    if (tid == 0) {
+        for (int i = 0; i < kStages; ++i) {
+            tc::mbar_init(&full[i], 1);
+            tc::mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < kAcc; ++i) {
+            tc::mbar_init(&accf[i], 1);
+            tc::mbar_init(&acce[i], kEpiWarps);
+        }
+        tc::mbar_init(qbar, 1);
+        tc::fence_barrier_init();
+    }
+    {  // zero the band histograms
+        uint4* h4 = reinterpret_cast<uint4*>(histp);
+        for (int i = tid; i < Lay::kHist / 16; i += kThreads) h4[i] = make_uint4(0, 0, 0, 0);
+    }
+    if (warp == 0) tc::tmem_alloc<kAcc * kNQ>(tmem_slot);
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == kEpiWarps) {
+        // ------------------------------------------------------ producer
+        if (lane == 0) {
+            const uint32_t ring_s = tc::smem_addr(ring), q_s = tc::smem_addr(q_sm);
+            auto load = [&](int s, int tile) {
+                const int row0 = tile * kMT;
+                const int rows = L - row0 < kMT ? L - row0 : kMT;
+                tc::mbar_expect_tx(&full[s], static_cast<uint32_t>(rows * 16 * Lay::kPlanesA));
+#pragma unroll
+                for (int c = 0; c < Lay::kPlanesA; ++c)
+                    tc::bulk_g2s(ring_s + s * Lay::kTile + c * (kMT * 16),
+                                 lkp + (static_cast<int64_t>(c) * L + row0) * 8, static_cast<uint32_t>(rows * 16),
+                                 &full[s]);
+            };
+            {
+                const int rows = L - q0 < kNQ ? L - q0 : kNQ;
+                tc::mbar_expect_tx(qbar, static_cast<uint32_t>(rows * 16 * Lay::kPlanesA));
+#pragma unroll
+                for (int c = 0; c < Lay::kPlanesA; ++c)
+                    tc::bulk_g2s(q_s + c * (kNQ * 16), lqp + (static_cast<int64_t>(c) * L + q0) * 8,
+                                 static_cast<uint32_t>(rows * 16), qbar);
+            }
+            for (int s = 0; s < kStages && s < nt; ++s) load(s, s);
+            const uint32_t idesc = tc::idesc_bf16_f32(kMT, kNQ);
+            tc::mbar_wait(qbar, 0);
+            for (int t = 0; t < nt; ++t) {
+                const int s = t % kStages, a = t % kAcc;
+                tc::mbar_wait(&full[s], (t / kStages) & 1);
+                if (t >= kAcc) tc::mbar_wait(&acce[a], ((t / kAcc) - 1) & 1);
+                tc::fence_after_sync();
+#pragma unroll
+                for (int ks = 0; ks < KD / 16; ++ks) {
+                    // K-major, no swizzle: 8-row x 16-byte core matrices; the
+                    // two K-adjacent ones are the two 8-column planes
+                    // (LBO = plane stride), 8-row groups 128 B apart (SBO)
+                    const uint64_t ad = tc::desc_kmajor_nosw(ring_s + s * Lay::kTile + ks * 2 * (kMT * 16), kMT * 16, 128);
+                    const uint64_t bd = tc::desc_kmajor_nosw(q_s + ks * 2 * (kNQ * 16), kNQ * 16, 128);
+                    tc::mma_bf16(tmem + a * kNQ, ad, bd, idesc, ks > 0);
+                }
+                tc::commit(&accf[a]);
+                tc::commit(&empty[s]);
+                if (t >= 1 && t - 1 + kStages < nt) {
+                    const int sp = (t - 1) % kStages;
+                    tc::mbar_wait(&empty[sp], ((t - 1) / kStages) & 1);
+                    load(sp, t - 1 + kStages);
+                }
+            }
+        }
+        return;
+    }
+
+    // ---------------------------------------------------------- epilogue
+    const int quarter = warp & 3, half = warp >> 2;
+    const uint32_t tl = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + half * 32;
+    const uint32_t pooled_s = tc::smem_addr(pooled);
+    const uint32_t hist_s = tc::smem_addr(histp);
+    const uint32_t row_bytes = static_cast<uint32_t>(Lp) * 2;
+    // histogram word of band b, value v: pair (b / 2), index M - v; the code
+    // bits are kCodeBias + v, so the address is one IMAD: C_b - 4 code
+    uint32_t hc[4], inc[4], prow[4];
+    bool bvalid[4];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        const int band = half * 4 + b;
+        hc[b] = hist_s + static_cast<uint32_t>((band >> 1) * Lay::kBins * 4) + 4u * static_cast<uint32_t>(M) + 4u * kCodeBias;
+        inc[b] = (band & 1) ? 0x10000u : 1u;
+        prow[b] = pooled_s + static_cast<uint32_t>(band) * row_bytes;
+        bvalid[b] = q0 + band * 8 < L;
+    }
+    const bool ragged_q = q0 + kNQ > L;
+    const int cbase = quarter * 4 + (lane >> 3);  // this thread's 16-byte chunk in a 128-key segment
+    const uint32_t ebyte = static_cast<uint32_t>(lane & 7) << 1;
+
+    auto process = [&](int t, const uint32_t (&r)[32], bool edge) {
+        const int key = t * kMT + quarter * 32 + lane;
+        const uint32_t off = (static_cast<uint32_t>((t << 4) + (cbase ^ (t & 7))) << 4) + ebyte;
+        const bool kv = !edge || key < L;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const float* f = reinterpret_cast<const float*>(&r[b * 8]);
+            float m0, m1, m2;
+            asm("max.f32 %0, %1, %2, %3;" : "=f"(m0) : "f"(f[0]), "f"(f[1]), "f"(f[2]));
+            asm("max.f32 %0, %1, %2, %3;" : "=f"(m1) : "f"(f[3]), "f"(f[4]), "f"(f[5]));
+            asm("max.f32 %0, %1, %2, %3;" : "=f"(m2) : "f"(m0), "f"(m1), "f"(f[6]));
+            const uint32_t code = __float_as_uint(fmaxf(m2, f[7]) + kCodeMagic);
+            const bool ok = kv && (!edge || bvalid[b]);
+            sts_u16(prow[b] + off, ok ? code : 0u);  // 0: below every valid code
+            if (ok) red_add(hc[b] - 4u * code, inc[b]);
+        }
+    };
+
+    for (int t = 0; t < nt; ++t) {
+        const int a = t % kAcc;
+        tc::mbar_wait(&accf[a], (t / kAcc) & 1);
+        tc::fence_after_sync();
+        uint32_t r[32];
+        tc::ld_32x32b_x32(tl + a * kNQ, r);
+        tc::wait_ld();
+        tc::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&acce[a]);
+        const bool edge = ragged_q || (t == nt - 1 && Lp != L);
+        if (ragged_q) {
+#pragma unroll
+            for (int x = 0; x < 32; ++x)
+                if (q0 + half * 32 + x >= L) r[x] = __float_as_uint(-INFINITY);
+        }
+        if (edge) process(t, r, true);
+        else process(t, r, false);
+    }
+    named_sync_epi();  // every score drained, every code and count in place
+    if (warp == 0) tc::tmem_dealloc<kAcc * kNQ>(tmem);
+
+    // ------------------------------------------------ per-band selection
+    const int band = q0 / 8 + warp;  // this warp's band (global index within the pair)
+    const int nbands = (L + 7) / 8;
+    const bool live = band < nbands;
+    int T = 0;
+    uint32_t n_gt = 0, n_eq = 0;
+    if (live) {
+        // keep-th largest value: cumulative counts from the top bin (v = M)
+        const uint32_t hp = hist_s + static_cast<uint32_t>((warp >> 1) * Lay::kBins * 4);
+        const int sh = (warp & 1) * 16;
+        const int nbins = 2 * M + 1;
+        uint32_t carry = 0;
+        for (int h0 = 0; h0 < nbins; h0 += 256) {
+            const uint4 x = lds128(hp + (h0 + 8 * lane) * 4), y = lds128(hp + (h0 + 8 * lane + 4) * 4);
+            const uint32_t mine = ((x.x + x.y + x.z + x.w + y.x + y.y + y.z + y.w) >> sh) & 0xFFFFu;
+            uint32_t incl = mine;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += u;
+            }
+            const unsigned hit = __ballot_sync(0xffffffffu, carry + incl >= static_cast<uint32_t>(keep));
+            if (hit) {
+                const int f = __ffs(hit) - 1;
+                uint32_t run = carry + __shfl_sync(0xffffffffu, incl - mine, f);
+                const int hb = h0 + 8 * f;
+                int tt = 0;
+                uint32_t gt = 0, eq = 0;
+                if (lane == 0) {
+                    for (int i = 0; i < 8; ++i) {
+                        const uint32_t c = (lds_u16(hp + (hb + i) * 4 + (sh >> 3))) & 0xFFFFu;
+                        if (run + c >= static_cast<uint32_t>(keep)) {
+                            tt = M - (hb + i);
+                            gt = run;
+                            eq = c;
+                            break;
+                        }
+                        run += c;
+                    }
+                }
+                T = __shfl_sync(0xffffffffu, tt, 0);
+                n_gt = __shfl_sync(0xffffffffu, gt, 0);
+                n_eq = __shfl_sync(0xffffffffu, eq, 0);
+                break;
+            }
+            carry += __shfl_sync(0xffffffffu, incl, 31);
+        }
+    }
+    named_sync_epi();  // histograms consumed: the staging lists reuse them
+
+    uint32_t* obuf = reinterpret_cast<uint32_t*>(histp) + warp * kList;
+    const uint32_t obuf_s = hist_s + static_cast<uint32_t>(warp * kList * 4);
+    if (live) {
+        const uint32_t prow_s = pooled_s + static_cast<uint32_t>(warp) * row_bytes;
+        const uint32_t codeT = 0x4000u + static_cast<uint32_t>(T);
+        const uint32_t rem = static_cast<uint32_t>(keep) - n_gt;  // ties admitted, lowest keys first
+        const uint32_t n_ge = n_gt + n_eq;
+        uint32_t* o = out ? out + (pair * nbands + band) * static_cast<int64_t>(keep) : nullptr;
+        const int nseg = Lp / kMT;
+        const unsigned lt = lanemask_lt();
+        if (n_ge <= static_cast<uint32_t>(kList)) {
+            // (a) every key with v >= T, ascending, into the staging list
+            const uint32_t T2 = codeT | (codeT << 16);
+            uint32_t base = 0;
+            for (int s0 = 0; s0 < nseg; s0 += 32) {
+                const int seg = s0 + lane;
+                uint32_t w[4] = {0u, 0u, 0u, 0u};
+                if (seg < nseg) {
+                    const uint32_t sb = prow_s + static_cast<uint32_t>(seg) * 256;
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) {
+                        const uint4 x = lds128(sb + static_cast<uint32_t>((c ^ (seg & 7)) << 4));
+                        uint32_t tb = hge2(x.x, T2) & 0x00020001u;
+                        tb |= hge2(x.y, T2) & 0x00080004u;
+                        tb |= hge2(x.z, T2) & 0x00200010u;
+                        tb |= hge2(x.w, T2) & 0x00800040u;
+                        w[c >> 2] |= ((tb | (tb >> 16)) & 0xFFu) << ((c & 3) * 8);
+                    }
+                }
+                const uint32_t n = __popc(w[0]) + __popc(w[1]) + __popc(w[2]) + __popc(w[3]);
+                uint32_t incl = n;
+#pragma unroll
+                for (int q = 1; q < 32; q <<= 1) {
+                    const uint32_t u = __shfl_up_sync(0xffffffffu, incl, q);
+                    if (lane >= q) incl += u;
+                }
+                uint32_t pos = base + incl - n;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    uint32_t x = w[j];
+                    while (x) {
+                        const int bit = __ffs(x) - 1;
+                        x &= x - 1;
+                        obuf[pos++] = static_cast<uint32_t>(seg * kMT + j * 32 + bit);
+                    }
+                }
+                base += __shfl_sync(0xffffffffu, incl, 31);
+            }
+            __syncwarp();
+            if (n_ge == static_cast<uint32_t>(keep)) {
+                if (o)
+                    for (int i = lane; i < keep; i += 32) o[i] = obuf[i];
+            } else {
+                // (b) drop the ties beyond `rem` (compacted in place)
+                uint32_t eq_seen = 0, outp = 0;
+                for (uint32_t i0 = 0; i0 < n_ge; i0 += 32) {
+                    const uint32_t i = i0 + lane;
+                    const bool valid = i < n_ge;
+                    const uint32_t col = valid ? obuf[i] : 0u;
+                    const bool eq = valid && lds_u16(prow_s + code_off(static_cast<int>(col))) == codeT;
+                    const unsigned be = __ballot_sync(0xffffffffu, eq);
+                    const bool kp = valid && (!eq || eq_seen + __popc(be & lt) < rem);
+                    const unsigned bk = __ballot_sync(0xffffffffu, kp);
+                    __syncwarp();  // every lane read its entry before any write below
+                    if (kp) {
+                        obuf[outp + __popc(bk & lt)] = col;
+                        if (o) o[outp + __popc(bk & lt)] = col;
+                    }
+                    outp += __popc(bk);
+                    eq_seen += __popc(be);
+                }
+            }
+        } else {
+            // rare (a flood of ties at T): one ascending pass, two ballots per
+            // 32 keys -- v > T, or v == T among the first `rem` ties
+            const uint32_t trash = static_cast<uint32_t>(kList - 32 + lane);
+            uint32_t taken = 0, eq_seen = 0;
+            for (int j0 = 0; j0 < Lp; j0 += 32) {
+                const int j = j0 + lane;
+                const uint32_t c = lds_u16(prow_s + code_off(j));
+                const bool gt = c > codeT && c != 0u, eq = c == codeT;
+                const unsigned be = __ballot_sync(0xffffffffu, eq);
+                const bool take = gt || (eq && eq_seen + __popc(be & lt) < rem);
+                const unsigned bt = __ballot_sync(0xffffffffu, take);
+                const uint32_t slot = take ? taken + __popc(bt & lt) : trash;
+                obuf[slot] = static_cast<uint32_t>(j);
+                if (take && o) o[slot] = static_cast<uint32_t>(j);
+                taken += __popc(bt);
+                eq_seen += __popc(be);
+            }
+        }
+        __syncwarp();
+    }
+    (void)obuf_s;
+    if constexpr (FUSED) {
+        named_sync_epi();  // ring + pooled codes free: per-warp attention buffers
+        using BS = bc::BandSmemV2<64>;
+        BS& sm = reinterpret_cast<BS*>(ring)[warp];
+        if (live) {
+            auto chunk_idx = [&](int ch) -> uint32_t {
+                const int p = ch * 32 + lane;
+                return p < keep ? obuf[p] : 0u;
+            };
+            bc::band_core<64, 8, false>(sm, fa.q, fa.k + pair * static_cast<int64_t>(L) * 64,
+                                        fa.v + pair * static_cast<int64_t>(L) * 64, pair, L,
+                                        static_cast<int64_t>(band) * 8, keep, 0, 0, 0, fa.scale, fa.z, chunk_idx,
+                                        lane);
+        }
+    }
+}
+
+template <int KD, bool FUSED>
+void launch(const SelectArgs& s, const FusedAttn& fa, cudaStream_t st) {
+    const size_t smem = Layout<KD>::smem_bytes(s.L, FUSED);
+    auto kern = colvec_kernel<KD, FUSED>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    const dim3 grid(static_cast<unsigned>(ceil_div_i(s.L, kNQ)), static_cast<unsigned>(s.pairs));
+    const int M = static_cast<int>(s.KD) * s.qmax * s.qmax;
+    kern<<<grid, kThreads, smem, st>>>(s.lq, s.lk, static_cast<int>(s.L), static_cast<int>(s.keep), M, s.cols, fa);
+    note_launch();
+}
+
+}  // namespace
+
+bool colvec_tc_supported(const SelectArgs& a) {
+    if (a.mode != kColvec || a.vec_v != 8 || a.per_row || a.qmax > 7) return false;
+    if (a.KD != 16 && a.KD != 32) return false;
+    if (a.keep > kList - 32) return false;
+    const size_t smem = a.KD == 16 ? Layout<16>::smem_bytes(a.L, false) : Layout<32>::smem_bytes(a.L, false);
+    return smem <= 227 * 1024;
+}
+
+void run_colvec_tc(const SelectArgs& a, cudaStream_t st) {
+    if (a.KD == 16) launch<16, false>(a, FusedAttn{}, st);
+    else launch<32, false>(a, FusedAttn{}, st);
+}
+
+bool colvec_fused_supported(const SelectArgs& s, const AttnArgs& a) {
+    if (options().no_fuse) return false;
+    if (!colvec_tc_supported(s) || s.KD != 16 || !a.bf16 || a.D != 64 || a.vec_v != 8) return false;
+    return Layout<16>::smem_bytes(s.L, true) <= 227 * 1024;
+}
+
+void run_colvec_fused(const SelectArgs& s, const AttnArgs& a, cudaStream_t st) {
+    const FusedAttn fa{static_cast<const __nv_bfloat16*>(a.q), static_cast<const __nv_bfloat16*>(a.k),
+                       static_cast<const __nv_bfloat16*>(a.v), static_cast<__nv_bfloat16*>(a.z), a.scale};
+    launch<16, true>(s, fa, st);
+}
+
+}  // namespace dsa
