@@ -8,12 +8,14 @@
 // S~[i][j], keep `keep` keys per band by row_topk_indices (value desc, the
 // LOWER key first among equals, P/src/linalg.cpp:77-80), ascending list.
 //
-// One CTA = 64 queries (8 bands) of one (b,h) pair, 9 warps:
-//   * warp 8 (producer, one lane): K~ tiles (128 keys) by bulk TMA copies
+// One CTA = 64 queries (8 bands) of one (b,h) pair, 10 warps:
+//   * warp 8 (TMA producer, one lane): K~ tiles (128 keys) by bulk copies
 //     straight from the chunk-planar levels (one copy per 8-column plane)
-//     into a 4-stage ring, one tcgen05.mma (M = 128 keys, N = 64 queries,
-//     K = 16 per instruction) per tile into one of 4 TMEM accumulators,
-//     commits to the accumulator's "full" and the stage's "empty" barrier;
+//     into a 4-stage ring, refilling a stage as soon as its MMA completed;
+//   * warp 9 (MMA issuer, one lane): one tcgen05.mma (M = 128 keys, N = 64
+//     queries, K = 16 per instruction) per tile into one of 4 TMEM
+//     accumulators, committed to the accumulator's "full" and the stage's
+//     "empty" barrier;
 //   * warps 0-7 (epilogue): warp w drains TMEM lanes 32 (w & 3).. (= keys)
 //     x columns 32 (w >> 2).. (= 4 bands) with ONE tcgen05.ld per tile and
 //     frees the accumulator, then per band: max over 8 columns (FMNMX3), one
@@ -49,7 +51,9 @@ constexpr int kBands = kNQ / 8;
 constexpr int kStages = 4;     // K~ ring
 constexpr int kAcc = 4;        // TMEM accumulators (kNQ columns each)
 constexpr int kEpiWarps = 8;
-constexpr int kThreads = (kEpiWarps + 1) * 32;
+constexpr int kLoadWarp = kEpiWarps;      // TMA producer
+constexpr int kMmaWarp = kEpiWarps + 1;   // tcgen05.mma issuer
+constexpr int kThreads = (kEpiWarps + 2) * 32;
 constexpr int kList = 512;     // per-band staging list (keys)
 constexpr uint32_t kCodeBias = 0x4B404000u;  // bits of 1.5 * 2^23 + 2^14
 constexpr float kCodeMagic = 12599296.0f;    // 1.5 * 2^23 + 2^14
@@ -169,20 +173,10 @@ __global__ void __launch_bounds__(kThreads, 2)
     tc::fence_after_sync();
     const uint32_t tmem = *tmem_slot;
 
-    if (warp == kEpiWarps) {
-        // ------------------------------------------------------ producer
+    if (warp == kLoadWarp) {
+        // ------------------------------------------------- TMA producer
         if (lane == 0) {
             const uint32_t ring_s = tc::smem_addr(ring), q_s = tc::smem_addr(q_sm);
-            auto load = [&](int s, int tile) {
-                const int row0 = tile * kMT;
-                const int rows = L - row0 < kMT ? L - row0 : kMT;
-                tc::mbar_expect_tx(&full[s], static_cast<uint32_t>(rows * 16 * Lay::kPlanesA));
-#pragma unroll
-                for (int c = 0; c < Lay::kPlanesA; ++c)
-                    tc::bulk_g2s(ring_s + s * Lay::kTile + c * (kMT * 16),
-                                 lkp + (static_cast<int64_t>(c) * L + row0) * 8, static_cast<uint32_t>(rows * 16),
-                                 &full[s]);
-            };
             {
                 const int rows = L - q0 < kNQ ? L - q0 : kNQ;
                 tc::mbar_expect_tx(qbar, static_cast<uint32_t>(rows * 16 * Lay::kPlanesA));
@@ -191,7 +185,25 @@ __global__ void __launch_bounds__(kThreads, 2)
                     tc::bulk_g2s(q_s + c * (kNQ * 16), lqp + (static_cast<int64_t>(c) * L + q0) * 8,
                                  static_cast<uint32_t>(rows * 16), qbar);
             }
-            for (int s = 0; s < kStages && s < nt; ++s) load(s, s);
+            for (int t = 0; t < nt; ++t) {
+                const int s = t % kStages;
+                if (t >= kStages) tc::mbar_wait(&empty[s], ((t / kStages) - 1) & 1);  // MMA t - kStages done
+                const int row0 = t * kMT;
+                const int rows = L - row0 < kMT ? L - row0 : kMT;
+                tc::mbar_expect_tx(&full[s], static_cast<uint32_t>(rows * 16 * Lay::kPlanesA));
+#pragma unroll
+                for (int c = 0; c < Lay::kPlanesA; ++c)
+                    tc::bulk_g2s(ring_s + s * Lay::kTile + c * (kMT * 16),
+                                 lkp + (static_cast<int64_t>(c) * L + row0) * 8, static_cast<uint32_t>(rows * 16),
+                                 &full[s]);
+            }
+        }
+        return;
+    }
+    if (warp == kMmaWarp) {
+        // ------------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            const uint32_t ring_s = tc::smem_addr(ring), q_s = tc::smem_addr(q_sm);
             const uint32_t idesc = tc::idesc_bf16_f32(kMT, kNQ);
             tc::mbar_wait(qbar, 0);
             for (int t = 0; t < nt; ++t) {
@@ -210,11 +222,6 @@ __global__ void __launch_bounds__(kThreads, 2)
                 }
                 tc::commit(&accf[a]);
                 tc::commit(&empty[s]);
-                if (t >= 1 && t - 1 + kStages < nt) {
-                    const int sp = (t - 1) % kStages;
-                    tc::mbar_wait(&empty[sp], ((t - 1) / kStages) & 1);
-                    load(sp, t - 1 + kStages);
-                }
             }
         }
         return;

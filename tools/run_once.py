@@ -12,6 +12,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c2_vector")
 ap.add_argument("--pairs", type=int, default=0)
 ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--pipeline", action="store_true", help="dsa_pipeline (fused kernels) instead of the phases")
 a = ap.parse_args()
 p = load_preset(a.config)
 n = a.pairs or p.pairs
@@ -20,7 +21,11 @@ q, k, v, P = ops.generate(sub, npairs=n)
 qd, kd, vd, Pd = (t.cuda() for t in (q, k, v, P))
 ph = ops.Phases(sub, n)
 z = torch.empty_like(qd)
+pipe = ops.Pipeline(sub, pairs=n)
 for _ in range(a.reps):
+    if a.pipeline:
+        pipe(qd, kd, vd, Pd, out=z)
+        continue
     ph.predict(qd, kd, Pd)
     ph.select()
     ph.attend(qd, kd, vd, z)
