@@ -409,7 +409,7 @@ Options read_options() {
     o.block_generic = env_flag("DSA_BLOCK_GENERIC");
     o.topk_generic = env_flag("DSA_TOPK_GENERIC");
     o.predict_dfma = env_flag("DSA_PREDICT_DFMA");
-    o.no_fuse = env_flag("DSA_NO_FUSE");
+    o.fuse = env_flag("DSA_FUSE");
     const char* e = std::getenv("DSA_PIPELINE_CHUNKS");
     o.pipeline_chunks = e ? std::atoi(e) : -1;
     return o;

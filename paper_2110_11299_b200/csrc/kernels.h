@@ -25,7 +25,7 @@ struct Options {
     bool block_generic;      // DSA_BLOCK_GENERIC: CTA-per-row block selection
     bool topk_generic;       // DSA_TOPK_GENERIC: CTA-per-row radix top-k
     bool predict_dfma;       // DSA_PREDICT_DFMA: exact fp64 projection chain
-    bool no_fuse;            // DSA_NO_FUSE: unfused COLVEC select + attention
+    bool fuse;               // DSA_FUSE: COLVEC select + attention in one kernel (measured slower on C2)
     int pipeline_chunks;     // DSA_PIPELINE_CHUNKS: pair chunks overlapped on 3 streams
 };
 const Options& options();

@@ -49,7 +49,7 @@ constexpr int kMT = 128;       // keys per tile (UMMA M)
 constexpr int kNQ = 64;        // queries per CTA (UMMA N) = 8 bands
 constexpr int kBands = kNQ / 8;
 constexpr int kStages = 4;     // K~ ring
-constexpr int kAcc = 4;        // TMEM accumulators (kNQ columns each)
+constexpr int kAcc = 2;        // TMEM accumulator slots, two key tiles (2 kNQ columns) each
 constexpr int kEpiWarps = 8;
 constexpr int kLoadWarp = kEpiWarps;      // TMA producer
 constexpr int kMmaWarp = kEpiWarps + 1;   // tcgen05.mma issuer
@@ -140,8 +140,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     uint64_t* bars = reinterpret_cast<uint64_t*>(histp + Lay::kHistRegion);
     uint64_t* full = bars;                   // [kStages] TMA -> MMA
     uint64_t* empty = bars + kStages;        // [kStages] MMA done -> refill
-    uint64_t* accf = bars + 2 * kStages;     // [kAcc] MMA done -> epilogue
-    uint64_t* acce = accf + kAcc;            // [kAcc] epilogue drained -> MMA (8 arrivals)
+    uint64_t* accf = bars + 2 * kStages;     // [kAcc] MMAs of a slot done -> epilogue
+    uint64_t* acce = accf + kAcc;            // [kAcc] slot drained -> MMA (8 arrivals)
     uint64_t* qbar = acce + kAcc;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(qbar + 1);
 
@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         uint4* h4 = reinterpret_cast<uint4*>(histp);
         for (int i = tid; i < Lay::kHist / 16; i += kThreads) h4[i] = make_uint4(0, 0, 0, 0);
     }
-    if (warp == 0) tc::tmem_alloc<kAcc * kNQ>(tmem_slot);
+    if (warp == 0) tc::tmem_alloc<kAcc * 2 * kNQ>(tmem_slot);
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             }
             for (int t = 0; t < nt; ++t) {
                 const int s = t % kStages;
-                if (t >= kStages) tc::mbar_wait(&empty[s], ((t / kStages) - 1) & 1);  // MMA t - kStages done
+                if (t >= kStages) tc::mbar_wait_susp(&empty[s], ((t / kStages) - 1) & 1);  // MMA t - kStages done
                 const int row0 = t * kMT;
                 const int rows = L - row0 < kMT ? L - row0 : kMT;
                 tc::mbar_expect_tx(&full[s], static_cast<uint32_t>(rows * 16 * Lay::kPlanesA));
@@ -206,22 +206,27 @@ __global__ void __launch_bounds__(kThreads, 2)
             const uint32_t ring_s = tc::smem_addr(ring), q_s = tc::smem_addr(q_sm);
             const uint32_t idesc = tc::idesc_bf16_f32(kMT, kNQ);
             tc::mbar_wait(qbar, 0);
-            for (int t = 0; t < nt; ++t) {
-                const int s = t % kStages, a = t % kAcc;
-                tc::mbar_wait(&full[s], (t / kStages) & 1);
-                if (t >= kAcc) tc::mbar_wait(&acce[a], ((t / kAcc) - 1) & 1);
-                tc::fence_after_sync();
+            // steps of two key tiles: one accumulator slot (2 x kNQ columns), one commit
+            for (int u = 0; 2 * u < nt; ++u) {
+                const int a = u % kAcc;
+                if (u >= kAcc) tc::mbar_wait_susp(&acce[a], ((u / kAcc) - 1) & 1);
+                for (int i = 0; i < 2 && 2 * u + i < nt; ++i) {
+                    const int t = 2 * u + i, s = t % kStages;
+                    tc::mbar_wait_susp(&full[s], (t / kStages) & 1);
+                    tc::fence_after_sync();
 #pragma unroll
-                for (int ks = 0; ks < KD / 16; ++ks) {
-                    // K-major, no swizzle: 8-row x 16-byte core matrices; the
-                    // two K-adjacent ones are the two 8-column planes
-                    // (LBO = plane stride), 8-row groups 128 B apart (SBO)
-                    const uint64_t ad = tc::desc_kmajor_nosw(ring_s + s * Lay::kTile + ks * 2 * (kMT * 16), kMT * 16, 128);
-                    const uint64_t bd = tc::desc_kmajor_nosw(q_s + ks * 2 * (kNQ * 16), kNQ * 16, 128);
-                    tc::mma_bf16(tmem + a * kNQ, ad, bd, idesc, ks > 0);
+                    for (int ks = 0; ks < KD / 16; ++ks) {
+                        // K-major, no swizzle: 8-row x 16-byte core matrices; the
+                        // two K-adjacent ones are the two 8-column planes
+                        // (LBO = plane stride), 8-row groups 128 B apart (SBO)
+                        const uint64_t ad =
+                            tc::desc_kmajor_nosw(ring_s + s * Lay::kTile + ks * 2 * (kMT * 16), kMT * 16, 128);
+                        const uint64_t bd = tc::desc_kmajor_nosw(q_s + ks * 2 * (kNQ * 16), kNQ * 16, 128);
+                        tc::mma_bf16(tmem + (2 * a + i) * kNQ, ad, bd, idesc, ks > 0);
+                    }
+                    tc::commit(&empty[s]);
                 }
                 tc::commit(&accf[a]);
-                tc::commit(&empty[s]);
             }
         }
         return;
@@ -249,10 +254,9 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int cbase = quarter * 4 + (lane >> 3);  // this thread's 16-byte chunk in a 128-key segment
     const uint32_t ebyte = static_cast<uint32_t>(lane & 7) << 1;
 
-    auto process = [&](int t, const uint32_t (&r)[32], bool edge) {
-        const int key = t * kMT + quarter * 32 + lane;
+    // per tile: 4 bands x (max of 8 columns, code, pooled store, histogram RED)
+    auto process = [&](int t, const uint32_t (&r)[32]) {
         const uint32_t off = (static_cast<uint32_t>((t << 4) + (cbase ^ (t & 7))) << 4) + ebyte;
-        const bool kv = !edge || key < L;
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
             const float* f = reinterpret_cast<const float*>(&r[b * 8]);
@@ -261,33 +265,53 @@ __global__ void __launch_bounds__(kThreads, 2)
             asm("max.f32 %0, %1, %2, %3;" : "=f"(m1) : "f"(f[3]), "f"(f[4]), "f"(f[5]));
             asm("max.f32 %0, %1, %2, %3;" : "=f"(m2) : "f"(m0), "f"(m1), "f"(f[6]));
             const uint32_t code = __float_as_uint(fmaxf(m2, f[7]) + kCodeMagic);
-            const bool ok = kv && (!edge || bvalid[b]);
+            sts_u16(prow[b] + off, code);
+            red_add(hc[b] - 4u * code, inc[b]);
+        }
+    };
+    // the same with ragged keys (last tile) / ragged queries (last CTA of a pair)
+    auto process_edge = [&](int t, uint32_t (&r)[32]) {
+        const int key = t * kMT + quarter * 32 + lane;
+        const uint32_t off = (static_cast<uint32_t>((t << 4) + (cbase ^ (t & 7))) << 4) + ebyte;
+#pragma unroll
+        for (int x = 0; x < 32; ++x)
+            if (q0 + half * 32 + x >= L) r[x] = __float_as_uint(-INFINITY);
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const float* f = reinterpret_cast<const float*>(&r[b * 8]);
+            float m = f[0];
+#pragma unroll
+            for (int x = 1; x < 8; ++x) m = fmaxf(m, f[x]);
+            const uint32_t code = __float_as_uint(m + kCodeMagic);
+            const bool ok = key < L && bvalid[b];
             sts_u16(prow[b] + off, ok ? code : 0u);  // 0: below every valid code
             if (ok) red_add(hc[b] - 4u * code, inc[b]);
         }
     };
+    const int edge_from = ragged_q ? 0 : (Lp != L ? nt - 1 : nt);  // first tile needing the edge path
 
-    for (int t = 0; t < nt; ++t) {
-        const int a = t % kAcc;
-        tc::mbar_wait(&accf[a], (t / kAcc) & 1);
+    for (int u = 0; 2 * u < nt; ++u) {
+        const int a = u % kAcc;
+        tc::mbar_wait_susp(&accf[a], (u / kAcc) & 1);
         tc::fence_after_sync();
-        uint32_t r[32];
-        tc::ld_32x32b_x32(tl + a * kNQ, r);
-        tc::wait_ld();
-        tc::fence_before_sync();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&acce[a]);
-        const bool edge = ragged_q || (t == nt - 1 && Lp != L);
-        if (ragged_q) {
 #pragma unroll
-            for (int x = 0; x < 32; ++x)
-                if (q0 + half * 32 + x >= L) r[x] = __float_as_uint(-INFINITY);
+        for (int i = 0; i < 2; ++i) {
+            const int t = 2 * u + i;
+            if (t >= nt) break;
+            uint32_t r[32];
+            tc::ld_32x32b_x32(tl + (2 * a + i) * kNQ, r);
+            tc::wait_ld();
+            if (i == 1 || t + 1 == nt) {  // slot drained
+                tc::fence_before_sync();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&acce[a]);
+            }
+            if (t < edge_from) process(t, r);
+            else process_edge(t, r);
         }
-        if (edge) process(t, r, true);
-        else process(t, r, false);
     }
     named_sync_epi();  // every score drained, every code and count in place
-    if (warp == 0) tc::tmem_dealloc<kAcc * kNQ>(tmem);
+    if (warp == 0) tc::tmem_dealloc<kAcc * 2 * kNQ>(tmem);
 
     // ------------------------------------------------ per-band selection
     const int band = q0 / 8 + warp;  // this warp's band (global index within the pair)
@@ -477,7 +501,7 @@ void run_colvec_tc(const SelectArgs& a, cudaStream_t st) {
 }
 
 bool colvec_fused_supported(const SelectArgs& s, const AttnArgs& a) {
-    if (options().no_fuse) return false;
+    if (!options().fuse) return false;
     if (!colvec_tc_supported(s) || s.KD != 16 || !a.bf16 || a.D != 64 || a.vec_v != 8) return false;
     return Layout<16>::smem_bytes(s.L, true) <= 227 * 1024;
 }

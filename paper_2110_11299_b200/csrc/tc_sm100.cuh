@@ -33,6 +33,18 @@ __device__ __forceinline__ void mbar_wait_a(uint32_t bar_smem, uint32_t parity) 
         "r"(parity)
         : "memory");
 }
+// The same wait with a suspend-time hint: the warp sleeps in the barrier
+// unit until the phase completes (or the hint expires) instead of spinning
+// on issue slots other warps need.
+__device__ __forceinline__ void mbar_wait_susp(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 10000000;\n\t"
+        "@!p bra WAIT_%=;\n}\n" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
 // Same wait with a nanosleep backoff between probes, for warps whose wait is
 // long (keeps spinning warps from stealing issue slots from working warps).
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
