@@ -9,7 +9,10 @@ from pathlib import Path
 from . import errors
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "libdsa_b200.so"
+import os
+
+# DSA_LIB: an alternative build of the same library (tools/ablate.py variants)
+LIB_PATH = Path(os.environ["DSA_LIB"]) if os.environ.get("DSA_LIB") else PKG / "libdsa_b200.so"
 HEADER = PKG.parent / "include" / "dsa_b200.h"
 
 

@@ -42,13 +42,21 @@
 #include "kernels.h"
 #include "tc_sm100.cuh"
 
+// DSA_ABLATE: profiling builds only (tools/ablate.py); 0 in the library
+#ifndef DSA_ABLATE
+#define DSA_ABLATE 0
+#endif
+
 namespace dsa {
 namespace {
 
 constexpr int kMT = 128;       // keys per tile (UMMA M)
 constexpr int kNQ = 64;        // queries per CTA (UMMA N) = 8 bands
 constexpr int kBands = kNQ / 8;
-constexpr int kStages = 4;     // K~ ring
+#ifndef DSA_ABL_STAGES
+#define DSA_ABL_STAGES 4
+#endif
+constexpr int kStages = DSA_ABL_STAGES;  // K~ ring
 constexpr int kAcc = 2;        // TMEM accumulator slots, two key tiles (2 kNQ columns) each
 constexpr int kEpiWarps = 8;
 constexpr int kLoadWarp = kEpiWarps;      // TMA producer
@@ -72,7 +80,7 @@ struct Layout {
     // ring + pooled codes (reused by the fused attention's per-warp buffers)
     __host__ __device__ static size_t work_bytes(int64_t L, bool fused) {
         const size_t nt = static_cast<size_t>((L + kMT - 1) / kMT);
-        const size_t w = static_cast<size_t>(kStages) * kTile + static_cast<size_t>(kBands) * nt * kMT * 2;
+        const size_t w = static_cast<size_t>(kStages) * kTile + ((DSA_ABLATE & 2) ? 0 : static_cast<size_t>(kBands) * nt * kMT * 2);
         const size_t f = fused ? sizeof(bc::BandSmemV2<64>) * kEpiWarps : 0;
         return w > f ? w : f;
     }
@@ -130,8 +138,8 @@ __global__ void __launch_bounds__(kThreads, 2)
                   uint32_t* __restrict__ out, FusedAttn fa) {
     using Lay = Layout<KD>;
     extern __shared__ __align__(1024) unsigned char smem[];
-    const int nt = (L + kMT - 1) / kMT;
-    const int Lp = nt * kMT;
+    const int Lp = (L + kMT - 1) / kMT * kMT;
+    const int nt = (DSA_ABLATE & 32) ? Lp / kMT / 2 : Lp / kMT;  // profiling: half the key tiles
     const size_t work = Lay::work_bytes(L, FUSED);
     unsigned char* q_sm = smem;
     unsigned char* ring = smem + Lay::kQ;
@@ -204,7 +212,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         // ------------------------------------------------------ MMA issuer
         if (lane == 0) {
             const uint32_t ring_s = tc::smem_addr(ring), q_s = tc::smem_addr(q_sm);
-            const uint32_t idesc = tc::idesc_bf16_f32(kMT, kNQ);
+            const uint32_t idesc = (DSA_ABLATE & 8) ? tc::idesc_f16_f16(kMT, kNQ) : tc::idesc_bf16_f32(kMT, kNQ);
             tc::mbar_wait(qbar, 0);
             // steps of two key tiles: one accumulator slot (2 x kNQ columns), one commit
             for (int u = 0; 2 * u < nt; ++u) {
@@ -266,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             asm("max.f32 %0, %1, %2, %3;" : "=f"(m2) : "f"(m0), "f"(m1), "f"(f[6]));
             const uint32_t code = __float_as_uint(fmaxf(m2, f[7]) + kCodeMagic);
             sts_u16(prow[b] + off, code);
-            red_add(hc[b] - 4u * code, inc[b]);
+            if (!(DSA_ABLATE & 4)) red_add(hc[b] - 4u * code, inc[b]);
         }
     };
     // the same with ragged keys (last tile) / ragged queries (last CTA of a pair)
@@ -299,19 +307,33 @@ __global__ void __launch_bounds__(kThreads, 2)
             const int t = 2 * u + i;
             if (t >= nt) break;
             uint32_t r[32];
-            tc::ld_32x32b_x32(tl + (2 * a + i) * kNQ, r);
+            if (DSA_ABLATE & 16) {
+                uint32_t h[16];
+                tc::ld_32x32b_x16(tl + (2 * a + i) * kNQ, h);
+#pragma unroll
+                for (int x = 0; x < 16; ++x) r[x] = r[x + 16] = h[x];
+            } else if (DSA_ABLATE & 8) {
+                uint32_t h[16];
+                tc::ld_32x32b_x16_pack16(tl + (2 * a + i) * kNQ, h);
+#pragma unroll
+                for (int x = 0; x < 16; ++x) r[x] = r[x + 16] = h[x];
+            } else {
+                tc::ld_32x32b_x32(tl + (2 * a + i) * kNQ, r);
+            }
             tc::wait_ld();
             if (i == 1 || t + 1 == nt) {  // slot drained
                 tc::fence_before_sync();
                 __syncwarp();
                 if (lane == 0) tc::mbar_arrive(&acce[a]);
             }
+            if (DSA_ABLATE & 2) { if (r[0] == 0x7fffffffu) red_add(hc[0], r[1]); continue; }  // profiling build only
             if (t < edge_from) process(t, r);
             else process_edge(t, r);
         }
     }
     named_sync_epi();  // every score drained, every code and count in place
     if (warp == 0) tc::tmem_dealloc<kAcc * 2 * kNQ>(tmem);
+    if (DSA_ABLATE & 1) return;  // profiling build only: no selection
 
     // ------------------------------------------------ per-band selection
     const int band = q0 / 8 + warp;  // this warp's band (global index within the pair)

@@ -47,6 +47,7 @@ for r in rows:
 tot = sum(stall.values()) or 1
 toti = sum(inst.values()) or 1
 print(f"total stall samples {tot:.0f}, warp instructions {toti:.3g}")
-for key in sorted(stall, key=lambda k: -stall[k])[:top]:
+order = inst if "--by-inst" in sys.argv else stall
+for key in sorted(order, key=lambda k: -order[k])[:top]:
     print(f"{stall[key] / tot * 100:5.1f}% stall {inst[key] / toti * 100:5.1f}% inst  "
           f"{key[0]}:{key[1]:<4d} {src[key].strip()[:90]}")
