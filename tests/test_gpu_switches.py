@@ -4,7 +4,7 @@ switch runs in a fresh process against a default-path run of the same
 seeded inputs:
 
 * levels, scales and masks: bit-identical;
-* Z: within the dtype tolerance (bit-identical for DSA_FUSE and the
+* Z: within the dtype tolerance (bit-identical for the
   chunked pipeline, which run the same attention kernels).
 
 DSA_PIPELINE_CHUNKS=3 on 7 pairs starts chunks at odd pairs 2 and 4 (the
@@ -38,7 +38,7 @@ CASES = [
     ("DSA_TOPK_GENERIC", "1", C1S, True),
     ("DSA_PREDICT_DFMA", "1", C2S, True),
     ("DSA_PREDICT_DFMA", "1", C0T, True),
-    ("DSA_FUSE", "1", C2S, True),
+    ("DSA_FUSE", "1", C2S, False),
     ("DSA_PIPELINE_CHUNKS", "3", {"preset": "c2_vector", "pairs": 7, "over": {"L": 512, "keep": 26}}, True),
     ("DSA_PIPELINE_CHUNKS", "2", {"preset": "c3_block", "pairs": 3, "over": {"L": 512, "keep": 4}}, True),
 ]
