@@ -184,6 +184,10 @@ void dispatch(const AttnArgs& a, cudaStream_t st) {
 }  // namespace
 
 void run_attention(const AttnArgs& a, cudaStream_t st) {
+    if (block_tc_supported(a)) {
+        run_block_tc(a, st);
+        return;
+    }
     if (band_attention_supported(a)) {
         run_band_attention(a, st);
         return;

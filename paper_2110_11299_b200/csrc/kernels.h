@@ -159,6 +159,9 @@ void run_attention(const AttnArgs& a, cudaStream_t st);
 // prediction_accuracy counts {intersection, total, rows with unequal counts}
 void run_prediction_accuracy(const AttnArgs& pred, const AttnArgs& orc, unsigned long long* out, cudaStream_t st);
 bool band_attention_supported(const AttnArgs& a);
+// block masks, 32 x 32 blocks, d = 128: tcgen05 + TMA (attention_block_tc.cu)
+bool block_tc_supported(const AttnArgs& a);
+void run_block_tc(const AttnArgs& a, cudaStream_t st);
 void run_band_attention(const AttnArgs& a, cudaStream_t st);
 // fused COLVEC select + band attention (mask optional): dsa_pipeline
 bool colvec_fused_supported(const SelectArgs& s, const AttnArgs& a);

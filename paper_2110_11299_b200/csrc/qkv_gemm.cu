@@ -34,6 +34,7 @@
 #include "device_common.cuh"
 #include "kernels.h"
 #include "tc_sm100.cuh"
+#include "tma_map.h"
 
 namespace dsa {
 namespace {
@@ -324,8 +325,10 @@ EncodeFn encode_fn() {
     return fn;
 }
 
-// 2-D bf16 row-major [rows][cols] -> box [box_rows][64] with 128-byte swizzle
-CUtensorMap make_map(const void* ptr, int64_t rows, int64_t cols, int box_rows, int box_cols = kBK) {
+}  // namespace
+
+// 2-D bf16 row-major [rows][cols] -> box [box_rows][box_cols] with 128-byte swizzle
+CUtensorMap make_map(const void* ptr, int64_t rows, int64_t cols, int box_rows, int box_cols) {
     CUtensorMap m;
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
     const cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols * 2)};
@@ -339,8 +342,6 @@ CUtensorMap make_map(const void* ptr, int64_t rows, int64_t cols, int box_rows, 
     if (r != CUDA_SUCCESS) throw_unsupported("cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
     return m;
 }
-
-}  // namespace
 
 void run_qkv_gemm(const QkvGemmArgs& g, cudaStream_t st) {
     QkvArgs a{};
@@ -356,19 +357,14 @@ void run_qkv_gemm(const QkvGemmArgs& g, cudaStream_t st) {
     a.k = static_cast<__nv_bfloat16*>(g.k);
     a.v = static_cast<__nv_bfloat16*>(g.v);
     a.r = g.r;
-    const CUtensorMap mx = make_map(g.x, a.M, a.kdim, kBM);
-    const CUtensorMap mw = make_map(g.w, a.n_out, a.kdim, kBN);
+    const CUtensorMap mx = make_map(g.x, a.M, a.kdim, kBM, kBK);
+    const CUtensorMap mw = make_map(g.w, a.n_out, a.kdim, kBN, kBK);
     a.tma_store = (g.dk % 64 == 0 && g.dv % 64 == 0 && g.L % 32 == 0) ? 1 : 0;
     // store maps: each head slab as rows of d columns, [32 rows][64 cols] boxes
     const CUtensorMap mq = a.tma_store ? make_map(g.q, g.batch * g.heads * g.L, g.dk, 32, 64) : mx;
     const CUtensorMap mk = a.tma_store ? make_map(g.k, g.batch * g.heads * g.L, g.dk, 32, 64) : mx;
     const CUtensorMap mv = a.tma_store ? make_map(g.v, g.batch * g.heads * g.L, g.dv, 32, 64) : mx;
-    static int sms = 0;
-    if (sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int sms = sm_count();
     const int64_t ntiles = ceil_div_i(a.M, kBM) * ceil_div_i(a.n_out, kBN);
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>(ntiles, sms));
     cudaFuncSetAttribute(qkv_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);

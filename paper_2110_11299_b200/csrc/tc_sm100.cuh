@@ -87,6 +87,14 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                  : "memory");
 }
 
+// 2-D tensor-map load (TMA) into shared memory, completion counted on `bar`.
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* map, int x, int y, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_addr(bar))
+        : "memory");
+}
+
 // ----------------------------------------------------------------- TMEM
 template <int NCOLS>
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem) {  // whole warp
@@ -170,6 +178,20 @@ __device__ __forceinline__ uint64_t desc_kmajor_nosw(uint32_t saddr, uint32_t lb
     return d;  // base offset 0, lbo mode 0, layout SWIZZLE_NONE (0)
 }
 
+// Shared-memory descriptor of a 128-byte-swizzled tile (TMA SWIZZLE_128B,
+// 1024-byte aligned): K-major -- rows of 128 B, 8-row atoms `sbo` apart (LBO
+// unused); MN-major -- 64 MN-contiguous elements per 128-byte row, 8 K-rows
+// per atom, atoms along K `sbo` apart, 64-element MN blocks `lbo` apart.
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+    d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+    d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+    d |= static_cast<uint64_t>(1) << 46;
+    d |= static_cast<uint64_t>(2) << 61;  // SWIZZLE_128B
+    return d;
+}
+
 // Instruction descriptor, kind::f16: bf16 A/B (K-major), f32 accumulator.
 __host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N) {
     return (1u << 4)                                   // D format: F32
@@ -177,6 +199,12 @@ __host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N) {
            | (1u << 10)                                // B format: BF16
            | (static_cast<uint32_t>(N >> 3) << 17)     // N
            | (static_cast<uint32_t>(M >> 4) << 24);    // M
+}
+
+// bf16 A/B, f32 accumulator, with the A and/or B operand MN-major
+// (instruction descriptor bits 15 / 16).
+__host__ __device__ constexpr uint32_t idesc_bf16_f32_mn(int M, int N, bool a_mn, bool b_mn) {
+    return idesc_bf16_f32(M, N) | (a_mn ? 1u << 15 : 0u) | (b_mn ? 1u << 16 : 0u);
 }
 
 // f16 A/B (format 0) with an f16 accumulator (D format 0): one 16-bit
