@@ -31,6 +31,8 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <algorithm>
+
 #include "device_common.cuh"
 #include "kernels.h"
 #include "tc_sm100.cuh"
@@ -45,11 +47,15 @@ constexpr int kG = 4;               // blocks per key group (M = 128 keys)
 constexpr int kMaxGroups = 4;       // keep <= 16 blocks (S^T in <= 128 TMEM columns)
 constexpr int kHalf = kG * kBlk * 128;       // one d-half (64 columns) of a group: 16 KB
 constexpr int kStage = 2 * kHalf;            // K or V group: 32 KB
+constexpr int kNS = 4;                       // operand ring stages
 constexpr int kQBytes = kBlk * kD * 2;       // 8 KB (two 4 KB d-halves)
 constexpr int kPBytes = kMaxGroups * kG * kBlk * kBlk * 2;  // P^T: 512 keys x 32 q, 32 KB
 constexpr int kEpi = 4;                      // softmax / output warps (128 TMEM lanes)
-constexpr int kThreads = (kEpi + 1) * 32;
-constexpr int kSmem = 1024 + 2 * kStage + kQBytes + kPBytes + 2 * 4 * 32 * 4 + 256;
+constexpr int kLoadWarp = kEpi, kMmaWarp = kEpi + 1;
+constexpr int kThreads = (kEpi + 2) * 32;
+constexpr int kSmem = 1024 + kNS * kStage + 2 * kQBytes + kPBytes + (4 * 32 + 3 * 32) * 4 + 512;
+// TMEM columns: S^T slots [0, 128), [128, 256); Z^T slots [256, 288), [288, 320)
+constexpr uint32_t kTmemZ = 256;
 
 __device__ __forceinline__ float bc_ex2(float x) {  // 2^x on the SFU
     float y;
@@ -78,209 +84,273 @@ __device__ __forceinline__ float warp_colreduce(float (&v)[32], int lane) {
     return v[0];
 }
 
-__global__ void __launch_bounds__(kThreads, 2)
+// The work list: block rows r = blockIdx.x + j * gridDim.x (j < n) of all
+// pairs.  Operand groups are loaded and consumed in ONE order, the MMA
+// issuer's: K(0), K(1), V(0), K(2), V(1), ..., K(n-1), V(n-2), V(n-1) --
+// S^T(j + 1) is computed while the softmax of row j runs.
+struct Item {
+    int j;
+    bool v;
+};
+__device__ __forceinline__ Item item_at(int i, int n) {
+    if (i == 0) return {0, false};
+    if (i >= 2 * n - 1) return {n - 1, true};
+    return (i & 1) ? Item{(i + 1) / 2, false} : Item{i / 2 - 1, true};
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
     attn_block_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                          const __grid_constant__ CUtensorMap map_v, const uint32_t* __restrict__ block_cols,
-                         int L, int keep, int scale, __nv_bfloat16* __restrict__ Z) {
+                         int L, int64_t nrows, int keep, int scale, __nv_bfloat16* __restrict__ Z) {
     extern __shared__ unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t{1023});
-    unsigned char* stage_p = smem;                       // [2][kStage], 1024-aligned
-    unsigned char* q_p = stage_p + 2 * kStage;           // [2 halves][32 rows][128 B]
-    unsigned char* p_p = q_p + kQBytes;                  // P^T, MN-major, no swizzle
+    unsigned char* stage_p = smem;                       // [kNS][kStage], 1024-aligned
+    unsigned char* q_p = stage_p + kNS * kStage;         // [2 slots][2 halves][32 rows][128 B]
+    unsigned char* p_p = q_p + 2 * kQBytes;              // P^T, MN-major, no swizzle
     float* red = reinterpret_cast<float*>(p_p + kPBytes);  // [4 warps][32] partials
-    float* colv = red + 4 * 32;                          // [32] column max, then 1/sum
-    uint64_t* bars = reinterpret_cast<uint64_t*>(colv + 32 + 32);
-    uint64_t* full = bars;       // [2]
-    uint64_t* empty = bars + 2;  // [2]
-    uint64_t* qbar = bars + 4;
-    uint64_t* sbar = bars + 5;   // S^T complete
-    uint64_t* pbar = bars + 6;   // P^T written
-    uint64_t* zbar = bars + 7;   // Z^T complete
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+    float* mcv = red + 4 * 32;                           // [32] scaled column max
+    float* linv = mcv + 32;                              // [2 slots][32] 1 / column sum
+    uint64_t* bars = reinterpret_cast<uint64_t*>(linv + 64);
+    uint64_t* full = bars;                  // [kNS]
+    uint64_t* empty = full + kNS;           // [kNS]
+    uint64_t* qfull = empty + kNS;          // [2]
+    uint64_t* qempty = qfull + 2;           // [2]
+    uint64_t* sfull = qempty + 2;           // [2]
+    uint64_t* sempty = sfull + 2;           // [2]
+    uint64_t* zfull = sempty + 2;           // [2]
+    uint64_t* zempty = zfull + 2;           // [2]
+    uint64_t* pfull = zempty + 2;
+    uint64_t* pempty = pfull + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pempty + 1);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int64_t pair = blockIdx.y;
-    const int ib = blockIdx.x;
     const int nbr = L / kBlk;
-    const uint32_t* blist = block_cols + (pair * nbr + ib) * static_cast<int64_t>(keep);
+    const int n = nrows > blockIdx.x ? static_cast<int>((nrows - 1 - blockIdx.x) / gridDim.x) + 1 : 0;
     const int ng = (keep + kG - 1) / kG;
-    const int row_q = static_cast<int>(pair * L) + ib * kBlk;  // Q / Z row of query 0
+    auto row_of = [&](int j) -> int64_t { return blockIdx.x + static_cast<int64_t>(j) * gridDim.x; };
 
     if (tid == 0) {
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kNS; ++i) {
             tc::mbar_init(&full[i], 1);
             tc::mbar_init(&empty[i], 1);
         }
-        tc::mbar_init(qbar, 1);
-        tc::mbar_init(sbar, 1);
-        tc::mbar_init(pbar, 1);
-        tc::mbar_init(zbar, 1);
+        for (int i = 0; i < 2; ++i) {
+            tc::mbar_init(&qfull[i], 1);
+            tc::mbar_init(&qempty[i], 1);
+            tc::mbar_init(&sfull[i], 1);
+            tc::mbar_init(&sempty[i], 1);
+            tc::mbar_init(&zfull[i], 1);
+            tc::mbar_init(&zempty[i], 1);
+        }
+        tc::mbar_init(pfull, 1);
+        tc::mbar_init(pempty, 1);
         tc::fence_barrier_init();
     }
-    if (warp == 0) tc::tmem_alloc<256>(tmem_slot);
+    if (warp == 0) tc::tmem_alloc<512>(tmem_slot);
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
-    const uint32_t tmem = *tmem_slot;  // S^T: columns [0, 32 ng); Z^T: [128, 160)
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t st0 = tc::smem_addr(stage_p), q_s = tc::smem_addr(q_p), p_s = tc::smem_addr(p_p);
 
-    if (warp == kEpi) {
-        // ---------------------------------------- TMA producer + MMA issuer
+    if (warp == kLoadWarp) {
+        // ------------------------------------------------------ TMA producer
         if (lane == 0) {
-            const uint32_t st0 = tc::smem_addr(stage_p), q_s = tc::smem_addr(q_p), p_s = tc::smem_addr(p_p);
-            tc::mbar_expect_tx(qbar, kQBytes);
-            tc::tma_load_2d(q_s, &map_q, 0, row_q, qbar);
-            tc::tma_load_2d(q_s + kQBytes / 2, &map_q, 64, row_q, qbar);
-            // load li: groups 0..ng-1 of K, then of V; a missing block of the
-            // last group repeats a kept one (finite data, masked / P = 0)
-            auto load = [&](int li) {
-                const int s = li & 1;
-                const bool isv = li >= ng;
-                const int g = isv ? li - ng : li;
-                if (li >= 2) tc::mbar_wait_sleep(&empty[s], ((li >> 1) - 1) & 1);
-                tc::mbar_expect_tx(&full[s], kStage);
-                const uint32_t dst = st0 + s * kStage;
-#pragma unroll
-                for (int b = 0; b < kG; ++b) {
-                    const int slot = g * kG + b;
-                    const int blk = static_cast<int>(__ldg(blist + (slot < keep ? slot : keep - 1)));
-                    const int row = static_cast<int>(pair * L) + blk * kBlk;
-                    const CUtensorMap* m = isv ? &map_v : &map_k;
-                    tc::tma_load_2d(dst + b * (kBlk * 128), m, 0, row, &full[s]);
-                    tc::tma_load_2d(dst + kHalf + b * (kBlk * 128), m, 64, row, &full[s]);
+            int sc = 0;  // operand groups issued
+            for (int i = 0; i < 2 * n; ++i) {
+                const Item it = item_at(i, n);
+                const int64_t r = row_of(it.j);
+                const int64_t pair = r / nbr;
+                const int ib = static_cast<int>(r % nbr);
+                const int row0 = static_cast<int>(pair * L);
+                if (!it.v) {
+                    const int qs = it.j & 1;
+                    if (it.j >= 2) tc::mbar_wait_sleep(&qempty[qs], ((it.j >> 1) - 1) & 1);
+                    tc::mbar_expect_tx(&qfull[qs], kQBytes);
+                    tc::tma_load_2d(q_s + qs * kQBytes, &map_q, 0, row0 + ib * kBlk, &qfull[qs]);
+                    tc::tma_load_2d(q_s + qs * kQBytes + kQBytes / 2, &map_q, 64, row0 + ib * kBlk, &qfull[qs]);
                 }
-            };
-            const int nload = 2 * ng;
-            int next = 0;
-            for (; next < 2 && next < nload; ++next) load(next);
-            // S^T = K_group . Q^T: M = 128 keys, N = 32, K = 128 (two 64-wide halves)
+                const uint32_t* blist = block_cols + r * keep;
+                const CUtensorMap* m = it.v ? &map_v : &map_k;
+                for (int g = 0; g < ng; ++g, ++sc) {
+                    const int s = sc % kNS;
+                    if (sc >= kNS) tc::mbar_wait_sleep(&empty[s], ((sc / kNS) - 1) & 1);
+                    tc::mbar_expect_tx(&full[s], kStage);
+                    const uint32_t dst = st0 + s * kStage;
+#pragma unroll
+                    for (int b = 0; b < kG; ++b) {
+                        // a missing block of the last group repeats a kept one
+                        // (finite data; masked in S^T, P = 0 in Z^T)
+                        const int slot = g * kG + b;
+                        const int blk = static_cast<int>(__ldg(blist + (slot < keep ? slot : keep - 1)));
+                        tc::tma_load_2d(dst + b * (kBlk * 128), m, 0, row0 + blk * kBlk, &full[s]);
+                        tc::tma_load_2d(dst + kHalf + b * (kBlk * 128), m, 64, row0 + blk * kBlk, &full[s]);
+                    }
+                }
+            }
+        }
+        return;
+    }
+    if (warp == kMmaWarp) {
+        // ------------------------------------------------------- MMA issuer
+        if (lane == 0) {
+            // S^T = K_group . Q^T: M = 128 keys, N = 32, K = 128 (two 64-wide,
+            // 128-byte-swizzled halves; 16-column steps advance 32 B)
             const uint32_t id1 = tc::idesc_bf16_f32(128, kBlk);
-            tc::mbar_wait(qbar, 0);
-            for (int g = 0; g < ng; ++g) {
-                const int s = g & 1;
-                tc::mbar_wait(&full[s], (g >> 1) & 1);
-                tc::fence_after_sync();
-#pragma unroll
-                for (int ks = 0; ks < kD / 16; ++ks) {
-                    const int h = ks >> 2, kk = ks & 3;  // d-half, 16-column step inside it (32 B)
-                    const uint64_t ad = tc::desc_sw128(st0 + s * kStage + h * kHalf + kk * 32, 16, 1024);
-                    const uint64_t bd = tc::desc_sw128(q_s + h * (kQBytes / 2) + kk * 32, 16, 1024);
-                    tc::mma_bf16(tmem + g * kBlk, ad, bd, id1, ks > 0);
-                }
-                tc::commit(&empty[s]);
-                if (next < nload) load(next++);
-            }
-            tc::commit(sbar);
-            // Z^T = V^T . P^T: M = d = 128, N = 32, K = the keys; A = V (MN-major,
-            // swizzled: d-halves 16 KB apart (LBO), 8-key atoms 1024 B (SBO)),
-            // B = P^T (MN-major, no swizzle: 8-query chunks 128 B apart (SBO),
-            // 8-key groups 512 B (LBO))
+            // Z^T = V^T . P^T: M = d = 128, N = 32, K = keys; A = V as loaded
+            // (MN-major, swizzled: d-halves 16 KB apart (LBO), 8-key atoms
+            // 1024 B (SBO)); B = P^T (MN-major, no swizzle: 8-query chunks
+            // 128 B apart (SBO), 8-key groups 512 B (LBO))
             const uint32_t id2 = tc::idesc_bf16_f32_mn(128, kBlk, true, true);
-            tc::mbar_wait_sleep(pbar, 0);
-            tc::fence_after_sync();
-            for (int g = 0; g < ng; ++g) {
-                const int li = ng + g, s = li & 1;
-                tc::mbar_wait(&full[s], (li >> 1) & 1);
-                tc::fence_after_sync();
-#pragma unroll
-                for (int kk = 0; kk < kG * kBlk / 16; ++kk) {
-                    const uint64_t ad = tc::desc_sw128(st0 + s * kStage + kk * 2048, kHalf, 1024);
-                    const uint64_t bd = tc::desc_kmajor_nosw(p_s + (g * 16 + kk * 2) * 512, 512, 128);
-                    tc::mma_bf16(tmem + 128, ad, bd, id2, (g > 0 || kk > 0) ? 1u : 0u);
+            int sc = 0;
+            for (int i = 0; i < 2 * n; ++i) {
+                const Item it = item_at(i, n);
+                const int sl = it.j & 1;
+                if (!it.v) {
+                    tc::mbar_wait(&qfull[sl], (it.j >> 1) & 1);
+                    if (it.j >= 2) tc::mbar_wait(&sempty[sl], ((it.j >> 1) - 1) & 1);
+                } else {
+                    tc::mbar_wait(pfull, it.j & 1);
+                    if (it.j >= 2) tc::mbar_wait(&zempty[sl], ((it.j >> 1) - 1) & 1);
                 }
-                tc::commit(&empty[s]);
-                if (next < nload) load(next++);
+                tc::fence_after_sync();
+                for (int g = 0; g < ng; ++g, ++sc) {
+                    const int s = sc % kNS;
+                    tc::mbar_wait(&full[s], (sc / kNS) & 1);
+                    tc::fence_after_sync();
+                    const uint32_t sb = st0 + s * kStage;
+                    if (!it.v) {
+#pragma unroll
+                        for (int ks = 0; ks < kD / 16; ++ks) {
+                            const int h = ks >> 2, kk = ks & 3;
+                            const uint64_t ad = tc::desc_sw128(sb + h * kHalf + kk * 32, 16, 1024);
+                            const uint64_t bd = tc::desc_sw128(q_s + sl * kQBytes + h * (kQBytes / 2) + kk * 32, 16, 1024);
+                            tc::mma_bf16(tmem + sl * 128 + g * kBlk, ad, bd, id1, ks > 0);
+                        }
+                    } else {
+#pragma unroll
+                        for (int kk = 0; kk < kG * kBlk / 16; ++kk) {
+                            const uint64_t ad = tc::desc_sw128(sb + kk * 2048, kHalf, 1024);
+                            const uint64_t bd = tc::desc_kmajor_nosw(p_s + (g * 16 + kk * 2) * 512, 512, 128);
+                            tc::mma_bf16(tmem + kTmemZ + sl * kBlk, ad, bd, id2, (g > 0 || kk > 0) ? 1u : 0u);
+                        }
+                    }
+                    tc::commit(&empty[s]);
+                }
+                if (!it.v) {
+                    tc::commit(&sfull[sl]);
+                    tc::commit(&qempty[sl]);
+                } else {
+                    tc::commit(&zfull[sl]);
+                    tc::commit(pempty);
+                }
             }
-            tc::commit(zbar);
         }
         return;
     }
 
-    // ------------------------------------------------ softmax (thread = key)
+    // --------------------------------------- softmax + output (4 warps)
     const float c2 = (scale ? rsqrtf(static_cast<float>(kD)) : 1.f) * 1.4426950408889634f;
     const uint32_t tl = tmem + (static_cast<uint32_t>(warp * 32) << 16);
-    tc::mbar_wait_susp(sbar, 0);
-    tc::fence_after_sync();
-    float v[32];
-    float acc[32];
-#pragma unroll
-    for (int q = 0; q < 32; ++q) acc[q] = -INFINITY;
-    for (int g = 0; g < ng; ++g) {
-        uint32_t r[32];
-        tc::ld_32x32b_x32(tl + g * kBlk, r);
+
+    // Z rows of row j: thread = TMEM lane = d; columns = the 32 queries
+    auto output = [&](int j) {
+        const int sl = j & 1;
+        tc::mbar_wait_susp(&zfull[sl], (j >> 1) & 1);
+        tc::fence_after_sync();
+        uint32_t zr[32];
+        tc::ld_32x32b_x32(tl + kTmemZ + sl * kBlk, zr);
         tc::wait_ld();
-        const bool kv = g * kG + warp < keep;  // key slot g*4 + warp of this block row
-        if (kv) {
+        tc::fence_before_sync();
+        const int64_t r = row_of(j);
+        const int64_t q0 = (r / nbr) * L + (r % nbr) * kBlk;
+        const int d = warp * 32 + lane;
+#pragma unroll
+        for (int q = 0; q < 32; ++q)
+            Z[(q0 + q) * kD + d] = __float2bfloat16_rn(__uint_as_float(zr[q]) * linv[sl * 32 + q]);
+        epi_sync();
+        if (tid == 0) tc::mbar_arrive(&zempty[sl]);
+    };
+
+    for (int j = 0; j < n; ++j) {
+        const int sl = j & 1;
+        tc::mbar_wait_susp(&sfull[sl], (j >> 1) & 1);
+        tc::fence_after_sync();
+        const uint32_t ts = tl + sl * 128;
+        float v[32], acc[32];
+#pragma unroll
+        for (int q = 0; q < 32; ++q) acc[q] = -INFINITY;
+        for (int g = 0; g < ng; ++g) {
+            if (g * kG + warp >= keep) continue;  // key slot g*4 + warp not kept
+            uint32_t r[32];
+            tc::ld_32x32b_x32(ts + g * kBlk, r);
+            tc::wait_ld();
 #pragma unroll
             for (int q = 0; q < 32; ++q) acc[q] = fmaxf(acc[q], __uint_as_float(r[q]));
         }
-    }
 #pragma unroll
-    for (int q = 0; q < 32; ++q) v[q] = acc[q];
-    red[warp * 32 + lane] = warp_colreduce<true>(v, lane);
-    epi_sync();
-    if (warp == 0) {
-        const float m = fmaxf(fmaxf(red[lane], red[32 + lane]), fmaxf(red[64 + lane], red[96 + lane]));
-        colv[lane] = m * c2;
-    }
-    epi_sync();
-    float mc[32];
+        for (int q = 0; q < 32; ++q) v[q] = acc[q];
+        red[warp * 32 + lane] = warp_colreduce<true>(v, lane);
+        epi_sync();
+        if (warp == 0)
+            mcv[lane] = fmaxf(fmaxf(red[lane], red[32 + lane]), fmaxf(red[64 + lane], red[96 + lane])) * c2;
+        epi_sync();
+        float mc[32];
 #pragma unroll
-    for (int q = 0; q < 32; q += 4) {
-        const float4 x = *reinterpret_cast<const float4*>(&colv[q]);
-        mc[q] = x.x;
-        mc[q + 1] = x.y;
-        mc[q + 2] = x.z;
-        mc[q + 3] = x.w;
-    }
-#pragma unroll
-    for (int q = 0; q < 32; ++q) acc[q] = 0.f;
-    for (int g = 0; g < ng; ++g) {
-        uint32_t r[32];
-        tc::ld_32x32b_x32(tl + g * kBlk, r);
-        tc::wait_ld();
-        const bool kv = g * kG + warp < keep;
-        uint32_t pk[16];
-#pragma unroll
-        for (int q = 0; q < 32; q += 2) {
-            const float p0 = kv ? bc_ex2(fmaf(__uint_as_float(r[q]), c2, -mc[q])) : 0.f;
-            const float p1 = kv ? bc_ex2(fmaf(__uint_as_float(r[q + 1]), c2, -mc[q + 1])) : 0.f;
-            acc[q] += p0;
-            acc[q + 1] += p1;
-            __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
-            pk[q >> 1] = *reinterpret_cast<uint32_t*>(&h);
+        for (int q = 0; q < 32; q += 4) {
+            const float4 x = *reinterpret_cast<const float4*>(&mcv[q]);
+            mc[q] = x.x;
+            mc[q + 1] = x.y;
+            mc[q + 2] = x.z;
+            mc[q + 3] = x.w;
         }
-        // P^T row `key` (MN-major core matrices: 8 keys x 8 queries, 128 B)
-        const int key = g * (kG * kBlk) + warp * 32 + lane;
-        unsigned char* dst = p_p + (key >> 3) * 512 + (key & 7) * 16;
+        if (j >= 1) tc::mbar_wait_susp(pempty, (j - 1) & 1);  // Z^T(j - 1) has read P^T
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-            *reinterpret_cast<uint4*>(dst + c * 128) = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+        for (int q = 0; q < 32; ++q) acc[q] = 0.f;
+        for (int g = 0; g < ng; ++g) {
+            const bool kv = g * kG + warp < keep;
+            uint32_t r[32];
+            tc::ld_32x32b_x32(ts + g * kBlk, r);
+            tc::wait_ld();
+            uint32_t pk[16];
+#pragma unroll
+            for (int q = 0; q < 32; q += 2) {
+                const float p0 = kv ? bc_ex2(fmaf(__uint_as_float(r[q]), c2, -mc[q])) : 0.f;
+                const float p1 = kv ? bc_ex2(fmaf(__uint_as_float(r[q + 1]), c2, -mc[q + 1])) : 0.f;
+                acc[q] += p0;
+                acc[q + 1] += p1;
+                __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
+                pk[q >> 1] = *reinterpret_cast<uint32_t*>(&h);
+            }
+            // P^T row `key` (MN-major core matrices: 8 keys x 8 queries, 128 B)
+            const int key = g * (kG * kBlk) + warp * 32 + lane;
+            unsigned char* dst = p_p + (key >> 3) * 512 + (key & 7) * 16;
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                *reinterpret_cast<uint4*>(dst + c * 128) =
+                    make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+        }
+        tc::fence_proxy_async();  // P^T (generic stores) -> visible to the tensor core
+        tc::fence_before_sync();
+#pragma unroll
+        for (int q = 0; q < 32; ++q) v[q] = acc[q];
+        red[warp * 32 + lane] = warp_colreduce<false>(v, lane);
+        epi_sync();
+        if (tid == 0) {
+            tc::mbar_arrive(pfull);
+            tc::mbar_arrive(&sempty[sl]);
+        }
+        if (warp == 0) {
+            const float l = red[lane] + red[32 + lane] + red[64 + lane] + red[96 + lane];
+            linv[sl * 32 + lane] = l > 0.f ? 1.f / l : 0.f;
+        }
+        epi_sync();
+        if (j >= 1) output(j - 1);
     }
-    tc::fence_proxy_async();  // P^T (generic stores) -> visible to the tensor core
-#pragma unroll
-    for (int q = 0; q < 32; ++q) v[q] = acc[q];
-    red[warp * 32 + lane] = warp_colreduce<false>(v, lane);
-    epi_sync();
-    if (tid == 0) tc::mbar_arrive(pbar);
-    if (warp == 0) {
-        const float l = red[lane] + red[32 + lane] + red[64 + lane] + red[96 + lane];
-        colv[lane] = l > 0.f ? 1.f / l : 0.f;
-    }
-    epi_sync();
-
-    // ------------------------------------------------ output (thread = d)
-    tc::mbar_wait_susp(zbar, 0);
-    tc::fence_after_sync();
-    uint32_t zr[32];
-    tc::ld_32x32b_x32(tl + 128, zr);
-    tc::wait_ld();
-    const int d = warp * 32 + lane;
-#pragma unroll
-    for (int q = 0; q < 32; ++q)
-        Z[static_cast<int64_t>(row_q + q) * kD + d] = __float2bfloat16_rn(__uint_as_float(zr[q]) * colv[q]);
+    if (n >= 1) output(n - 1);
     tc::fence_before_sync();
     epi_sync();
-    if (warp == 0) tc::tmem_dealloc<256>(tmem);
+    if (warp == 0) tc::tmem_dealloc<512>(tmem);
 }
 
 }  // namespace
@@ -296,8 +366,9 @@ void run_block_tc(const AttnArgs& a, cudaStream_t st) {
     const CUtensorMap mk = make_map(a.k, rows, kD, kBlk, 64);
     const CUtensorMap mv = make_map(a.v, rows, kD, kBlk, 64);
     cudaFuncSetAttribute(attn_block_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-    const dim3 grid(static_cast<unsigned>(a.L / kBlk), static_cast<unsigned>(a.pairs));
-    attn_block_tc_kernel<<<grid, kThreads, kSmem, st>>>(mq, mk, mv, a.cols, static_cast<int>(a.L),
+    const int64_t nrows = a.pairs * (a.L / kBlk);  // block rows of every pair
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(nrows, sm_count()));
+    attn_block_tc_kernel<<<grid, kThreads, kSmem, st>>>(mq, mk, mv, a.cols, static_cast<int>(a.L), nrows,
                                                          static_cast<int>(a.keep), a.scale,
                                                          static_cast<__nv_bfloat16*>(a.z));
     note_launch();
