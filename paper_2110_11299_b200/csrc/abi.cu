@@ -410,6 +410,7 @@ Options read_options() {
     o.topk_generic = env_flag("DSA_TOPK_GENERIC");
     o.predict_dfma = env_flag("DSA_PREDICT_DFMA");
     o.fuse = env_flag("DSA_FUSE");
+    o.block_tc = env_flag("DSA_BLOCK_TC");
     const char* e = std::getenv("DSA_PIPELINE_CHUNKS");
     o.pipeline_chunks = e ? std::atoi(e) : -1;
     return o;

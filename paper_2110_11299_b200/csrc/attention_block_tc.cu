@@ -50,10 +50,10 @@ constexpr int kStage = 2 * kHalf;            // K or V group: 32 KB
 constexpr int kNS = 4;                       // operand ring stages
 constexpr int kQBytes = kBlk * kD * 2;       // 8 KB (two 4 KB d-halves)
 constexpr int kPBytes = kMaxGroups * kG * kBlk * kBlk * 2;  // P^T: 512 keys x 32 q, 32 KB
-constexpr int kEpi = 4;                      // softmax / output warps (128 TMEM lanes)
+constexpr int kEpi = 8;                      // softmax / output warps: 2 groups x 4 (128 TMEM lanes)
 constexpr int kLoadWarp = kEpi, kMmaWarp = kEpi + 1;
 constexpr int kThreads = (kEpi + 2) * 32;
-constexpr int kSmem = 1024 + kNS * kStage + 2 * kQBytes + kPBytes + (4 * 32 + 3 * 32) * 4 + 512;
+constexpr int kSmem = 1024 + kNS * kStage + 2 * kQBytes + 2 * kPBytes + 2 * (4 * 32 + 2 * 32) * 4 + 512;
 // TMEM columns: S^T slots [0, 128), [128, 256); Z^T slots [256, 288), [288, 320)
 constexpr uint32_t kTmemZ = 256;
 
@@ -63,7 +63,9 @@ __device__ __forceinline__ float bc_ex2(float x) {  // 2^x on the SFU
     return y;
 }
 
-__device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, %0;\n" ::"n"(kEpi * 32) : "memory"); }
+// named barriers: 1 + group for one softmax group (4 warps), 3 for all 8 warps
+__device__ __forceinline__ void grp_sync(int grp) { asm volatile("bar.sync %0, 128;\n" ::"r"(1 + grp) : "memory"); }
+__device__ __forceinline__ void epi_sync_all() { asm volatile("bar.sync 3, %0;\n" ::"n"(kEpi * 32) : "memory"); }
 
 // transpose-reduction over a warp: lane l ends with the reduction of
 // column l over the warp's 32 lanes (31 shuffles)
@@ -106,11 +108,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t{1023});
     unsigned char* stage_p = smem;                       // [kNS][kStage], 1024-aligned
     unsigned char* q_p = stage_p + kNS * kStage;         // [2 slots][2 halves][32 rows][128 B]
-    unsigned char* p_p = q_p + 2 * kQBytes;              // P^T, MN-major, no swizzle
-    float* red = reinterpret_cast<float*>(p_p + kPBytes);  // [4 warps][32] partials
-    float* mcv = red + 4 * 32;                           // [32] scaled column max
-    float* linv = mcv + 32;                              // [2 slots][32] 1 / column sum
-    uint64_t* bars = reinterpret_cast<uint64_t*>(linv + 64);
+    unsigned char* p_p = q_p + 2 * kQBytes;              // [2 slots] P^T, MN-major, no swizzle
+    float* redb = reinterpret_cast<float*>(p_p + 2 * kPBytes);  // per group: [4 warps][32] partials,
+                                                                // [32] scaled column max, [32] 1 / column sum
+    uint64_t* bars = reinterpret_cast<uint64_t*>(redb + 2 * (4 * 32 + 2 * 32));
     uint64_t* full = bars;                  // [kNS]
     uint64_t* empty = full + kNS;           // [kNS]
     uint64_t* qfull = empty + kNS;          // [2]
@@ -119,9 +120,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* sempty = sfull + 2;           // [2]
     uint64_t* zfull = sempty + 2;           // [2]
     uint64_t* zempty = zfull + 2;           // [2]
-    uint64_t* pfull = zempty + 2;
-    uint64_t* pempty = pfull + 1;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pempty + 1);
+    uint64_t* pfull = zempty + 2;           // [2]
+    uint64_t* pempty = pfull + 2;           // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pempty + 2);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nbr = L / kBlk;
@@ -142,8 +143,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::mbar_init(&zfull[i], 1);
             tc::mbar_init(&zempty[i], 1);
         }
-        tc::mbar_init(pfull, 1);
-        tc::mbar_init(pempty, 1);
+        for (int i = 0; i < 2; ++i) {
+            tc::mbar_init(&pfull[i], 1);
+            tc::mbar_init(&pempty[i], 1);
+        }
         tc::fence_barrier_init();
     }
     if (warp == 0) tc::tmem_alloc<512>(tmem_slot);
@@ -210,7 +213,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tc::mbar_wait(&qfull[sl], (it.j >> 1) & 1);
                     if (it.j >= 2) tc::mbar_wait(&sempty[sl], ((it.j >> 1) - 1) & 1);
                 } else {
-                    tc::mbar_wait(pfull, it.j & 1);
+                    tc::mbar_wait(&pfull[sl], (it.j >> 1) & 1);
                     if (it.j >= 2) tc::mbar_wait(&zempty[sl], ((it.j >> 1) - 1) & 1);
                 }
                 tc::fence_after_sync();
@@ -231,7 +234,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (int kk = 0; kk < kG * kBlk / 16; ++kk) {
                             const uint64_t ad = tc::desc_sw128(sb + kk * 2048, kHalf, 1024);
-                            const uint64_t bd = tc::desc_kmajor_nosw(p_s + (g * 16 + kk * 2) * 512, 512, 128);
+                            const uint64_t bd = tc::desc_kmajor_nosw(p_s + sl * kPBytes + (g * 16 + kk * 2) * 512, 512, 128);
                             tc::mma_bf16(tmem + kTmemZ + sl * kBlk, ad, bd, id2, (g > 0 || kk > 0) ? 1u : 0u);
                         }
                     }
@@ -242,16 +245,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tc::commit(&qempty[sl]);
                 } else {
                     tc::commit(&zfull[sl]);
-                    tc::commit(pempty);
+                    tc::commit(&pempty[sl]);
                 }
             }
         }
         return;
     }
 
-    // --------------------------------------- softmax + output (4 warps)
+    // ------------------ softmax + output: group grp = rows j = grp (mod 2)
+    // (their S^T / P^T / Z^T slot is grp); 4 warps = the 128 TMEM lanes
     const float c2 = (scale ? rsqrtf(static_cast<float>(kD)) : 1.f) * 1.4426950408889634f;
-    const uint32_t tl = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+    const int grp = warp >> 2, wq = warp & 3, gt = tid & 127;
+    const uint32_t tl = tmem + (static_cast<uint32_t>(wq * 32) << 16);
+    float* red = redb + grp * (4 * 32 + 2 * 32);
+    float* mcv = red + 4 * 32;
+    float* linv = mcv + 32;
 
     // Z rows of row j: thread = TMEM lane = d; columns = the 32 queries
     auto output = [&](int j) {
@@ -264,16 +272,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::fence_before_sync();
         const int64_t r = row_of(j);
         const int64_t q0 = (r / nbr) * L + (r % nbr) * kBlk;
-        const int d = warp * 32 + lane;
+        const int d = wq * 32 + lane;
 #pragma unroll
         for (int q = 0; q < 32; ++q)
-            Z[(q0 + q) * kD + d] = __float2bfloat16_rn(__uint_as_float(zr[q]) * linv[sl * 32 + q]);
-        epi_sync();
-        if (tid == 0) tc::mbar_arrive(&zempty[sl]);
+            Z[(q0 + q) * kD + d] = __float2bfloat16_rn(__uint_as_float(zr[q]) * linv[q]);
+        grp_sync(grp);
+        if (gt == 0) tc::mbar_arrive(&zempty[sl]);
     };
 
-    for (int j = 0; j < n; ++j) {
-        const int sl = j & 1;
+    for (int j = grp; j < n; j += 2) {
+        const int sl = grp;
         tc::mbar_wait_susp(&sfull[sl], (j >> 1) & 1);
         tc::fence_after_sync();
         const uint32_t ts = tl + sl * 128;
@@ -281,7 +289,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int q = 0; q < 32; ++q) acc[q] = -INFINITY;
         for (int g = 0; g < ng; ++g) {
-            if (g * kG + warp >= keep) continue;  // key slot g*4 + warp not kept
+            if (g * kG + wq >= keep) continue;  // key slot g*4 + wq not kept
             uint32_t r[32];
             tc::ld_32x32b_x32(ts + g * kBlk, r);
             tc::wait_ld();
@@ -290,11 +298,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
 #pragma unroll
         for (int q = 0; q < 32; ++q) v[q] = acc[q];
-        red[warp * 32 + lane] = warp_colreduce<true>(v, lane);
-        epi_sync();
-        if (warp == 0)
+        red[wq * 32 + lane] = warp_colreduce<true>(v, lane);
+        grp_sync(grp);
+        if (wq == 0)
             mcv[lane] = fmaxf(fmaxf(red[lane], red[32 + lane]), fmaxf(red[64 + lane], red[96 + lane])) * c2;
-        epi_sync();
+        grp_sync(grp);
         float mc[32];
 #pragma unroll
         for (int q = 0; q < 32; q += 4) {
@@ -304,11 +312,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             mc[q + 2] = x.z;
             mc[q + 3] = x.w;
         }
-        if (j >= 1) tc::mbar_wait_susp(pempty, (j - 1) & 1);  // Z^T(j - 1) has read P^T
+        if (j >= 2) tc::mbar_wait_susp(&pempty[sl], ((j >> 1) - 1) & 1);  // Z^T(j - 2) has read P^T slot
 #pragma unroll
         for (int q = 0; q < 32; ++q) acc[q] = 0.f;
         for (int g = 0; g < ng; ++g) {
-            const bool kv = g * kG + warp < keep;
+            const bool kv = g * kG + wq < keep;
             uint32_t r[32];
             tc::ld_32x32b_x32(ts + g * kBlk, r);
             tc::wait_ld();
@@ -323,8 +331,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 pk[q >> 1] = *reinterpret_cast<uint32_t*>(&h);
             }
             // P^T row `key` (MN-major core matrices: 8 keys x 8 queries, 128 B)
-            const int key = g * (kG * kBlk) + warp * 32 + lane;
-            unsigned char* dst = p_p + (key >> 3) * 512 + (key & 7) * 16;
+            const int key = g * (kG * kBlk) + wq * 32 + lane;
+            unsigned char* dst = p_p + sl * kPBytes + (key >> 3) * 512 + (key & 7) * 16;
 #pragma unroll
             for (int c = 0; c < 4; ++c)
                 *reinterpret_cast<uint4*>(dst + c * 128) =
@@ -334,22 +342,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::fence_before_sync();
 #pragma unroll
         for (int q = 0; q < 32; ++q) v[q] = acc[q];
-        red[warp * 32 + lane] = warp_colreduce<false>(v, lane);
-        epi_sync();
-        if (tid == 0) {
-            tc::mbar_arrive(pfull);
+        if (j >= 2) output(j - 2);  // the group's previous row (reads linv before it is rewritten)
+        red[wq * 32 + lane] = warp_colreduce<false>(v, lane);
+        grp_sync(grp);
+        if (gt == 0) {
+            tc::mbar_arrive(&pfull[sl]);
             tc::mbar_arrive(&sempty[sl]);
         }
-        if (warp == 0) {
+        if (wq == 0) {
             const float l = red[lane] + red[32 + lane] + red[64 + lane] + red[96 + lane];
-            linv[sl * 32 + lane] = l > 0.f ? 1.f / l : 0.f;
+            linv[lane] = l > 0.f ? 1.f / l : 0.f;
         }
-        epi_sync();
-        if (j >= 1) output(j - 1);
+        grp_sync(grp);
     }
-    if (n >= 1) output(n - 1);
+    {
+        const int last = n - 1 - ((n - 1 - grp) & 1);  // this group's last row
+        if (last >= grp && last >= 0) output(last);
+    }
     tc::fence_before_sync();
-    epi_sync();
+    epi_sync_all();
     if (warp == 0) tc::tmem_dealloc<512>(tmem);
 }
 
@@ -357,7 +368,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 bool block_tc_supported(const AttnArgs& a) {
     return a.mode == kBlock && a.bf16 && a.D == kD && a.block == kBlk && a.L % kBlk == 0 && a.keep >= 1 &&
-           a.keep <= kG * kMaxGroups && !options().attn_generic;
+           a.keep <= kG * kMaxGroups && !options().attn_generic && options().block_tc;
 }
 
 void run_block_tc(const AttnArgs& a, cudaStream_t st) {

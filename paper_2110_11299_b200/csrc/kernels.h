@@ -26,6 +26,7 @@ struct Options {
     bool topk_generic;       // DSA_TOPK_GENERIC: CTA-per-row radix top-k
     bool predict_dfma;       // DSA_PREDICT_DFMA: exact fp64 projection chain
     bool fuse;               // DSA_FUSE: COLVEC select + attention in one kernel (measured slower on C2)
+    bool block_tc;           // DSA_BLOCK_TC: tcgen05 + TMA block attention (measured slower on C3)
     int pipeline_chunks;     // DSA_PIPELINE_CHUNKS: pair chunks overlapped on 3 streams
 };
 const Options& options();

@@ -39,6 +39,8 @@ CASES = [
     ("DSA_PREDICT_DFMA", "1", C2S, True),
     ("DSA_PREDICT_DFMA", "1", C0T, True),
     ("DSA_FUSE", "1", C2S, False),
+    ("DSA_BLOCK_TC", "1", {"preset": "c3_block", "pairs": 2, "over": {"L": 1024, "keep": 5}}, False),
+    ("DSA_BLOCK_TC", "1", {"preset": "c3_block", "pairs": 3, "over": {"L": 2048, "keep": 16}}, False),
     ("DSA_PIPELINE_CHUNKS", "3", {"preset": "c2_vector", "pairs": 7, "over": {"L": 512, "keep": 26}}, True),
     ("DSA_PIPELINE_CHUNKS", "2", {"preset": "c3_block", "pairs": 3, "over": {"L": 512, "keep": 4}}, True),
 ]
