@@ -217,10 +217,14 @@ __global__ void __launch_bounds__(kThreads, 2)
             // steps of two key tiles: one accumulator slot (2 x kNQ columns), one commit
             for (int u = 0; 2 * u < nt; ++u) {
                 const int a = u % kAcc;
-                if (u >= kAcc) tc::mbar_wait_susp(&acce[a], ((u / kAcc) - 1) & 1);
+                if (u >= kAcc) {
+                    if (DSA_ABLATE & 64) tc::mbar_wait(&acce[a], ((u / kAcc) - 1) & 1);
+                    else tc::mbar_wait_susp(&acce[a], ((u / kAcc) - 1) & 1);
+                }
                 for (int i = 0; i < 2 && 2 * u + i < nt; ++i) {
                     const int t = 2 * u + i, s = t % kStages;
-                    tc::mbar_wait_susp(&full[s], (t / kStages) & 1);
+                    if (DSA_ABLATE & 64) tc::mbar_wait(&full[s], (t / kStages) & 1);
+                    else tc::mbar_wait_susp(&full[s], (t / kStages) & 1);
                     tc::fence_after_sync();
 #pragma unroll
                     for (int ks = 0; ks < KD / 16; ++ks) {
@@ -300,7 +304,8 @@ __global__ void __launch_bounds__(kThreads, 2)
 
     for (int u = 0; 2 * u < nt; ++u) {
         const int a = u % kAcc;
-        tc::mbar_wait_susp(&accf[a], (u / kAcc) & 1);
+        if (DSA_ABLATE & 64) tc::mbar_wait(&accf[a], (u / kAcc) & 1);
+        else tc::mbar_wait_susp(&accf[a], (u / kAcc) & 1);
         tc::fence_after_sync();
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
