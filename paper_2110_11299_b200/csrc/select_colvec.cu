@@ -57,7 +57,7 @@ constexpr int kBands = kNQ / 8;
 #define DSA_ABL_STAGES 4
 #endif
 constexpr int kStages = DSA_ABL_STAGES;  // K~ ring
-constexpr int kAcc = 2;        // TMEM accumulator slots, two key tiles (2 kNQ columns) each
+constexpr int kAcc = (DSA_ABLATE & 256) ? 1 : 2;  // TMEM accumulator slots, two key tiles (2 kNQ columns) each
 constexpr int kEpiWarps = 8;
 constexpr int kLoadWarp = kEpiWarps;      // TMA producer
 constexpr int kMmaWarp = kEpiWarps + 1;   // tcgen05.mma issuer
