@@ -42,7 +42,9 @@
 #include "kernels.h"
 #include "tc_sm100.cuh"
 
-// DSA_ABLATE: profiling builds only (tools/ablate.py); 0 in the library
+// DSA_ABLATE: profiling builds only (tools/ablate.py; bit 1 -- no selection,
+// bit 2 -- no pooling / histogram / codes, bit 32 -- half the key tiles); 0 in
+// the library
 #ifndef DSA_ABLATE
 #define DSA_ABLATE 0
 #endif
@@ -57,7 +59,7 @@ constexpr int kBands = kNQ / 8;
 #define DSA_ABL_STAGES 4
 #endif
 constexpr int kStages = DSA_ABL_STAGES;  // K~ ring
-constexpr int kAcc = (DSA_ABLATE & 256) ? 1 : 2;  // TMEM accumulator slots, two key tiles (2 kNQ columns) each
+constexpr int kAcc = 2;        // TMEM accumulator slots, two key tiles (2 kNQ columns) each
 constexpr int kEpiWarps = 8;
 constexpr int kLoadWarp = kEpiWarps;      // TMA producer
 constexpr int kMmaWarp = kEpiWarps + 1;   // tcgen05.mma issuer
@@ -212,19 +214,15 @@ __global__ void __launch_bounds__(kThreads, 2)
         // ------------------------------------------------------ MMA issuer
         if (lane == 0) {
             const uint32_t ring_s = tc::smem_addr(ring), q_s = tc::smem_addr(q_sm);
-            const uint32_t idesc = (DSA_ABLATE & 8) ? tc::idesc_f16_f16(kMT, kNQ) : tc::idesc_bf16_f32(kMT, kNQ);
+            const uint32_t idesc = tc::idesc_bf16_f32(kMT, kNQ);
             tc::mbar_wait(qbar, 0);
             // steps of two key tiles: one accumulator slot (2 x kNQ columns), one commit
             for (int u = 0; 2 * u < nt; ++u) {
                 const int a = u % kAcc;
-                if (u >= kAcc) {
-                    if (DSA_ABLATE & 64) tc::mbar_wait(&acce[a], ((u / kAcc) - 1) & 1);
-                    else tc::mbar_wait_susp(&acce[a], ((u / kAcc) - 1) & 1);
-                }
+                if (u >= kAcc) tc::mbar_wait_susp(&acce[a], ((u / kAcc) - 1) & 1);
                 for (int i = 0; i < 2 && 2 * u + i < nt; ++i) {
                     const int t = 2 * u + i, s = t % kStages;
-                    if (DSA_ABLATE & 64) tc::mbar_wait(&full[s], (t / kStages) & 1);
-                    else tc::mbar_wait_susp(&full[s], (t / kStages) & 1);
+                    tc::mbar_wait_susp(&full[s], (t / kStages) & 1);
                     tc::fence_after_sync();
 #pragma unroll
                     for (int ks = 0; ks < KD / 16; ++ks) {
@@ -278,7 +276,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             asm("max.f32 %0, %1, %2, %3;" : "=f"(m2) : "f"(m0), "f"(m1), "f"(f[6]));
             const uint32_t code = __float_as_uint(fmaxf(m2, f[7]) + kCodeMagic);
             sts_u16(prow[b] + off, code);
-            if (!(DSA_ABLATE & 4)) red_add(hc[b] - 4u * code, inc[b]);
+            red_add(hc[b] - 4u * code, inc[b]);
         }
     };
     // the same with ragged keys (last tile) / ragged queries (last CTA of a pair)
@@ -304,34 +302,21 @@ __global__ void __launch_bounds__(kThreads, 2)
 
     for (int u = 0; 2 * u < nt; ++u) {
         const int a = u % kAcc;
-        if (DSA_ABLATE & 64) tc::mbar_wait(&accf[a], (u / kAcc) & 1);
-        else tc::mbar_wait_susp(&accf[a], (u / kAcc) & 1);
+        tc::mbar_wait_susp(&accf[a], (u / kAcc) & 1);
         tc::fence_after_sync();
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
             const int t = 2 * u + i;
             if (t >= nt) break;
             uint32_t r[32];
-            if (DSA_ABLATE & 16) {
-                uint32_t h[16];
-                tc::ld_32x32b_x16(tl + (2 * a + i) * kNQ, h);
-#pragma unroll
-                for (int x = 0; x < 16; ++x) r[x] = r[x + 16] = h[x];
-            } else if (DSA_ABLATE & 8) {
-                uint32_t h[16];
-                tc::ld_32x32b_x16_pack16(tl + (2 * a + i) * kNQ, h);
-#pragma unroll
-                for (int x = 0; x < 16; ++x) r[x] = r[x + 16] = h[x];
-            } else {
-                tc::ld_32x32b_x32(tl + (2 * a + i) * kNQ, r);
-            }
+            tc::ld_32x32b_x32(tl + (2 * a + i) * kNQ, r);
             tc::wait_ld();
             if (i == 1 || t + 1 == nt) {  // slot drained
                 tc::fence_before_sync();
                 __syncwarp();
                 if (lane == 0) tc::mbar_arrive(&acce[a]);
             }
-            if (DSA_ABLATE & 2) { if (r[0] == 0x7fffffffu) red_add(hc[0], r[1]); continue; }  // profiling build only
+            if (DSA_ABLATE & 2) { if (r[0] == 0x7fffffffu) red_add(hist_s, r[1]); continue; }  // profiling build only
             if (t < edge_from) process(t, r);
             else process_edge(t, r);
         }
