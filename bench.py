@@ -101,10 +101,21 @@ def dist_setup():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
+        import torch
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl" if os.environ.get("DSA_BENCH_BACKEND") != "gloo" else "gloo")
+        # NCCL needs one GPU per rank; more ranks than GPUs (a 1-GPU box
+        # checking the partition logic) or a CPU run fall back to gloo
+        ndev = torch.cuda.device_count() if torch.cuda.is_available() else 0
+        backend = os.environ.get("DSA_BENCH_BACKEND") or ("nccl" if ndev >= world else "gloo")
+        dist.init_process_group(backend)
     return rank, local, world
+
+
+def dist_device(device):
+    """Device for collective tensors: the GPU under NCCL, the host under gloo."""
+    import torch.distributed as dist
+    return device if dist.get_backend() == "nccl" else "cpu"
 
 
 def barrier(world):
@@ -118,7 +129,7 @@ def max_over_ranks(x: float, world: int, device) -> float:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device=device)
+    t = torch.tensor([x], dtype=torch.float64, device=dist_device(device))
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -245,7 +256,7 @@ def global_checksum(z_local, p, world: int):
     from paper_2110_11299_b200.shard import gather_checksums, pair_checksums
     cs = pair_checksums(z_local)
     if world > 1:
-        cs = gather_checksums(cs, p.pairs)
+        cs = gather_checksums(cs.to(dist_device(cs.device)), p.pairs)
     return [float(cs[:, 0].sum().item()), float(cs[:, 1].max().item())] if cs.shape[0] else [0.0, 0.0]
 
 
