@@ -411,6 +411,7 @@ Options read_options() {
     o.predict_dfma = env_flag("DSA_PREDICT_DFMA");
     o.fuse = env_flag("DSA_FUSE");
     o.block_tc = env_flag("DSA_BLOCK_TC");
+    o.predict_tiles = env_flag("DSA_PREDICT_TILES");
     const char* e = std::getenv("DSA_PIPELINE_CHUNKS");
     o.pipeline_chunks = e ? std::atoi(e) : -1;
     return o;

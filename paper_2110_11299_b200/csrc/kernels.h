@@ -27,6 +27,7 @@ struct Options {
     bool predict_dfma;       // DSA_PREDICT_DFMA: exact fp64 projection chain
     bool fuse;               // DSA_FUSE: COLVEC select + attention in one kernel (measured slower on C2)
     bool block_tc;           // DSA_BLOCK_TC: tcgen05 + TMA block attention (measured slower on C3)
+    bool predict_tiles;      // DSA_PREDICT_TILES: tile kernels instead of the one-CTA-per-tensor pass
     int pipeline_chunks;     // DSA_PIPELINE_CHUNKS: pair chunks overlapped on 3 streams
 };
 const Options& options();
@@ -64,6 +65,8 @@ void run_predict_fast(const PredictArgs& a, cudaStream_t st);
 bool predict_tc_supported(const PredictArgs& a);
 size_t predict_tc_image_bytes(int64_t D, int64_t KD);
 void run_predict_tc(const PredictArgs& a, cudaStream_t st);
+bool predict_tensor_supported(const PredictArgs& a);
+void run_predict_tensor(const PredictArgs& a, cudaStream_t st);
 
 // approx_scores_from_r with the per-head k x k W~ (P/src/predictor.cpp:67-80)
 struct WtildeArgs {

@@ -197,6 +197,10 @@ void launch_quantize_x64(const double* x64, const unsigned long long* amax, int6
 
 void run_predict(const PredictArgs& a, cudaStream_t st) {
     const bool force_dfma = options().predict_dfma;
+    if (!force_dfma && predict_tensor_supported(a)) {
+        run_predict_tensor(a, st);
+        return;
+    }
     if (!force_dfma && predict_tc_supported(a)) {
         run_predict_tc(a, st);
         return;

@@ -30,7 +30,7 @@
 // and the per-row pass they go to a shared list recomputed by the whole CTA
 // (the reference chain is sequential, so one element per thread); in the
 // streaming x^ pass (<= 4-bit levels) they go to a global deferred list
-// (one atomic per block) that quantize_fix_kernel recomputes, one thread per
+// (one atomic per warp that has any) that quantize_fix_kernel recomputes, one thread per
 // entry, grid = 2 x SM count.  When the list is full the streaming pass
 // recomputes the level in place.
 // HBM traffic: Q and K read twice (amax pass, quantise pass) or once plus
@@ -117,9 +117,11 @@ __global__ void psplit_kernel(const float* __restrict__ p, unsigned char* __rest
     if (lcnt != nullptr && threadIdx.x == 0) *lcnt = 0ull;  // deferred-recompute list
     if (amax != nullptr)
         for (int64_t i = threadIdx.x; i < namax; i += blockDim.x) amax[i] = 0ull;  // amax pass accumulators
+    __shared__ float p_s[D * KD];  // P staged once: the norm chains below read it from shared memory
     for (int i = threadIdx.x; i < D * KD; i += blockDim.x) {
         const int c = i / KD, j = i % KD;
-        const float v = p[i];
+        const float v = __ldg(p + i);
+        p_s[i] = v;
         const __nv_bfloat16 b1 = __float2bfloat16_rn(v);
         const float r1 = v - __bfloat162float(b1);
         const __nv_bfloat16 b2 = __float2bfloat16_rn(r1);
@@ -129,10 +131,11 @@ __global__ void psplit_kernel(const float* __restrict__ p, unsigned char* __rest
         *reinterpret_cast<__nv_bfloat16*>(img + opnd_off<D>(KD + j, c)) = b2;
         *reinterpret_cast<__nv_bfloat16*>(img + opnd_off<D>(2 * KD + j, c)) = b3;
     }
+    __syncthreads();
     if (threadIdx.x < KD) {
         double s2 = 0.0;
         for (int u = 0; u < D; ++u) {
-            const double v = static_cast<double>(p[u * KD + threadIdx.x]);
+            const double v = static_cast<double>(p_s[u * KD + threadIdx.x]);
             s2 = fma(v, v, s2);
         }
         reinterpret_cast<float*>(img + Sm::kB)[threadIdx.x] = static_cast<float>(sqrt(s2) * 1.001);
@@ -428,7 +431,7 @@ __global__ void __launch_bounds__(R)
 
 // Streaming quantise pass over the stored x^ (thread = row x 8 columns):
 // certified levels; the uncertified ones get list slots (one global atomic
-// per block) and are recomputed by quantize_fix_kernel, one thread each
+// per warp that has any) and are recomputed by quantize_fix_kernel, one thread each
 // (in place, by the reference chain, only if the list is full).
 template <int D, int KD>
 __global__ void __launch_bounds__(256)
@@ -451,7 +454,7 @@ __global__ void __launch_bounds__(256)
         s_inv = static_cast<float>(qmax / am0);
     }
     __syncthreads();
-    // no early exit: the deferred-list slots are allocated block-wide
+    // no early exit before the warp-wide slot allocation below
     const bool active = idx < L * NC;
     const int c = static_cast<int>(idx % NC);
     const int64_t r = active ? idx / NC : 0;
@@ -492,30 +495,24 @@ __global__ void __launch_bounds__(256)
             }
         }
     }
-    // block-wide slot allocation: one global atomic per block
-    __shared__ unsigned wsum[8];
-    __shared__ unsigned long long lbase;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    // warp-aggregated slot allocation: uncertified levels are rare (~0.04 %),
+    // so almost every warp skips the atomic and no block barrier is needed
+    const int lane = threadIdx.x & 31;
     const unsigned cnt = static_cast<unsigned>(__popc(um));
-    unsigned incl = cnt;
+    unsigned long long slot = 0;
+    if (__any_sync(0xffffffffu, cnt != 0)) {
+        unsigned incl = cnt;
 #pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        const unsigned y = __shfl_up_sync(0xffffffffu, incl, off);
-        if (lane >= off) incl += y;
-    }
-    if (lane == 31) wsum[wid] = incl;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned tot = 0;
-        for (int x = 0; x < static_cast<int>(blockDim.x >> 5); ++x) {
-            const unsigned t = wsum[x];
-            wsum[x] = tot;
-            tot += t;
+        for (int off = 1; off < 32; off <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += y;
         }
-        lbase = tot ? atomicAdd(lcnt, static_cast<unsigned long long>(tot)) : 0ull;
+        const unsigned tot = __shfl_sync(0xffffffffu, incl, 31);
+        unsigned long long base = 0;
+        if (lane == 31) base = atomicAdd(lcnt, static_cast<unsigned long long>(tot));
+        base = __shfl_sync(0xffffffffu, base, 31);
+        slot = base + (incl - cnt);
     }
-    __syncthreads();
-    unsigned long long slot = lbase + wsum[wid] + (incl - cnt);
     while (um) {
         const int u = __ffs(um) - 1;
         um &= um - 1u;
@@ -553,7 +550,14 @@ __global__ void __launch_bounds__(256)
     const unsigned long long* lcnt =
         reinterpret_cast<const unsigned long long*>(xhat + pairs * 2 * L * (KD + 1));
     const unsigned long long* list = lcnt + 1;
+    // P (exact f32 -> f64) staged in shared memory, so the 64- / 128-step
+    // chain below waits on FMAs only, not on a load per step; its loads are
+    // issued alongside the list-count read
+    __shared__ double ps[D * KD];
     const int64_t n = min(static_cast<int64_t>(*lcnt), pairs * L * KD / 4);
+    for (int i = threadIdx.x; i < D * KD; i += blockDim.x) ps[i] = static_cast<double>(__ldg(p + i));
+    if (static_cast<int64_t>(blockIdx.x) * blockDim.x >= n) return;  // the list is short: most blocks idle
+    __syncthreads();
     for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const unsigned long long v = list[e];
@@ -562,9 +566,14 @@ __global__ void __launch_bounds__(256)
         const int which = static_cast<int>(pw & 1);
         const int64_t pair = pw >> 1;
         const double s = __longlong_as_double(static_cast<long long>(amax[pw])) / qmax;
-        const __nv_bfloat16* row = (which ? k : q) + (pair * L + r) * D;
+        const uint4* row = reinterpret_cast<const uint4*>((which ? k : q) + (pair * L + r) * D);
+        uint4 xr[D / 8];
+#pragma unroll
+        for (int t = 0; t < D / 8; ++t) xr[t] = __ldg(row + t);  // the whole row in flight at once
+        const __nv_bfloat16* xe = reinterpret_cast<const __nv_bfloat16*>(xr);
         double acc = 0.0;
-        for (int t = 0; t < D; ++t) acc = fma(to_double(row[t]), static_cast<double>(__ldg(p + t * KD + j)), acc);
+#pragma unroll
+        for (int t = 0; t < D; ++t) acc = fma(to_double(xe[t]), ps[t * KD + j], acc);
         if (round_f32) acc = static_cast<double>(static_cast<float>(acc));
         const float lv = static_cast<float>(fmin(fmax(round_half_away(acc / s), -qmax), qmax));
         (which ? lk : lq)[pair * L * KD + lvl_index(L, r, j)] = static_cast<uint16_t>(__float_as_uint(lv) >> 16);

@@ -38,6 +38,10 @@ CASES = [
     ("DSA_TOPK_GENERIC", "1", C1S, True),
     ("DSA_PREDICT_DFMA", "1", C2S, True),
     ("DSA_PREDICT_DFMA", "1", C0T, True),
+    ("DSA_PREDICT_TILES", "1", C2S, True),
+    ("DSA_PREDICT_TILES", "1", {"preset": "c2_vector", "pairs": 3, "over": {"L": 1000, "keep": 50}}, True),
+    ("DSA_PREDICT_TILES", "1", {"preset": "c2_vector", "pairs": 2, "over": {"L": 4096, "keep": 205}}, True),
+    ("DSA_PREDICT_TILES", "1", {"preset": "c2_vector", "pairs": 2, "over": {"L": 3000, "keep": 150, "bits": 8}}, True),
     ("DSA_FUSE", "1", C2S, False),
     ("DSA_BLOCK_TC", "1", {"preset": "c3_block", "pairs": 2, "over": {"L": 1024, "keep": 5}}, False),
     ("DSA_BLOCK_TC", "1", {"preset": "c3_block", "pairs": 3, "over": {"L": 2048, "keep": 16}}, False),
