@@ -9,13 +9,17 @@
 // LOWER key first among equals, P/src/linalg.cpp:77-80), ascending list.
 //
 // One CTA = 64 queries (8 bands) of one (b,h) pair, 10 warps:
-//   * warp 8 (TMA producer, one lane): K~ tiles (128 keys) by bulk copies
-//     straight from the chunk-planar levels (one copy per 8-column plane)
-//     into a 4-stage ring, refilling a stage as soon as its MMA completed;
-//   * warp 9 (MMA issuer, one lane): one tcgen05.mma (M = 128 keys, N = 64
-//     queries, K = 16 per instruction) per tile into one of 4 TMEM
-//     accumulators, committed to the accumulator's "full" and the stage's
-//     "empty" barrier;
+//   * warp 8 (TMA producer, one lane): per accumulator slot, its two K~ tiles
+//     (256 keys) by ONE bulk copy per 8-column plane straight from the
+//     chunk-planar levels into the slot's stage, refilled as soon as the
+//     slot's MMAs completed;
+//   * warp 9 (MMA issuer, one lane): per slot two tcgen05.mma (M = 128 keys,
+//     N = 64 queries, K = 16 per instruction) and ONE commit, which both
+//     hands the slot to the epilogue and frees its stage.  (A commit or a
+//     bulk copy costs a single issuing thread hundreds of cycles once the SM
+//     is busy -- tools/mma_issue_bench.cu, tools/tma_issue_bench.cu -- so a
+//     commit per tile plus one per slot capped the score loop: 0.415 ms ->
+//     0.371 ms on C2 with one per slot);
 //   * warps 0-7 (epilogue): warp w drains TMEM lanes 32 (w & 3).. (= keys)
 //     x columns 32 (w >> 2).. (= 4 bands) with ONE tcgen05.ld per tile and
 //     frees the accumulator, then per band: max over 8 columns (FMNMX3), one
@@ -34,6 +38,8 @@
 // FUSED (d = 64, k = 16): the 8 warps then run the band attention
 // (band_core.cuh) on their lists straight from shared memory, so the mask
 // never touches HBM unless the caller asks for it.
+#include <algorithm>
+
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -55,10 +61,6 @@ namespace {
 constexpr int kMT = 128;       // keys per tile (UMMA M)
 constexpr int kNQ = 64;        // queries per CTA (UMMA N) = 8 bands
 constexpr int kBands = kNQ / 8;
-#ifndef DSA_ABL_STAGES
-#define DSA_ABL_STAGES 4
-#endif
-constexpr int kStages = DSA_ABL_STAGES;  // K~ ring
 constexpr int kAcc = 2;        // TMEM accumulator slots, two key tiles (2 kNQ columns) each
 constexpr int kEpiWarps = 8;
 constexpr int kLoadWarp = kEpiWarps;      // TMA producer
@@ -72,17 +74,18 @@ template <int KD>
 struct Layout {
     static constexpr int kPlanesA = KD / 8;
     static constexpr int kTile = kMT * KD * 2;          // one K~ tile (bytes)
+    static constexpr int kStage = 2 * kTile;            // one accumulator slot's two tiles
     static constexpr int kQ = kNQ * KD * 2;             // the Q~ block
     static constexpr int kMaxM = KD * 49;               // |score| bound, qmax <= 7
     static constexpr int kBins = (2 * kMaxM + 1 + 255) / 256 * 256;  // per band pair (u32 = 2 x u16)
     static constexpr int kHist = (kBands / 2) * kBins * 4;
     static constexpr int kObuf = kBands * kList * 4;
     static constexpr int kHistRegion = kHist > kObuf ? kHist : kObuf;
-    static constexpr int kBars = (2 * kStages + 2 * kAcc + 1) * 8 + 16;
+    static constexpr int kBars = (3 * kAcc + 1) * 8 + 16;
     // ring + pooled codes (reused by the fused attention's per-warp buffers)
     __host__ __device__ static size_t work_bytes(int64_t L, bool fused) {
         const size_t nt = static_cast<size_t>((L + kMT - 1) / kMT);
-        const size_t w = static_cast<size_t>(kStages) * kTile + ((DSA_ABLATE & 2) ? 0 : static_cast<size_t>(kBands) * nt * kMT * 2);
+        const size_t w = static_cast<size_t>(kAcc) * kStage + ((DSA_ABLATE & 2) ? 0 : static_cast<size_t>(kBands) * nt * kMT * 2);
         const size_t f = fused ? sizeof(bc::BandSmemV2<64>) * kEpiWarps : 0;
         return w > f ? w : f;
     }
@@ -126,6 +129,153 @@ __device__ __forceinline__ uint32_t code_off(int j) {
     return static_cast<uint32_t>(((seg << 4) + (c ^ (seg & 7))) << 4) + ((j & 7) << 1);
 }
 
+// The keep-th largest pooled value T of one band and the counts above / at
+// it, from the band's histogram (bins v = M .. -M at word offsets 0 ..;
+// 16-bit half `sh` of each u32 word): cumulative counts from the top bin,
+// 256 bins per warp step.  One warp.
+struct BandCut {
+    int T = 0;
+    uint32_t n_gt = 0, n_eq = 0;
+};
+__device__ __forceinline__ BandCut band_cut(uint32_t hp, int sh, int M, int keep, int lane) {
+    BandCut r;
+    const int nbins = 2 * M + 1;
+    uint32_t carry = 0;
+    for (int h0 = 0; h0 < nbins; h0 += 256) {
+        const uint4 x = lds128(hp + (h0 + 8 * lane) * 4), y = lds128(hp + (h0 + 8 * lane + 4) * 4);
+        const uint32_t mine = ((x.x + x.y + x.z + x.w + y.x + y.y + y.z + y.w) >> sh) & 0xFFFFu;
+        uint32_t incl = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += u;
+        }
+        const unsigned hit = __ballot_sync(0xffffffffu, carry + incl >= static_cast<uint32_t>(keep));
+        if (hit) {
+            const int f = __ffs(hit) - 1;
+            uint32_t run = carry + __shfl_sync(0xffffffffu, incl - mine, f);
+            const int hb = h0 + 8 * f;
+            int tt = 0;
+            uint32_t gt = 0, eq = 0;
+            if (lane == 0) {
+                for (int i = 0; i < 8; ++i) {
+                    const uint32_t c = (lds_u16(hp + (hb + i) * 4 + (sh >> 3))) & 0xFFFFu;
+                    if (run + c >= static_cast<uint32_t>(keep)) {
+                        tt = M - (hb + i);
+                        gt = run;
+                        eq = c;
+                        break;
+                    }
+                    run += c;
+                }
+            }
+            r.T = __shfl_sync(0xffffffffu, tt, 0);
+            r.n_gt = __shfl_sync(0xffffffffu, gt, 0);
+            r.n_eq = __shfl_sync(0xffffffffu, eq, 0);
+            break;
+        }
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    return r;
+}
+
+// The band's ascending list of kept keys (value desc, lowest key first among
+// equals at T) from its pooled codes `prow_s`: one pass with packed f16
+// compares building a key bitmap of v >= T, a warp prefix sum placing those
+// keys in order in the staging list `obuf` (kList entries), then the ties
+// beyond `rem` dropped; written to `o` when given (obuf holds the list on
+// return).  One warp.
+__device__ __forceinline__ void band_emit(const BandCut& cut, uint32_t prow_s, uint32_t* obuf, uint32_t* o, int keep,
+                                          int Lp, int lane) {
+    const uint32_t codeT = 0x4000u + static_cast<uint32_t>(cut.T);
+    const uint32_t rem = static_cast<uint32_t>(keep) - cut.n_gt;  // ties admitted, lowest keys first
+    const uint32_t n_ge = cut.n_gt + cut.n_eq;
+    const int nseg = Lp / kMT;
+    const unsigned lt = lanemask_lt();
+    if (n_ge <= static_cast<uint32_t>(kList)) {
+        // (a) every key with v >= T, ascending, into the staging list
+        const uint32_t T2 = codeT | (codeT << 16);
+        uint32_t base = 0;
+        for (int s0 = 0; s0 < nseg; s0 += 32) {
+            const int seg = s0 + lane;
+            uint32_t w[4] = {0u, 0u, 0u, 0u};
+            if (seg < nseg) {
+                const uint32_t sb = prow_s + static_cast<uint32_t>(seg) * 256;
+#pragma unroll
+                for (int c = 0; c < 16; ++c) {
+                    const uint4 x = lds128(sb + static_cast<uint32_t>((c ^ (seg & 7)) << 4));
+                    uint32_t tb = hge2(x.x, T2) & 0x00020001u;
+                    tb |= hge2(x.y, T2) & 0x00080004u;
+                    tb |= hge2(x.z, T2) & 0x00200010u;
+                    tb |= hge2(x.w, T2) & 0x00800040u;
+                    w[c >> 2] |= ((tb | (tb >> 16)) & 0xFFu) << ((c & 3) * 8);
+                }
+            }
+            const uint32_t n = __popc(w[0]) + __popc(w[1]) + __popc(w[2]) + __popc(w[3]);
+            uint32_t incl = n;
+#pragma unroll
+            for (int q = 1; q < 32; q <<= 1) {
+                const uint32_t u = __shfl_up_sync(0xffffffffu, incl, q);
+                if (lane >= q) incl += u;
+            }
+            uint32_t pos = base + incl - n;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                uint32_t x = w[j];
+                while (x) {
+                    const int bit = __ffs(x) - 1;
+                    x &= x - 1;
+                    obuf[pos++] = static_cast<uint32_t>(seg * kMT + j * 32 + bit);
+                }
+            }
+            base += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        __syncwarp();
+        if (n_ge == static_cast<uint32_t>(keep)) {
+            if (o)
+                for (int i = lane; i < keep; i += 32) o[i] = obuf[i];
+        } else {
+            // (b) drop the ties beyond `rem` (compacted in place)
+            uint32_t eq_seen = 0, outp = 0;
+            for (uint32_t i0 = 0; i0 < n_ge; i0 += 32) {
+                const uint32_t i = i0 + lane;
+                const bool valid = i < n_ge;
+                const uint32_t col = valid ? obuf[i] : 0u;
+                const bool eq = valid && lds_u16(prow_s + code_off(static_cast<int>(col))) == codeT;
+                const unsigned be = __ballot_sync(0xffffffffu, eq);
+                const bool kp = valid && (!eq || eq_seen + __popc(be & lt) < rem);
+                const unsigned bk = __ballot_sync(0xffffffffu, kp);
+                __syncwarp();  // every lane read its entry before any write below
+                if (kp) {
+                    obuf[outp + __popc(bk & lt)] = col;
+                    if (o) o[outp + __popc(bk & lt)] = col;
+                }
+                outp += __popc(bk);
+                eq_seen += __popc(be);
+            }
+        }
+    } else {
+        // rare (a flood of ties at T): one ascending pass, two ballots per
+        // 32 keys -- v > T, or v == T among the first `rem` ties
+        const uint32_t trash = static_cast<uint32_t>(kList - 32 + lane);
+        uint32_t taken = 0, eq_seen = 0;
+        for (int j0 = 0; j0 < Lp; j0 += 32) {
+            const int j = j0 + lane;
+            const uint32_t c = lds_u16(prow_s + code_off(j));
+            const bool gt = c > codeT && c != 0u, eq = c == codeT;
+            const unsigned be = __ballot_sync(0xffffffffu, eq);
+            const bool take = gt || (eq && eq_seen + __popc(be & lt) < rem);
+            const unsigned bt = __ballot_sync(0xffffffffu, take);
+            const uint32_t slot = take ? taken + __popc(bt & lt) : trash;
+            obuf[slot] = static_cast<uint32_t>(j);
+            if (take && o) o[slot] = static_cast<uint32_t>(j);
+            taken += __popc(bt);
+            eq_seen += __popc(be);
+        }
+    }
+    __syncwarp();
+}
+
 struct FusedAttn {
     const __nv_bfloat16* q;
     const __nv_bfloat16* k;
@@ -145,12 +295,11 @@ __global__ void __launch_bounds__(kThreads, 2)
     const size_t work = Lay::work_bytes(L, FUSED);
     unsigned char* q_sm = smem;
     unsigned char* ring = smem + Lay::kQ;
-    unsigned char* pooled = ring + kStages * Lay::kTile;
+    unsigned char* pooled = ring + kAcc * Lay::kStage;
     unsigned char* histp = smem + Lay::kQ + work;
     uint64_t* bars = reinterpret_cast<uint64_t*>(histp + Lay::kHistRegion);
-    uint64_t* full = bars;                   // [kStages] TMA -> MMA
-    uint64_t* empty = bars + kStages;        // [kStages] MMA done -> refill
-    uint64_t* accf = bars + 2 * kStages;     // [kAcc] MMAs of a slot done -> epilogue
+    uint64_t* full = bars;                   // [kAcc] a slot's stage landed (TMA -> MMA)
+    uint64_t* accf = bars + kAcc;            // [kAcc] MMAs of a slot done -> epilogue, stage free
     uint64_t* acce = accf + kAcc;            // [kAcc] slot drained -> MMA (8 arrivals)
     uint64_t* qbar = acce + kAcc;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(qbar + 1);
@@ -162,11 +311,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     const uint16_t* lkp = lk + pair * static_cast<int64_t>(L) * KD;
 
     if (tid == 0) {
-        for (int i = 0; i < kStages; ++i) {
-            tc::mbar_init(&full[i], 1);
-            tc::mbar_init(&empty[i], 1);
-        }
         for (int i = 0; i < kAcc; ++i) {
+            tc::mbar_init(&full[i], 1);
             tc::mbar_init(&accf[i], 1);
             tc::mbar_init(&acce[i], kEpiWarps);
         }
@@ -195,17 +341,19 @@ __global__ void __launch_bounds__(kThreads, 2)
                     tc::bulk_g2s(q_s + c * (kNQ * 16), lqp + (static_cast<int64_t>(c) * L + q0) * 8,
                                  static_cast<uint32_t>(rows * 16), qbar);
             }
-            for (int t = 0; t < nt; ++t) {
-                const int s = t % kStages;
-                if (t >= kStages) tc::mbar_wait_susp(&empty[s], ((t / kStages) - 1) & 1);  // MMA t - kStages done
-                const int row0 = t * kMT;
-                const int rows = L - row0 < kMT ? L - row0 : kMT;
-                tc::mbar_expect_tx(&full[s], static_cast<uint32_t>(rows * 16 * Lay::kPlanesA));
+            // one stage per accumulator slot (two key tiles, [plane][256 keys][16 B]:
+            // ONE bulk copy per plane), refilled once the slot's MMAs completed
+            for (int u = 0; 2 * u < nt; ++u) {
+                const int a = u % kAcc;
+                if (u >= kAcc) tc::mbar_wait_susp(&accf[a], ((u / kAcc) - 1) & 1);
+                const int row0 = 2 * u * kMT;
+                const int rows = L - row0 < 2 * kMT ? L - row0 : 2 * kMT;
+                tc::mbar_expect_tx(&full[a], static_cast<uint32_t>(rows * 16 * Lay::kPlanesA));
 #pragma unroll
                 for (int c = 0; c < Lay::kPlanesA; ++c)
-                    tc::bulk_g2s(ring_s + s * Lay::kTile + c * (kMT * 16),
+                    tc::bulk_g2s(ring_s + a * Lay::kStage + c * (2 * kMT * 16),
                                  lkp + (static_cast<int64_t>(c) * L + row0) * 8, static_cast<uint32_t>(rows * 16),
-                                 &full[s]);
+                                 &full[a]);
             }
         }
         return;
@@ -216,25 +364,25 @@ __global__ void __launch_bounds__(kThreads, 2)
             const uint32_t ring_s = tc::smem_addr(ring), q_s = tc::smem_addr(q_sm);
             const uint32_t idesc = tc::idesc_bf16_f32(kMT, kNQ);
             tc::mbar_wait(qbar, 0);
-            // steps of two key tiles: one accumulator slot (2 x kNQ columns), one commit
+            // per slot: two key tiles, ONE commit (it frees the stage and hands the
+            // slot to the epilogue) -- a commit costs the issuing thread hundreds
+            // of cycles (tools/mma_issue_bench.cu), a commit per tile capped the loop
             for (int u = 0; 2 * u < nt; ++u) {
                 const int a = u % kAcc;
                 if (u >= kAcc) tc::mbar_wait_susp(&acce[a], ((u / kAcc) - 1) & 1);
+                tc::mbar_wait_susp(&full[a], (u / kAcc) & 1);
+                tc::fence_after_sync();
                 for (int i = 0; i < 2 && 2 * u + i < nt; ++i) {
-                    const int t = 2 * u + i, s = t % kStages;
-                    tc::mbar_wait_susp(&full[s], (t / kStages) & 1);
-                    tc::fence_after_sync();
 #pragma unroll
                     for (int ks = 0; ks < KD / 16; ++ks) {
                         // K-major, no swizzle: 8-row x 16-byte core matrices; the
                         // two K-adjacent ones are the two 8-column planes
-                        // (LBO = plane stride), 8-row groups 128 B apart (SBO)
-                        const uint64_t ad =
-                            tc::desc_kmajor_nosw(ring_s + s * Lay::kTile + ks * 2 * (kMT * 16), kMT * 16, 128);
+                        // (LBO = the stage's plane stride), 8-row groups 128 B apart (SBO)
+                        const uint64_t ad = tc::desc_kmajor_nosw(
+                            ring_s + a * Lay::kStage + i * (kMT * 16) + ks * 2 * (2 * kMT * 16), 2 * kMT * 16, 128);
                         const uint64_t bd = tc::desc_kmajor_nosw(q_s + ks * 2 * (kNQ * 16), kNQ * 16, 128);
                         tc::mma_bf16(tmem + (2 * a + i) * kNQ, ad, bd, idesc, ks > 0);
                     }
-                    tc::commit(&empty[s]);
                 }
                 tc::commit(&accf[a]);
             }
@@ -329,146 +477,14 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int band = q0 / 8 + warp;  // this warp's band (global index within the pair)
     const int nbands = (L + 7) / 8;
     const bool live = band < nbands;
-    int T = 0;
-    uint32_t n_gt = 0, n_eq = 0;
-    if (live) {
-        // keep-th largest value: cumulative counts from the top bin (v = M)
-        const uint32_t hp = hist_s + static_cast<uint32_t>((warp >> 1) * Lay::kBins * 4);
-        const int sh = (warp & 1) * 16;
-        const int nbins = 2 * M + 1;
-        uint32_t carry = 0;
-        for (int h0 = 0; h0 < nbins; h0 += 256) {
-            const uint4 x = lds128(hp + (h0 + 8 * lane) * 4), y = lds128(hp + (h0 + 8 * lane + 4) * 4);
-            const uint32_t mine = ((x.x + x.y + x.z + x.w + y.x + y.y + y.z + y.w) >> sh) & 0xFFFFu;
-            uint32_t incl = mine;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += u;
-            }
-            const unsigned hit = __ballot_sync(0xffffffffu, carry + incl >= static_cast<uint32_t>(keep));
-            if (hit) {
-                const int f = __ffs(hit) - 1;
-                uint32_t run = carry + __shfl_sync(0xffffffffu, incl - mine, f);
-                const int hb = h0 + 8 * f;
-                int tt = 0;
-                uint32_t gt = 0, eq = 0;
-                if (lane == 0) {
-                    for (int i = 0; i < 8; ++i) {
-                        const uint32_t c = (lds_u16(hp + (hb + i) * 4 + (sh >> 3))) & 0xFFFFu;
-                        if (run + c >= static_cast<uint32_t>(keep)) {
-                            tt = M - (hb + i);
-                            gt = run;
-                            eq = c;
-                            break;
-                        }
-                        run += c;
-                    }
-                }
-                T = __shfl_sync(0xffffffffu, tt, 0);
-                n_gt = __shfl_sync(0xffffffffu, gt, 0);
-                n_eq = __shfl_sync(0xffffffffu, eq, 0);
-                break;
-            }
-            carry += __shfl_sync(0xffffffffu, incl, 31);
-        }
-    }
+    const BandCut cut = live ? band_cut(hist_s + static_cast<uint32_t>((warp >> 1) * Lay::kBins * 4), (warp & 1) * 16,
+                                            M, keep, lane)
+                             : BandCut{};
     named_sync_epi();  // histograms consumed: the staging lists reuse them
-
     uint32_t* obuf = reinterpret_cast<uint32_t*>(histp) + warp * kList;
-    const uint32_t obuf_s = hist_s + static_cast<uint32_t>(warp * kList * 4);
-    if (live) {
-        const uint32_t prow_s = pooled_s + static_cast<uint32_t>(warp) * row_bytes;
-        const uint32_t codeT = 0x4000u + static_cast<uint32_t>(T);
-        const uint32_t rem = static_cast<uint32_t>(keep) - n_gt;  // ties admitted, lowest keys first
-        const uint32_t n_ge = n_gt + n_eq;
-        uint32_t* o = out ? out + (pair * nbands + band) * static_cast<int64_t>(keep) : nullptr;
-        const int nseg = Lp / kMT;
-        const unsigned lt = lanemask_lt();
-        if (n_ge <= static_cast<uint32_t>(kList)) {
-            // (a) every key with v >= T, ascending, into the staging list
-            const uint32_t T2 = codeT | (codeT << 16);
-            uint32_t base = 0;
-            for (int s0 = 0; s0 < nseg; s0 += 32) {
-                const int seg = s0 + lane;
-                uint32_t w[4] = {0u, 0u, 0u, 0u};
-                if (seg < nseg) {
-                    const uint32_t sb = prow_s + static_cast<uint32_t>(seg) * 256;
-#pragma unroll
-                    for (int c = 0; c < 16; ++c) {
-                        const uint4 x = lds128(sb + static_cast<uint32_t>((c ^ (seg & 7)) << 4));
-                        uint32_t tb = hge2(x.x, T2) & 0x00020001u;
-                        tb |= hge2(x.y, T2) & 0x00080004u;
-                        tb |= hge2(x.z, T2) & 0x00200010u;
-                        tb |= hge2(x.w, T2) & 0x00800040u;
-                        w[c >> 2] |= ((tb | (tb >> 16)) & 0xFFu) << ((c & 3) * 8);
-                    }
-                }
-                const uint32_t n = __popc(w[0]) + __popc(w[1]) + __popc(w[2]) + __popc(w[3]);
-                uint32_t incl = n;
-#pragma unroll
-                for (int q = 1; q < 32; q <<= 1) {
-                    const uint32_t u = __shfl_up_sync(0xffffffffu, incl, q);
-                    if (lane >= q) incl += u;
-                }
-                uint32_t pos = base + incl - n;
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    uint32_t x = w[j];
-                    while (x) {
-                        const int bit = __ffs(x) - 1;
-                        x &= x - 1;
-                        obuf[pos++] = static_cast<uint32_t>(seg * kMT + j * 32 + bit);
-                    }
-                }
-                base += __shfl_sync(0xffffffffu, incl, 31);
-            }
-            __syncwarp();
-            if (n_ge == static_cast<uint32_t>(keep)) {
-                if (o)
-                    for (int i = lane; i < keep; i += 32) o[i] = obuf[i];
-            } else {
-                // (b) drop the ties beyond `rem` (compacted in place)
-                uint32_t eq_seen = 0, outp = 0;
-                for (uint32_t i0 = 0; i0 < n_ge; i0 += 32) {
-                    const uint32_t i = i0 + lane;
-                    const bool valid = i < n_ge;
-                    const uint32_t col = valid ? obuf[i] : 0u;
-                    const bool eq = valid && lds_u16(prow_s + code_off(static_cast<int>(col))) == codeT;
-                    const unsigned be = __ballot_sync(0xffffffffu, eq);
-                    const bool kp = valid && (!eq || eq_seen + __popc(be & lt) < rem);
-                    const unsigned bk = __ballot_sync(0xffffffffu, kp);
-                    __syncwarp();  // every lane read its entry before any write below
-                    if (kp) {
-                        obuf[outp + __popc(bk & lt)] = col;
-                        if (o) o[outp + __popc(bk & lt)] = col;
-                    }
-                    outp += __popc(bk);
-                    eq_seen += __popc(be);
-                }
-            }
-        } else {
-            // rare (a flood of ties at T): one ascending pass, two ballots per
-            // 32 keys -- v > T, or v == T among the first `rem` ties
-            const uint32_t trash = static_cast<uint32_t>(kList - 32 + lane);
-            uint32_t taken = 0, eq_seen = 0;
-            for (int j0 = 0; j0 < Lp; j0 += 32) {
-                const int j = j0 + lane;
-                const uint32_t c = lds_u16(prow_s + code_off(j));
-                const bool gt = c > codeT && c != 0u, eq = c == codeT;
-                const unsigned be = __ballot_sync(0xffffffffu, eq);
-                const bool take = gt || (eq && eq_seen + __popc(be & lt) < rem);
-                const unsigned bt = __ballot_sync(0xffffffffu, take);
-                const uint32_t slot = take ? taken + __popc(bt & lt) : trash;
-                obuf[slot] = static_cast<uint32_t>(j);
-                if (take && o) o[slot] = static_cast<uint32_t>(j);
-                taken += __popc(bt);
-                eq_seen += __popc(be);
-            }
-        }
-        __syncwarp();
-    }
-    (void)obuf_s;
+    if (live)
+        band_emit(cut, pooled_s + static_cast<uint32_t>(warp) * row_bytes, obuf,
+                  out ? out + (pair * nbands + band) * static_cast<int64_t>(keep) : nullptr, keep, Lp, lane);
     if constexpr (FUSED) {
         named_sync_epi();  // ring + pooled codes free: per-warp attention buffers
         using BS = bc::BandSmemV2<64>;

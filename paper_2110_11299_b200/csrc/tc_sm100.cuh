@@ -47,6 +47,7 @@ __device__ __forceinline__ void mbar_wait_susp(uint64_t* bar, uint32_t parity) {
 }
 // Same wait with a nanosleep backoff between probes, for warps whose wait is
 // long (keeps spinning warps from stealing issue slots from working warps).
+template <int NS = 128>
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
     const uint32_t a = smem_addr(bar);
     uint32_t ok = 0;
@@ -59,7 +60,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
             : "r"(a), "r"(parity)
             : "memory");
         if (ok) break;
-        __nanosleep(128);
+        __nanosleep(NS);
     }
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {

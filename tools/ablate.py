@@ -9,8 +9,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_2110_11299_b200 import build as b  # noqa: E402
 
 for spec in sys.argv[1:]:
-    # "<bits>" or "<bits>s<stages>"
-    bits, _, stages = spec.partition("s")
+    bits = spec
     out = b.ROOT / "ablate" / spec
     out.mkdir(parents=True, exist_ok=True)
     objs = []
@@ -19,7 +18,7 @@ for spec in sys.argv[1:]:
         o = b.OBJ / (s.stem + ".o")
         if s.name == "select_colvec.cu":
             o = out / "select_colvec.o"
-            subprocess.run([b.NVCC, *b.ARCH, *b.COMMON, f"-DDSA_ABLATE={bits}", *([f"-DDSA_ABL_STAGES={stages}"] if stages else []), "-c", str(s), "-o", str(o)],
+            subprocess.run([b.NVCC, *b.ARCH, *b.COMMON, f"-DDSA_ABLATE={bits}", "-c", str(s), "-o", str(o)],
                            check=True, capture_output=True)
         objs.append(str(o))
     subprocess.run([b.NVCC, *b.ARCH, "-shared", "-o", str(out / "libdsa_b200.so"), *objs, "-lcudart", "-lpthread"],
