@@ -131,148 +131,159 @@ __device__ __forceinline__ uint32_t code_off(int j) {
 
 // The keep-th largest pooled value T of one band and the counts above / at
 // it, from the band's histogram (bins v = M .. -M at word offsets 0 ..;
-// 16-bit half `sh` of each u32 word): cumulative counts from the top bin,
-// 256 bins per warp step.  One warp.
+// 16-bit half `sh` of each u32 word; W * 32 words).  One warp, two scans:
+// lane l sums its W consecutive bins (a band's counts fit 16 bits, so the
+// other band's half never carries into this one), a warp prefix sum finds
+// the lane whose range holds the keep-th value, then that range's bins are
+// spread over the warp (W / 32 rounded up per lane) and scanned again.
 struct BandCut {
     int T = 0;
     uint32_t n_gt = 0, n_eq = 0;
 };
-__device__ __forceinline__ BandCut band_cut(uint32_t hp, int sh, int M, int keep, int lane) {
-    BandCut r;
-    const int nbins = 2 * M + 1;
-    uint32_t carry = 0;
-    for (int h0 = 0; h0 < nbins; h0 += 256) {
-        const uint4 x = lds128(hp + (h0 + 8 * lane) * 4), y = lds128(hp + (h0 + 8 * lane + 4) * 4);
-        const uint32_t mine = ((x.x + x.y + x.z + x.w + y.x + y.y + y.z + y.w) >> sh) & 0xFFFFu;
-        uint32_t incl = mine;
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += u;
-        }
-        const unsigned hit = __ballot_sync(0xffffffffu, carry + incl >= static_cast<uint32_t>(keep));
-        if (hit) {
-            const int f = __ffs(hit) - 1;
-            uint32_t run = carry + __shfl_sync(0xffffffffu, incl - mine, f);
-            const int hb = h0 + 8 * f;
-            int tt = 0;
-            uint32_t gt = 0, eq = 0;
-            if (lane == 0) {
-                for (int i = 0; i < 8; ++i) {
-                    const uint32_t c = (lds_u16(hp + (hb + i) * 4 + (sh >> 3))) & 0xFFFFu;
-                    if (run + c >= static_cast<uint32_t>(keep)) {
-                        tt = M - (hb + i);
-                        gt = run;
-                        eq = c;
-                        break;
-                    }
-                    run += c;
-                }
-            }
-            r.T = __shfl_sync(0xffffffffu, tt, 0);
-            r.n_gt = __shfl_sync(0xffffffffu, gt, 0);
-            r.n_eq = __shfl_sync(0xffffffffu, eq, 0);
-            break;
-        }
-        carry += __shfl_sync(0xffffffffu, incl, 31);
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += u;
     }
+    return v;
+}
+template <int W>
+__device__ __forceinline__ BandCut band_cut(uint32_t hp, int sh, int M, int keep, int lane) {
+    static_assert(W % 4 == 0, "16-byte histogram reads");
+    constexpr int kPer = W <= 64 ? 2 : 4;  // bins per lane in the second scan
+    static_assert(W <= 32 * kPer, "second scan covers the range");
+    uint32_t acc = 0;
+    const uint32_t base = hp + static_cast<uint32_t>(lane * W * 4);
+#pragma unroll
+    for (int i = 0; i < W; i += 4) {
+        const uint4 x = lds128(base + i * 4);
+        acc += x.x + x.y + x.z + x.w;
+    }
+    const uint32_t mine = (acc >> sh) & 0xFFFFu;
+    const uint32_t incl = warp_incl_scan(mine, lane);
+    const unsigned hit = __ballot_sync(0xffffffffu, incl >= static_cast<uint32_t>(keep));
+    const int f = hit ? __ffs(hit) - 1 : 31;
+    const uint32_t carry = __shfl_sync(0xffffffffu, incl - mine, f);
+    // the W bins of lane f, kPer per lane
+    const int b0 = f * W + kPer * lane;
+    uint32_t c[kPer];
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) c[i] = 0;
+    if (kPer * lane < W) {
+        if constexpr (kPer == 2) {
+            uint32_t x, y;
+            asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];\n" : "=r"(x), "=r"(y) : "r"(hp + b0 * 4));
+            c[0] = (x >> sh) & 0xFFFFu;
+            c[1] = (y >> sh) & 0xFFFFu;
+        } else {
+            const uint4 x = lds128(hp + b0 * 4);
+            c[0] = (x.x >> sh) & 0xFFFFu;
+            c[1] = (x.y >> sh) & 0xFFFFu;
+            c[2] = (x.z >> sh) & 0xFFFFu;
+            c[3] = (x.w >> sh) & 0xFFFFu;
+        }
+    }
+    uint32_t m2 = 0;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) m2 += c[i];
+    const uint32_t incl2 = warp_incl_scan(m2, lane);
+    const unsigned hit2 = __ballot_sync(0xffffffffu, carry + incl2 >= static_cast<uint32_t>(keep));
+    const int f2 = hit2 ? __ffs(hit2) - 1 : 31;
+    int tt = 0;
+    uint32_t gt = 0, eq = 0;
+    if (lane == f2) {
+        uint32_t run = carry + incl2 - m2;
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
+            if (run + c[i] >= static_cast<uint32_t>(keep)) {
+                tt = M - (b0 + i);
+                gt = run;
+                eq = c[i];
+                break;
+            }
+            run += c[i];
+        }
+    }
+    BandCut r;
+    r.T = __shfl_sync(0xffffffffu, tt, f2);
+    r.n_gt = __shfl_sync(0xffffffffu, gt, f2);
+    r.n_eq = __shfl_sync(0xffffffffu, eq, f2);
     return r;
 }
 
 // The band's ascending list of kept keys (value desc, lowest key first among
-// equals at T) from its pooled codes `prow_s`: one pass with packed f16
-// compares building a key bitmap of v >= T, a warp prefix sum placing those
-// keys in order in the staging list `obuf` (kList entries), then the ties
-// beyond `rem` dropped; written to `o` when given (obuf holds the list on
-// return).  One warp.
+// equals at T) from its pooled codes `prow_s`, in ONE pass: per 128-key
+// segment (one per lane) packed f16 compares build bitmaps of v > T and
+// v >= T, a warp prefix sum over the tie counts admits the first `rem` ties
+// (lowest keys first), a second prefix sum over the kept counts places each
+// lane's keys in the staging list `obuf` (keep entries, ascending); then the
+// list is copied to `o` when given.  One warp.
 __device__ __forceinline__ void band_emit(const BandCut& cut, uint32_t prow_s, uint32_t* obuf, uint32_t* o, int keep,
                                           int Lp, int lane) {
     const uint32_t codeT = 0x4000u + static_cast<uint32_t>(cut.T);
     const uint32_t rem = static_cast<uint32_t>(keep) - cut.n_gt;  // ties admitted, lowest keys first
-    const uint32_t n_ge = cut.n_gt + cut.n_eq;
     const int nseg = Lp / kMT;
-    const unsigned lt = lanemask_lt();
-    if (n_ge <= static_cast<uint32_t>(kList)) {
-        // (a) every key with v >= T, ascending, into the staging list
-        const uint32_t T2 = codeT | (codeT << 16);
-        uint32_t base = 0;
-        for (int s0 = 0; s0 < nseg; s0 += 32) {
-            const int seg = s0 + lane;
-            uint32_t w[4] = {0u, 0u, 0u, 0u};
-            if (seg < nseg) {
-                const uint32_t sb = prow_s + static_cast<uint32_t>(seg) * 256;
+    const uint32_t T2 = codeT | (codeT << 16), U2 = (codeT + 1u) | ((codeT + 1u) << 16);
+    uint32_t eq_base = 0, k_base = 0;
+    for (int s0 = 0; s0 < nseg; s0 += 32) {
+        const int seg = s0 + lane;
+        uint32_t wg[4] = {0u, 0u, 0u, 0u}, we[4] = {0u, 0u, 0u, 0u};  // v > T, v >= T
+        if (seg < nseg) {
+            const uint32_t sb = prow_s + static_cast<uint32_t>(seg) * 256;
 #pragma unroll
-                for (int c = 0; c < 16; ++c) {
-                    const uint4 x = lds128(sb + static_cast<uint32_t>((c ^ (seg & 7)) << 4));
-                    uint32_t tb = hge2(x.x, T2) & 0x00020001u;
-                    tb |= hge2(x.y, T2) & 0x00080004u;
-                    tb |= hge2(x.z, T2) & 0x00200010u;
-                    tb |= hge2(x.w, T2) & 0x00800040u;
-                    w[c >> 2] |= ((tb | (tb >> 16)) & 0xFFu) << ((c & 3) * 8);
-                }
-            }
-            const uint32_t n = __popc(w[0]) + __popc(w[1]) + __popc(w[2]) + __popc(w[3]);
-            uint32_t incl = n;
-#pragma unroll
-            for (int q = 1; q < 32; q <<= 1) {
-                const uint32_t u = __shfl_up_sync(0xffffffffu, incl, q);
-                if (lane >= q) incl += u;
-            }
-            uint32_t pos = base + incl - n;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                uint32_t x = w[j];
-                while (x) {
-                    const int bit = __ffs(x) - 1;
-                    x &= x - 1;
-                    obuf[pos++] = static_cast<uint32_t>(seg * kMT + j * 32 + bit);
-                }
-            }
-            base += __shfl_sync(0xffffffffu, incl, 31);
-        }
-        __syncwarp();
-        if (n_ge == static_cast<uint32_t>(keep)) {
-            if (o)
-                for (int i = lane; i < keep; i += 32) o[i] = obuf[i];
-        } else {
-            // (b) drop the ties beyond `rem` (compacted in place)
-            uint32_t eq_seen = 0, outp = 0;
-            for (uint32_t i0 = 0; i0 < n_ge; i0 += 32) {
-                const uint32_t i = i0 + lane;
-                const bool valid = i < n_ge;
-                const uint32_t col = valid ? obuf[i] : 0u;
-                const bool eq = valid && lds_u16(prow_s + code_off(static_cast<int>(col))) == codeT;
-                const unsigned be = __ballot_sync(0xffffffffu, eq);
-                const bool kp = valid && (!eq || eq_seen + __popc(be & lt) < rem);
-                const unsigned bk = __ballot_sync(0xffffffffu, kp);
-                __syncwarp();  // every lane read its entry before any write below
-                if (kp) {
-                    obuf[outp + __popc(bk & lt)] = col;
-                    if (o) o[outp + __popc(bk & lt)] = col;
-                }
-                outp += __popc(bk);
-                eq_seen += __popc(be);
+            for (int c = 0; c < 16; ++c) {
+                const uint4 x = lds128(sb + static_cast<uint32_t>((c ^ (seg & 7)) << 4));
+                uint32_t te = hge2(x.x, T2) & 0x00020001u, tg = hge2(x.x, U2) & 0x00020001u;
+                te |= hge2(x.y, T2) & 0x00080004u;
+                tg |= hge2(x.y, U2) & 0x00080004u;
+                te |= hge2(x.z, T2) & 0x00200010u;
+                tg |= hge2(x.z, U2) & 0x00200010u;
+                te |= hge2(x.w, T2) & 0x00800040u;
+                tg |= hge2(x.w, U2) & 0x00800040u;
+                we[c >> 2] |= ((te | (te >> 16)) & 0xFFu) << ((c & 3) * 8);
+                wg[c >> 2] |= ((tg | (tg >> 16)) & 0xFFu) << ((c & 3) * 8);
             }
         }
-    } else {
-        // rare (a flood of ties at T): one ascending pass, two ballots per
-        // 32 keys -- v > T, or v == T among the first `rem` ties
-        const uint32_t trash = static_cast<uint32_t>(kList - 32 + lane);
-        uint32_t taken = 0, eq_seen = 0;
-        for (int j0 = 0; j0 < Lp; j0 += 32) {
-            const int j = j0 + lane;
-            const uint32_t c = lds_u16(prow_s + code_off(j));
-            const bool gt = c > codeT && c != 0u, eq = c == codeT;
-            const unsigned be = __ballot_sync(0xffffffffu, eq);
-            const bool take = gt || (eq && eq_seen + __popc(be & lt) < rem);
-            const unsigned bt = __ballot_sync(0xffffffffu, take);
-            const uint32_t slot = take ? taken + __popc(bt & lt) : trash;
-            obuf[slot] = static_cast<uint32_t>(j);
-            if (take && o) o[slot] = static_cast<uint32_t>(j);
-            taken += __popc(bt);
-            eq_seen += __popc(be);
+        // ties: admit this lane's first (rem - ties before it) tie keys
+        uint32_t ne = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) ne += __popc(we[j] & ~wg[j]);
+        const uint32_t eincl = warp_incl_scan(ne, lane);
+        const uint32_t ebefore = eq_base + eincl - ne;
+        uint32_t allow = rem > ebefore ? rem - ebefore : 0u;
+        uint32_t nk = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            uint32_t eqj = we[j] & ~wg[j];
+            const uint32_t cj = __popc(eqj);
+            if (allow < cj) {
+                // keep the first `allow` ties of this word: bits below the (allow+1)-th set bit
+                eqj = allow == 0 ? 0u : eqj & ((1u << __fns(eqj, 0, allow + 1)) - 1u);
+                allow = 0;
+            } else {
+                allow -= cj;
+            }
+            we[j] = wg[j] | eqj;
+            nk += __popc(we[j]);
         }
+        const uint32_t kincl = warp_incl_scan(nk, lane);
+        uint32_t pos = k_base + kincl - nk;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            uint32_t x = we[j];
+            while (x) {
+                const int bit = __ffs(x) - 1;
+                x &= x - 1;
+                obuf[pos++] = static_cast<uint32_t>(seg * kMT + j * 32 + bit);
+            }
+        }
+        eq_base += __shfl_sync(0xffffffffu, eincl, 31);
+        k_base += __shfl_sync(0xffffffffu, kincl, 31);
     }
+    __syncwarp();
+    if (o)
+        for (int i = lane; i < keep; i += 32) o[i] = obuf[i];
     __syncwarp();
 }
 
@@ -477,14 +488,27 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int band = q0 / 8 + warp;  // this warp's band (global index within the pair)
     const int nbands = (L + 7) / 8;
     const bool live = band < nbands;
-    const BandCut cut = live ? band_cut(hist_s + static_cast<uint32_t>((warp >> 1) * Lay::kBins * 4), (warp & 1) * 16,
-                                            M, keep, lane)
+#if DSA_ABLATE & 128  // profiling build only: selection phase cycles (CTA 0, warp 0)
+    const long long c0 = clock64();
+#endif
+    const BandCut cut = live ? band_cut<Lay::kBins / 32>(hist_s + static_cast<uint32_t>((warp >> 1) * Lay::kBins * 4),
+                                                         (warp & 1) * 16, M, keep, lane)
                              : BandCut{};
+#if DSA_ABLATE & 128
+    const long long c1 = clock64();
+#endif
     named_sync_epi();  // histograms consumed: the staging lists reuse them
+#if DSA_ABLATE & 128
+    const long long c2 = clock64();
+#endif
     uint32_t* obuf = reinterpret_cast<uint32_t*>(histp) + warp * kList;
     if (live)
         band_emit(cut, pooled_s + static_cast<uint32_t>(warp) * row_bytes, obuf,
                   out ? out + (pair * nbands + band) * static_cast<int64_t>(keep) : nullptr, keep, Lp, lane);
+#if DSA_ABLATE & 128
+    if ((blockIdx.x == 5 && blockIdx.y == 3) && lane == 0)
+        printf("warp %d cut %lld sync %lld emit %lld T %d ngt %u neq %u\n", warp, c1 - c0, c2 - c1, clock64() - c2, cut.T, cut.n_gt, cut.n_eq);
+#endif
     if constexpr (FUSED) {
         named_sync_epi();  // ring + pooled codes free: per-warp attention buffers
         using BS = bc::BandSmemV2<64>;
