@@ -42,6 +42,10 @@
 #include "kernels.h"
 #include "tc_sm100.cuh"
 
+#ifndef DSA_ABLATE  // profiling builds only (tools/ablate.py); 0 in the library
+#define DSA_ABLATE 0
+#endif
+
 namespace dsa {
 namespace {
 
@@ -75,6 +79,52 @@ __device__ __forceinline__ double ref_chain_s(const unsigned char* xa, int r, co
 }
 
 constexpr int kMaxList = 1024;  // uncertified (row, column) entries recomputed cooperatively
+
+// Level of element (row r, column j) of the staged tile, bit-identical to
+// the reference's clamp(round_half_away(chain / s)) (chain = the sequential
+// fp64 fma chain of ref_chain_s) without walking that d-long dependent
+// chain: the d products x_t p_tj are exact in fp64 (bf16 x f32: <= 32
+// significant bits) and are summed into 8 independent partial sums, then
+// combined pairwise.  That sum and the chain are both within (steps)
+// 2^-53 sum|x_t p_tj| of the exact dot product, so |chain - sum| <=
+// (d + d/8 + 3) 2^-53 sum|.| (widened by 1 %); when both ends of that
+// interval, scaled by 1/s (plus 2^-50 relative for the reciprocal's and the
+// reference division's rounding), round to the same level, it is the
+// reference's.  Otherwise (a quotient within ~1e-14 relative of a .5
+// boundary) the sequential chain itself.
+template <int D, int KD>
+__device__ __forceinline__ float level_split(const unsigned char* xa, int r, const float* __restrict__ p, int j,
+                                             double s, double inv_s, double qmax) {
+    double ps[8], pa[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) ps[u] = pa[u] = 0.0;
+#pragma unroll
+    for (int t0 = 0; t0 < D; t0 += 8) {
+        const uint4 xv = *reinterpret_cast<const uint4*>(xa + opnd_off<D>(r, t0));  // 8 consecutive t
+        const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(&xv);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const double pr = to_double(xb[u]) * static_cast<double>(__ldg(p + (t0 + u) * KD + j));
+            ps[u] += pr;
+            pa[u] += fabs(pr);
+        }
+    }
+#pragma unroll
+    for (int w = 4; w >= 1; w >>= 1)
+#pragma unroll
+        for (int u = 0; u < w; ++u) {
+            ps[u] += ps[u + w];
+            pa[u] += pa[u + w];
+        }
+    const double sum = ps[0];
+    const double e = pa[0] * (static_cast<double>(D + D / 8 + 3) * 1.1102230246251565e-16 * 1.01) + 1e-300;
+    const double dq = fabs(sum * inv_s) * 8.881784197001252e-16;  // 2^-50 |q|
+    const double lo = fmin(fmax(round_half_away((sum - e) * inv_s - dq), -qmax), qmax);
+    const double hi = fmin(fmax(round_half_away((sum + e) * inv_s + dq), -qmax), qmax);
+    if (lo == hi) return static_cast<float>(lo);
+    // within the bound of a .5 boundary: the reference's own chain
+    return static_cast<float>(fmin(fmax(round_half_away(ref_chain_s<D, KD>(xa, r, p, j, 0) / s), -qmax), qmax));
+}
 
 __device__ __forceinline__ float xbound(float x, float qp, int round_f32, float dscale) {
     return fmaf(qp, dscale, fabsf(x) * (round_f32 ? 2.4e-7f : 1.2e-7f)) + 1e-30f;
@@ -372,7 +422,10 @@ __global__ void __launch_bounds__(R)
                                           fabs(ref_chain_s<D, KD>(xa, tid, p, j, round_f32)))));
             }
         __syncthreads();
-        const unsigned n = min(*lcount, static_cast<unsigned>(kMaxList));
+        const unsigned n = (DSA_ABLATE & 2048) ? 0u : min(*lcount, static_cast<unsigned>(kMaxList));  // profiling: no chains
+#if DSA_ABLATE & 128
+        if (tid == 0 && blockIdx.x % 8 == 3 && blockIdx.z == 5) printf("amax pass: tile %d tensor %d candidates %u\n", blockIdx.x, which, *lcount);
+#endif
         double am = 0.0;
         for (unsigned e = tid; e < n; e += R)
             am = fmax(am, fabs(ref_chain_s<D, KD>(xa, static_cast<int>(list[e] >> 6), p, list[e] & 63, round_f32)));
@@ -409,12 +462,25 @@ __global__ void __launch_bounds__(R)
             lvl_s[tid * KD + j] = static_cast<uint16_t>(__float_as_uint(lv) >> 16);
         }
         __syncthreads();
-        const unsigned n = min(*lcount, static_cast<unsigned>(kMaxList));
-        for (unsigned e = tid; e < n; e += R) {
-            const int rr = static_cast<int>(list[e] >> 6), j = static_cast<int>(list[e] & 63);
-            const double xe = ref_chain_s<D, KD>(xa, rr, p, j, round_f32);
-            const float lv = static_cast<float>(fmin(fmax(round_half_away(xe / s), -qmax), qmax));
-            lvl_s[rr * KD + j] = static_cast<uint16_t>(__float_as_uint(lv) >> 16);
+        const unsigned n = (DSA_ABLATE & 2048) ? 0u : min(*lcount, static_cast<unsigned>(kMaxList));  // profiling: no chains
+#if DSA_ABLATE & 128
+        if (tid == 0 && blockIdx.x % 8 == 3 && blockIdx.z == 5) printf("quant pass: tile %d tensor %d uncertified %u\n", blockIdx.x, which, *lcount);
+#endif
+        if (!round_f32) {
+            // one thread per entry: split sum + certification, rarely the chain
+            const double inv_s = qmax / am;
+            for (unsigned e = tid; e < n; e += R) {
+                const int rr = static_cast<int>(list[e] >> 6), j = static_cast<int>(list[e] & 63);
+                const float lv = level_split<D, KD>(xa, rr, p, j, s, inv_s, qmax);
+                lvl_s[rr * KD + j] = static_cast<uint16_t>(__float_as_uint(lv) >> 16);
+            }
+        } else {
+            for (unsigned e = tid; e < n; e += R) {
+                const int rr = static_cast<int>(list[e] >> 6), j = static_cast<int>(list[e] & 63);
+                const double xe = ref_chain_s<D, KD>(xa, rr, p, j, round_f32);
+                const float lv = static_cast<float>(fmin(fmax(round_half_away(xe / s), -qmax), qmax));
+                lvl_s[rr * KD + j] = static_cast<uint16_t>(__float_as_uint(lv) >> 16);
+            }
         }
         __syncthreads();
         if (valid) {
@@ -628,7 +694,7 @@ void launch_tc(const PredictArgs& a, cudaStream_t st) {
 template <int D, int KD>
 void launch_tc(const PredictArgs& a, cudaStream_t st) {
     // d = 128: 256 rows per CTA (two M = 128 MMAs share the P image and prologue)
-    if (D == 128) launch_tc<D, KD, 256>(a, st);
+    if (D == 128 && !(DSA_ABLATE & 1024)) launch_tc<D, KD, 256>(a, st);
     else launch_tc<D, KD, 128>(a, st);
 }
 
