@@ -67,6 +67,8 @@ size_t predict_tc_image_bytes(int64_t D, int64_t KD);
 void run_predict_tc(const PredictArgs& a, cudaStream_t st);
 bool predict_tensor_supported(const PredictArgs& a);
 void run_predict_tensor(const PredictArgs& a, cudaStream_t st);
+bool predict_tensor2_supported(const PredictArgs& a);
+void run_predict_tensor2(const PredictArgs& a, cudaStream_t st);
 
 // approx_scores_from_r with the per-head k x k W~ (P/src/predictor.cpp:67-80)
 struct WtildeArgs {

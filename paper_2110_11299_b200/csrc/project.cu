@@ -201,6 +201,10 @@ void run_predict(const PredictArgs& a, cudaStream_t st) {
         run_predict_tensor(a, st);
         return;
     }
+    if (!force_dfma && predict_tensor2_supported(a)) {
+        run_predict_tensor2(a, st);
+        return;
+    }
     if (!force_dfma && predict_tc_supported(a)) {
         run_predict_tc(a, st);
         return;

@@ -42,6 +42,9 @@ CASES = [
     ("DSA_PREDICT_TILES", "1", {"preset": "c2_vector", "pairs": 3, "over": {"L": 1000, "keep": 50}}, True),
     ("DSA_PREDICT_TILES", "1", {"preset": "c2_vector", "pairs": 2, "over": {"L": 4096, "keep": 205}}, True),
     ("DSA_PREDICT_TILES", "1", {"preset": "c2_vector", "pairs": 2, "over": {"L": 3000, "keep": 150, "bits": 8}}, True),
+    ("DSA_PREDICT_TILES", "1", {"preset": "c3_block", "pairs": 3, "over": {"L": 1500, "keep": 8}}, True),
+    ("DSA_PREDICT_TILES", "1", {"preset": "c4_threshold", "pairs": 2, "over": {"L": 5000, "cap": 300}}, True),
+    ("DSA_PREDICT_TILES", "1", {"preset": "c2_vector", "pairs": 2, "over": {"L": 4500, "keep": 200, "bits": 8}}, True),
     ("DSA_FUSE", "1", C2S, False),
     ("DSA_BLOCK_TC", "1", {"preset": "c3_block", "pairs": 2, "over": {"L": 1024, "keep": 5}}, False),
     ("DSA_BLOCK_TC", "1", {"preset": "c3_block", "pairs": 3, "over": {"L": 2048, "keep": 16}}, False),
