@@ -148,7 +148,10 @@ Plan plan(const dsa_config& c, bool pipeline, bool own_mask) {
     // the two-read pass: with x^ they measured slower (C3 0.533 vs 0.471 ms:
     // the amax pass of the d = 128 shape is latency-bound and the x^ writes
     // lengthen it).
-    p.has_xhat = per_tensor && tc_path && c.bits <= 4 && !options().predict_dfma;
+    // (the tile kernels only run for L > 16384 or under DSA_PREDICT_TILES:
+    // the per-tensor CTA kernels of project_tensor.cu take the rest)
+    p.has_xhat = per_tensor && tc_path && c.bits <= 4 && !options().predict_dfma &&
+                 (options().predict_tiles || c.L > 128 * 128);
     p.xhat = take(p.has_xhat ? sizeof(float) * P * xhat_floats_per_pair(c.L, c.k) : 0);
     p.amax = take(per_tensor ? sizeof(unsigned long long) * P * 2 : 0);
     p.pimg = take(tc_path ? align_up(predict_tc_image_bytes(c.d, c.k)) * kMaxChunks : 0);

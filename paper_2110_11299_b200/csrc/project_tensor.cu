@@ -524,9 +524,19 @@ __global__ void __launch_bounds__(kThreads, 1)
 // TMA warp, MMA warp (M = 128, N = 3 k, K = d: 2 x 64-column SWIZZLE_128B
 // boxes per tile for d = 128), 4 norm warps (the row's |q|), two groups of
 // 4 drain warps (tiles g = group mod 2; TMEM slot g & 1).
+// The accumulation error dominates the certification margin, so the P1
+// part (the leading 8 bits of P, i.e. almost all of x) is accumulated in
+// d / 32 separate 32-row chunks (TMEM columns of their own) and summed in
+// fp32 after the drain: the worst-case bound of a 32-term accumulation
+// replaces that of a d-term one (e = (32 + d/64 + 2) 2^-22 |q| |p_j| +
+// 3 2^-24 |x^| instead of d 2^-22 |q| |p_j| + 2^-23 |x^|: ~3.6x tighter at
+// d = 128, so ~0.5 % of the 8-bit levels stay uncertified instead of ~1.7 %).
+// P2 | P3 (P's bits 9-24, 2^-8 of the magnitude) accumulate over all of d.
 template <int D, int KD>
 struct Tensor2Smem {
     static constexpr int N = 3 * KD;
+    static constexpr int kChunks = D / 32;               // P1 accumulation chunks
+    static constexpr int kCols = 2 * KD + kChunks * KD;  // TMEM columns per tile: P2 | P3 | P1 chunks
     static constexpr int kStages = D == 128 ? 3 : 4;
     static constexpr int kTile = 128 * D * 2;
     static constexpr int kList = 4096;         // u32 entries (pass A: (entry, bound) pairs)
@@ -585,7 +595,7 @@ __device__ __noinline__ float level_split_g(const __nv_bfloat16* __restrict__ ro
     return static_cast<float>(fmin(fmax(round_half_away(chain_g<D, KD>(row, pd, j, 0) / s), -qmax), qmax));
 }
 
-template <int D, int KD>
+template <int D, int KD, bool CH>
 __global__ void __launch_bounds__(kThreads, 1)
     project_tensor2_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
                            const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k,
@@ -594,7 +604,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                            double* __restrict__ sk) {
     using Sm = Tensor2Smem<D, KD>;
     constexpr int N = Sm::N, S = Sm::kStages, kH = D / 64;
-    static_assert(N <= 128, "one 128-column TMEM slot per tile");
+    static_assert(Sm::kCols <= 256, "one 256-column TMEM slot per tile");
     extern __shared__ __align__(1024) unsigned char sm[];
     unsigned char* ring = sm + Sm::oRing;
     unsigned char* img = sm + Sm::oImg;
@@ -665,13 +675,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         cnt[0] = cnt[1] = 0u;
         *am_u = 0ull;
     }
-    if (warp == 9) tc::tmem_alloc<256>(tslot);
+    if (warp == 9) tc::tmem_alloc<512>(tslot);
     tc::fence_proxy_async();  // the P image (generic stores) -> the MMA's async proxy
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
     const uint32_t tmem = *tslot;
-    const float rel = round_f32 ? 2.4e-7f : 1.2e-7f;
+    // CH: three fp32 roundings combine the partial sums (|x^| 3 2^-24), else
+    // two (2^-23); plus the reference's own f32 rounding when it rounds
+    // through float
+    const float rel = CH ? (round_f32 ? 3.0e-7f : 1.8e-7f) : (round_f32 ? 2.4e-7f : 1.2e-7f);
 
     if (warp == 8) {
         if (lane == 0)
@@ -681,7 +694,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
     } else if (warp == 9) {
         if (lane == 0) {
-            constexpr uint32_t idesc = tc::idesc_bf16_f32(128, N);
+            constexpr uint32_t id23 = tc::idesc_bf16_f32(128, 2 * KD), id1 = tc::idesc_bf16_f32(128, KD);
             const uint32_t bs = tc::smem_addr(img);
             for (int g = 0; g < TT; ++g) {
                 const int s = g % S, a = g & 1;
@@ -689,11 +702,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc::mbar_wait_sleep<32>(&acce[a], ((g >> 1) & 1) ^ 1);
                 tc::fence_after_sync();
                 const uint32_t xs = tc::smem_addr(ring + s * Sm::kTile);
+                const uint32_t acc = tmem + a * 256;
 #pragma unroll
                 for (int ks = 0; ks < D / 16; ++ks) {
                     const uint64_t ad = tc::desc_sw128(xs + (ks >> 2) * (128 * 128) + (ks & 3) * 32, 16, 1024);
-                    const uint64_t bd = tc::desc_kmajor_nosw(bs + ks * 256, 128, D * 16);
-                    tc::mma_bf16(tmem + a * 128, ad, bd, idesc, ks > 0);
+                    if constexpr (!CH) {  // P1 | P2 | P3 in one accumulation -> columns [0, 3KD)
+                        tc::mma_bf16(acc, ad, tc::desc_kmajor_nosw(bs + ks * 256, 128, D * 16),
+                                     tc::idesc_bf16_f32(128, 3 * KD), ks > 0);
+                        continue;
+                    }
+                    // P2 | P3 (image rows KD..3KD) over all of d -> columns [0, 2KD)
+                    const uint64_t b23 = tc::desc_kmajor_nosw(bs + (KD / 8) * (D * 16) + ks * 256, 128, D * 16);
+                    tc::mma_bf16(acc, ad, b23, id23, ks > 0);
+                    // P1 (image rows 0..KD) per 32-row chunk of d -> columns 2KD + chunk KD
+                    const uint64_t b1 = tc::desc_kmajor_nosw(bs + ks * 256, 128, D * 16);
+                    tc::mma_bf16(acc + 2 * KD + (ks >> 1) * KD, ad, b1, id1, ks & 1);
                 }
                 tc::commit(&accf[a]);
                 tc::commit(&empty[s]);
@@ -719,8 +742,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                         a2 = __ffma2_rn(f, f, a2);
                     }
                 }
-            dq_st[s * 128 + rr] =
-                (sqrtf(a2.x + a2.y) * 1.001f + 1e-30f) * (static_cast<float>(D) * 2.384185791015625e-7f);
+            // |q| (32 + d/64 + 2) 2^-22: the chunked accumulation bound (see Tensor2Smem)
+            dq_st[s * 128 + rr] = (sqrtf(a2.x + a2.y) * 1.001f + 1e-30f) *
+                                  (static_cast<float>(CH ? 32 + D / 64 + 2 : D) * 2.384185791015625e-7f);
             __syncwarp();
             if (lane == 0) {
                 tc::mbar_arrive(&empty[s]);
@@ -751,26 +775,73 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int s = g % S, a = g & 1;
             tc::mbar_wait(&accf[a], (g >> 1) & 1);
             tc::fence_after_sync();
-            uint32_t d0[32], d1[32], d2[32];
-            if constexpr (KD == 16) {
-                tc::ld_32x32b_x32(tmem + lanes + a * 128, d0);
-                tc::ld_32x32b_x16(tmem + lanes + a * 128 + 32, *reinterpret_cast<uint32_t(*)[16]>(d1));
+            // x^ = (sum of the P1 chunks, pairwise) + (P2 + P3)
+            const uint32_t base = tmem + lanes + a * 256;
+            float y[KD];
+            if constexpr (!CH) {  // x^ = P1 + (P2 + P3), columns [0, 3KD)
+                uint32_t u0[32], u1[32], u2[32];
+                if constexpr (KD == 16) {
+                    tc::ld_32x32b_x32(base, u0);
+                    tc::ld_32x32b_x16(base + 32, *reinterpret_cast<uint32_t(*)[16]>(u1));
+                } else {
+                    tc::ld_32x32b_x32(base, u0);
+                    tc::ld_32x32b_x32(base + 32, u1);
+                    tc::ld_32x32b_x32(base + 64, u2);
+                }
+                tc::wait_ld();
+#pragma unroll
+                for (int j = 0; j < KD; ++j) {
+                    if constexpr (KD == 16)
+                        y[j] = __uint_as_float(u0[j]) + (__uint_as_float(u0[16 + j]) + __uint_as_float(u1[j]));
+                    else
+                        y[j] = __uint_as_float(u0[j]) + (__uint_as_float(u1[j]) + __uint_as_float(u2[j]));
+                }
+            } else if constexpr (KD == 16) {
+                uint32_t u0[32], u1[32];
+                tc::ld_32x32b_x32(base, u0);       // P2 | P3
+                tc::ld_32x32b_x32(base + 32, u1);  // P1 chunks 0 | 1
+                float c23[16];
+                if constexpr (D == 128) {
+                    uint32_t u2[32];
+                    tc::ld_32x32b_x32(base + 64, u2);  // P1 chunks 2 | 3
+                    tc::wait_ld();
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) c23[j] = __uint_as_float(u2[j]) + __uint_as_float(u2[16 + j]);
+                } else {
+                    tc::wait_ld();
+                }
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    float c = __uint_as_float(u1[j]) + __uint_as_float(u1[16 + j]);
+                    if constexpr (D == 128) c = c + c23[j];
+                    y[j] = c + (__uint_as_float(u0[j]) + __uint_as_float(u0[16 + j]));
+                }
             } else {
-                tc::ld_32x32b_x32(tmem + lanes + a * 128, d0);
-                tc::ld_32x32b_x32(tmem + lanes + a * 128 + 32, d1);
-                tc::ld_32x32b_x32(tmem + lanes + a * 128 + 64, d2);
+                uint32_t u0[32], u1[32];
+                float c[32];
+                tc::ld_32x32b_x32(base + 64, u0);  // P1 chunk 0
+                tc::ld_32x32b_x32(base + 96, u1);  // P1 chunk 1
+                tc::wait_ld();
+#pragma unroll
+                for (int j = 0; j < 32; ++j) c[j] = __uint_as_float(u0[j]) + __uint_as_float(u1[j]);
+                if constexpr (D == 128) {
+                    tc::ld_32x32b_x32(base + 128, u0);  // P1 chunk 2
+                    tc::ld_32x32b_x32(base + 160, u1);  // P1 chunk 3
+                    tc::wait_ld();
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) c[j] = c[j] + (__uint_as_float(u0[j]) + __uint_as_float(u1[j]));
+                }
+                tc::ld_32x32b_x32(base, u0);       // P2
+                tc::ld_32x32b_x32(base + 32, u1);  // P3
+                tc::wait_ld();
+#pragma unroll
+                for (int j = 0; j < 32; ++j) y[j] = c[j] + (__uint_as_float(u0[j]) + __uint_as_float(u1[j]));
             }
-            tc::wait_ld();
             tc::fence_before_sync();
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&acce[a]);
 #pragma unroll
-            for (int j = 0; j < KD; ++j) {
-                if constexpr (KD == 16)
-                    x[j] = __uint_as_float(d0[j]) + (__uint_as_float(d0[16 + j]) + __uint_as_float(d1[j]));
-                else
-                    x[j] = __uint_as_float(d0[j]) + (__uint_as_float(d1[j]) + __uint_as_float(d2[j]));
-            }
+            for (int j = 0; j < KD; ++j) x[j] = y[j];
             while (*reinterpret_cast<volatile unsigned*>(&ready[g]) < 4u) __nanosleep(32);
             __threadfence_block();
             dq = dq_st[s * 128 + rr];
@@ -897,7 +968,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     tc::fence_before_sync();
     __syncthreads();
-    if (warp == 9) tc::tmem_dealloc<256>(tmem);
+    if (warp == 9) tc::tmem_dealloc<512>(tmem);
 }
 
 }  // namespace
@@ -931,10 +1002,12 @@ bool predict_tensor2_supported(const PredictArgs& a) {
     return al(a.q) && al(a.k) && a.lq != nullptr && a.lk != nullptr;
 }
 
+// chunked P1 accumulation (tighter certification) where levels are fine
+// enough for it to matter (> 4 bits); coarse levels take one accumulation
 template <int D, int KD>
 static void launch_tensor2(const PredictArgs& a, cudaStream_t st) {
     using Sm = Tensor2Smem<D, KD>;
-    auto kf = project_tensor2_kernel<D, KD>;
+    auto kf = a.qmax > 7.5 ? project_tensor2_kernel<D, KD, true> : project_tensor2_kernel<D, KD, false>;
     cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, Sm::bytes);
     const CUtensorMap mq = make_map(a.q, a.pairs * a.L, D, 128, 64);
     const CUtensorMap mk = make_map(a.k, a.pairs * a.L, D, 128, 64);
