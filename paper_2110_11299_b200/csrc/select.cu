@@ -411,13 +411,24 @@ __global__ void __launch_bounds__(kNT) block_generic(SelectArgs a, int64_t nb) {
 // "value desc, lowest block first"; `keep` rounds of a warp arg-max (the
 // forced diagonal ranks above everything) and a 32-lane bitonic sort give
 // the ascending block list.  Same ranking as block_generic / the oracle.
+// A CTA (8 warps) takes kBRows consecutive block rows of one pair, the
+// pair's pooled K staged ONCE in shared memory (row jb's 16-byte chunk t4 at
+// position (t4 + jb) mod KD/4, so the 32 lanes' rows spread over the banks).
+constexpr int kBRows = 32;
 template <int KD, int NPL>
 __global__ void __launch_bounds__(256) block_select_warp(SelectArgs a, int64_t nb) {
+    extern __shared__ __align__(16) int4 pk_s[];  // [nb][KD / 4], rotated
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t pair = blockIdx.y;
-    const int32_t* pks = a.pooled + (pair * 2 + 1) * nb * KD;  // pooled K (L1/L2 resident)
-    const int64_t ib = static_cast<int64_t>(blockIdx.x) * 8 + warp;
-    if (ib >= nb) return;
+    {
+        const int4* pks = reinterpret_cast<const int4*>(a.pooled + (pair * 2 + 1) * nb * KD);
+        for (int i = threadIdx.x; i < nb * (KD / 4); i += 256) {
+            const int jb = i / (KD / 4), t4 = i % (KD / 4);
+            pk_s[jb * (KD / 4) + ((t4 + jb) & (KD / 4 - 1))] = __ldg(pks + i);
+        }
+    }
+    __syncthreads();
+    for (int64_t ib = static_cast<int64_t>(blockIdx.x) * kBRows + warp; ib < nb && ib < (blockIdx.x + 1) * static_cast<int64_t>(kBRows); ib += 8) {
     const int32_t* pq = a.pooled + ((pair * 2 + 0) * nb + ib) * KD;
     int32_t qv[KD];
 #pragma unroll
@@ -429,10 +440,10 @@ __global__ void __launch_bounds__(256) block_select_warp(SelectArgs a, int64_t n
         key[u] = 0ull;
         if (jb < nb) {
             int32_t sum = 0;
-            const int4* row = reinterpret_cast<const int4*>(pks + static_cast<int64_t>(jb) * KD);
+            const int4* row = pk_s + jb * (KD / 4);
 #pragma unroll
             for (int t4 = 0; t4 < KD / 4; ++t4) {
-                const int4 w = __ldg(row + t4);
+                const int4 w = row[(t4 + jb) & (KD / 4 - 1)];
                 sum += qv[4 * t4] * w.x + qv[4 * t4 + 1] * w.y + qv[4 * t4 + 2] * w.z + qv[4 * t4 + 3] * w.w;
             }
             const uint32_t hi = (a.force_diag && jb == ib) ? 0xffffffffu : (static_cast<uint32_t>(sum) ^ 0x80000000u);
@@ -466,6 +477,7 @@ __global__ void __launch_bounds__(256) block_select_warp(SelectArgs a, int64_t n
         }
     }
     if (lane < a.keep) a.cols[(pair * nb + ib) * a.keep + lane] = static_cast<uint32_t>(mine);
+    }
 }
 
 // ----------------------------------------------------------- threshold
@@ -607,13 +619,18 @@ void launch_select(const SelectArgs& a, cudaStream_t st) {
             const bool warp_ok = a.keep <= 32 && a.L % a.block == 0 && nb <= 512 &&
                                  static_cast<double>(a.KD) * bq * bq < 2147483647.0 &&  // int32 dot exact
                                  !options().block_generic;
-            const dim3 gw(static_cast<unsigned>(ceil_div_i(nb, 8)), P);
+            const dim3 gw(static_cast<unsigned>(ceil_div_i(nb, kBRows)), P);
+            const size_t psm = static_cast<size_t>(nb) * KD * 4;  // pooled K of the pair
+            auto bsw = [&](auto kern) {
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(psm));
+                kern<<<gw, 256, psm, st>>>(a, nb);
+            };
             if (warp_ok && nb <= 128) {
-                block_select_warp<KD, 4><<<gw, 256, 0, st>>>(a, nb);
+                bsw(block_select_warp<KD, 4>);
             } else if (warp_ok && nb <= 256) {
-                block_select_warp<KD, 8><<<gw, 256, 0, st>>>(a, nb);
+                bsw(block_select_warp<KD, 8>);
             } else if (warp_ok) {
-                block_select_warp<KD, 16><<<gw, 256, 0, st>>>(a, nb);
+                bsw(block_select_warp<KD, 16>);
             } else {
                 const size_t sm = static_cast<size_t>(nb) * 8;
                 cudaFuncSetAttribute(block_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
