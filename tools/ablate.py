@@ -16,7 +16,7 @@ for spec in sys.argv[1:]:
     for src in b.SOURCES:
         s = b.CSRC / src
         o = b.OBJ / (s.stem + ".o")
-        if s.name in ("select_colvec.cu", "project_tc.cu"):
+        if s.name in ("select_colvec.cu", "project_tc.cu", "select_thr.cu"):
             o = out / (s.stem + ".o")
             subprocess.run([b.NVCC, *b.ARCH, *b.COMMON, f"-DDSA_ABLATE={bits}", "-c", str(s), "-o", str(o)],
                            check=True, capture_output=True)
