@@ -415,6 +415,7 @@ Options read_options() {
     o.fuse = env_flag("DSA_FUSE");
     o.block_tc = env_flag("DSA_BLOCK_TC");
     o.predict_tiles = env_flag("DSA_PREDICT_TILES");
+    o.block_cpasync = env_flag("DSA_BLOCK_CPASYNC");
     const char* e = std::getenv("DSA_PIPELINE_CHUNKS");
     o.pipeline_chunks = e ? std::atoi(e) : -1;
     return o;

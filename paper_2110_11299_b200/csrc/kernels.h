@@ -28,6 +28,7 @@ struct Options {
     bool fuse;               // DSA_FUSE: COLVEC select + attention in one kernel (measured slower on C2)
     bool block_tc;           // DSA_BLOCK_TC: tcgen05 + TMA block attention (measured slower on C3)
     bool predict_tiles;      // DSA_PREDICT_TILES: tile kernels instead of the one-CTA-per-tensor pass
+    bool block_cpasync;      // DSA_BLOCK_CPASYNC: block attention with cp.async staging instead of TMA
     int pipeline_chunks;     // DSA_PIPELINE_CHUNKS: pair chunks overlapped on 3 streams
 };
 const Options& options();

@@ -46,6 +46,8 @@ CASES = [
     ("DSA_PREDICT_TILES", "1", {"preset": "c4_threshold", "pairs": 2, "over": {"L": 5000, "cap": 300}}, True),
     ("DSA_PREDICT_TILES", "1", {"preset": "c2_vector", "pairs": 2, "over": {"L": 4500, "keep": 200, "bits": 8}}, True),
     ("DSA_FUSE", "1", C2S, False),
+    ("DSA_BLOCK_CPASYNC", "1", {"preset": "c3_block", "pairs": 2, "over": {"L": 1024, "keep": 5}}, True),
+    ("DSA_BLOCK_CPASYNC", "1", {"preset": "c3_block", "pairs": 3, "over": {"L": 2048, "keep": 16}}, True),
     ("DSA_BLOCK_TC", "1", {"preset": "c3_block", "pairs": 2, "over": {"L": 1024, "keep": 5}}, False),
     ("DSA_BLOCK_TC", "1", {"preset": "c3_block", "pairs": 3, "over": {"L": 2048, "keep": 16}}, False),
     ("DSA_PIPELINE_CHUNKS", "3", {"preset": "c2_vector", "pairs": 7, "over": {"L": 512, "keep": 26}}, True),
