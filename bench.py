@@ -360,37 +360,47 @@ def run_gpu_arm(args, p, rank, local, world):
     barrier(world)
 
     # ---- end to end through the C-ABI with host buffers.  Every step copies
-    # its Q/K/V/P in from pinned host memory and Z back out; steps are
-    # software-pipelined over two device buffer sets so step i+1's H2D and
-    # step i-1's D2H (separate copy engines / directions) overlap step i's
-    # kernels.  Timed from the first H2D to the last D2H.
+    # its Q/K/V/P in from pinned host memory and Z back out; each step is cut
+    # into pair chunks (the public dsa_pipeline on a contiguous pair range)
+    # software-pipelined over two device buffer sets, so chunk c+1's H2D and
+    # chunk c-1's D2H (separate copy engines / directions) overlap chunk c's
+    # kernels and the pipeline's fill / drain shrinks to one chunk.  Timed
+    # from the first H2D to the last D2H.
     h2d = in_bytes + Pm.numel() * 4
     d2h = zh.numel() * zh.element_size()
     bufs = [(qd, kd, vd, Pd, zd)] + [tuple(torch.empty_like(t) for t in (qd, kd, vd, Pd, zd))]
+    nch = next(c for c in (4, 2, 1) if P_ % c == 0)  # pair chunks per step
+    cp = P_ // nch
+    cpipe = ops.Pipeline(p, pairs=cp, device=dev) if nch > 1 else pipe
     s_in, s_out = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
-    ev_in = [torch.cuda.Event() for _ in range(2)]
-    ev_comp = [torch.cuda.Event() for _ in range(2)]
-    ev_out = [torch.cuda.Event() for _ in range(2)]
+    ev_in = [[torch.cuda.Event() for _ in range(nch)] for _ in range(2)]
+    ev_comp = [[torch.cuda.Event() for _ in range(nch)] for _ in range(2)]
+    ev_out = [[torch.cuda.Event() for _ in range(nch)] for _ in range(2)]
 
     def e2e_steps(n):
         for i in range(n):
             b = i & 1
             bq, bk, bv, bp, bz = bufs[b]
-            with torch.cuda.stream(s_in):
+            for c in range(nch):
+                sl = slice(c * cp, (c + 1) * cp)
+                with torch.cuda.stream(s_in):
+                    if i >= 2:
+                        s_in.wait_event(ev_comp[b][c])  # chunk c of buffer b free (step i-2 computed)
+                    bq[sl].copy_(q[sl], non_blocking=True)
+                    bk[sl].copy_(k[sl], non_blocking=True)
+                    bv[sl].copy_(v[sl], non_blocking=True)
+                    if c == 0:
+                        bp.copy_(Pm, non_blocking=True)
+                    ev_in[b][c].record(s_in)
+                stream.wait_event(ev_in[b][c])
                 if i >= 2:
-                    s_in.wait_event(ev_comp[b])  # buffer b free (step i-2 computed)
-                bq.copy_(q, non_blocking=True); bk.copy_(k, non_blocking=True)
-                bv.copy_(v, non_blocking=True); bp.copy_(Pm, non_blocking=True)
-                ev_in[b].record(s_in)
-            stream.wait_event(ev_in[b])
-            if i >= 2:
-                stream.wait_event(ev_out[b])  # z buffer b drained (step i-2 copied out)
-            pipe(bq, bk, bv, bp, out=bz, stream=stream)
-            ev_comp[b].record(stream)
-            with torch.cuda.stream(s_out):
-                s_out.wait_event(ev_comp[b])
-                zh.copy_(bz, non_blocking=True)
-                ev_out[b].record(s_out)
+                    stream.wait_event(ev_out[b][c])  # z chunk drained (step i-2 copied out)
+                cpipe(bq[sl], bk[sl], bv[sl], bp, out=bz[sl], stream=stream)
+                ev_comp[b][c].record(stream)
+                with torch.cuda.stream(s_out):
+                    s_out.wait_event(ev_comp[b][c])
+                    zh[sl].copy_(bz[sl], non_blocking=True)
+                    ev_out[b][c].record(s_out)
 
     e2e_steps(2)
     torch.cuda.synchronize(dev)
@@ -401,7 +411,7 @@ def run_gpu_arm(args, p, rank, local, world):
     stream.wait_event(t_start)
     s_out.wait_event(t_start)
     e2e_steps(args.steps)
-    s_out.wait_event(ev_comp[(args.steps - 1) & 1])
+    s_out.wait_event(ev_comp[(args.steps - 1) & 1][nch - 1])
     t_end.record(s_out)
     t_end.synchronize()
     e2e_ms = max_over_ranks(t_start.elapsed_time(t_end) / args.steps, world, dev)
@@ -507,7 +517,7 @@ def run_gpu_arm(args, p, rank, local, world):
                    "launch": "cuda graph per step" if graph is not None else "eager",
                    "l2": l2_note, **({"oversubscribed_gpus": True} if world > ndev else {})},
         "e2e": {"value": tokens / (e2e_ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h},
+                "d2h_bytes_per_step": d2h, "pair_chunks_per_step": nch},
         "roofline": {"kernel": dom, "bound": w["bound"], "achieved": achieved, "peak": peak,
                      "unit": w["unit"], "frac": achieved / peak, "traffic": traffic,
                      "peak_source": peak_src,
