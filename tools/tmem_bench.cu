@@ -1,5 +1,7 @@
 // Microbenchmark: tcgen05.ld 32x32b throughput (bytes / clock / SM) by warps
-// per SM (measured r01: 230 B/clk at 4 warps, 340 B/clk at 8).  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tmem_bench tools/tmem_bench.cu
+// per SM (measured r01: 230 B/clk at 4 warps, 340 B/clk at 8), and the
+// .pack::16b variant (two 16-bit columns per register: bytes delivered to
+// registers; twice as many TMEM columns per byte).  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tmem_bench tools/tmem_bench.cu
 #include <cstdio>
 #include <cstdint>
 
@@ -13,6 +15,7 @@ __device__ __forceinline__ void ld32(uint32_t a, uint32_t (&r)[32]) {
     if (SHAPE == 1) asm volatile("tcgen05.ld.sync.aligned.16x64b.x32.b32 " R32 : OUTS : "r"(a));
     if (SHAPE == 2) asm volatile("tcgen05.ld.sync.aligned.16x128b.x16.b32 " R32 : OUTS : "r"(a));
     if (SHAPE == 3) asm volatile("tcgen05.ld.sync.aligned.16x256b.x8.b32 " R32 : OUTS : "r"(a));
+    if (SHAPE == 4) asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.pack::16b.b32 " R32 : OUTS : "r"(a));
 }
 
 template <int SHAPE>
@@ -33,7 +36,8 @@ __global__ void bench(int iters, unsigned long long* out, uint32_t* sink) {
     long long t0 = clock64();
     for (int i = 0; i < iters; ++i) {
         uint32_t r0[32], r1[32];
-        const uint32_t col = ((i * 64) + (warp >> 2) * 32) & 511;
+        // pack::16b reads 64 columns per x32 instruction
+        const uint32_t col = SHAPE == 4 ? (((i * 128) + (warp >> 2) * 64) & 511) : (((i * 64) + (warp >> 2) * 32) & 511);
         ld32<SHAPE>(tm + lane_base + col, r0);
         ld32<SHAPE>(tm + lane_base + ((col + 256) & 511), r1);
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
@@ -63,6 +67,7 @@ void run(const char* name, int warps) {
     double avg = 0;
     for (int i = 0; i < 148; ++i) avg += h[i];
     avg /= 148;
+    // bytes delivered to registers (pack::16b: 2 columns per register)
     const double bytes = double(iters) * 2 * 32 * 32 * 4 * warps;  // per SM
     printf("%-14s warps=%2d  %7.1f B/clk/SM  (%s)\n", name, warps, bytes / avg, cudaGetErrorString(e));
     cudaFree(d);
@@ -72,6 +77,7 @@ void run(const char* name, int warps) {
 int main() {
     for (int w : {4, 8, 16}) {
         run<0>("32x32b.x32", w);
+        run<4>("x32.pack::16b", w);
     }
     return 0;
 }
