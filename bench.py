@@ -503,6 +503,18 @@ def run_gpu_arm(args, p, rank, local, world):
     reuse = {"colvec": p.vec_v, "block": p.block}.get(p.mask_mode, 1)
     phases["attention"]["gathered_GBps"] = 2 * nnz * d * e / reuse / (attend_ms * 1e-3) / 1e9
     phases["attention"]["gather_reuse"] = reuse
+    # the reference's dataflow cost model (P/src/dataflow.cpp:10-62, SURVEY
+    # 8(f)4) on this mask: operand fetches of row-parallel bands of 8 rows,
+    # in kept order and reordered (the band column union) -- the reuse a
+    # query-tile union staging could exploit (built, slower)
+    try:
+        df = {}
+        for sched in ("row_parallel", "row_parallel_reordered"):
+            f, _ = ops.dataflow_trace(p, ph.mask, pairs, sched, 8, stream=stream)
+            df[sched] = nnz / max(int(f.sum()), 1)
+        phases["attention"]["dataflow_reuse_band8"] = df
+    except Exception as ex:  # noqa: BLE001 -- explanatory only (L > 65536)
+        phases["attention"]["dataflow_reuse_band8"] = {"unavailable": str(ex)[:80]}
     tokens = p.tokens  # the whole config: every rank's pairs
     value = tokens / (ms * 1e-3)
     adjacent = None

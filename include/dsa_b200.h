@@ -202,6 +202,28 @@ uint64_t dsa_launch_counter(void);
 dsa_status dsa_prediction_accuracy(const dsa_config* cfg, const dsa_mask* pred, const dsa_mask* oracle,
                                    double* accuracy, void* stream);
 
+/* The reference's dataflow fetch-count model on a device mask
+ * (dataflow::simulate, P/include/dsattn/dataflow.hpp:14-46,
+ * P/src/dataflow.cpp:10-62): second-operand fetches of SDDMM / SpMM under
+ * one of three schedules over bands of `band` consecutive rows (1 <= band
+ * <= 32; row_by_row always uses bands of one row, as the reference):
+ *   DSA_SCHED_ROW_BY_ROW             fetches = nnz
+ *   DSA_SCHED_ROW_PARALLEL           per step t, one fetch per distinct t-th
+ *                                    kept column of the band
+ *   DSA_SCHED_ROW_PARALLEL_REORDERED one fetch per distinct column of the
+ *                                    band (the column union)
+ * and pe_idle_steps (sum of band max kept - own kept).  fetches / idle:
+ * HOST arrays of cfg's pairs (per (b,h) pair).  The cost model SURVEY
+ * 8(f) item 4 names for grouping query rows (bench reports the reordered
+ * reuse nnz / fetches). */
+typedef enum dsa_schedule {
+    DSA_SCHED_ROW_BY_ROW = 0,
+    DSA_SCHED_ROW_PARALLEL = 1,
+    DSA_SCHED_ROW_PARALLEL_REORDERED = 2
+} dsa_schedule;
+dsa_status dsa_dataflow_trace(const dsa_config* cfg, const dsa_mask* mask, int32_t schedule, int64_t band,
+                              uint64_t* fetches, uint64_t* idle, void* stream);
+
 /* Exact operation counts for a computed mask (synchronises `stream`). */
 dsa_status dsa_counters(const dsa_config* cfg, const dsa_mask* mask, dsa_counts* out,
                         void* stream);

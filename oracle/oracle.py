@@ -209,6 +209,7 @@ class Reference:
                                         C.c_void_p, _i32, C.POINTER(C.c_double)]),
             "ref_init_projection": (I32, [I64, I64, C.c_uint64, _d]),
             "ref_prediction_accuracy": (I32, [I64, _u64, _u32, _u64, _u32, C.POINTER(C.c_double)]),
+            "ref_dataflow_simulate": (I32, [I64, _u64, _u32, I32, I64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
             "ref_block_mask": (I32, [_i32, _i32, I64, I64, I64, I64, I32, _u32]),
             "ref_causal_threshold_mask": (I32, [_i32, _i32, I64, I64, D, D, I64, I32, _u64, C.c_void_p]),
             "ref_threshold_row_probs": (I32, [_i32, _i32, I64, I64, D, I64, I32, _d]),
@@ -401,6 +402,15 @@ class Reference:
         self._chk(self.L.ref_prediction_accuracy(len(rp_pred) - 1, f(rp_pred, np.uint64), f(c_pred, np.uint32),
                                                  f(rp_orc, np.uint64), f(c_orc, np.uint32), C.byref(out)))
         return out.value
+
+    def dataflow_simulate(self, rp, cols, schedule, band):
+        """dataflow::simulate (P/src/dataflow.cpp:48-62): (operand_fetches, pe_idle_steps)."""
+        f, i = C.c_uint64(), C.c_uint64()
+        kind = {"row_by_row": 0, "row_parallel": 1, "row_parallel_reordered": 2}[schedule]
+        cc = np.ascontiguousarray(cols if len(cols) else np.zeros(1), np.uint32)
+        self._chk(self.L.ref_dataflow_simulate(len(rp) - 1, np.ascontiguousarray(rp, np.uint64), cc, kind, band,
+                                               C.byref(f), C.byref(i)))
+        return f.value, i.value
 
     def init_projection(self, d, k, seed):
         out = np.empty((d, k))

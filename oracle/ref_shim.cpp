@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "dsattn/attention.hpp"
+#include "dsattn/dataflow.hpp"
 #include "dsattn/kernels.hpp"
 #include "dsattn/linalg.hpp"
 #include "dsattn/maskgen.hpp"
@@ -140,6 +141,22 @@ int ref_prediction_accuracy(int64_t L, const uint64_t* rp_pred, const uint32_t* 
     return guarded([&] {
         *out = prediction_accuracy(mask_from_csr(static_cast<size_t>(L), rp_pred, c_pred),
                                    mask_from_csr(static_cast<size_t>(L), rp_orc, c_orc));
+    });
+}
+
+// dataflow::simulate (P/src/dataflow.cpp:48-62) on a CSR mask: total
+// operand_fetches and pe_idle_steps for schedule kind (0 row_by_row,
+// 1 row_parallel, 2 row_parallel_reordered) and band height.
+int ref_dataflow_simulate(int64_t L, const uint64_t* rp, const uint32_t* cols, int kind, int64_t band,
+                          uint64_t* fetches, uint64_t* idle) {
+    return guarded([&] {
+        const dataflow::ScheduleKind k = kind == 0 ? dataflow::ScheduleKind::row_by_row
+                                         : kind == 1 ? dataflow::ScheduleKind::row_parallel
+                                                     : dataflow::ScheduleKind::row_parallel_reordered;
+        const dataflow::AccessTrace t =
+            dataflow::simulate(mask_from_csr(static_cast<size_t>(L), rp, cols), {k, static_cast<size_t>(band)});
+        *fetches = t.operand_fetches;
+        *idle = t.pe_idle_steps;
     });
 }
 

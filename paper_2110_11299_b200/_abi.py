@@ -63,6 +63,7 @@ _SIGS = {
     "dsa_project_qkv": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
                                   C.c_int64, _P, _P, _P, _P, _P, _P, _P]),
     "dsa_counters": (C.c_int, [C.POINTER(DsaConfig), C.POINTER(DsaMask), C.POINTER(DsaCounts), _P]),
+    "dsa_dataflow_trace": (C.c_int, [C.POINTER(DsaConfig), C.POINTER(DsaMask), C.c_int32, C.c_int64, _P, _P, _P]),
     "dsa_generate": (C.c_int, [C.POINTER(DsaConfig), C.c_uint64, C.c_int32, C.c_int32, C.c_int64,
                                C.c_int64, _P, _P, _P, _P, C.c_int32]),
 }

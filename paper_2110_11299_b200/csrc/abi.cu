@@ -689,6 +689,33 @@ dsa_status dsa_prediction_accuracy(const dsa_config* cfg, const dsa_mask* pred, 
     });
 }
 
+dsa_status dsa_dataflow_trace(const dsa_config* cfg, const dsa_mask* mask, int32_t schedule, int64_t band,
+                              uint64_t* fetches, uint64_t* idle, void* stream) {
+    return guard([&] {
+        validate(cfg);
+        require_device();
+        if (!mask || !mask->cols || !fetches || !idle) throw Error(DSA_ERR_PARAM, "dsa_dataflow_trace: null pointer");
+        if (cfg->mask_mode == DSA_MASK_THRESHOLD && !mask->rowptr)
+            throw Error(DSA_ERR_PARAM, "dsa_dataflow_trace: threshold masks need rowptr");
+        if (schedule < 0 || schedule > 2) throw Error(DSA_ERR_PARAM, "dsa_dataflow_trace: unknown schedule");
+        // the reference: "simulate: band height must be >= 1" (P/src/dataflow.cpp:49)
+        if (band < 1) throw Error(DSA_ERR_PARAM, "simulate: band height must be >= 1");
+        if (band > 32) throw Error(DSA_ERR_UNSUPPORTED, "dsa_dataflow_trace: band <= 32 rows");
+        if (cfg->L > 65536) throw Error(DSA_ERR_UNSUPPORTED, "dsa_dataflow_trace: L <= 65536");
+        const int64_t P = pairs_of(*cfg);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        unsigned long long* d = nullptr;
+        check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&d), 2 * P * sizeof(unsigned long long), st), "alloc");
+        check_cuda(cudaMemsetAsync(d, 0, 2 * P * sizeof(unsigned long long), st), "memset");
+        run_dataflow(attn_args(*cfg, nullptr, nullptr, nullptr, *mask, nullptr), static_cast<int>(band), schedule, d,
+                     d + P, st);
+        check_cuda(cudaMemcpyAsync(fetches, d, P * sizeof(uint64_t), cudaMemcpyDeviceToHost, st), "copy");
+        check_cuda(cudaMemcpyAsync(idle, d + P, P * sizeof(uint64_t), cudaMemcpyDeviceToHost, st), "copy");
+        check_cuda(cudaFreeAsync(d, st), "free");
+        check_cuda(cudaStreamSynchronize(st), "sync");
+    });
+}
+
 int dsa_pipeline_fused(const dsa_config* cfg) {
     int out = -1;
     guard([&] {

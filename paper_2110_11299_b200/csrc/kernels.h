@@ -165,6 +165,8 @@ struct AttnArgs {
 void run_attention(const AttnArgs& a, cudaStream_t st);
 // prediction_accuracy counts {intersection, total, rows with unequal counts}
 void run_prediction_accuracy(const AttnArgs& pred, const AttnArgs& orc, unsigned long long* out, cudaStream_t st);
+void run_dataflow(const AttnArgs& m, int band, int kind, unsigned long long* fetches, unsigned long long* idle,
+                  cudaStream_t st);
 bool band_attention_supported(const AttnArgs& a);
 // block masks, 32 x 32 blocks, d = 128: tcgen05 + TMA (attention_block_tc.cu)
 bool block_tc_supported(const AttnArgs& a);

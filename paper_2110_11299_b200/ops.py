@@ -350,6 +350,21 @@ def prediction_accuracy(p: Preset, pred: Mask, oracle: Mask, pairs: int, stream=
     return out.value
 
 
+SCHEDULES = {"row_by_row": 0, "row_parallel": 1, "row_parallel_reordered": 2}
+
+
+def dataflow_trace(p: Preset, mask: Mask, pairs: int, schedule: str, band: int, stream=None):
+    """The reference's dataflow::simulate (P/src/dataflow.cpp:10-62) on a device
+    mask: per (b,h) pair, (operand_fetches, pe_idle_steps) as two uint64 arrays."""
+    c = config_of(p, pairs)
+    cm = mask.as_c()
+    f = np.zeros(pairs, dtype=np.uint64)
+    i = np.zeros(pairs, dtype=np.uint64)
+    _abi.check(_abi.lib().dsa_dataflow_trace(C.byref(c), C.byref(cm), SCHEDULES[schedule], band,
+                                             f.ctypes.data, i.ctypes.data, _stream(stream)))
+    return f, i
+
+
 def launch_counter() -> int:
     return int(_abi.lib().dsa_launch_counter())
 
