@@ -35,6 +35,7 @@
 #include <cuda_fp16.h>
 
 #include <cstdlib>
+#include <type_traits>
 
 #include "device_common.cuh"
 #include "kernels.h"
@@ -64,6 +65,7 @@ struct ThrParams {
     const int64_t* etab;  // [pairs][span]
     int64_t span, L, cap;
     int causal;
+    int faddr;            // KD * qmax^2 < 15000: one-FFMA bin addresses (pass 2)
     uint64_t ln, den;     // L * frac_num, frac_den
     uint64_t* counts;     // [pairs * L]
     int2* cut;            // [pairs * L]: {v_cut, quota}
@@ -182,18 +184,41 @@ __global__ void __launch_bounds__(kTQ, 4) threshold_tc_kernel(ThrParams a) {
         const uint32_t hinc = tid < kHC ? 1u : 0x10000u;
         const int hsh = tid < kHC ? 0 : 16;
         {
-            // bin bits = kMagicBits + t (float magic), clamped to the trash
-            // bin; one IMAD gives the thread's bin address bits * 4 kTQ + base
-            const uint32_t lim = static_cast<uint32_t>(kMagicBits + wh);
-            const uint32_t abase = tc::smem_addr(hcol) - static_cast<uint32_t>(kMagicBits) * (kHC * 4u);
+            // The bin ADDRESS comes out of one FFMA in the subnormal range:
+            // with D(n) = n * 2^-149 (bit pattern n), D(-256) * s + D(A)
+            // with A = col address + 256 m is exactly D(A - 256 s) = D(col
+            // address + 256 t) -- every term is an integer multiple of
+            // 2^-149 below 2^-126, so the product and the sum are exact
+            // (fma.rn without .ftz keeps subnormals).  Bits of positive
+            // floats are monotone, so an unsigned min clamps to the trash
+            // bin (t >= wh, the masked keys' -inf -> +inf).  FFMA + VIMNMX
+            // + ATOMS per key instead of FADD + VIMNMX + IMAD + ATOMS.
+            const uint32_t cbase = tc::smem_addr(hcol);
+            const uint32_t lim = cbase + static_cast<uint32_t>(wh) * (kHC * 4u);
+            const float dneg = __uint_as_float(0x80000000u | (kHC * 4u));  // -D(256)
+            // A = cbase + 256 m as a signed subnormal (|A| < 2^23 when faddr)
+            const int32_t A = static_cast<int32_t>(cbase) + __float2int_rn(m) * static_cast<int32_t>(kHC * 4);
+            const float dA = __uint_as_float(A >= 0 ? static_cast<uint32_t>(A) : (0x80000000u | static_cast<uint32_t>(-A)));
+            // otherwise: bin bits = kMagicBits + t (float magic) and one IMAD
+            const uint32_t mlim = static_cast<uint32_t>(kMagicBits + wh);
+            const uint32_t abase = cbase - static_cast<uint32_t>(kMagicBits) * (kHC * 4u);
+            // two instantiations of the pass (no per-key branch)
+            auto hist_pass = [&](auto FA) {
             score_pass<KD>(c, g, [&](int u, const uint32_t* r, int col0) {
                 const float* f = reinterpret_cast<const float*>(r);
                 const int64_t k0 = static_cast<int64_t>(u) * kTN + col0;
                 auto one = [&](float v) {
-                    const uint32_t bits = min(__float_as_uint(fmaf(v, -1.0f, mb)), lim);
+                    uint32_t addr;
+                    if (decltype(FA)::value) {
+                        float d;
+                        asm("fma.rn.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(v), "f"(dneg), "f"(dA));
+                        addr = min(__float_as_uint(d), lim);
+                    } else {
+                        addr = min(__float_as_uint(fmaf(v, -1.0f, mb)), mlim) * (kHC * 4u) + abase;
+                    }
                     // shared-memory reduction without return value: no
                     // load -> add -> store chain between consecutive keys
-                    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(bits * (kHC * 4u) + abase), "r"(hinc) : "memory");
+                    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(hinc) : "memory");
                 };
                 if (k0 + 32 <= kfree) {
 #pragma unroll
@@ -203,6 +228,9 @@ __global__ void __launch_bounds__(kTQ, 4) threshold_tc_kernel(ThrParams a) {
                     for (int x = 0; x < 32; ++x) one(k0 + x < klim ? f[x] : -INFINITY);
                 }
             });
+            };
+            if (a.faddr) hist_pass(std::true_type{});
+            else hist_pass(std::false_type{});
         }
         // ---- per-row rule from the histogram
         auto bin = [&](int t) -> uint32_t { return (hcol[t * kHC] >> hsh) & 0xffffu; };
@@ -451,6 +479,7 @@ void run_threshold_tc(const SelectArgs& a, cudaStream_t st) {
     p.L = a.L;
     p.cap = a.cap;
     p.causal = a.causal;
+    p.faddr = a.KD * static_cast<int64_t>(a.qmax) * a.qmax < 15000;
     p.ln = static_cast<uint64_t>(a.L) * static_cast<uint64_t>(a.frac_num);
     p.den = static_cast<uint64_t>(a.frac_den);
     p.counts = a.counts;
