@@ -44,6 +44,15 @@ CASES = [
     ("row_topk", 2048, 64, 32, 8, "bf16", "row", {"keep": 1}),
     ("row_topk", 512, 64, 16, 4, "f32", "row", {"keep": 33}),
     ("row_topk", 1024, 64, 16, 4, "bf16", "row", {"keep": 64}),
+    # per-row scales off the warp-per-row kernel's L grid: ragged L, k = 32,
+    # 8-bit / 2-bit levels (tied keys), keep near L/2, L = 4096
+    ("row_topk", 300, 64, 16, 4, "bf16", "row", {"keep": 30}),
+    ("row_topk", 1000, 64, 32, 4, "bf16", "row", {"keep": 100}),
+    ("row_topk", 513, 128, 16, 8, "bf16", "row", {"keep": 250}),
+    ("row_topk", 2048, 64, 16, 4, "bf16", "row", {"keep": 200}),
+    ("row_topk", 777, 64, 16, 2, "bf16", "row", {"keep": 97}),
+    ("row_topk", 4096, 64, 16, 4, "bf16", "row", {"keep": 64}),
+    ("row_topk", 65, 64, 16, 4, "bf16", "row", {"keep": 8}),
     ("threshold", 700, 64, 16, 4, "bf16", "tensor", {"cap": 5, "causal": True}),
     # theta = 400 / L: most rows keep one key or none (empty-row flags)
     ("threshold", 700, 64, 16, 4, "bf16", "tensor", {"cap": 50, "causal": True, "frac_num": 1, "frac_den": 400}),
