@@ -35,6 +35,7 @@
 #include "dsattn/attention.hpp"
 #include "dsattn/errors.hpp"
 #include "dsattn/mask.hpp"
+#include "dsattn/maskgen.hpp"
 #include "dsattn/matrix.hpp"
 #include "dsattn/predictor.hpp"
 
@@ -268,14 +269,24 @@ inline DeviceLevels run_predict_wtilde(const dsa_config& c, const Matrix* x, con
     return lv;
 }
 
-// Every operand f32 (true) or every operand f64 (false): the device chain
-// rounds all of the predictor's matmuls alike (round_proj_f32).
-inline bool uniform_f32(std::initializer_list<const Matrix*> ms) {
-    size_t n32 = 0;
-    for (const Matrix* m : ms) n32 += m->precision() == Precision::f32;
-    if (n32 != 0 && n32 != ms.size())
+// Does the reference round the predictor's matmuls to f32?  A product is
+// f32 only when BOTH operands are (combine(), P/include/dsattn/matrix.hpp:
+// 90-93): R = X P rounds iff X and P are f32, R W~ rounds iff R and W~ are.
+// The device chain has one switch for both stages (round_proj_f32), so the
+// answer is true when every operand is f32, false when the chain is f64
+// from its first product on (X or P f64 -- the ToyModel case: f32 weights,
+// f64 ternary P -- or a given R that is f64 or meets f64 W~), and the one
+// remaining mix (stage one rounds, stage two does not, or W~_Q and W~_K
+// differ) is rejected.  `x`/`p` are null when R is given.
+inline bool chain_f32(const Matrix* x, const Matrix* p, const Matrix* r, const Matrix& wq, const Matrix& wk) {
+    const auto f32 = [](const Matrix& m) { return m.precision() == Precision::f32; };
+    const bool r32 = r ? f32(*r) : (f32(*x) && f32(*p));
+    if (f32(wq) != f32(wk))
+        throw ParamError("dsattn::gpu: W~_Q and W~_K of different precisions are not supported");
+    const bool s32 = r32 && f32(wq);
+    if (!r && r32 && !s32)
         throw ParamError("dsattn::gpu: mixed f32/f64 predictor operands are not supported");
-    return n32 != 0;
+    return s32;
 }
 
 inline dsa_config wtilde_config(size_t L, const PredictorParams& pp, bool f32) {
@@ -355,7 +366,7 @@ inline Levels predict(const Matrix& q, const Matrix& k, const Matrix& p, QuantSp
 // reference's (fp64 chains on the device; f32 when every operand is f32).
 // S~ = s_q s_k (levels_q levels_k^T).
 inline Levels approx_levels(const Matrix& x, const PredictorParams& pp) {
-    const bool f32 = detail::uniform_f32({&x, &pp.proj->p, &pp.wq, &pp.wk});
+    const bool f32 = detail::chain_f32(&x, &pp.proj->p, nullptr, pp.wq, pp.wk);
     dsa_config c = detail::wtilde_config(x.rows(), pp, f32);
     check(dsa_config_validate(&c));
     detail::DeviceLevels lv = detail::run_predict_wtilde(c, &x, nullptr, pp);
@@ -370,7 +381,7 @@ inline Levels approx_levels(const Matrix& x, const PredictorParams& pp) {
 // pp), keep) (P/src/trainer.cpp:190-195), ranked on the exact integer S~
 // (ties to the lowest column).
 inline SparseMask predicted_topk_mask(const Matrix& x, const PredictorParams& pp, size_t keep_per_row) {
-    const bool f32 = detail::uniform_f32({&x, &pp.proj->p, &pp.wq, &pp.wk});
+    const bool f32 = detail::chain_f32(&x, &pp.proj->p, nullptr, pp.wq, pp.wk);
     dsa_config c = detail::wtilde_config(x.rows(), pp, f32);
     c.mask_mode = DSA_MASK_ROW_TOPK;
     c.keep = static_cast<int64_t>(keep_per_row);
@@ -380,7 +391,7 @@ inline SparseMask predicted_topk_mask(const Matrix& x, const PredictorParams& pp
 
 // Same from a precomputed R = X P (approx_scores_from_r).
 inline SparseMask predicted_topk_mask_from_r(const Matrix& r, const PredictorParams& pp, size_t keep_per_row) {
-    const bool f32 = detail::uniform_f32({&r, &pp.wq, &pp.wk});
+    const bool f32 = detail::chain_f32(nullptr, nullptr, &r, pp.wq, pp.wk);
     dsa_config c = detail::wtilde_config(r.rows(), pp, f32);
     c.mask_mode = DSA_MASK_ROW_TOPK;
     c.keep = static_cast<int64_t>(keep_per_row);

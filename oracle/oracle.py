@@ -30,7 +30,7 @@ I64, I32, D = C.c_int64, C.c_int, C.c_double
 
 
 def build(ref: bool = True) -> None:
-    targets = ["oracle"] + (["ref", "shim_test"] if ref and REF_SRC.exists() else [])
+    targets = ["oracle"] + (["ref", "shim_test", "eval_test"] if ref and REF_SRC.exists() else [])
     subprocess.run(["make", "-s", "-C", str(HERE), *targets], check=True)
 
 

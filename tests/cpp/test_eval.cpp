@@ -1,0 +1,268 @@
+// SURVEY 8(f) item 1 gate: the reference's product caller (`evaluate` ->
+// `forward_batch`, P/src/trainer.cpp:120-294, 422-469) against the same
+// forward routed through the GPU path (include/dsattn_gpu_eval.hpp), both in
+// ONE binary: the reference's trainer / model / autodiff / task objects are
+// linked unchanged (oracle/Makefile target eval_test).  Gates: identical
+// masks, identical predictions, unchanged eval accuracy.
+// Run on a GPU by tests/test_gpu_cpp_shim.py.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "dsattn/linalg.hpp"
+#include "dsattn/maskgen.hpp"
+#include "dsattn/predictor.hpp"
+#include "dsattn/trainer.hpp"
+#include "dsattn_gpu_eval.hpp"
+
+using namespace dsattn;
+
+static int g_fail = 0, g_pass = 0;
+#define CHECK(cond)                                                        \
+    do {                                                                   \
+        if (cond) {                                                        \
+            ++g_pass;                                                      \
+        } else {                                                           \
+            ++g_fail;                                                      \
+            std::printf("FAIL %s:%d  %s\n", __FILE__, __LINE__, #cond);   \
+        }                                                                  \
+    } while (0)
+
+struct RefSample {
+    uint32_t prediction;
+    std::vector<double> logits;
+    std::vector<std::vector<SparseMask>> masks;
+};
+
+// the reference forward of one sample (batch of one, so the captured masks
+// and logits_last are this sample's); `pinned` = ForwardOptions::mask_override
+static RefSample ref_forward(ToyModel& model, const TaskSpec& spec, const Sample& s, double sparsity, int bits,
+                             const std::vector<std::vector<SparseMask>>* pinned = nullptr) {
+    ad::Tape tape(false);
+    ForwardOptions fo;
+    fo.dsa = true;
+    fo.mask_kind = MaskKind::predicted;
+    fo.sparsity = sparsity;
+    fo.lambda = 0.0;
+    fo.train_model = fo.train_predictor = false;
+    fo.bits_override = bits;
+    fo.capture_masks = true;
+    fo.mask_override = pinned;
+    BatchResult r = forward_batch(tape, model, spec, {&s}, fo);
+    RefSample out;
+    out.prediction = r.predictions[0];
+    const Matrix& lg = tape.value(r.logits_last);
+    for (size_t j = 0; j < lg.cols(); ++j) out.logits.push_back(lg(0, j));
+    out.masks = r.stats.masks;
+    return out;
+}
+
+// Integer levels by the reference's own operators: quantize(R W~) / s
+static Matrix ref_levels(const Matrix& r, const Matrix& w, int bits) {
+    Matrix xw = matmul(r, w);
+    Matrix qt = quantize(xw, QuantSpec{bits});
+    const double s = max_abs(xw) / ((1 << (bits - 1)) - 1);
+    Matrix lv(qt.rows(), qt.cols());
+    for (size_t i = 0; i < qt.size(); ++i) lv.raw()[i] = s == 0 ? 0 : std::lround(qt.data()[i] / s);
+    return lv;
+}
+
+// The mask rule: the reference's predictor operators
+// (matmul, quantize -- P/src/predictor.cpp:67-80) and the reference's
+// predicted_topk_mask (value desc, lowest column among equals) on the EXACT
+// integer S~ = levels_q levels_k^T.  (forward_batch itself ranks the
+// dequantised float S~ = (s_q l_q)(s_k l_k)^T, whose rounding noise breaks
+// the integer ties arbitrarily -- SURVEY F2; `ref_float_overlap` reports how
+// close the two are.)
+static SparseMask ref_integer_mask(const Matrix& h, const ToyModel& model, size_t layer, size_t head, int bits,
+                                   size_t keep) {
+    const std::string hp = "layer" + std::to_string(layer) + ".h" + std::to_string(head) + ".";
+    Matrix r = matmul(h, model.projections()[layer]->p);
+    Matrix lq = ref_levels(r, model.param(hp + "pred.wq").value, bits);
+    Matrix lk = ref_levels(r, model.param(hp + "pred.wk").value, bits);
+    return predicted_topk_mask(matmul_nt(lq, lk), keep);
+}
+
+static double mask_overlap(const SparseMask& a, const SparseMask& b) {
+    size_t same = 0, total = 0;
+    for (size_t i = 0; i < a.l; ++i) {
+        std::vector<uint32_t> x;
+        std::set_intersection(a.kept[i].begin(), a.kept[i].end(), b.kept[i].begin(), b.kept[i].end(),
+                              std::back_inserter(x));
+        same += x.size();
+        total += std::max(a.kept[i].size(), b.kept[i].size());
+    }
+    return total ? static_cast<double>(same) / static_cast<double>(total) : 1.0;
+}
+
+static double max_logit_diff(const std::vector<double>& a, const std::vector<double>& b) {
+    double m = 0;
+    for (size_t j = 0; j < a.size(); ++j) m = std::max(m, std::abs(a[j] - b[j]));
+    return m;
+}
+
+static void run_case(size_t l, size_t dense_steps, size_t adapt_steps, double sparsity, int bits, size_t n_eval,
+                     uint64_t seed, double acc_tol) {
+    std::printf("-- case l=%zu sparsity=%.2f bits=%d dense_steps=%zu adapt_steps=%zu\n", l, sparsity, bits, dense_steps,
+                adapt_steps);
+    ModelConfig mc;
+    mc.layers = 2;
+    mc.d = 64;
+    mc.heads = 2;
+    mc.ffn = 128;
+    mc.seq_len = l;
+    mc.vocab = 31;
+    mc.n_classes = 4;
+    mc.sigma = 0.5;
+    mc.precision = Precision::f32;
+    Rng master(seed * 1000 + 7);
+    Rng train_rng = master.split(1), eval_rng = master.split(2);
+    ToyTask train_task = make_toy_task(l, 31, 4096, train_rng);
+    ToyTask eval_task = make_toy_task(l, 31, n_eval, eval_rng);
+    ToyModel model(mc, master.split(3).next_u64());
+    const size_t threads = std::max(2u, std::min(8u, std::thread::hardware_concurrency()));
+    if (dense_steps) {  // the reference acceptance recipe (P/tests/acceptance/acceptance_main.cpp:226-256)
+        TrainConfig tc;
+        tc.schedule = TrainSchedule::dense_pretrain;
+        tc.steps = dense_steps;
+        tc.batch = 16;
+        tc.lr = 1e-3;
+        tc.mask_kind = MaskKind::none;
+        tc.seed = seed * 10 + 1;
+        tc.threads = threads;
+        tc.stats_every = 0;
+        const double acc = train(model, train_task, eval_task, tc).final_accuracy;
+        std::printf("   reference dense pretrain: eval accuracy %.4f\n", acc);
+    }
+    if (adapt_steps) {
+        TrainConfig tc;
+        tc.schedule = TrainSchedule::adapt_finetune;
+        tc.phase1_steps = adapt_steps;
+        tc.steps = adapt_steps;
+        tc.batch = 16;
+        tc.lr = 3e-4;
+        tc.predictor_lr = 3e-3;
+        tc.warmup_lr = 1e-2;
+        tc.lambda = 0.02;
+        tc.sparsity = sparsity;
+        tc.mask_kind = MaskKind::predicted;
+        tc.seed = seed * 10 + 2;
+        tc.threads = threads;
+        tc.stats_every = 0;
+        const double acc = train(model, train_task, eval_task, tc).final_accuracy;
+        std::printf("   reference adapt finetune: eval accuracy %.4f (full-precision predictor)\n", acc);
+    }
+    const size_t keep = keep_per_row(l, sparsity);
+
+    // the reference caller as it stands (float S~ ranking)
+    EvalOptions eo;
+    eo.dsa = true;
+    eo.mask_kind = MaskKind::predicted;
+    eo.sparsity = sparsity;
+    eo.bits_override = bits;
+    const double ref_acc = evaluate(model, eval_task, eo).accuracy;
+
+    gpu::GpuEvalOptions go;
+    go.sparsity = sparsity;
+    go.bits_override = bits;
+    go.capture_masks = true;
+
+    // (1) GPU masks + the reference's dense additive-mask softmax.
+    //  (a) every mask == the reference operators' integer-ranked mask on the same layer input;
+    //  (b) forward_batch with those masks pinned (mask_override) gives bit-identical logits.
+    go.attention = gpu::EvalAttention::reference_dense;
+    gpu::GpuEvalResult gd = gpu::evaluate(model, eval_task, go);
+    size_t mask_diff = 0, logit_diff = 0, pred_diff = 0, pinned_correct = 0;
+    double float_overlap = 1.0;
+    for (size_t i = 0; i < n_eval; ++i) {
+        for (size_t la = 0; la < mc.layers; ++la)
+            for (size_t h = 0; h < mc.heads; ++h)
+                mask_diff += !(gd.masks[i][la][h] == ref_integer_mask(gd.layer_inputs[i][la], model, la, h, bits, keep));
+        RefSample pinned = ref_forward(model, eval_task.spec, eval_task.samples[i], sparsity, bits, &gd.masks[i]);
+        logit_diff += !(gd.logits[i] == pinned.logits);
+        pred_diff += gd.predictions[i] != pinned.prediction;
+        pinned_correct += pinned.prediction == eval_task.samples[i].label;
+        RefSample free_run = ref_forward(model, eval_task.spec, eval_task.samples[i], sparsity, bits);
+        for (size_t h = 0; h < mc.heads; ++h)
+            float_overlap = std::min(float_overlap, mask_overlap(gd.masks[i][0][h], free_run.masks[0][h]));
+    }
+    std::printf("   GPU masks + reference dense softmax: %zu of %zu masks differ from the reference integer rule, "
+                "%zu of %zu logit rows differ from forward_batch(mask_override), accuracy %.4f\n",
+                mask_diff, n_eval * mc.layers * mc.heads, logit_diff, n_eval, gd.accuracy);
+    std::printf("   reference evaluate() as it stands (float S~ ties): accuracy %.4f; min layer-0 overlap with the integer rule %.4f\n",
+                ref_acc, float_overlap);
+    CHECK(mask_diff == 0);
+    CHECK(logit_diff == 0);
+    CHECK(pred_diff == 0);
+    CHECK(gd.accuracy == static_cast<double>(pinned_correct) / static_cast<double>(n_eval));
+    CHECK(std::abs(gd.accuracy - ref_acc) <= acc_tol);
+
+    // (2) GPU masks + GPU sparse attention per head (the tensors' own f32
+    // precision), against forward_batch with this run's masks pinned
+    go.attention = gpu::EvalAttention::sparse_per_head;
+    gpu::GpuEvalResult gs = gpu::evaluate(model, eval_task, go);
+    size_t l0_diff = 0, pred_diff_s = 0, mask_diff_s = 0;
+    double max_d = 0.0;
+    for (size_t i = 0; i < n_eval; ++i) {
+        for (size_t h = 0; h < mc.heads; ++h) l0_diff += !(gs.masks[i][0][h] == gd.masks[i][0][h]);
+        for (size_t la = 0; la < mc.layers; ++la)
+            for (size_t h = 0; h < mc.heads; ++h)
+                mask_diff_s += !(gs.masks[i][la][h] == ref_integer_mask(gs.layer_inputs[i][la], model, la, h, bits, keep));
+        RefSample pinned = ref_forward(model, eval_task.spec, eval_task.samples[i], sparsity, bits, &gs.masks[i]);
+        max_d = std::max(max_d, max_logit_diff(gs.logits[i], pinned.logits));
+        pred_diff_s += gs.predictions[i] != pinned.prediction;
+    }
+    std::printf("   GPU masks + GPU sparse attention (per head, f32): masks differing from the integer rule %zu, "
+                "max |dlogit| vs forward_batch(mask_override) %.3e, predictions differing %zu, accuracy %.4f\n",
+                mask_diff_s, max_d, pred_diff_s, gs.accuracy);
+    CHECK(l0_diff == 0);
+    CHECK(mask_diff_s == 0);
+    CHECK(max_d <= 1e-4);
+    CHECK(pred_diff_s == 0);
+    CHECK(std::abs(gs.accuracy - ref_acc) <= acc_tol);
+
+    // (3) the layer-level bf16 tensor-core path (dsa_project_qkv + one
+    // batched attention call): the BASELINE bf16 tolerance
+    go.attention = gpu::EvalAttention::sparse_layer;
+    gpu::GpuEvalResult gb = gpu::evaluate(model, eval_task, go);
+    size_t pred_diff_b = 0;
+    double max_d_b = 0.0, max_logit = 0.0;
+    for (size_t i = 0; i < n_eval; ++i) {
+        RefSample pinned = ref_forward(model, eval_task.spec, eval_task.samples[i], sparsity, bits, &gb.masks[i]);
+        max_d_b = std::max(max_d_b, max_logit_diff(gb.logits[i], pinned.logits));
+        for (double v : pinned.logits) max_logit = std::max(max_logit, std::abs(v));
+        pred_diff_b += gb.predictions[i] != pinned.prediction;
+    }
+    std::printf("   GPU masks + layer-level bf16 sparse attention: max |dlogit| %.3e (max |logit| %.3f), predictions "
+                "differing %zu of %zu, accuracy %.4f\n", max_d_b, max_logit, pred_diff_b, n_eval, gb.accuracy);
+    CHECK(max_d_b <= 5e-2 * std::max(1.0, max_logit));
+    CHECK(std::abs(gb.accuracy - ref_acc) <= std::max(acc_tol, 0.05));
+}
+
+int main() {
+    std::setvbuf(stdout, nullptr, _IONBF, 0);
+    // the reference acceptance recipe (l = 128, 90 % sparsity; shortened schedule), INT4 levels at eval time
+    run_case(128, 420, 200, 0.9, 4, 128, 1, 0.04);
+    run_case(64, 0, 0, 0.75, 8, 16, 5, 1.0);    // untrained weights (accuracy is chance: no accuracy gate), INT8, keep = 16
+    run_case(128, 0, 0, 0.95, 2, 16, 7, 1.0);   // 2-bit levels: heavy ties, lowest-index rule
+    {  // full-precision predictor (bits = 0) is not a device mode: ParamError like the reference's validators
+        ModelConfig mc;
+        mc.seq_len = 64;
+        ToyModel model(mc, 3);
+        Rng r(4);
+        ToyTask t = make_toy_task(64, 31, 2, r);
+        gpu::GpuEvalOptions go;
+        bool threw = false;
+        try {
+            (void)gpu::evaluate(model, t, go);
+        } catch (const ParamError&) {
+            threw = true;
+        }
+        CHECK(threw);
+    }
+    std::printf("%d passed, %d failed\n", g_pass, g_fail);
+    return g_fail ? 1 : 0;
+}
