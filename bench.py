@@ -694,14 +694,16 @@ def main():
     from paper_2110_11299_b200 import load_preset
 
     p = load_preset(args.config)
-    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl != "reference":
         spawn_ranks(args.gpus)
+    if args.impl == "reference":
+        # CPU only: rank 0 runs and prints, the other ranks exit 0 without
+        # work -- no process group (no collective is needed)
+        run_reference_arm(args, p, int(os.environ.get("RANK", "0")), max(args.gpus, int(os.environ.get("WORLD_SIZE", "1"))))
+        return
     rank, local, world = dist_setup()
     try:
-        if args.impl == "reference":
-            run_reference_arm(args, p, rank, world)
-        else:
-            run_gpu_arm(args, p, rank, local, world)
+        run_gpu_arm(args, p, rank, local, world)
     finally:
         if world > 1:
             import torch.distributed as dist
