@@ -224,6 +224,29 @@ typedef enum dsa_schedule {
 dsa_status dsa_dataflow_trace(const dsa_config* cfg, const dsa_mask* mask, int32_t schedule, int64_t band,
                               uint64_t* fetches, uint64_t* idle, void* stream);
 
+/* The reference's UNFUSED sparse operators, in its own value type (f64) and
+ * CSR layout, for callers that use the three steps separately
+ * (P/include/dsattn/sparse.hpp:47-55, P/src/sparse.cpp:38-91 over
+ * P/src/kernels/scalar.cpp:34-58); the fused hot path is
+ * dsa_sparse_attention.  All pointers are DEVICE pointers; rowptr has
+ * rows + 1 entries (u64), cols the kept columns (u32, ascending per row).
+ *   dsa_sddmm_f64           values[p] = <Q_i, K_cols[p]> (* 1/sqrt(d) when scale),
+ *                           one fma per term in index order (the scalar kernel's
+ *                           rounding: bit-identical to it)
+ *   dsa_sparse_softmax_f64  max-subtracted softmax over each row's stored
+ *                           entries, terms summed in entry order; an empty row
+ *                           stays empty and is flagged in empty_rows (optional,
+ *                           rows bytes, written 0 / 1)
+ *   dsa_spmm_f64            Z_i = sum_p weights[p] V_cols[p] (fma in entry order),
+ *                           empty rows give zero rows; z is rows x dv (f64)
+ * Stream-ordered, no allocation, no host synchronisation. */
+dsa_status dsa_sddmm_f64(int64_t rows, int64_t d, const double* q, const double* k, const uint64_t* rowptr,
+                         const uint32_t* cols, int32_t scale, double* values, void* stream);
+dsa_status dsa_sparse_softmax_f64(int64_t rows, const uint64_t* rowptr, const double* scores, double* weights,
+                                  uint8_t* empty_rows, void* stream);
+dsa_status dsa_spmm_f64(int64_t rows, int64_t dv, const uint64_t* rowptr, const uint32_t* cols, const double* weights,
+                        const double* v, double* z, void* stream);
+
 /* Exact operation counts for a computed mask (synchronises `stream`). */
 dsa_status dsa_counters(const dsa_config* cfg, const dsa_mask* mask, dsa_counts* out,
                         void* stream);

@@ -38,6 +38,7 @@
 #include "dsattn/maskgen.hpp"
 #include "dsattn/matrix.hpp"
 #include "dsattn/predictor.hpp"
+#include "dsattn/sparse.hpp"
 
 namespace dsattn::gpu {
 
@@ -567,6 +568,85 @@ inline Matrix sparse_attention(const Matrix& q, const Matrix& k, const Matrix& v
         empty_rows->resize(mask.l);
         check_cuda(cudaMemcpy(empty_rows->data(), de.get(), mask.l, cudaMemcpyDeviceToHost));
     }
+    return z;
+}
+
+// The three operators separately, as the reference exposes them
+// (P/include/dsattn/sparse.hpp:47-55): same types, same exceptions, f64
+// values.  sddmm and spmm reproduce the reference's scalar kernels bit for
+// bit (one fma per term in index order), sparse_softmax to the last ulp of
+// exp().  The fused sparse_attention above is the hot path; these are for
+// callers that inspect the scores or weights in between.
+namespace detail {
+inline void csr_of(const SparseMask& mask, std::vector<uint64_t>& rowptr, std::vector<uint32_t>& cols) {
+    rowptr.assign(mask.l + 1, 0);
+    cols.clear();
+    for (size_t i = 0; i < mask.l; ++i) {
+        cols.insert(cols.end(), mask.kept[i].begin(), mask.kept[i].end());
+        rowptr[i + 1] = cols.size();
+    }
+}
+inline DeviceBuffer upload_raw(const void* p, size_t bytes) {
+    DeviceBuffer d(std::max<size_t>(bytes, 8));
+    if (bytes) check_cuda(cudaMemcpy(d.get(), p, bytes, cudaMemcpyHostToDevice));
+    return d;
+}
+}  // namespace detail
+
+inline SparseScores sddmm(const Matrix& q, const Matrix& k, const SparseMask& mask, bool scale) {
+    if (q.cols() != k.cols()) throw ShapeError("sddmm: Q/K feature dims differ");
+    if (q.rows() != mask.l || k.rows() != mask.l) throw ShapeError("sddmm: mask size != sequence length");
+    mask.validate();
+    SparseScores out;
+    out.mask = mask;
+    std::vector<uint32_t> cols;
+    detail::csr_of(mask, out.row_offsets, cols);
+    out.values.resize(cols.size());
+    DeviceBuffer dq = detail::upload_f64(q), dk = detail::upload_f64(k),
+                 drp = detail::upload_raw(out.row_offsets.data(), out.row_offsets.size() * 8),
+                 dc = detail::upload_raw(cols.data(), cols.size() * 4), dv(std::max<size_t>(cols.size(), 1) * 8);
+    check(dsa_sddmm_f64(static_cast<int64_t>(mask.l), static_cast<int64_t>(q.cols()), dq.as<double>(), dk.as<double>(),
+                        drp.as<uint64_t>(), dc.as<uint32_t>(), scale ? 1 : 0, dv.as<double>(), nullptr));
+    if (!cols.empty())
+        check_cuda(cudaMemcpy(out.values.data(), dv.get(), cols.size() * 8, cudaMemcpyDeviceToHost));
+    else
+        check_cuda(cudaDeviceSynchronize());
+    return out;
+}
+
+inline SparseWeights sparse_softmax(const SparseScores& s) {
+    SparseWeights out;
+    out.mask = s.mask;
+    out.row_offsets = s.row_offsets;
+    out.values.resize(s.values.size());
+    out.empty_row.assign(s.mask.l, 0);
+    if (s.mask.l == 0) return out;
+    DeviceBuffer drp = detail::upload_raw(s.row_offsets.data(), s.row_offsets.size() * 8),
+                 ds = detail::upload_raw(s.values.data(), s.values.size() * 8),
+                 dw(std::max<size_t>(s.values.size(), 1) * 8), de(s.mask.l);
+    check(dsa_sparse_softmax_f64(static_cast<int64_t>(s.mask.l), drp.as<uint64_t>(), ds.as<double>(), dw.as<double>(),
+                                 de.as<uint8_t>(), nullptr));
+    if (!s.values.empty())
+        check_cuda(cudaMemcpy(out.values.data(), dw.get(), s.values.size() * 8, cudaMemcpyDeviceToHost));
+    check_cuda(cudaMemcpy(out.empty_row.data(), de.get(), s.mask.l, cudaMemcpyDeviceToHost));
+    return out;
+}
+
+inline Matrix spmm(const SparseWeights& a, const Matrix& v) {
+    if (a.mask.l != v.rows()) throw ShapeError("spmm: V rows != sequence length");
+    Matrix z(a.mask.l, v.cols(), v.precision());
+    if (z.size() == 0) return z;
+    std::vector<uint32_t> cols;
+    cols.reserve(a.values.size());
+    for (const auto& row : a.mask.kept) cols.insert(cols.end(), row.begin(), row.end());
+    DeviceBuffer drp = detail::upload_raw(a.row_offsets.data(), a.row_offsets.size() * 8),
+                 dc = detail::upload_raw(cols.data(), cols.size() * 4),
+                 dw = detail::upload_raw(a.values.data(), a.values.size() * 8), dv = detail::upload_f64(v),
+                 dz(z.size() * 8);
+    check(dsa_spmm_f64(static_cast<int64_t>(a.mask.l), static_cast<int64_t>(v.cols()), drp.as<uint64_t>(),
+                       dc.as<uint32_t>(), dw.as<double>(), dv.as<double>(), dz.as<double>(), nullptr));
+    check_cuda(cudaMemcpy(z.raw(), dz.get(), z.size() * 8, cudaMemcpyDeviceToHost));
+    z.round_to_precision();
     return z;
 }
 

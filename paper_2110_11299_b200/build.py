@@ -21,7 +21,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
           f"-I{ROOT / 'include'}", f"-I{CSRC}", "--expt-relaxed-constexpr", "-Xptxas", "-v"]
-SOURCES = ["project.cu", "project_fast.cu", "project_tc.cu", "project_tensor.cu", "select.cu", "attention.cu", "attention_band.cu", "attention_block_tc.cu", "select_colvec.cu", "select_thr.cu", "select_rowsel.cu", "predict_wtilde.cu", "mask_ops.cu", "qkv_gemm.cu", "abi.cu", "gen.cpp"]
+SOURCES = ["project.cu", "project_fast.cu", "project_tc.cu", "project_tensor.cu", "select.cu", "attention.cu", "attention_band.cu", "attention_block_tc.cu", "select_colvec.cu", "select_thr.cu", "select_rowsel.cu", "predict_wtilde.cu", "mask_ops.cu", "sparse_ops.cu", "qkv_gemm.cu", "abi.cu", "gen.cpp"]
 
 
 def _needs(obj: Path, deps: list[Path]) -> bool:

@@ -716,6 +716,43 @@ dsa_status dsa_dataflow_trace(const dsa_config* cfg, const dsa_mask* mask, int32
     });
 }
 
+dsa_status dsa_sddmm_f64(int64_t rows, int64_t d, const double* q, const double* k, const uint64_t* rowptr,
+                         const uint32_t* cols, int32_t scale, double* values, void* stream) {
+    return guard([&] {
+        require_device();
+        if (rows < 0 || d < 1) throw Error(DSA_ERR_SHAPE, "sddmm: rows >= 0 and d >= 1");
+        if (rows == 0) return;
+        if (!q || !k || !rowptr || !values) throw Error(DSA_ERR_PARAM, "dsa_sddmm_f64: null pointer");
+        const double sc = scale ? 1.0 / std::sqrt(static_cast<double>(d)) : 1.0;  // P/src/sparse.cpp:47
+        run_sddmm_f64(q, k, rowptr, cols, rows, d, sc, values, static_cast<cudaStream_t>(stream));
+        check_cuda(cudaGetLastError(), "dsa_sddmm_f64");
+    });
+}
+
+dsa_status dsa_sparse_softmax_f64(int64_t rows, const uint64_t* rowptr, const double* scores, double* weights,
+                                  uint8_t* empty_rows, void* stream) {
+    return guard([&] {
+        require_device();
+        if (rows < 0) throw Error(DSA_ERR_SHAPE, "sparse_softmax: rows >= 0");
+        if (rows == 0) return;
+        if (!rowptr || !scores || !weights) throw Error(DSA_ERR_PARAM, "dsa_sparse_softmax_f64: null pointer");
+        run_sparse_softmax_f64(scores, rowptr, rows, weights, empty_rows, static_cast<cudaStream_t>(stream));
+        check_cuda(cudaGetLastError(), "dsa_sparse_softmax_f64");
+    });
+}
+
+dsa_status dsa_spmm_f64(int64_t rows, int64_t dv, const uint64_t* rowptr, const uint32_t* cols, const double* weights,
+                        const double* v, double* z, void* stream) {
+    return guard([&] {
+        require_device();
+        if (rows < 0 || dv < 1) throw Error(DSA_ERR_SHAPE, "spmm: rows >= 0 and d_v >= 1");
+        if (rows == 0) return;
+        if (!rowptr || !weights || !v || !z) throw Error(DSA_ERR_PARAM, "dsa_spmm_f64: null pointer");
+        run_spmm_f64(weights, rowptr, cols, rows, v, dv, z, static_cast<cudaStream_t>(stream));
+        check_cuda(cudaGetLastError(), "dsa_spmm_f64");
+    });
+}
+
 int dsa_pipeline_fused(const dsa_config* cfg) {
     int out = -1;
     guard([&] {

@@ -167,6 +167,13 @@ void run_attention(const AttnArgs& a, cudaStream_t st);
 void run_prediction_accuracy(const AttnArgs& pred, const AttnArgs& orc, unsigned long long* out, cudaStream_t st);
 void run_dataflow(const AttnArgs& m, int band, int kind, unsigned long long* fetches, unsigned long long* idle,
                   cudaStream_t st);
+// the reference's unfused f64 operators on CSR (sparse_ops.cu)
+void run_sddmm_f64(const double* q, const double* k, const uint64_t* rowptr, const uint32_t* cols, int64_t rows,
+                   int64_t d, double scale, double* out, cudaStream_t st);
+void run_sparse_softmax_f64(const double* s, const uint64_t* rowptr, int64_t rows, double* w, uint8_t* empty_rows,
+                            cudaStream_t st);
+void run_spmm_f64(const double* w, const uint64_t* rowptr, const uint32_t* cols, int64_t rows, const double* v,
+                  int64_t dv, double* z, cudaStream_t st);
 bool band_attention_supported(const AttnArgs& a);
 // block masks, 32 x 32 blocks, d = 128: tcgen05 + TMA (attention_block_tc.cu)
 bool block_tc_supported(const AttnArgs& a);
