@@ -107,7 +107,7 @@ inline std::vector<double> forward_sample(ToyModel& model, const TaskSpec& spec,
             pp.wq = model.param(hp + "pred.wq").value;
             pp.wk = model.param(hp + "pred.wk").value;
             pp.quant = quant;
-            masks[hd] = predicted_topk_mask(hv, pp, keep);
+            masks[hd] = gpu::predicted_topk_mask(hv, pp, keep);
         }
         if (masks_out) (*masks_out)[layer] = masks;
 
@@ -122,7 +122,7 @@ inline std::vector<double> forward_sample(ToyModel& model, const TaskSpec& spec,
                 ap.wv.push_back(model.param(hp + "wv").value);
             }
             ap.heads = cfg.heads;
-            z = tape.constant(sparse_attention(hv, ap, std::span<const SparseMask>(masks)));
+            z = tape.constant(gpu::sparse_attention(hv, ap, std::span<const SparseMask>(masks)));
         } else {
             std::vector<ad::Var> head_outputs;
             for (size_t hd = 0; hd < cfg.heads; ++hd) {
@@ -138,7 +138,7 @@ inline std::vector<double> forward_sample(ToyModel& model, const TaskSpec& spec,
                     head_outputs.push_back(tape.matmul(a, v));
                 } else {
                     head_outputs.push_back(tape.constant(
-                        sparse_attention(tape.value(q), tape.value(k), tape.value(v), masks[hd], cfg.scale_scores)));
+                        gpu::sparse_attention(tape.value(q), tape.value(k), tape.value(v), masks[hd], cfg.scale_scores)));
                 }
             }
             z = cfg.heads == 1 ? head_outputs[0] : tape.concat_cols(head_outputs);

@@ -64,6 +64,9 @@ _SIGS = {
                                   C.c_int64, _P, _P, _P, _P, _P, _P, _P]),
     "dsa_counters": (C.c_int, [C.POINTER(DsaConfig), C.POINTER(DsaMask), C.POINTER(DsaCounts), _P]),
     "dsa_dataflow_trace": (C.c_int, [C.POINTER(DsaConfig), C.POINTER(DsaMask), C.c_int32, C.c_int64, _P, _P, _P]),
+    "dsa_sddmm_f64": (C.c_int, [C.c_int64, C.c_int64, _P, _P, _P, _P, C.c_int32, _P, _P]),
+    "dsa_sparse_softmax_f64": (C.c_int, [C.c_int64, _P, _P, _P, _P, _P]),
+    "dsa_spmm_f64": (C.c_int, [C.c_int64, C.c_int64, _P, _P, _P, _P, _P, _P]),
     "dsa_generate": (C.c_int, [C.POINTER(DsaConfig), C.c_uint64, C.c_int32, C.c_int32, C.c_int64,
                                C.c_int64, _P, _P, _P, _P, C.c_int32]),
 }
@@ -95,4 +98,4 @@ def check(status: int) -> None:
 def header_symbols() -> list[str]:
     """Every function the public header declares."""
     text = HEADER.read_text()
-    return sorted(set(re.findall(r"\b(dsa_[a-z_]+)\s*\(", text)) - {"dsa_status"})
+    return sorted(set(re.findall(r"\b(dsa_[a-z0-9_]+)\s*\(", text)) - {"dsa_status"})

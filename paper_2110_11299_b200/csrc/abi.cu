@@ -722,7 +722,8 @@ dsa_status dsa_sddmm_f64(int64_t rows, int64_t d, const double* q, const double*
         require_device();
         if (rows < 0 || d < 1) throw Error(DSA_ERR_SHAPE, "sddmm: rows >= 0 and d >= 1");
         if (rows == 0) return;
-        if (!q || !k || !rowptr || !values) throw Error(DSA_ERR_PARAM, "dsa_sddmm_f64: null pointer");
+        // cols / values may be null when no position is kept (nnz = 0)
+        if (!q || !k || !rowptr) throw Error(DSA_ERR_PARAM, "dsa_sddmm_f64: null pointer");
         const double sc = scale ? 1.0 / std::sqrt(static_cast<double>(d)) : 1.0;  // P/src/sparse.cpp:47
         run_sddmm_f64(q, k, rowptr, cols, rows, d, sc, values, static_cast<cudaStream_t>(stream));
         check_cuda(cudaGetLastError(), "dsa_sddmm_f64");
@@ -735,7 +736,7 @@ dsa_status dsa_sparse_softmax_f64(int64_t rows, const uint64_t* rowptr, const do
         require_device();
         if (rows < 0) throw Error(DSA_ERR_SHAPE, "sparse_softmax: rows >= 0");
         if (rows == 0) return;
-        if (!rowptr || !scores || !weights) throw Error(DSA_ERR_PARAM, "dsa_sparse_softmax_f64: null pointer");
+        if (!rowptr) throw Error(DSA_ERR_PARAM, "dsa_sparse_softmax_f64: null pointer");
         run_sparse_softmax_f64(scores, rowptr, rows, weights, empty_rows, static_cast<cudaStream_t>(stream));
         check_cuda(cudaGetLastError(), "dsa_sparse_softmax_f64");
     });
@@ -747,7 +748,7 @@ dsa_status dsa_spmm_f64(int64_t rows, int64_t dv, const uint64_t* rowptr, const 
         require_device();
         if (rows < 0 || dv < 1) throw Error(DSA_ERR_SHAPE, "spmm: rows >= 0 and d_v >= 1");
         if (rows == 0) return;
-        if (!rowptr || !weights || !v || !z) throw Error(DSA_ERR_PARAM, "dsa_spmm_f64: null pointer");
+        if (!rowptr || !v || !z) throw Error(DSA_ERR_PARAM, "dsa_spmm_f64: null pointer");
         run_spmm_f64(weights, rowptr, cols, rows, v, dv, z, static_cast<cudaStream_t>(stream));
         check_cuda(cudaGetLastError(), "dsa_spmm_f64");
     });

@@ -365,6 +365,50 @@ def dataflow_trace(p: Preset, mask: Mask, pairs: int, schedule: str, band: int, 
     return f, i
 
 
+def _check_csr(rowptr: torch.Tensor, cols: torch.Tensor, *vals: torch.Tensor) -> None:
+    if rowptr.dtype != torch.int64 or cols.dtype != torch.int32 or not rowptr.is_cuda or not cols.is_cuda:
+        raise ParamError("dsa: CSR needs CUDA int64 rowptr (u64 bits) and int32 cols (u32 bits)")
+    for t in vals:
+        if t.dtype != torch.float64 or not t.is_cuda or not t.is_contiguous():
+            raise ParamError("dsa: the unfused operators take contiguous CUDA float64 tensors")
+
+
+def sddmm(q: torch.Tensor, k: torch.Tensor, rowptr: torch.Tensor, cols: torch.Tensor, scale: bool = True,
+          stream=None) -> torch.Tensor:
+    """The reference's sddmm (P/src/sparse.cpp:38-53) for one head: f64 Q, K
+    [L, d], CSR (rowptr [L + 1], cols [nnz]); returns the nnz scores."""
+    _check_csr(rowptr, cols, q, k)
+    if q.shape != k.shape:
+        raise ShapeError("sddmm: Q/K feature dims differ")
+    vals = torch.empty(cols.numel(), dtype=torch.float64, device=q.device)
+    _abi.check(_abi.lib().dsa_sddmm_f64(q.shape[0], q.shape[1], _ptr(q), _ptr(k), _ptr(rowptr), _ptr(cols),
+                                        1 if scale else 0, _ptr(vals), _stream(stream)))
+    return vals
+
+
+def sparse_softmax(scores: torch.Tensor, rowptr: torch.Tensor, stream=None) -> tuple[torch.Tensor, torch.Tensor]:
+    """The reference's sparse_softmax (P/src/sparse.cpp:55-78): (weights, empty_row flags)."""
+    _check_csr(rowptr, torch.empty(0, dtype=torch.int32, device=scores.device), scores)
+    rows = rowptr.numel() - 1
+    w = torch.zeros_like(scores)
+    empty = torch.zeros(rows, dtype=torch.uint8, device=scores.device)
+    _abi.check(_abi.lib().dsa_sparse_softmax_f64(rows, _ptr(rowptr), _ptr(scores), _ptr(w), _ptr(empty),
+                                                 _stream(stream)))
+    return w, empty
+
+
+def spmm(weights: torch.Tensor, rowptr: torch.Tensor, cols: torch.Tensor, v: torch.Tensor, stream=None) -> torch.Tensor:
+    """The reference's spmm (P/src/sparse.cpp:80-91): Z [L, d_v] in f64, empty rows zero."""
+    _check_csr(rowptr, cols, weights, v)
+    rows = rowptr.numel() - 1
+    if v.shape[0] != rows:
+        raise ShapeError("spmm: V rows != sequence length")
+    z = torch.empty((rows, v.shape[1]), dtype=torch.float64, device=v.device)
+    _abi.check(_abi.lib().dsa_spmm_f64(rows, v.shape[1], _ptr(rowptr), _ptr(cols), _ptr(weights), _ptr(v), _ptr(z),
+                                       _stream(stream)))
+    return z
+
+
 def launch_counter() -> int:
     return int(_abi.lib().dsa_launch_counter())
 

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "dsattn/attention.hpp"
+#include "dsattn/kernels.hpp"
 #include "dsattn/linalg.hpp"
 #include "dsattn/maskgen.hpp"
 #include "dsattn/predictor.hpp"
@@ -287,6 +288,89 @@ int main() {
             Matrix zr = spmm(sparse_softmax(sddmm(qb, kb, *m, true)), vb);
             CHECK(max_abs_diff(zg, zr) <= 1e-2 * max_abs(zr));
         }
+    }
+
+    STEP("unfused operators");
+    // sddmm / sparse_softmax / spmm separately (P/include/dsattn/sparse.hpp:47-55):
+    // bit-identical to the reference's scalar kernels (fma per term in index
+    // order), within a few ulps of its AVX2 kernels; softmax to the ulp of exp
+    {
+        SparseMask e = r;  // row top-k mask from above; one empty row, one single-entry row
+        e.kept[3].clear();
+        e.kept[5] = {7};
+        for (kernels::Isa isa : {kernels::Isa::scalar, kernels::Isa::avx2}) {
+            kernels::force_isa(isa);
+            const bool exact = isa == kernels::Isa::scalar;
+            for (bool scale : {true, false}) {
+                SparseScores sr = sddmm(q, kk, e, scale), sg = gpu::sddmm(q, kk, e, scale);
+                CHECK(sg.row_offsets == sr.row_offsets && sg.mask == sr.mask && sg.values.size() == sr.values.size());
+                double ds = 0, ms = 0;
+                for (size_t i = 0; i < sr.values.size(); ++i) {
+                    ds = std::max(ds, std::abs(sg.values[i] - sr.values[i]));
+                    ms = std::max(ms, std::abs(sr.values[i]));
+                }
+                CHECK(exact ? ds == 0.0 : ds <= 1e-13 * ms);
+                // the softmax and the product on the SAME scores, so each operator is checked alone
+                SparseWeights wr = sparse_softmax(sr), wg = gpu::sparse_softmax(sr);
+                CHECK(wg.empty_row == wr.empty_row && wg.empty_row[3] == 1 && wg.row_offsets == wr.row_offsets);
+                double dw = 0;
+                for (size_t i = 0; i < wr.values.size(); ++i) dw = std::max(dw, std::abs(wg.values[i] - wr.values[i]));
+                CHECK(dw <= 4e-16);
+                CHECK(wg.values[wg.row_offsets[5]] == 1.0);
+                Matrix zr = spmm(wr, v), zg = gpu::spmm(wr, v);
+                CHECK(exact ? max_abs_diff(zg, zr) == 0.0 : max_abs_diff(zg, zr) <= 1e-13 * max_abs(zr));
+                bool zero = true;
+                for (size_t j = 0; j < d; ++j) zero &= zg(3, j) == 0.0;
+                CHECK(zero);
+                // the chain on the device end to end == the fused kernel within the f32 bar
+                Matrix zc = gpu::spmm(gpu::sparse_softmax(gpu::sddmm(q, kk, e, scale)), v);
+                CHECK(max_abs_diff(zc, zr) <= 1e-12 * std::max(1.0, max_abs(zr)));
+            }
+        }
+        kernels::reset_isa();
+        OpCounters before = op_counters();  // the device operators do not touch the host counters
+        (void)gpu::sddmm(q, kk, e, true);
+        CHECK(op_counters().sddmm_mults == before.sddmm_mults);
+        CHECK(throws<ShapeError>([&] { gpu::sddmm(q, Matrix(L, d + 1), e, true); }));
+        CHECK(throws<ShapeError>([&] { gpu::sddmm(Matrix(L + 1, d), kk, e, true); }));
+        CHECK(throws<ShapeError>([&] { gpu::spmm(sparse_softmax(sddmm(q, kk, e, true)), Matrix(L + 1, d)); }));
+        SparseMask none(L);  // nothing kept anywhere: empty values, every row flagged, zero output
+        SparseWeights wn = gpu::sparse_softmax(gpu::sddmm(q, kk, none, true));
+        CHECK(wn.values.empty() && std::count(wn.empty_row.begin(), wn.empty_row.end(), 1) == static_cast<long>(L));
+        CHECK(max_abs(gpu::spmm(wn, v)) == 0.0);
+    }
+
+    STEP("predictor precision rule");
+    // combine() (P/include/dsattn/matrix.hpp:90-93): a product is f32 only when
+    // both operands are.  The ToyModel case -- f32 activations and W~, f64
+    // ternary P -- runs the whole chain in f64; all-f32 rounds every product.
+    {
+        Rng prng(77);
+        auto proj = std::make_shared<ProjectionMatrix>(init_projection(d, 16, 9));  // f64
+        Matrix xf = bf16_normal(96, d, prng).as_precision(Precision::f32);
+        PredictorParams pp = random_predictor_params(proj, 0.3, prng, QuantSpec{4}, Precision::f32);
+        auto ref_mask = [&](const PredictorParams& a, const Matrix& x) {
+            Matrix rr = matmul(x, a.proj->p);
+            Matrix xq = matmul(rr, a.wq), xk = matmul(rr, a.wk);
+            auto lv = [&](const Matrix& m) {
+                Matrix qt = quantize(m, a.quant);
+                const double sc = max_abs(m) / 7.0;
+                Matrix o(qt.rows(), qt.cols());
+                for (size_t i = 0; i < qt.size(); ++i) o.raw()[i] = sc == 0 ? 0 : std::lround(qt.data()[i] / sc);
+                return o;
+            };
+            return predicted_topk_mask(matmul_nt(lv(xq), lv(xk)), 11);
+        };
+        CHECK(gpu::predicted_topk_mask(xf, pp, 11) == ref_mask(pp, xf));            // f32 x, f64 P, f32 W~
+        auto proj32 = std::make_shared<ProjectionMatrix>(*proj);
+        proj32->p = proj->p.as_precision(Precision::f32);
+        PredictorParams pp32 = pp;
+        pp32.proj = proj32;
+        CHECK(gpu::predicted_topk_mask(xf, pp32, 11) == ref_mask(pp32, xf));        // everything f32
+        PredictorParams mixed = pp32;
+        mixed.wq = pp.wq.as_precision(Precision::f64);
+        mixed.wk = pp.wk.as_precision(Precision::f64);
+        CHECK(throws<ParamError>([&] { gpu::predicted_topk_mask(xf, mixed, 11); }));  // stage one rounds, stage two not
     }
 
     // reference exception types (P/include/dsattn/errors.hpp)
