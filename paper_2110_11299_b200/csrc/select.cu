@@ -391,7 +391,9 @@ __global__ void __launch_bounds__(kNT) block_generic(SelectArgs a, int64_t nb) {
         const int64_t width = jb == nb - 1 ? r : a.block;
         // mean ranking, exactly: common denominator block * r
         const int64_t val = width == a.block ? sum * r : sum * a.block;
-        keys[jb] = (a.force_diag && jb == ib) ? 0ull : rank_key_i64(val) | 1ull;
+        // 2 val keeps the key odd (INT64_MAX is odd), so the forced diagonal's 0 stays
+        // unique without folding neighbouring values together (r = 1: val = sum)
+        keys[jb] = (a.force_diag && jb == ib) ? 0ull : rank_key_i64(2 * val);
     }
     __syncthreads();
     uint64_t T;

@@ -33,6 +33,10 @@ CASES = [
     ("block", 333, 128, 32, 8, "bf16", "tensor", {"keep": 3, "block": 16, "force_diag": False}),
     ("block", 1024, 128, 32, 8, "bf16", "tensor", {"keep": 7, "block": 32, "force_diag": False}),
     ("block", 512, 64, 16, 4, "bf16", "tensor", {"keep": 16, "block": 16, "force_diag": True}),
+    # last block ONE key wide (cross-multiplied means = the plain sums: adjacent
+    # integers must not share a rank key -- found by test_gpu_sweep)
+    ("block", 513, 32, 16, 4, "f32", "tensor", {"keep": 13, "block": 16, "force_diag": True}),
+    ("block", 1025, 64, 16, 4, "bf16", "tensor", {"keep": 9, "block": 32, "force_diag": True}),
     ("row_topk", 512, 64, 16, 8, "bf16", "row", {"keep": 40}),
     ("row_topk", 640, 128, 32, 4, "bf16", "row", {"keep": 3}),
     ("row_topk", 1024, 64, 16, 4, "bf16", "tensor", {"keep": 64}),
@@ -66,8 +70,7 @@ CASES = [
 ]
 
 
-@pytest.mark.parametrize("mode,L,d,k,bits,dtype,scope,extra", CASES)
-def test_shape(mode, L, d, k, bits, dtype, scope, extra, oracle):
+def check_shape(mode, L, d, k, bits, dtype, scope, extra, oracle):
     p = load_preset(BASE[mode]).replace(L=L, d=d, k=k, bits=bits, dtype=dtype, quant_scope=scope,
                                         round_proj_f32=(dtype == "f32"), seed=1234 + L, **extra)
     npairs = 2
@@ -91,3 +94,8 @@ def test_shape(mode, L, d, k, bits, dtype, scope, extra, oracle):
             assert np.array_equal(ge.astype(bool), er.astype(bool)), "empty-row flags differ"
         worst = max(worst, np.abs(zg - zr).max() / max(np.abs(zr).max(), 1e-30))
     assert worst <= TOL[dtype], worst
+
+
+@pytest.mark.parametrize("mode,L,d,k,bits,dtype,scope,extra", CASES)
+def test_shape(mode, L, d, k, bits, dtype, scope, extra, oracle):
+    check_shape(mode, L, d, k, bits, dtype, scope, extra, oracle)
