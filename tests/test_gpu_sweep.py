@@ -4,6 +4,8 @@ fixed generator (so failures reproduce), each case checked like
 test_gpu_shapes (levels, scales and masks bit-exact, Z within tolerance,
 empty-row flags) against the oracle.  Complements the hand-picked shapes: odd
 L around every tile boundary, keep from 1 to L, every d / k / bits pairing."""
+import os
+
 import numpy as np
 import pytest
 
@@ -46,7 +48,9 @@ def _cases(n=72, seed=20211021):
     return out
 
 
-@pytest.mark.parametrize("mode,L,d,k,bits,dtype,scope,extra", _cases(),
+# DSA_SWEEP_N / DSA_SWEEP_SEED: a longer one-off hunt (the committed default is what the suite runs)
+@pytest.mark.parametrize("mode,L,d,k,bits,dtype,scope,extra",
+                         _cases(int(os.environ.get("DSA_SWEEP_N", "72")), int(os.environ.get("DSA_SWEEP_SEED", "20211021"))),
                          ids=lambda v: str(v) if not isinstance(v, dict) else "-".join(f"{a}{b}" for a, b in v.items()))
 def test_random_config(mode, L, d, k, bits, dtype, scope, extra, oracle):
     check_shape(mode, L, d, k, bits, dtype, scope, extra, oracle)
