@@ -97,3 +97,33 @@ def test_qkv_errors():
         ops.project_qkv(torch.zeros(1, 64, 128, dtype=torch.bfloat16, device="cuda"), w, 1, 64, 64)
     with pytest.raises(ParamError):
         ops.project_qkv(x.float(), w, 1, 64, 64)
+
+
+def _sweep(n=20, seed=2718):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n):
+        out.append((int(rng.integers(1, 4)), int(rng.choice([1, 31, 32, 33, 127, 128, 129, 255, 384, int(rng.integers(2, 700))])),
+                    int(rng.choice([64, 128, 192, 320, 512])), int(rng.integers(1, 7)), int(rng.choice([32, 64, 96, 128])),
+                    int(rng.choice([32, 64, 96, 128])), int(rng.choice([0, 1, 7, 8, 16, 17, 32]))))
+    return out
+
+
+@pytest.mark.parametrize("batch,L,dm,heads,dk,dv,npred", _sweep())
+def test_qkv_random_shapes(batch, L, dm, heads, dk, dv, npred):
+    """Seeded random (batch, L, d_model, heads, d_k, d_v, npred) incl. L = 1, one
+    row past / short of a tile, n_out spanning several 256-column tiles, odd
+    predictor widths: every element within half a bf16 ulp (+ fp32 accumulation
+    noise) of an fp32 matmul of the same bf16 operands; R within 1e-5."""
+    x, wq, wk, wv, pm, w, q, k, v, r = _run(batch, L, dm, heads, dk, dv, npred, seed=11 + L + dm)
+    xs = x.float()
+    for b in range(batch):
+        for h in range(heads):
+            pr = b * heads + h
+            for got, wl in ((q, wq), (k, wk), (v, wv)):
+                want = xs[b] @ wl[h].float()
+                tol = want.abs() * 2.0 ** -8 + 1e-5 * want.abs().max()   # half a bf16 ulp is 2^-9 relative
+                assert bool(((got[pr].float() - want).abs() <= tol).all()), (b, h)
+        if npred:
+            want = xs[b] @ pm.to(torch.bfloat16).float()
+            assert _rel(r[b], want) <= 1e-5

@@ -91,3 +91,37 @@ def test_wtilde_per_row_scope(reference):
     for i in range(L):  # per-row scope: quantize() of each 1 x k row of R W~
         lvr, s, _ = reference.levels_wtilde(wq[0], 4, r=rr[i:i + 1])
         assert np.array_equal(glq[i], lvr[0]) and lv.sq[0, i].item() == s
+
+
+def _sweep(n=16, seed=31337):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n):
+        out.append((int(rng.integers(1, 4)), int(rng.integers(1, 5)), int(rng.choice([1, 31, 64, 129, 255, 777, int(rng.integers(2, 900))])),
+                    int(rng.choice([16, 32, 48, 64, 100, 256])), int(rng.choice([16, 32])), int(rng.choice([2, 4, 8])),
+                    bool(rng.random() < 0.5)))
+    return [c for c in out if c[4] <= c[3]]
+
+
+@pytest.mark.parametrize("batch,heads,L,dm,k,bits,f32", _sweep())
+def test_wtilde_random_shapes(batch, heads, L, dm, k, bits, f32, reference):
+    """Seeded random (batch, heads, L, d_model, k, bits, precision): R, levels and
+    scales bit-exact against the reference library, degenerate L = 1 included."""
+    x, P, wq, wk = _inputs(batch, heads, L, dm, k, f32, 5 * L + dm + bits, reference)
+    p = load_preset("c0_smoke").replace(batch=batch, heads=heads, L=L, k=k, bits=bits,
+                                        round_proj_f32=f32, d=64, keep=1)
+    dev = torch.device("cuda:0")
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    lv, r = ops.predict_wtilde(p, t(wq), t(wk), x=t(x), P=t(P))
+    torch.cuda.synchronize()
+    glq = ops.levels_rows(lv.lq).float().cpu().numpy().astype(np.int32)
+    glk = ops.levels_rows(lv.lk).float().cpu().numpy().astype(np.int32)
+    rg = r.cpu().numpy()
+    for b in range(batch):
+        for h in range(heads):
+            pr = b * heads + h
+            lq, sq, rr = reference.levels_wtilde(wq[h], bits, f32, x=x[b], p=P)
+            lk, sk, _ = reference.levels_wtilde(wk[h], bits, f32, x=x[b], p=P)
+            assert np.array_equal(rg[b], rr), "R = X P differs"
+            assert np.array_equal(glq[pr], lq) and np.array_equal(glk[pr], lk), (b, h)
+            assert lv.sq[pr].item() == sq and lv.sk[pr].item() == sk
