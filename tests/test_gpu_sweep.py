@@ -20,8 +20,8 @@ def _cases(n=72, seed=20211021):
     out = []
     for i in range(n):
         mode = ["row_topk", "colvec", "block", "threshold"][i % 4]
-        d = int(rng.choice([32, 64, 128]))
-        k = int(rng.choice([16, 32]))
+        d = int(rng.choice([16, 32, 64, 128]))
+        k = 16 if d == 16 else int(rng.choice([16, 32]))
         bits = int(rng.choice([2, 4, 8]))
         dtype = "f32" if rng.random() < 0.25 else "bf16"
         L = int(rng.choice(edges[6:])) if rng.random() < 0.5 else int(rng.integers(40, 1400 if i % 3 else 4200))
@@ -34,7 +34,7 @@ def _cases(n=72, seed=20211021):
             extra["vec_v"] = 8 if rng.random() < 0.7 else int(rng.integers(1, 17))
             extra["keep"] = int(rng.choice([1, L, int(rng.integers(1, L + 1))]))
         elif mode == "block":
-            blk = int(rng.choice([16, 32]))
+            blk = int(rng.choice([8, 16, 32, 64, int(rng.integers(3, 41))]))
             nb = -(-L // blk)
             extra["block"] = blk
             extra["keep"] = int(rng.integers(1, nb + 1))
@@ -42,7 +42,7 @@ def _cases(n=72, seed=20211021):
         else:
             extra["causal"] = bool(rng.random() < 0.6)
             extra["cap"] = int(rng.choice([1, L, int(rng.integers(1, L + 1))]))
-            extra["frac_num"] = 1
+            extra["frac_num"] = int(rng.choice([1, 1, 2, 3]))
             extra["frac_den"] = int(rng.choice([20, 5, 100]))
         out.append((mode, L, d, k, bits, dtype, scope, extra))
     return out
