@@ -240,6 +240,13 @@ dsa_status dsa_dataflow_trace(const dsa_config* cfg, const dsa_mask* mask, int32
  *   dsa_spmm_f64            Z_i = sum_p weights[p] V_cols[p] (fma in entry order),
  *                           empty rows give zero rows; z is rows x dv (f64)
  * Stream-ordered, no allocation, no host synchronisation. */
+/* row_topk_indices on any f64 matrix (P/src/linalg.cpp:69-85; the reference's
+ * oracle_topk_mask is this on the exact Q K^T, P/src/maskgen.cpp:11-16):
+ * scores rows x cols (DEVICE, row-major), out rows x keep column indices
+ * (DEVICE, ascending per row) -- value descending, the LOWEST column first
+ * among equal values (-0 == +0), 1 <= keep <= cols <= 25600. */
+dsa_status dsa_row_topk_f64(int64_t rows, int64_t cols, const double* scores, int64_t keep, uint32_t* out,
+                            void* stream);
 dsa_status dsa_sddmm_f64(int64_t rows, int64_t d, const double* q, const double* k, const uint64_t* rowptr,
                          const uint32_t* cols, int32_t scale, double* values, void* stream);
 dsa_status dsa_sparse_softmax_f64(int64_t rows, const uint64_t* rowptr, const double* scores, double* weights,

@@ -571,12 +571,6 @@ inline Matrix sparse_attention(const Matrix& q, const Matrix& k, const Matrix& v
     return z;
 }
 
-// The three operators separately, as the reference exposes them
-// (P/include/dsattn/sparse.hpp:47-55): same types, same exceptions, f64
-// values.  sddmm and spmm reproduce the reference's scalar kernels bit for
-// bit (one fma per term in index order), sparse_softmax to the last ulp of
-// exp().  The fused sparse_attention above is the hot path; these are for
-// callers that inspect the scores or weights in between.
 namespace detail {
 inline void csr_of(const SparseMask& mask, std::vector<uint64_t>& rowptr, std::vector<uint32_t>& cols) {
     rowptr.assign(mask.l + 1, 0);
@@ -592,6 +586,76 @@ inline DeviceBuffer upload_raw(const void* p, size_t bytes) {
     return d;
 }
 }  // namespace detail
+
+// row_topk_indices (P/src/linalg.cpp:69-85) and oracle_topk_mask
+// (P/src/maskgen.cpp:11-16) on a score matrix the caller holds: value
+// descending, the lowest column among equals, ascending lists -- identical
+// to the reference for every input without NaNs.
+inline std::vector<std::vector<uint32_t>> row_topk_indices(const Matrix& s, size_t k_keep) {
+    if (k_keep < 1 || k_keep > s.cols()) throw ParamError("row_topk_indices: k_keep out of range");
+    DeviceBuffer ds = detail::upload_f64(s), dout(s.rows() * k_keep * 4);
+    check(dsa_row_topk_f64(static_cast<int64_t>(s.rows()), static_cast<int64_t>(s.cols()), ds.as<double>(),
+                           static_cast<int64_t>(k_keep), dout.as<uint32_t>(), nullptr));
+    std::vector<uint32_t> flat(s.rows() * k_keep);
+    check_cuda(cudaMemcpy(flat.data(), dout.get(), flat.size() * 4, cudaMemcpyDeviceToHost));
+    std::vector<std::vector<uint32_t>> out(s.rows());
+    for (size_t i = 0; i < s.rows(); ++i) out[i].assign(flat.begin() + i * k_keep, flat.begin() + (i + 1) * k_keep);
+    return out;
+}
+
+inline SparseMask oracle_topk_mask(const Matrix& s, size_t keep_per_row) {
+    if (s.rows() != s.cols()) throw ShapeError("oracle_topk_mask: scores must be square");
+    SparseMask m(s.rows());
+    m.kept = gpu::row_topk_indices(s, keep_per_row);
+    return m;
+}
+
+// prediction_accuracy (P/src/maskgen.cpp:94-107) on the device: the fraction
+// of predicted positions the oracle mask also keeps (dsa_prediction_accuracy
+// over both masks' CSR); the reference's ParamErrors for a size mismatch,
+// unequal per-row counts and empty masks.
+inline double prediction_accuracy(const SparseMask& pred, const SparseMask& oracle) {
+    if (pred.l != oracle.l) throw ParamError("prediction_accuracy: size mismatch");
+    std::vector<uint64_t> rp, ro;
+    std::vector<uint32_t> cp, co;
+    detail::csr_of(pred, rp, cp);
+    detail::csr_of(oracle, ro, co);
+    if (pred.l == 0 || cp.empty()) {
+        for (size_t i = 0; i < pred.l; ++i)
+            if (pred.kept[i].size() != oracle.kept[i].size())
+                throw ParamError("prediction_accuracy: per-row counts differ");
+        throw ParamError("prediction_accuracy: empty masks");
+    }
+    dsa_config c{};
+    c.batch = c.heads = 1;
+    c.L = static_cast<int64_t>(pred.l);
+    c.d = 64;
+    c.k = 16;
+    c.dtype = DSA_BF16;
+    c.bits = 4;
+    c.mask_mode = DSA_MASK_THRESHOLD;  // general CSR
+    c.scale = 1;
+    c.keep = 1;
+    c.vec_v = 8;
+    c.block = 32;
+    c.frac_num = c.frac_den = 1;
+    c.cap = c.L;
+    check(dsa_config_validate(&c));
+    DeviceBuffer drp = detail::upload_raw(rp.data(), rp.size() * 8), dcp = detail::upload_raw(cp.data(), cp.size() * 4),
+                 dro = detail::upload_raw(ro.data(), ro.size() * 8), dco = detail::upload_raw(co.data(), co.size() * 4);
+    dsa_mask mp{dcp.as<uint32_t>(), drp.as<uint64_t>(), static_cast<int64_t>(cp.size()), nullptr};
+    dsa_mask mo{dco.as<uint32_t>(), dro.as<uint64_t>(), static_cast<int64_t>(co.size()), nullptr};
+    double acc = 0.0;
+    check(dsa_prediction_accuracy(&c, &mp, &mo, &acc, nullptr));
+    return acc;
+}
+
+// The three operators separately, as the reference exposes them
+// (P/include/dsattn/sparse.hpp:47-55): same types, same exceptions, f64
+// values.  sddmm and spmm reproduce the reference's scalar kernels bit for
+// bit (one fma per term in index order), sparse_softmax to the last ulp of
+// exp().  The fused sparse_attention above is the hot path; these are for
+// callers that inspect the scores or weights in between.
 
 inline SparseScores sddmm(const Matrix& q, const Matrix& k, const SparseMask& mask, bool scale) {
     if (q.cols() != k.cols()) throw ShapeError("sddmm: Q/K feature dims differ");

@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "dsattn/autodiff.hpp"
+#include "dsattn/linalg.hpp"
 #include "dsattn/model.hpp"
 #include "dsattn/task.hpp"
 #include "dsattn/trainer.hpp"
@@ -43,6 +44,10 @@ struct GpuEvalOptions {
     int bits_override = -1;  // as EvalOptions::bits_override; the device predictor needs 2, 4 or 8 bits
     EvalAttention attention = EvalAttention::sparse_per_head;
     bool capture_masks = false;  // keep every sample's masks and predictor inputs in the result
+    // evaluate(collect_stats = true) (P/src/trainer.cpp:204-207, 459-463): the predicted mask's
+    // accuracy against oracle_topk_mask(Q K^T, keep), mean over heads and samples per layer --
+    // the oracle mask (dsa_row_topk_f64) and the comparison (dsa_prediction_accuracy) on the device
+    bool collect_stats = false;
 };
 
 struct GpuEvalResult {
@@ -51,6 +56,7 @@ struct GpuEvalResult {
     std::vector<std::vector<double>> logits;                    // per sample
     std::vector<std::vector<std::vector<SparseMask>>> masks;    // [sample][layer][head] when captured
     std::vector<std::vector<Matrix>> layer_inputs;              // [sample][layer]: the predictor input h, when captured
+    std::vector<double> pred_acc_per_layer;                     // with collect_stats
 };
 
 namespace detail {
@@ -73,7 +79,8 @@ inline SparseMask full_mask(size_t l) {
 inline std::vector<double> forward_sample(ToyModel& model, const TaskSpec& spec, const Sample& sample,
                                           const GpuEvalOptions& opts,
                                           std::vector<std::vector<SparseMask>>* masks_out = nullptr,
-                                          std::vector<Matrix>* layer_inputs_out = nullptr) {
+                                          std::vector<Matrix>* layer_inputs_out = nullptr,
+                                          std::vector<double>* pred_acc_sum = nullptr) {
     const ModelConfig& cfg = model.config();
     const size_t l = cfg.seq_len;
     if (spec.l != l || spec.vocab != cfg.vocab) throw ShapeError("forward_batch: task/model shape mismatch");
@@ -110,6 +117,14 @@ inline std::vector<double> forward_sample(ToyModel& model, const TaskSpec& spec,
             masks[hd] = gpu::predicted_topk_mask(hv, pp, keep);
         }
         if (masks_out) (*masks_out)[layer] = masks;
+        if (pred_acc_sum && keep < l) {
+            for (size_t hd = 0; hd < cfg.heads; ++hd) {
+                const std::string hp = lp + "h" + std::to_string(hd) + ".";
+                const Matrix s_raw = matmul_nt(matmul(hv, model.param(hp + "wq").value),
+                                               matmul(hv, model.param(hp + "wk").value));  // unscaled, :170
+                (*pred_acc_sum)[layer] += gpu::prediction_accuracy(masks[hd], gpu::oracle_topk_mask(s_raw, keep));
+            }
+        }
 
         ad::Var z;
         if (opts.attention == EvalAttention::sparse_layer) {
@@ -166,8 +181,11 @@ inline GpuEvalResult evaluate(ToyModel& model, const ToyTask& task, const GpuEva
     for (const Sample& s : task.samples) {
         std::vector<std::vector<SparseMask>> masks;
         std::vector<Matrix> inputs;
+        if (opts.collect_stats && res.pred_acc_per_layer.empty())
+            res.pred_acc_per_layer.assign(model.config().layers, 0.0);
         std::vector<double> lg = forward_sample(model, task.spec, s, opts, opts.capture_masks ? &masks : nullptr,
-                                                opts.capture_masks ? &inputs : nullptr);
+                                                opts.capture_masks ? &inputs : nullptr,
+                                                opts.collect_stats ? &res.pred_acc_per_layer : nullptr);
         uint32_t best = 0;
         for (size_t j = 1; j < lg.size(); ++j)
             if (lg[j] > lg[best]) best = static_cast<uint32_t>(j);
@@ -179,6 +197,8 @@ inline GpuEvalResult evaluate(ToyModel& model, const ToyTask& task, const GpuEva
         }
         correct += best == s.label;
     }
+    for (double& a : res.pred_acc_per_layer)
+        a /= static_cast<double>(task.samples.size() * model.config().heads);
     res.accuracy = task.samples.empty() ? 0.0 : static_cast<double>(correct) / static_cast<double>(task.samples.size());
     return res;
 }

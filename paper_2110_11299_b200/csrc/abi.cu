@@ -716,6 +716,21 @@ dsa_status dsa_dataflow_trace(const dsa_config* cfg, const dsa_mask* mask, int32
     });
 }
 
+dsa_status dsa_row_topk_f64(int64_t rows, int64_t cols, const double* scores, int64_t keep, uint32_t* out,
+                            void* stream) {
+    return guard([&] {
+        require_device();
+        if (rows < 0 || cols < 1) throw Error(DSA_ERR_SHAPE, "Matrix: dimensions must be positive");
+        if (keep < 1 || keep > cols) throw Error(DSA_ERR_PARAM, "row_topk_indices: k_keep out of range");
+        if (cols * 8 > 200 * 1024) throw Error(DSA_ERR_UNSUPPORTED, "dsa_row_topk_f64: cols <= 25600");
+        if (rows > 2147483647) throw Error(DSA_ERR_SHAPE, "dsa_row_topk_f64: rows < 2^31");
+        if (rows == 0) return;
+        if (!scores || !out) throw Error(DSA_ERR_PARAM, "dsa_row_topk_f64: null pointer");
+        run_row_topk_f64(scores, rows, cols, keep, out, static_cast<cudaStream_t>(stream));
+        check_cuda(cudaGetLastError(), "dsa_row_topk_f64");
+    });
+}
+
 dsa_status dsa_sddmm_f64(int64_t rows, int64_t d, const double* q, const double* k, const uint64_t* rowptr,
                          const uint32_t* cols, int32_t scale, double* values, void* stream) {
     return guard([&] {

@@ -167,6 +167,8 @@ void run_attention(const AttnArgs& a, cudaStream_t st);
 void run_prediction_accuracy(const AttnArgs& pred, const AttnArgs& orc, unsigned long long* out, cudaStream_t st);
 void run_dataflow(const AttnArgs& m, int band, int kind, unsigned long long* fetches, unsigned long long* idle,
                   cudaStream_t st);
+// row_topk_indices on an f64 matrix (select.cu)
+void run_row_topk_f64(const double* s, int64_t rows, int64_t cols, int64_t keep, uint32_t* out, cudaStream_t st);
 // the reference's unfused f64 operators on CSR (sparse_ops.cu)
 void run_sddmm_f64(const double* q, const double* k, const uint64_t* rowptr, const uint32_t* cols, int64_t rows,
                    int64_t d, double scale, double* out, cudaStream_t st);

@@ -234,6 +234,30 @@ __global__ void __launch_bounds__(kNT) topk_rows_generic(SelectArgs a) {
     }, out, s);
 }
 
+// row_topk_indices on ANY f64 matrix (P/src/linalg.cpp:69-85): the rule the
+// masks above apply to S~, for callers that rank scores of their own -- the
+// reference's oracle_topk_mask(Q K^T, keep) (P/src/maskgen.cpp:11-16) is this
+// on the exact scores.  One CTA per row, 64-bit radix select on the order-
+// preserving image of the double (value desc, lowest column among equals,
+// -0 == +0), ascending output.
+__global__ void __launch_bounds__(kNT) topk_rows_f64(const double* __restrict__ s, int64_t cols, int64_t keep,
+                                                      uint32_t* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    uint64_t* keys = reinterpret_cast<uint64_t*>(dsm);
+    __shared__ SelSmem sm;
+    const int64_t i = blockIdx.x;
+    const int n = static_cast<int>(cols);
+    for (int j = threadIdx.x; j < n; j += kNT) keys[j] = rank_key_f64(s[i * cols + j]);
+    __syncthreads();
+    uint64_t T;
+    uint32_t rem;
+    block_radix_select<uint64_t>(keys, n, static_cast<int>(keep), sm, T, rem);
+    block_emit(n, rem, [&](int j, bool& lt, bool& eq) {
+        lt = keys[j] < T;
+        eq = keys[j] == T;
+    }, out + i * keep, sm);
+}
+
 // Per-row-scaled top-k (quant_scope = row): the ranking key is
 // the double product s_ij * sk_j.  Selection runs on 32-bit keys f =
 // fl32(s * sk) (rounding is monotone, so f orders the products except
@@ -670,6 +694,14 @@ void scan_counts(const SelectArgs& a, cudaStream_t st) {
     cudaMemsetAsync(a.rowptr, 0, sizeof(uint64_t), st);
     size_t tb = a.scan_tmp_bytes;
     cub::DeviceScan::InclusiveSum(a.scan_tmp, tb, a.counts, a.rowptr + 1, static_cast<int64_t>(a.pairs * a.L), st);
+}
+
+void run_row_topk_f64(const double* s, int64_t rows, int64_t cols, int64_t keep, uint32_t* out, cudaStream_t st) {
+    if (rows == 0) return;
+    const size_t sm = static_cast<size_t>(cols) * 8;
+    cudaFuncSetAttribute(topk_rows_f64, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+    topk_rows_f64<<<static_cast<unsigned>(rows), kNT, sm, st>>>(s, cols, keep, out);
+    note_launch();
 }
 
 void launch_topk_scaled_list(const SelectArgs& a, const int64_t* list, const unsigned* nlist, cudaStream_t st) {

@@ -365,6 +365,17 @@ def dataflow_trace(p: Preset, mask: Mask, pairs: int, schedule: str, band: int, 
     return f, i
 
 
+def row_topk(scores: torch.Tensor, keep: int, stream=None) -> torch.Tensor:
+    """The reference's row_topk_indices (P/src/linalg.cpp:69-85) on a CUDA float64
+    matrix: [rows, keep] int32 column indices, ascending per row."""
+    if scores.dim() != 2 or scores.dtype != torch.float64 or not scores.is_cuda or not scores.is_contiguous():
+        raise ParamError("dsa: row_topk takes a contiguous CUDA float64 matrix")
+    out = torch.empty((scores.shape[0], max(keep, 0)), dtype=torch.int32, device=scores.device)
+    _abi.check(_abi.lib().dsa_row_topk_f64(scores.shape[0], scores.shape[1], _ptr(scores), keep, _ptr(out),
+                                           _stream(stream)))
+    return out
+
+
 def _check_csr(rowptr: torch.Tensor, cols: torch.Tensor, *vals: torch.Tensor) -> None:
     if rowptr.dtype != torch.int64 or cols.dtype != torch.int32 or not rowptr.is_cuda or not cols.is_cuda:
         raise ParamError("dsa: CSR needs CUDA int64 rowptr (u64 bits) and int32 cols (u32 bits)")

@@ -194,6 +194,34 @@ static void run_case(size_t l, size_t dense_steps, size_t adapt_steps, double sp
                 mask_diff, n_eval * mc.layers * mc.heads, logit_diff, n_eval, gd.accuracy);
     std::printf("   reference evaluate() as it stands (float S~ ties): accuracy %.4f; min layer-0 overlap with the integer rule %.4f\n",
                 ref_acc, float_overlap);
+    {   // evaluate(collect_stats): per-layer prediction accuracy.  The reference's value uses its
+        // float-ranked predicted masks; with the integer-ranked masks pinned the definition is the
+        // same (mean over heads and samples of prediction_accuracy(pm, oracle_topk_mask(QK^T))).
+        gpu::GpuEvalOptions gs2 = go;
+        gs2.collect_stats = true;
+        gs2.capture_masks = false;
+        gpu::GpuEvalResult st = gpu::evaluate(model, eval_task, gs2);
+        const EvalResult rst = evaluate(model, eval_task, eo, true);
+        CHECK(st.pred_acc_per_layer.size() == mc.layers && rst.pred_acc_per_layer.size() == mc.layers);
+        // exact restatement with the reference's own operators on the captured inputs and masks
+        std::vector<double> want(mc.layers, 0.0);
+        for (size_t i = 0; i < n_eval; ++i)
+            for (size_t la = 0; la < mc.layers; ++la)
+                for (size_t h = 0; h < mc.heads; ++h) {
+                    const std::string hp = "layer" + std::to_string(la) + ".h" + std::to_string(h) + ".";
+                    const Matrix& hin = gd.layer_inputs[i][la];
+                    Matrix sraw = matmul_nt(matmul(hin, model.param(hp + "wq").value), matmul(hin, model.param(hp + "wk").value));
+                    want[la] += prediction_accuracy(gd.masks[i][la][h], oracle_topk_mask(sraw, keep));
+                }
+        for (size_t la = 0; la < mc.layers; ++la) {
+            want[la] /= static_cast<double>(n_eval * mc.heads);
+            std::printf("   layer %zu prediction accuracy: GPU %.6f, reference operators on the same masks %.6f, "
+                        "reference evaluate(collect_stats) %.6f\n", la, st.pred_acc_per_layer[la], want[la],
+                        rst.pred_acc_per_layer[la]);
+            CHECK(std::abs(st.pred_acc_per_layer[la] - want[la]) <= 1e-12);
+            CHECK(std::abs(st.pred_acc_per_layer[la] - rst.pred_acc_per_layer[la]) <= 0.05);
+        }
+    }
     CHECK(mask_diff == 0);
     CHECK(logit_diff == 0);
     CHECK(pred_diff == 0);

@@ -340,6 +340,32 @@ int main() {
         CHECK(max_abs(gpu::spmm(wn, v)) == 0.0);
     }
 
+    STEP("row_topk_indices / oracle_topk_mask / prediction_accuracy");
+    {
+        Rng trng(5);
+        // non-square, heavy ties (values in {-2..2}), -0 / +0, keep = 1, cols, in between
+        Matrix t(37, 91);
+        for (size_t i = 0; i < t.size(); ++i) t.raw()[i] = std::floor(trng.normal() * 1.2);
+        t.raw()[3] = -0.0;
+        t.raw()[4] = 0.0;
+        for (size_t keep_n : {size_t{1}, size_t{7}, size_t{90}, size_t{91}})
+            CHECK(gpu::row_topk_indices(t, keep_n) == row_topk_indices(t, keep_n));
+        CHECK(throws<ParamError>([&] { gpu::row_topk_indices(t, 0); }));
+        CHECK(throws<ParamError>([&] { gpu::row_topk_indices(t, 92); }));
+        // the oracle mask of the exact scores, and the prediction accuracy of the predicted mask against it
+        Matrix sraw = matmul_nt(q, kk);
+        SparseMask om = oracle_topk_mask(sraw, 17), og = gpu::oracle_topk_mask(sraw, 17);
+        CHECK(og == om);
+        CHECK(throws<ShapeError>([&] { gpu::oracle_topk_mask(t, 3); }));
+        CHECK(gpu::prediction_accuracy(r, om) == prediction_accuracy(r, om));
+        CHECK(gpu::prediction_accuracy(om, om) == 1.0);
+        SparseMask shorter = om;
+        shorter.kept[2].pop_back();
+        CHECK(throws<ParamError>([&] { gpu::prediction_accuracy(shorter, om); }));
+        CHECK(throws<ParamError>([&] { gpu::prediction_accuracy(SparseMask(L), SparseMask(L)); }));
+        CHECK(throws<ParamError>([&] { gpu::prediction_accuracy(SparseMask(L), SparseMask(L + 1)); }));
+    }
+
     STEP("predictor precision rule");
     // combine() (P/include/dsattn/matrix.hpp:90-93): a product is f32 only when
     // both operands are.  The ToyModel case -- f32 activations and W~, f64

@@ -101,3 +101,23 @@ def test_unfused_operator_errors():
     with pytest.raises(ShapeError):
         ops.spmm(w, rp, cl, torch.zeros((5, 8), dtype=torch.float64, device="cuda"))
     assert not ops.spmm(w, rp, cl, q).any()
+
+
+@pytest.mark.parametrize("rows,cols,keep", [(1, 1, 1), (37, 91, 7), (64, 2048, 102), (5, 25600, 300), (9, 513, 513)])
+def test_row_topk_f64_matches_reference_rule(rows, cols, keep):
+    """dsa_row_topk_f64 == row_topk_indices (P/src/linalg.cpp:69-85): value desc,
+    lowest column among equals, ascending output; heavy ties, -0 == +0."""
+    import torch
+    from paper_2110_11299_b200 import ops
+    from paper_2110_11299_b200.errors import ParamError
+
+    rng = np.random.default_rng(rows * cols)
+    s = np.floor(rng.standard_normal((rows, cols)) * 1.5)     # a handful of distinct values: ties everywhere
+    s[0, : min(4, cols)] = [-0.0, 0.0, -0.0, 0.0][: min(4, cols)]
+    got = ops.row_topk(torch.from_numpy(s).cuda(), keep).cpu().numpy()
+    order = np.argsort(-s, axis=1, kind="stable")[:, :keep]   # stable: the lowest column first among equals
+    assert np.array_equal(got, np.sort(order, axis=1))
+    with pytest.raises(ParamError):
+        ops.row_topk(torch.from_numpy(s).cuda(), cols + 1)
+    with pytest.raises(ParamError):
+        ops.row_topk(torch.from_numpy(s).cuda(), 0)
