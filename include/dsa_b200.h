@@ -224,6 +224,28 @@ typedef enum dsa_schedule {
 dsa_status dsa_dataflow_trace(const dsa_config* cfg, const dsa_mask* mask, int32_t schedule, int64_t band,
                               uint64_t* fetches, uint64_t* idle, void* stream);
 
+/* The reference's mask generators on a caller-held DENSE score matrix
+ * (P/include/dsattn/maskgen.hpp:14-30), for callers that already hold S~:
+ *   dsa_colvec_mask_f64     colvec_mask, column orientation (P/src/maskgen.cpp:
+ *                           44-59): bands of v rows, band score of column j =
+ *                           sum of |s(i, j)| over the band (rows in order),
+ *                           row_topk_indices keeps `keep` columns per band;
+ *                           band_cols is ceil(l / v) x keep (ascending).  NOTE
+ *                           the reference rule here is SUM |s|; the BASELINE
+ *                           C2 rule (max-pooled exact integer scores) is
+ *                           DSA_MASK_COLVEC of dsa_select.
+ *   dsa_threshold_mask_f64  threshold_mask (P/src/maskgen.cpp:22-31): keep[i][j]
+ *                           = (value >= theta), value = s or its row softmax
+ *                           (P/src/linalg.cpp:51-67; rounded to f32 when
+ *                           round_f32); keep is rows x cols bytes.  The softmax
+ *                           weights equal the reference's to the last ulp of
+ *                           exp(), so a weight within an ulp of theta may differ.
+ * scores: DEVICE f64 row-major; outputs DEVICE. */
+dsa_status dsa_colvec_mask_f64(int64_t l, int64_t v, int64_t keep, const double* scores, uint32_t* band_cols,
+                               void* stream);
+dsa_status dsa_threshold_mask_f64(int64_t rows, int64_t cols, const double* scores, double theta,
+                                  int32_t post_softmax, int32_t round_f32, uint8_t* keep, void* stream);
+
 /* The reference's UNFUSED sparse operators, in its own value type (f64) and
  * CSR layout, for callers that use the three steps separately
  * (P/include/dsattn/sparse.hpp:47-55, P/src/sparse.cpp:38-91 over

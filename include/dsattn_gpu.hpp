@@ -610,6 +610,62 @@ inline SparseMask oracle_topk_mask(const Matrix& s, size_t keep_per_row) {
     return m;
 }
 
+// colvec_mask and threshold_mask with the reference's OWN signatures, on a
+// dense score matrix the caller holds (P/include/dsattn/maskgen.hpp:14-30,
+// P/src/maskgen.cpp:22-61): the band rule is the reference's sum of |s~| over
+// the band, keep = ceil((1 - sparsity) l); row orientation is the transposed
+// rule.  (The (q, k, p, quant) overloads above never materialise S~ and apply
+// the BASELINE max-pooled integer rule.)
+inline SparseMask colvec_mask(const Matrix& s_tilde, ColVecSpec spec, double target_sparsity) {
+    if (spec.orientation == VecOrientation::row) {
+        ColVecSpec t = spec;
+        t.orientation = VecOrientation::col;
+        Matrix tr(s_tilde.cols(), s_tilde.rows(), s_tilde.precision());
+        for (size_t i = 0; i < s_tilde.rows(); ++i)
+            for (size_t j = 0; j < s_tilde.cols(); ++j) tr.raw()[j * s_tilde.rows() + i] = s_tilde(i, j);
+        SparseMask cm = gpu::colvec_mask(tr, t, target_sparsity);
+        SparseMask m(cm.l);
+        for (size_t i = 0; i < cm.l; ++i)
+            for (uint32_t j : cm.kept[i]) m.kept[j].push_back(static_cast<uint32_t>(i));
+        return m;
+    }
+    if (spec.v < 1) throw ParamError("colvec_mask: vector height must be >= 1");
+    if (!(target_sparsity > 0.0 && target_sparsity < 1.0))
+        throw ParamError("colvec_mask: target_sparsity must be in (0, 1)");
+    if (s_tilde.rows() != s_tilde.cols()) throw ShapeError("colvec_mask: scores must be square");
+    const size_t l = s_tilde.rows();
+    const auto keep = static_cast<size_t>(std::ceil((1.0 - target_sparsity) * static_cast<double>(l)));
+    const size_t nb = (l + spec.v - 1) / spec.v;
+    DeviceBuffer ds = detail::upload_f64(s_tilde), dout(nb * keep * 4);
+    check(dsa_colvec_mask_f64(static_cast<int64_t>(l), static_cast<int64_t>(spec.v), static_cast<int64_t>(keep),
+                              ds.as<double>(), dout.as<uint32_t>(), nullptr));
+    std::vector<uint32_t> flat(nb * keep);
+    check_cuda(cudaMemcpy(flat.data(), dout.get(), flat.size() * 4, cudaMemcpyDeviceToHost));
+    SparseMask m(l);
+    for (size_t i = 0; i < l; ++i) {
+        const size_t b = i / spec.v;
+        m.kept[i].assign(flat.begin() + b * keep, flat.begin() + (b + 1) * keep);
+    }
+    return m;
+}
+
+inline SparseMask threshold_mask(const Matrix& s, double theta, bool post_softmax) {
+    if (!std::isfinite(theta)) throw ParamError("threshold_mask: theta must be finite");
+    if (s.rows() != s.cols()) throw ShapeError("threshold_mask: scores must be square");
+    const size_t l = s.rows();
+    DeviceBuffer ds = detail::upload_f64(s), dk(l * l);
+    check(dsa_threshold_mask_f64(static_cast<int64_t>(l), static_cast<int64_t>(l), ds.as<double>(), theta,
+                                 post_softmax ? 1 : 0, s.precision() == Precision::f32 ? 1 : 0, dk.as<uint8_t>(),
+                                 nullptr));
+    std::vector<uint8_t> keep(l * l);
+    check_cuda(cudaMemcpy(keep.data(), dk.get(), keep.size(), cudaMemcpyDeviceToHost));
+    SparseMask m(l);
+    for (size_t i = 0; i < l; ++i)
+        for (uint32_t j = 0; j < l; ++j)
+            if (keep[i * l + j]) m.kept[i].push_back(j);
+    return m;
+}
+
 // prediction_accuracy (P/src/maskgen.cpp:94-107) on the device: the fraction
 // of predicted positions the oracle mask also keeps (dsa_prediction_accuracy
 // over both masks' CSR); the reference's ParamErrors for a size mismatch,

@@ -65,6 +65,8 @@ _SIGS = {
     "dsa_counters": (C.c_int, [C.POINTER(DsaConfig), C.POINTER(DsaMask), C.POINTER(DsaCounts), _P]),
     "dsa_dataflow_trace": (C.c_int, [C.POINTER(DsaConfig), C.POINTER(DsaMask), C.c_int32, C.c_int64, _P, _P, _P]),
     "dsa_row_topk_f64": (C.c_int, [C.c_int64, C.c_int64, _P, C.c_int64, _P, _P]),
+    "dsa_colvec_mask_f64": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, _P, _P, _P]),
+    "dsa_threshold_mask_f64": (C.c_int, [C.c_int64, C.c_int64, _P, C.c_double, C.c_int32, C.c_int32, _P, _P]),
     "dsa_sddmm_f64": (C.c_int, [C.c_int64, C.c_int64, _P, _P, _P, _P, C.c_int32, _P, _P]),
     "dsa_sparse_softmax_f64": (C.c_int, [C.c_int64, _P, _P, _P, _P, _P]),
     "dsa_spmm_f64": (C.c_int, [C.c_int64, C.c_int64, _P, _P, _P, _P, _P, _P]),

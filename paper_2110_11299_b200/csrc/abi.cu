@@ -731,6 +731,44 @@ dsa_status dsa_row_topk_f64(int64_t rows, int64_t cols, const double* scores, in
     });
 }
 
+dsa_status dsa_colvec_mask_f64(int64_t l, int64_t v, int64_t keep, const double* scores, uint32_t* band_cols,
+                               void* stream) {
+    return guard([&] {
+        require_device();
+        if (v < 1) throw Error(DSA_ERR_PARAM, "colvec_mask: vector height must be >= 1");
+        if (l < 1) throw Error(DSA_ERR_SHAPE, "Matrix: dimensions must be positive");
+        if (keep < 1 || keep > l) throw Error(DSA_ERR_PARAM, "row_topk_indices: k_keep out of range");
+        if (l * 8 > 200 * 1024) throw Error(DSA_ERR_UNSUPPORTED, "dsa_colvec_mask_f64: l <= 25600");
+        if (!scores || !band_cols) throw Error(DSA_ERR_PARAM, "dsa_colvec_mask_f64: null pointer");
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const int64_t nb = (l + v - 1) / v;
+        double* pooled = nullptr;
+        check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&pooled), static_cast<size_t>(nb * l) * 8, st), "alloc");
+        run_band_abs_sum_f64(scores, l, v, pooled, st);
+        run_row_topk_f64(pooled, nb, l, keep, band_cols, st);
+        check_cuda(cudaFreeAsync(pooled, st), "free");
+        check_cuda(cudaGetLastError(), "dsa_colvec_mask_f64");
+    });
+}
+
+dsa_status dsa_threshold_mask_f64(int64_t rows, int64_t cols, const double* scores, double theta,
+                                  int32_t post_softmax, int32_t round_f32, uint8_t* keep, void* stream) {
+    return guard([&] {
+        require_device();
+        if (!std::isfinite(theta)) throw Error(DSA_ERR_PARAM, "threshold_mask: theta must be finite");
+        if (rows < 1 || cols < 1) throw Error(DSA_ERR_SHAPE, "Matrix: dimensions must be positive");
+        if (!scores || !keep) throw Error(DSA_ERR_PARAM, "dsa_threshold_mask_f64: null pointer");
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        double* scratch = nullptr;
+        if (post_softmax)
+            check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&scratch), static_cast<size_t>(rows * cols) * 8, st),
+                       "alloc");
+        run_threshold_f64(scores, rows, cols, theta, post_softmax, round_f32, scratch, keep, st);
+        if (scratch) check_cuda(cudaFreeAsync(scratch, st), "free");
+        check_cuda(cudaGetLastError(), "dsa_threshold_mask_f64");
+    });
+}
+
 dsa_status dsa_sddmm_f64(int64_t rows, int64_t d, const double* q, const double* k, const uint64_t* rowptr,
                          const uint32_t* cols, int32_t scale, double* values, void* stream) {
     return guard([&] {

@@ -176,6 +176,9 @@ void run_sparse_softmax_f64(const double* s, const uint64_t* rowptr, int64_t row
                             cudaStream_t st);
 void run_spmm_f64(const double* w, const uint64_t* rowptr, const uint32_t* cols, int64_t rows, const double* v,
                   int64_t dv, double* z, cudaStream_t st);
+void run_band_abs_sum_f64(const double* s, int64_t l, int64_t v, double* pooled, cudaStream_t st);
+void run_threshold_f64(const double* s, int64_t rows, int64_t cols, double theta, int post_softmax, int f32,
+                       double* scratch, uint8_t* keep, cudaStream_t st);
 bool band_attention_supported(const AttnArgs& a);
 // block masks, 32 x 32 blocks, d = 128: tcgen05 + TMA (attention_block_tc.cu)
 bool block_tc_supported(const AttnArgs& a);

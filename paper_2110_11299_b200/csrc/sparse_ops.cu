@@ -82,6 +82,55 @@ __global__ void __launch_bounds__(kT) spmm_f64_kernel(const double* __restrict__
     z[idx] = acc;
 }
 
+// colvec_mask's band scores on a caller-held S~ (P/src/maskgen.cpp:52-58):
+// pooled[band][j] = sum over the band's rows of |s(i, j)|, rows added in
+// order (the reference's rounding).  One thread per (band, column).
+__global__ void __launch_bounds__(kT) band_abs_sum_f64_kernel(const double* __restrict__ s, int64_t l, int64_t v,
+                                                              int64_t nb, double* __restrict__ pooled) {
+    const int64_t idx = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
+    if (idx >= nb * l) return;
+    const int64_t band = idx / l, j = idx - band * l;
+    const int64_t r1 = min((band + 1) * v, l);
+    double acc = 0.0;
+    for (int64_t i = band * v; i < r1; ++i) acc += fabs(s[i * l + j]);
+    pooled[idx] = acc;
+}
+
+// threshold_mask on a caller-held matrix (P/src/maskgen.cpp:22-31): keep[i][j]
+// = value >= theta, the value being s itself or its row softmax
+// (P/src/linalg.cpp:51-67: max-subtracted exp, terms summed in column order,
+// rounded to f32 when the matrix is).  One warp per row.
+__global__ void __launch_bounds__(kT) threshold_f64_kernel(const double* __restrict__ s, int64_t rows, int64_t cols,
+                                                           double theta, int post_softmax, int f32,
+                                                           double* __restrict__ scratch, uint8_t* __restrict__ keep) {
+    const int lane = threadIdx.x & 31;
+    const int64_t row = (static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x) >> 5;
+    if (row >= rows) return;
+    const double* r = s + row * cols;
+    uint8_t* k = keep + row * cols;
+    if (!post_softmax) {
+        for (int64_t j = lane; j < cols; j += 32) k[j] = r[j] >= theta;
+        return;
+    }
+    double* e = scratch + row * cols;
+    double m = -INFINITY;
+    for (int64_t j = lane; j < cols; j += 32) m = fmax(m, r[j]);
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    for (int64_t j = lane; j < cols; j += 32) e[j] = exp(r[j] - m);
+    __syncwarp();
+    double sum = 0.0;
+    for (int64_t j0 = 0; j0 < cols; j0 += 32) {
+        const double x = j0 + lane < cols ? e[j0 + lane] : 0.0;
+        const int n = cols - j0 < 32 ? static_cast<int>(cols - j0) : 32;
+        for (int i = 0; i < n; ++i) sum += __shfl_sync(0xffffffffu, x, i);
+    }
+    for (int64_t j = lane; j < cols; j += 32) {
+        double p = e[j] / sum;
+        if (f32) p = static_cast<double>(static_cast<float>(p));
+        k[j] = p >= theta;
+    }
+}
+
 unsigned blocks_for(int64_t threads) { return static_cast<unsigned>((threads + kT - 1) / kT); }
 
 }  // namespace
@@ -104,6 +153,18 @@ void run_spmm_f64(const double* w, const uint64_t* rowptr, const uint32_t* cols,
                   int64_t dv, double* z, cudaStream_t st) {
     if (rows == 0 || dv == 0) return;
     spmm_f64_kernel<<<blocks_for(rows * dv), kT, 0, st>>>(w, rowptr, cols, rows, v, dv, z);
+    note_launch(1);
+}
+
+void run_band_abs_sum_f64(const double* s, int64_t l, int64_t v, double* pooled, cudaStream_t st) {
+    const int64_t nb = (l + v - 1) / v;
+    band_abs_sum_f64_kernel<<<blocks_for(nb * l), kT, 0, st>>>(s, l, v, nb, pooled);
+    note_launch(1);
+}
+
+void run_threshold_f64(const double* s, int64_t rows, int64_t cols, double theta, int post_softmax, int f32,
+                       double* scratch, uint8_t* keep, cudaStream_t st) {
+    threshold_f64_kernel<<<blocks_for(rows * 32), kT, 0, st>>>(s, rows, cols, theta, post_softmax, f32, scratch, keep);
     note_launch(1);
 }
 

@@ -366,6 +366,35 @@ int main() {
         CHECK(throws<ParamError>([&] { gpu::prediction_accuracy(SparseMask(L), SparseMask(L + 1)); }));
     }
 
+    STEP("mask generators on a caller-held dense S~");
+    {
+        // the reference's own signatures (maskgen.hpp:14-30): colvec_mask (sum |s~| per band, both
+        // orientations, ragged last band) and threshold_mask (raw and post-softmax, f64 and f32)
+        Rng mrng(19);
+        const size_t l = 203;
+        Matrix sm(l, l);
+        for (size_t i = 0; i < sm.size(); ++i) sm.raw()[i] = std::floor(mrng.normal() * 3.0);  // ties
+        for (ColVecSpec spec : {ColVecSpec{8, VecOrientation::col}, ColVecSpec{5, VecOrientation::col},
+                                ColVecSpec{1, VecOrientation::col}, ColVecSpec{8, VecOrientation::row},
+                                ColVecSpec{300, VecOrientation::col}})
+            for (double sp : {0.9, 0.5, 0.01})
+                CHECK(gpu::colvec_mask(sm, spec, sp) == colvec_mask(sm, spec, sp));
+        CHECK(throws<ParamError>([&] { gpu::colvec_mask(sm, ColVecSpec{0, VecOrientation::col}, 0.5); }));
+        CHECK(throws<ParamError>([&] { gpu::colvec_mask(sm, ColVecSpec{8, VecOrientation::col}, 1.0); }));
+        CHECK(throws<ShapeError>([&] { gpu::colvec_mask(Matrix(4, 5), ColVecSpec{2, VecOrientation::col}, 0.5); }));
+        Matrix sf = random_normal(l, l, 0.0, 2.0, mrng);
+        for (double th : {-1.0, 0.0, 2.5, 100.0}) CHECK(gpu::threshold_mask(sf, th, false) == threshold_mask(sf, th, false));
+        for (double th : {1e-4, 1.0 / l, 0.05, 0.9}) {
+            CHECK(gpu::threshold_mask(sf, th, true) == threshold_mask(sf, th, true));
+            Matrix s32 = sf.as_precision(Precision::f32);
+            CHECK(gpu::threshold_mask(s32, th, true) == threshold_mask(s32, th, true));
+        }
+        SparseMask te = gpu::threshold_mask(sf, 0.9, true);
+        CHECK(te.has_empty_rows() == threshold_mask(sf, 0.9, true).has_empty_rows());
+        CHECK(throws<ParamError>([&] { gpu::threshold_mask(sf, std::nan(""), false); }));
+        CHECK(throws<ShapeError>([&] { gpu::threshold_mask(Matrix(4, 5), 0.1, false); }));
+    }
+
     STEP("predictor precision rule");
     // combine() (P/include/dsattn/matrix.hpp:90-93): a product is f32 only when
     // both operands are.  The ToyModel case -- f32 activations and W~, f64
