@@ -63,6 +63,16 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// 8 x 8 b16 transpose across the warp: the lane holding row lane/4, columns
+// 2 (lane%4), +1 gets row lane/4, columns 2 (lane%4), +1 of the TRANSPOSE --
+// turns an m16n8 accumulator half (keys x queries) into the k16n8 B-fragment
+// half (P^T[keys 2c4, 2c4+1][query g]) without a shared-memory round trip.
+__device__ __forceinline__ uint32_t movm_t(uint32_t x) {
+    uint32_t r;
+    asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;\n" : "=r"(r) : "r"(x));
+    return r;
+}
+
 // Row r of a [rows][D] bf16 tile, 16-byte chunk c, XOR-swizzled within 8 chunks.
 template <int D>
 __device__ __forceinline__ uint32_t swz(int r, int c) {
@@ -215,24 +225,29 @@ __device__ __forceinline__ void band_core(BandSmemV2<D>& sm, const __nv_bfloat16
             zacc[t][2] *= corr[0];
             zacc[t][3] *= corr[1];
         }
-        constexpr int PW = CH + 8;
+        // P^T as MMA B fragments straight from the S^T accumulators: bf16 pairs
+        // (key g / g + 8, queries 2 c4, 2 c4 + 1) transposed across the warp
+        uint32_t pb[2][2];
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
+        for (int mt = 0; mt < 2; ++mt) {
+            float pv[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 // a column may have no live key yet (m_run = -inf): weight 0
-                const float pv = (SEG && s[mt][u] == -INFINITY) ? 0.f : fast_ex2(s[mt][u] - m_run[u & 1]);
-                l_part[u & 1] += pv;
-                sm.p[(2 * c4 + (u & 1)) * PW + mt * 16 + g + (u >> 1) * 8] = __float2bfloat16_rn(pv);
+                pv[u] = (SEG && s[mt][u] == -INFINITY) ? 0.f : fast_ex2(s[mt][u] - m_run[u & 1]);
+                // the weight the MMA sees is the bf16 value; the row sum keeps fp32 (as before)
+                l_part[u & 1] += pv[u];
             }
+            pb[mt][0] = movm_t(pack_bf16(pv[0], pv[1]));
+            pb[mt][1] = movm_t(pack_bf16(pv[2], pv[3]));
+        }
         cp_async_wait<1>();
         __syncwarp();
         // ---- Z^T += V_chunk^T . P^T
         const uint32_t vb = smem_u32(sm.v[buf]);
 #pragma unroll
         for (int ks = 0; ks < CH / 16; ++ks) {
-            const uint32_t b0 = *reinterpret_cast<const uint32_t*>(&sm.p[g * PW + ks * 16 + 2 * c4]);
-            const uint32_t b1 = *reinterpret_cast<const uint32_t*>(&sm.p[g * PW + ks * 16 + 8 + 2 * c4]);
+            const uint32_t b0 = pb[ks][0], b1 = pb[ks][1];
 #pragma unroll
             for (int mt = 0; mt < D / 16; ++mt) {
                 const int mi = lane >> 3;
