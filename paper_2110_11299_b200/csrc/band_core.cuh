@@ -81,11 +81,14 @@ __device__ __forceinline__ uint32_t swz(int r, int c) {
     (void)kChunks;
 }
 
+// Per-warp shared memory: the double-buffered V rows of a 32-key chunk; the
+// Z rows are staged in v[0] once the key loop is done.  8 KB (d = 64) per
+// warp, 128 KB per 16-warp CTA: the rest of the SM's 256 KB stays L1, which
+// the K-row gathers hit 20-26 % of the time (a third V stage -- 213 KB per
+// CTA -- measured SLOWER: C1 0.51 -> 0.64 ms, C4 24.3 -> 30.7 ms).
 template <int D>
 struct BandSmemV2 {
     __nv_bfloat16 v[2][32 * D];
-    __nv_bfloat16 p[8 * 40];  // [query][key], padded rows
-    __nv_bfloat16 z[8 * D];
 };
 
 template <int D>
@@ -275,22 +278,24 @@ __device__ __forceinline__ void band_core(BandSmemV2<D>& sm, const __nv_bfloat16
         l_part[h] += __shfl_xor_sync(0xffffffffu, l_part[h], 8);
         l_part[h] += __shfl_xor_sync(0xffffffffu, l_part[h], 16);
     }
+    __syncwarp();  // every lane done with the V buffers: v[0] now stages Z
+    __nv_bfloat16* zst = sm.v[0];
     const float inv0 = l_part[0] > 0.f ? 1.f / l_part[0] : 0.f;
     const float inv1 = l_part[1] > 0.f ? 1.f / l_part[1] : 0.f;
 #pragma unroll
     for (int mt = 0; mt < D / 16; ++mt) {
         const int d0 = mt * 16 + g;
-        sm.z[(2 * c4) * D + d0] = __float2bfloat16_rn(zacc[mt][0] * inv0);
-        sm.z[(2 * c4 + 1) * D + d0] = __float2bfloat16_rn(zacc[mt][1] * inv1);
-        sm.z[(2 * c4) * D + d0 + 8] = __float2bfloat16_rn(zacc[mt][2] * inv0);
-        sm.z[(2 * c4 + 1) * D + d0 + 8] = __float2bfloat16_rn(zacc[mt][3] * inv1);
+        zst[(2 * c4) * D + d0] = __float2bfloat16_rn(zacc[mt][0] * inv0);
+        zst[(2 * c4 + 1) * D + d0] = __float2bfloat16_rn(zacc[mt][1] * inv1);
+        zst[(2 * c4) * D + d0 + 8] = __float2bfloat16_rn(zacc[mt][2] * inv0);
+        zst[(2 * c4 + 1) * D + d0 + 8] = __float2bfloat16_rn(zacc[mt][3] * inv1);
     }
     __syncwarp();
     for (int t = lane; t < kRows * kChunks16; t += 32) {
         const int r = t / kChunks16, c = t % kChunks16;
         if (r0 + r < L)
             *reinterpret_cast<uint4*>(Z + (pair * L + r0 + r) * D + c * 8) =
-                *reinterpret_cast<const uint4*>(&sm.z[r * D + c * 8]);
+                *reinterpret_cast<const uint4*>(&zst[r * D + c * 8]);
     }
 }
 
