@@ -248,7 +248,6 @@ struct BlockSmemT {
     static constexpr int kHalf = 32 * 128;      // one 32-row x 64-column panel
     static constexpr int kKV = D / 64 * kHalf;  // K (or V) of one block
     unsigned char ring[kStg][2][kKV];           // [stage][K, V][panels]; Z staging at the end
-    __nv_bfloat16 p[kWarps][NT][8 * 40];
     uint64_t full[kStg];
     static_assert(kStg * 2 * kKV >= kWarps * NT * 8 * D * 2, "Z staging fits the ring");
 };
@@ -341,7 +340,8 @@ __global__ void __launch_bounds__(128 / NT)
                 for (int n = 0; n < NT; ++n) mma16816(s[n][mt], a0, a1, a2, a3, qb[n][ks][0], qb[n][ks][1]);
             }
         }
-        constexpr int PW = CHUNK + 8;
+        // P^T as MMA B fragments straight from the S^T accumulators (movmatrix: no shared-memory round trip)
+        uint32_t pb[NT][CHUNK / 16][2];
 #pragma unroll
         for (int n = 0; n < NT; ++n) {
             float cmax[2] = {-INFINITY, -INFINITY};
@@ -375,23 +375,25 @@ __global__ void __launch_bounds__(128 / NT)
                 zacc[n][t][3] *= corr[1];
             }
 #pragma unroll
-            for (int mt = 0; mt < CHUNK / 16; ++mt)
+            for (int mt = 0; mt < CHUNK / 16; ++mt) {
+                float pv[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    const float pv = fast_ex2(s[n][mt][u] - m_run[n][u & 1]);
-                    l_part[n][u & 1] += pv;
-                    sm.p[warp][n][(2 * c4 + (u & 1)) * PW + mt * 16 + g + (u >> 1) * 8] = __float2bfloat16_rn(pv);
+                    pv[u] = fast_ex2(s[n][mt][u] - m_run[n][u & 1]);
+                    l_part[n][u & 1] += pv[u];
                 }
+                pb[n][mt][0] = bc::movm_t(bc::pack_bf16(pv[0], pv[1]));  // keys g: -> P^T[keys 2c4, 2c4+1][query g]
+                pb[n][mt][1] = bc::movm_t(bc::pack_bf16(pv[2], pv[3]));  // keys g + 8
+            }
         }
-        __syncwarp();
         const uint32_t vb = tc::smem_addr(sm.ring[st][1]);
 #pragma unroll
         for (int ks = 0; ks < CHUNK / 16; ++ks) {
             uint32_t b0[NT], b1[NT];
 #pragma unroll
             for (int n = 0; n < NT; ++n) {
-                b0[n] = *reinterpret_cast<const uint32_t*>(&sm.p[warp][n][g * PW + ks * 16 + 2 * c4]);
-                b1[n] = *reinterpret_cast<const uint32_t*>(&sm.p[warp][n][g * PW + ks * 16 + 8 + 2 * c4]);
+                b0[n] = pb[n][ks][0];
+                b1[n] = pb[n][ks][1];
             }
 #pragma unroll
             for (int mt = 0; mt < D / 16; ++mt) {
